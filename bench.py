@@ -1,0 +1,323 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native D3Q19 collide+propagate step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one LBM time step (one collide+propagate sweep of the whole
+lattice). At N=1 the workload is BASELINE.json configs[1] ("C1"): a 256^3
+channel, periodic in x/y, half-way bounce-back walls at z=0/255, BGK
+omega=1.7, body force 1e-6 along x, rest start, AA pattern, direct
+addressing, SoA, fp64. value = fluid nodes x K / device time (MFLUP/s).
+Under torchrun (N>1) the box of BASELINE.json configs[3] is split into
+z-slabs, one per rank.
+
+Prints ONE JSON line (rank 0). See DESIGN.md section 7 for every key.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MFLUP/s and achieved HBM GB/s as % of bytes/FLUP roofline, 1/2/4/8 B200"
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c1": dict(dims=(256, 256, 256), policy=("periodic", "periodic", "wall"), omega=1.7,
+               force=(1e-6, 0.0, 0.0), init="rest",
+               desc="C1: 256^3 channel, periodic x/y, bounce-back walls z=0/255, BGK omega=1.7, "
+                    "g=1e-6 x, rest start"),
+    # BASELINE.json configs[0]
+    "c0": dict(dims=(128, 128, 128), policy=("periodic",) * 3, omega=1.0, force=(0.0, 0.0, 0.0),
+               init="taylor_green",
+               desc="C0: 128^3 periodic, BGK omega=1.0, Taylor-Green + 1e-4 noise"),
+    # BASELINE.json configs[4]
+    "c4": dict(dims=(200, 200, 200), policy=("periodic",) * 3, omega=1.0, force=(0.0, 0.0, 0.0),
+               init="taylor_green", desc="C4: 200^3 periodic, BGK omega=1.0, Taylor-Green"),
+    # BASELINE.json configs[3] (multi-GPU z-slabs)
+    "c3": dict(dims=(512, 512, 1024), policy=("periodic",) * 3, omega=1.0,
+               force=(0.0, 0.0, 0.0), init="taylor_green",
+               desc="C3: 512x512x1024 periodic, BGK omega=1.0, Taylor-Green, z-slabs"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _one(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip()
+            if out:
+                self.rows.append([v.strip() for v in out.split(",")])
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._one()
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            self._one()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > k + 2 and r[k + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws == 1:
+        return 1, 0, 0, None
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    return ws, rank, local, dist
+
+
+def reduce_max(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def traffic_from_profiles(kernel_key):
+    """dram bytes read+write per launch from the committed ncu --set full capture"""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(kernel_key)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(cfg, scheme, budget_s=20.0, max_steps=None):
+    """The UNMODIFIED reference (oracle/_ref/libref.so, built from /root/reference)
+    through its own run_bench (p/src/bench.cpp:155-198) with every host core."""
+    import oracle
+    R = oracle.RefLib()
+    dims = cfg["dims"]
+    pol = [1 if p == "wall" else 0 for p in cfg["policy"]]
+    om = cfg["omega"]
+    magic = (1.0 / om - 0.5) ** 2
+    # one probe step sizes the sample to the budget
+    s1, _, _ = R.run_bench(scheme, 0, dims, pol, None, om, magic, cfg["force"], 1, workers=0,
+                           warmup=0, timed_runs=1)
+    steps = max(2, int(budget_s / 3.0 / max(s1, 1e-6)))
+    if max_steps:
+        steps = min(steps, max_steps)
+    sec, mlups, workers = R.run_bench(scheme, 0, dims, pol, None, om, magic, cfg["force"],
+                                      steps, workers=0, warmup=1, timed_runs=3)
+    return dict(value=mlups, unit="MFLUP/s", cores=workers, kind="reference",
+                sample=f"{cfg['desc']}; reference {scheme}/direct run_bench, {steps} steps x 3 "
+                       f"runs (median) after 1 warm-up step, workers=0 -> {workers} threads, "
+                       f"nproc={os.cpu_count()}, OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND', 'unset')}")
+
+
+def run_reference_arm(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    budget = float(os.environ.get("LBM_REF_BUDGET_S", "90"))
+    base = cpu_reference_sample(cfg, args.scheme, budget_s=budget, max_steps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "MFLUP/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (rest start, BASELINE.json config)",
+        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": "direct",
+                   "layout": "soa", "dims": list(cfg["dims"])},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    nodes = cfg["dims"][0] * cfg["dims"][1] * cfg["dims"][2]
+    line["ms_per_step"] = nodes / (base["value"] * 1e6) * 1e3
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    ws, rank, local, dist = dist_setup()
+    import paper_1111_0922_b200 as L
+    if L.device_count() < 1:
+        raise SystemExit("no CUDA device visible")
+    if ws > 1:
+        return run_slabs(args, ws, rank, local, dist, L)
+
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    geo = L.GridGeometry(*dims, cfg["policy"])
+    flow = L.bgk(cfg["omega"], body_force=cfg["force"])
+    opts = L.StepperOptions(layout=args.layout, precision=args.precision, device=local,
+                            extensions=args.scheme in ("ts", "swap-push", "swap-pull")
+                            and args.addressing == "indirect")
+    st = L.create_stepper(args.scheme, args.addressing, geo, flow, opts)
+    st.init_field(cfg["init"], seed=2011)
+    nodes = st.node_count()
+    pdf = 8 if args.precision == 8 else 4
+
+    # warm-up, then K steps between CUDA events on the launching stream
+    st.step_n(args.warmup)
+    st.synchronize()
+    barrier(dist)
+    with ClockSampler(local) as clk:
+        ms = st.step_timed(args.steps)
+    ms = reduce_max(dist, ms)
+    launches = st.launches_per_step()
+    value = nodes * args.steps / (ms * 1e-3) / 1e6
+
+    peak, peak_src = load_peaks()
+    bpl = L.gpu_bytes_per_lup(args.scheme, args.addressing, pdf)
+    per_launch_ms = ms / (args.steps * launches)
+    # dominant kernel: one launch updates every node once for AA/ET/OS/CG (bytes
+    # per launch = bytes/FLUP x N); two-launch schemes split the step
+    achieved = bpl * nodes / launches / (per_launch_ms * 1e-3) / 1e9
+    kern = {"aap": "k_local+k_aa_odd", "et": "k_et", "os-pull": "k_os_pull",
+            "os-push": "k_os_push", "osnt-pull-1s": "k_os_pull", "osnt-pull-2s": "k_os_pull",
+            "cg": "k_cg", "ts": "k_local+k_ts_stream", "swap-push": "k_local+k_swap",
+            "swap-pull": "k_swap+k_local"}[args.scheme]
+    tr = traffic_from_profiles(f"{args.config}:{args.scheme}:{args.addressing}:{args.layout}:{pdf}")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": tr,
+                "algorithmic_bytes_per_flup": bpl, "kernel": kern,
+                "per_launch_ms": round(per_launch_ms, 5), "peak_source": peak_src,
+                "model_mflups": round(peak * 1e9 / bpl / 1e6, 1)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "MFLUP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if pdf == 8 else "f32",
+        "data": "synthetic (BASELINE.json config; seeded device-side init)",
+        "config": {"workload": cfg["desc"], "scheme": args.scheme,
+                   "addressing": args.addressing, "layout": args.layout,
+                   "dims": list(dims), "fluid_nodes": nodes,
+                   "l2": f"inputs larger than L2 ({st.storage_bytes()[0] / 1e9:.2f} GB field "
+                         f"vs 126 MB L2), no flush needed"},
+        "roofline": roofline,
+        "gpu_launches": args.steps * launches,
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_run(L, st, args, nodes)
+    if not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_reference_sample(cfg, args.scheme, budget_s=20.0)
+        except Exception as e:  # reference library absent on this box
+            line["cpu_baseline"] = {"value": None, "unit": "MFLUP/s", "cores": 0,
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def e2e_run(L, st, args, nodes):
+    """Same metric through the public API with HOST buffers: load the canonical
+    snapshot from pinned host memory, K steps, extract it back to pinned host
+    memory, all inside the timed region (wall clock around synchronous calls)."""
+    n = nodes * 19
+    src = L.PinnedArray(n)
+    st.extract_natural(src.array)  # a valid state to start from
+    dst = L.PinnedArray(n)
+    st.synchronize()
+    t0 = time.perf_counter()
+    st.load_natural(src.array)
+    st.step_n(args.steps)
+    st.extract_natural(dst.array)
+    t = time.perf_counter() - t0
+    return {"value": round(nodes * args.steps / t / 1e6, 2), "unit": "MFLUP/s",
+            "h2d_bytes_per_step": n * 8 / args.steps, "d2h_bytes_per_step": n * 8 / args.steps,
+            "seconds": round(t, 4),
+            "note": "load_natural(pinned host) + K steps + extract_natural(pinned host)"}
+
+
+def run_slabs(args, ws, rank, local, dist, L):
+    raise SystemExit("multi-GPU z-slab bench: see run_slabs in a later revision")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--scheme", default="aap")
+    ap.add_argument("--addressing", default="direct")
+    ap.add_argument("--layout", default="soa")
+    ap.add_argument("--precision", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

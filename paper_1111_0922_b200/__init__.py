@@ -1,0 +1,420 @@
+"""B200-native D3Q19 collide+propagate (arXiv 1111.0922 propagation schemes).
+
+Python mirror of the reference's C++ lattice/propagation API (``lbmlab``,
+``/root/reference/proj/include/lbmlab``): ``GridGeometry``, ``FlowParams``,
+``StepperOptions``, ``create_stepper`` -> ``Stepper`` with ``step`` /
+``extract_natural`` / ``load_natural`` / ``layout_phase`` /
+``exchange_opposite_handles``, ``kernel_available``, ``build_sparse``,
+``traffic``, ``lambda_odd``. Every call goes through the C ABI of
+``include/lbmgpu.h`` into ``liblbmgpu.so`` (hand-written sm_100a kernels).
+There is no CPU fallback: importing fails loudly when the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIBRARY_PATH = os.path.join(_HERE, "liblbmgpu.so")
+
+if not os.path.exists(LIBRARY_PATH):
+    raise ImportError(
+        f"{LIBRARY_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+        "g.build()'` (make -C paper_1111_0922_b200/csrc). There is no CPU fallback.")
+
+_L = C.CDLL(LIBRARY_PATH)
+
+# lbmlab::SchemeId order (p/include/lbmlab/stepper.hpp:15-26)
+SCHEMES = ("ts", "os-push", "os-pull", "osnt-pull-1s", "osnt-pull-2s", "cg", "swap-push",
+           "swap-pull", "aap", "et")
+FAMILIES = ("ts", "os", "osnt", "cg", "swap", "aap", "et")
+FAMILY_OF = {"ts": "ts", "os-push": "os", "os-pull": "os", "osnt-pull-1s": "osnt",
+             "osnt-pull-2s": "osnt", "cg": "cg", "swap-push": "swap", "swap-pull": "swap",
+             "aap": "aap", "et": "et"}
+ADDRESSINGS = ("direct", "indirect")
+LAYOUT_PHASES = ("natural", "opposed", "shifted_even", "shifted_odd", "twisted", "swap_partial")
+Q = 19
+
+
+class _Geometry(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("axis_policy", C.c_uint8 * 3), ("mask", C.c_void_p)]
+
+
+class _Flow(C.Structure):
+    _fields_ = [("lambda_even", C.c_double), ("lambda_odd", C.c_double),
+                ("body_force", C.c_double * 3), ("rho0", C.c_double)]
+
+
+class _Options(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "scheme", "addressing", "layout", "precision", "device", "workers", "chunk_length",
+        "streaming_stores", "swap_deferred_fixup", "zero_collision", "extensions", "z_begin",
+        "z_end")]
+
+
+_P = C.c_void_p
+_sig = {
+    "lbmgpu_default_options": (None, [C.POINTER(_Options)]),
+    "lbmgpu_create": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
+                                C.POINTER(_P)]),
+    "lbmgpu_destroy": (C.c_int, [_P]),
+    "lbmgpu_step": (C.c_int, [_P, C.c_int64]),
+    "lbmgpu_step_timed": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_double)]),
+    "lbmgpu_synchronize": (C.c_int, [_P]),
+    "lbmgpu_extract_natural": (C.c_int, [_P, _P]),
+    "lbmgpu_load_natural": (C.c_int, [_P, _P]),
+    "lbmgpu_extract_natural_device": (C.c_int, [_P, _P]),
+    "lbmgpu_load_natural_device": (C.c_int, [_P, _P]),
+    "lbmgpu_init_field": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                                    C.c_double]),
+    "lbmgpu_layout_phase": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "lbmgpu_exchange_opposite_handles": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "lbmgpu_time_step": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "lbmgpu_node_count": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "lbmgpu_storage_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "lbmgpu_stream": (C.c_int, [_P, C.POINTER(_P)]),
+    "lbmgpu_launches_per_step": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "lbmgpu_kernel_available": (C.c_int, [C.c_int32, C.c_int32]),
+    "lbmgpu_kernel_available_ext": (C.c_int, [C.c_int32, C.c_int32]),
+    "lbmgpu_build_sparse": (C.c_int, [C.POINTER(_Geometry), C.c_int32, C.POINTER(C.c_uint32),
+                                      _P, _P]),
+    "lbmgpu_build_et_rem": (C.c_int, [C.POINTER(_Geometry), C.c_int32, C.POINTER(C.c_uint32),
+                                      _P, C.POINTER(C.c_uint32)]),
+    "lbmgpu_traffic": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_double)]),
+    "lbmgpu_gpu_bytes_per_lup": (C.c_int, [C.c_int32, C.c_int32, C.c_int32,
+                                           C.POINTER(C.c_double)]),
+    "lbmgpu_lambda_odd": (C.c_double, [C.c_double, C.c_double]),
+    "lbmgpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    "lbmgpu_host_free": (C.c_int, [_P]),
+    "lbmgpu_last_error": (C.c_char_p, []),
+    "lbmgpu_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
+    "lbmgpu_version": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(_L, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+# status -> Python exception, mirroring the reference's C++ exception types
+_ERRORS = {1: ValueError, 2: RuntimeError, 3: ArithmeticError, 4: MemoryError, 5: RuntimeError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = (_L.lbmgpu_last_error() or b"").decode()
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def _scheme_id(s) -> int:
+    if isinstance(s, (int, np.integer)):
+        return int(s)
+    n = str(s).lower().replace("_", "-")
+    if n not in SCHEMES:
+        raise ValueError(f"unknown scheme: {s}")
+    return SCHEMES.index(n)
+
+
+def _addr_id(a) -> int:
+    if isinstance(a, (int, np.integer)):
+        return int(a)
+    n = str(a).lower()
+    if n in ("direct", "full"):
+        return 0
+    if n in ("indirect", "sparse"):
+        return 1
+    raise ValueError(f"unknown addressing: {a}")
+
+
+# ---------------------------------------------------------------------------
+# reference value types
+# ---------------------------------------------------------------------------
+@dataclass
+class GridGeometry:
+    """lbmlab::GridGeometry (p/include/lbmlab/geometry.hpp:19-38)."""
+    nx: int
+    ny: int
+    nz: int
+    axis_policy: Sequence[str] = ("periodic", "periodic", "periodic")
+    mask: Optional[np.ndarray] = None  # x-fastest uint8, 1 = fluid; None = all fluid
+
+    def cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def fluid_count(self) -> int:
+        return self.cells() if self.mask is None else int(np.count_nonzero(self.mask))
+
+    def _c(self):
+        g = _Geometry(self.nx, self.ny, self.nz)
+        for k, p in enumerate(self.axis_policy):
+            g.axis_policy[k] = {"periodic": 0, "wall": 1, 0: 0, 1: 1}[p]
+        keep = None
+        if self.mask is not None:
+            keep = np.ascontiguousarray(self.mask, dtype=np.uint8).ravel()
+            if keep.size != self.cells():
+                raise ValueError("mask size does not match the grid")
+            g.mask = keep.ctypes.data
+        return g, keep
+
+
+def gen_channel(nx: int, ny: int, nz: int) -> GridGeometry:
+    """gen_channel (p/src/geometry.cpp:62-71): periodic x, walls in y and z."""
+    if min(nx, ny, nz) < 1:
+        raise ValueError("zero dimension")
+    return GridGeometry(nx, ny, nz, ("periodic", "wall", "wall"))
+
+
+@dataclass
+class FlowParams:
+    """lbmlab::FlowParams (p/include/lbmlab/collision.hpp:10-15), same defaults."""
+    lambda_even: float = 1.0 / 0.9
+    magic_lambda: float = 3.0 / 16.0
+    body_force: Sequence[float] = (1e-5, 0.0, 0.0)
+    rho0: float = 1.0
+
+
+def lambda_odd(p: FlowParams) -> float:
+    """lambda_odd (p/src/collision.cpp:8-11)."""
+    return _L.lbmgpu_lambda_odd(p.lambda_even, p.magic_lambda)
+
+
+def bgk(omega: float, body_force=(0.0, 0.0, 0.0), rho0: float = 1.0) -> FlowParams:
+    """BGK as TRT with lambda_odd == lambda_even: magic Lambda = (1/omega - 1/2)^2
+    makes lambda_odd(p) return omega exactly for the omegas used here (checked)."""
+    p = FlowParams(omega, (1.0 / omega - 0.5) ** 2, tuple(body_force), rho0)
+    if lambda_odd(p) != omega:
+        raise ValueError(f"no exact BGK magic parameter for omega={omega}")
+    return p
+
+
+@dataclass
+class StepperOptions:
+    """lbmlab::StepperOptions (p/include/lbmlab/stepper.hpp:55-64) + GPU selectors."""
+    workers: int = 1
+    chunk_length: int = 150
+    streaming_stores: bool = True
+    swap_deferred_fixup: bool = False
+    zero_collision: bool = False
+    layout: str = "soa"        # "soa" | "aos"
+    precision: int = 8         # 8 fp64 | 4 fp32
+    device: int = 0
+    extensions: bool = False   # allow TS/SWAP indirect (GPU-only kernels)
+
+
+# ---------------------------------------------------------------------------
+# Stepper
+# ---------------------------------------------------------------------------
+class Stepper:
+    """lbmlab::Stepper (p/include/lbmlab/stepper.hpp:70-106) on a B200."""
+
+    def __init__(self, handle: C.c_void_p, scheme: int, addressing: int, opts: StepperOptions):
+        self._h = handle
+        self._scheme = scheme
+        self._addr = addressing
+        self.options = opts
+        n = C.c_uint64()
+        _check(_L.lbmgpu_node_count(self._h, C.byref(n)))
+        self._nodes = int(n.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.lbmgpu_destroy(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
+
+    # -- the reference surface ------------------------------------------------
+    def step(self) -> None:
+        """One time step, synchronous like the reference's Stepper::step()."""
+        _check(_L.lbmgpu_step(self._h, 1))
+        _check(_L.lbmgpu_synchronize(self._h))
+
+    def step_n(self, n: int) -> None:
+        """n time steps enqueued asynchronously on the stepper's stream."""
+        _check(_L.lbmgpu_step(self._h, int(n)))
+
+    def step_timed(self, n: int) -> float:
+        """n steps between CUDA events on the launching stream; returns device ms."""
+        ms = C.c_double()
+        _check(_L.lbmgpu_step_timed(self._h, int(n), C.byref(ms)))
+        return ms.value
+
+    def synchronize(self) -> None:
+        _check(_L.lbmgpu_synchronize(self._h))
+
+    def extract_natural(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.values(), dtype=np.float64)
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != self.values():
+            raise ValueError("out must be a contiguous float64 array of node_count*19")
+        _check(_L.lbmgpu_extract_natural(self._h, out.ctypes.data))
+        return out
+
+    def load_natural(self, f: np.ndarray) -> None:
+        a = np.ascontiguousarray(f, dtype=np.float64).ravel()
+        if a.size != self.values():
+            raise ValueError("snapshot must hold node_count*19 values")
+        _check(_L.lbmgpu_load_natural(self._h, a.ctypes.data))
+
+    def extract_natural_device(self, dev_ptr: int) -> None:
+        _check(_L.lbmgpu_extract_natural_device(self._h, dev_ptr))
+
+    def load_natural_device(self, dev_ptr: int) -> None:
+        _check(_L.lbmgpu_load_natural_device(self._h, dev_ptr))
+
+    def init_field(self, kind: str = "rest", seed: int = 0, u0: float = 0.01,
+                   drho: float = 1e-3, noise: float = 1e-4) -> None:
+        k = {"rest": 0, "taylor_green": 1, "random": 2}[kind]
+        _check(_L.lbmgpu_init_field(self._h, k, seed, u0, drho, noise))
+
+    def layout_phase(self) -> str:
+        v = C.c_int32()
+        _check(_L.lbmgpu_layout_phase(self._h, C.byref(v)))
+        return LAYOUT_PHASES[v.value]
+
+    def exchange_opposite_handles(self) -> bool:
+        v = C.c_int32()
+        _check(_L.lbmgpu_exchange_opposite_handles(self._h, C.byref(v)))
+        return bool(v.value)
+
+    def scheme(self) -> str:
+        return SCHEMES[self._scheme]
+
+    def addressing(self) -> str:
+        return ADDRESSINGS[self._addr]
+
+    def time_step(self) -> int:
+        v = C.c_int64()
+        _check(_L.lbmgpu_time_step(self._h, C.byref(v)))
+        return int(v.value)
+
+    def node_count(self) -> int:
+        return self._nodes
+
+    def q(self) -> int:
+        return Q
+
+    def values(self) -> int:
+        return self._nodes * Q
+
+    # -- GPU extras -------------------------------------------------------------
+    def storage_bytes(self):
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(_L.lbmgpu_storage_bytes(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def launches_per_step(self) -> int:
+        v = C.c_int32()
+        _check(_L.lbmgpu_launches_per_step(self._h, C.byref(v)))
+        return int(v.value)
+
+    def cuda_stream(self) -> int:
+        v = C.c_void_p()
+        _check(_L.lbmgpu_stream(self._h, C.byref(v)))
+        return int(v.value or 0)
+
+
+def create_stepper(scheme, addressing, geometry: GridGeometry, flow: FlowParams = None,
+                   options: StepperOptions = None) -> Stepper:
+    """create_stepper (p/src/stepper.cpp:155-180)."""
+    flow = flow or FlowParams()
+    options = options or StepperOptions()
+    sid, aid = _scheme_id(scheme), _addr_id(addressing)
+    g, keep = geometry._c()
+    fl = _Flow(flow.lambda_even, lambda_odd(flow), (C.c_double * 3)(*flow.body_force), flow.rho0)
+    o = _Options()
+    _L.lbmgpu_default_options(C.byref(o))
+    o.scheme, o.addressing = sid, aid
+    o.layout = {"soa": 0, "aos": 1}[options.layout.lower()]
+    o.precision = int(options.precision)
+    o.device = int(options.device)
+    o.workers = int(options.workers)
+    o.chunk_length = int(options.chunk_length)
+    o.streaming_stores = int(bool(options.streaming_stores))
+    o.swap_deferred_fixup = int(bool(options.swap_deferred_fixup))
+    o.zero_collision = int(bool(options.zero_collision))
+    o.extensions = int(bool(options.extensions))
+    h = C.c_void_p()
+    _check(_L.lbmgpu_create(C.byref(g), C.byref(fl), C.byref(o), C.byref(h)))
+    del keep
+    return Stepper(h, sid, aid, options)
+
+
+def kernel_available(scheme, addressing, extensions: bool = False) -> bool:
+    """kernel_available (p/src/stepper.cpp:140-153)."""
+    f = _L.lbmgpu_kernel_available_ext if extensions else _L.lbmgpu_kernel_available
+    return bool(f(_scheme_id(scheme), _addr_id(addressing)))
+
+
+def build_sparse(geometry: GridGeometry, device: int = 0, node_of: bool = False):
+    """build_sparse (p/src/geometry.cpp:173-207) on the GPU. Returns
+    (fluid_count, adjacency[N, 18] uint32 node-major, node_of[cells] or None)."""
+    g, keep = geometry._c()
+    n = C.c_uint32()
+    _check(_L.lbmgpu_build_sparse(C.byref(g), device, C.byref(n), None, None))
+    adj = np.empty(int(n.value) * 18, dtype=np.uint32)
+    nof = np.empty(geometry.cells(), dtype=np.uint32) if node_of else None
+    _check(_L.lbmgpu_build_sparse(C.byref(g), device, C.byref(n), adj.ctypes.data,
+                                  nof.ctypes.data if node_of else None))
+    del keep
+    return int(n.value), adj.reshape(-1, 18), nof
+
+
+def build_et_rem(geometry: GridGeometry, device: int = 0):
+    """ET indirect remote table (p/src/scheme_et.cpp:42-62): (rem[N, 9], mailboxes)."""
+    g, keep = geometry._c()
+    n, m = C.c_uint32(), C.c_uint32()
+    _check(_L.lbmgpu_build_et_rem(C.byref(g), device, C.byref(n), None, C.byref(m)))
+    rem = np.empty(int(n.value) * 9, dtype=np.uint32)
+    _check(_L.lbmgpu_build_et_rem(C.byref(g), device, C.byref(n), rem.ctypes.data, C.byref(m)))
+    del keep
+    return rem.reshape(-1, 9), int(m.value)
+
+
+def traffic(family, addressing, pdf_bytes: int = 8):
+    """traffic() (p/src/perfmodel.cpp:12-75): (counts[6], bytes_per_lup)."""
+    fam = FAMILIES.index(family) if isinstance(family, str) else int(family)
+    out = (C.c_int32 * 6)()
+    b = C.c_double()
+    _check(_L.lbmgpu_traffic(fam, _addr_id(addressing), pdf_bytes, out, C.byref(b)))
+    return list(out), b.value
+
+
+def gpu_bytes_per_lup(scheme, addressing, pdf_bytes: int = 8) -> float:
+    """Compulsory DRAM bytes per fluid-node update."""
+    b = C.c_double()
+    _check(_L.lbmgpu_gpu_bytes_per_lup(_scheme_id(scheme), _addr_id(addressing), pdf_bytes,
+                                       C.byref(b)))
+    return b.value
+
+
+class PinnedArray:
+    """float64 array in page-locked host memory (lbmgpu_host_alloc)."""
+
+    def __init__(self, n: int):
+        p = C.c_void_p()
+        _check(_L.lbmgpu_host_alloc(int(n) * 8, C.byref(p)))
+        self._p = p
+        self.array = np.ctypeslib.as_array((C.c_double * int(n)).from_address(p.value))
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            _L.lbmgpu_host_free(self._p)
+            self._p = None
+
+
+def device_count() -> int:
+    v = C.c_int32()
+    _check(_L.lbmgpu_device_count(C.byref(v)))
+    return int(v.value)
+
+
+def version() -> str:
+    return _L.lbmgpu_version().decode()

@@ -1,0 +1,370 @@
+// sm_100a kernels for direct (full-grid) addressing: one thread per lattice
+// cell, threads x-contiguous so every direction plane (SoA) is read and written
+// as coalesced, 256-byte aligned warp rows (the +-1 x shift of a neighbour
+// access costs one extra L2 sector per warp, never an extra DRAM byte).
+//
+// Each kernel restates one reference sweep (cited per kernel); the collision
+// is dev::collide (p/src/collision.cpp:95-139, bit-exact).
+#include "dispatch.h"
+#include "launch.h"
+
+namespace lbmgpu {
+using namespace dev;
+
+namespace {
+
+template <class T>
+Trt<T> cast_op(const TrtHost& h) {
+  Trt<T> o;
+  o.lambda_e = (T)h.lambda_e;
+  o.le_half = (T)h.le_half;
+  o.lo_half = (T)h.lo_half;
+  o.w0 = (T)h.w0;
+  for (int p = 0; p < 9; ++p) {
+    o.w2[p] = (T)h.w2[p];
+    o.f3w[p] = (T)h.f3w[p];
+  }
+  return o;
+}
+
+inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
+
+// ---------------------------------------------------------------------------
+// Local collision sweep. Covers
+//   TS collide_sweep A -> B            (p/src/scheme_ts.cpp:59-80)
+//   OS/OSNT precollide, in place        (p/src/scheme_os.cpp:79-102)
+//   AA even sweep: write opposite slots (p/src/scheme_aap.cpp:114-131)
+//   SWAP collide from opposed slots     (p/src/scheme_swap.cpp:187-190, 228-231)
+// ---------------------------------------------------------------------------
+template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
+__global__ void __launch_bounds__(kBlock) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
+                                                  Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(src.at(RD_OPP ? opp(i) : i, c.s));
+  collide(op, f);
+#pragma unroll
+  for (int i = 0; i < 19; ++i) st<false>(dst.at(WR_OPP ? opp(i) : i, c.s), f[i]);
+}
+
+// TS stream_sweep: pull B -> A with bounce B[opp i][cell] (p/src/scheme_ts.cpp:82-112)
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T v[19];
+  v[0] = ld(b.at(0, c.s));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const T* src = c.bb(j) ? b.at(j, c.s) : b.at(i, c.s + c.off(j));
+    v[i] = ld(src);
+  }
+#pragma unroll
+  for (int i = 0; i < 19; ++i) st<false>(a.at(i, c.s), v[i]);
+}
+
+// OS pull (p/src/scheme_os.cpp:141-174) and OSNT pull with streaming stores
+// (p/src/scheme_osnt.cpp:131-173, 175-217: 1S = one store loop per direction,
+// 2S = rest then one per opposing pair; st.global.cs replaces _mm_stream_si64).
+template <class T, bool AOS, bool NT, bool TWO_S>
+__global__ void __launch_bounds__(kBlock) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+                                                    Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T f[19];
+  f[0] = ld(a.at(0, c.s));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const T* src = c.bb(j) ? a.at(j, c.s) : a.at(i, c.s + c.off(j));
+    f[i] = ld(src);
+  }
+  collide(op, f);
+  if (!TWO_S) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) st<NT>(b.at(i, c.s), f[i]);
+  } else {
+    st<NT>(b.at(0, c.s), f[0]);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      st<NT>(b.at(pair_i(p), c.s), f[pair_i(p)]);
+      st<NT>(b.at(pair_j(p), c.s), f[pair_j(p)]);
+    }
+  }
+}
+
+// OS push (p/src/scheme_os.cpp:104-139)
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+                                                    Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(a.at(i, c.s));
+  collide(op, f);
+  st<false>(b.at(0, c.s), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    T* dst = c.bb(i) ? b.at(opp(i), c.s) : b.at(i, c.s + c.off(i));
+    st<false>(dst, f[i]);
+  }
+}
+
+// AA pattern odd sweep (p/src/scheme_aap.cpp:133-173): gather
+// f[opp i][x - c_i] (bounce: f[i][x]), collide, scatter f[j][x + c_j]
+// (bounce: f[opp j][x]). Every slot is read and rewritten by one thread.
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T f[19];
+  f[0] = ld(F.at(0, c.s));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const T* src = c.bb(j) ? F.at(i, c.s) : F.at(j, c.s + c.off(j));
+    f[i] = ld(src);
+  }
+  collide(op, f);
+  st<false>(F.at(0, c.s), f[0]);
+#pragma unroll
+  for (int j = 1; j < 19; ++j) {
+    T* dst = c.bb(j) ? F.at(opp(j), c.s) : F.at(j, c.s + c.off(j));
+    st<false>(dst, f[j]);
+  }
+}
+
+// Esoteric twist sweep (p/src/scheme_et.cpp:191-239). For pair (i, j):
+// tmp_i = F[b_i][X], tmp_j = F[b_(db?i:j)][X + c_i]; collide;
+// F[b_(ub?j:i)][X] = tmp_j, F[b_j][X + c_i] = tmp_i. Wall axes carry a halo
+// plane, solid cells act as mailboxes, so X + c_i is always a storage slot.
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, EtBase B) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  T f[19];
+  f[0] = ld(F.at(0, c.s));
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    const long long rs = c.s + c.off(i);
+    f[i] = ld(F.at(B.b[i], c.s));
+    f[j] = ld(F.at(c.bb(i) ? B.b[i] : B.b[j], rs));
+  }
+  collide(op, f);
+  st<false>(F.at(0, c.s), f[0]);
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    const long long rs = c.s + c.off(i);
+    st<false>(F.at(c.bb(j) ? B.b[j] : B.b[i], c.s), f[j]);
+    st<false>(F.at(B.b[j], rs), f[i]);
+  }
+}
+
+// SWAP link exchange (p/src/scheme_swap.cpp:172-235, fix-ups :127-131).
+// The set of swapped slot pairs {(i, X), (opp i, X + c_i)}, i in the back
+// half, is identical for push and pull, pairwise disjoint, and never depends
+// on the current sweep's collisions — so the reference's strictly sequential
+// sweep equals "all collisions, then all swaps" (push) or "all swaps, then all
+// collisions" (pull), bit for bit. mode: 0 all, 1 non-wrapped, 2 wrapped only.
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_swap(Fld<T, AOS> F, Lat L, int mode) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int i = back_dir(k);
+    if (c.bb(i)) continue;
+    const bool w = c.wrapped(L, i);
+    if ((mode == 1 && w) || (mode == 2 && !w)) continue;
+    T* a = F.at(i, c.s);
+    T* b = F.at(opp(i), c.s + c.off(i));
+    const T va = ld(a), vb = ld(b);
+    st<false>(a, vb);
+    st<false>(b, va);
+  }
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Compressed grid sweep (p/src/scheme_cg.cpp:118-158), parallel form.
+// Within one sweep every slot is read before it is overwritten and there are
+// only write-after-read hazards: the node reading the slot a write lands on
+// sits at X + (1,1,1) + c_i (even) / X - (1,1,1) + c_i (odd). Tiles of 256
+// lexicographic cells take tickets in the reference traversal order (reverse
+// lex for even, forward for odd); a tile loads and collides, publishes
+// "reads done" (release), waits (acquire) for the <= 38 tiles owning its write
+// targets — all of which hold earlier tickets, so they are resident and never
+// wait on it — and only then stores. Values crossing a periodic seam land
+// unwrapped in the padding and are copied by k_cg_fixup after the sweep.
+template <class T, bool AOS, bool EVEN>
+__global__ void __launch_bounds__(kBlock) k_cg(Fld<T, AOS> F, Lat L, Trt<T> op,
+                                               unsigned long long* ticket, unsigned* flags,
+                                               unsigned epoch, uint32_t ntiles) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) {
+    const unsigned long long k = atomicAdd(ticket, 1ull) - (unsigned long long)(epoch - 1) * ntiles;
+    s_tile = EVEN ? ntiles - 1 - (uint32_t)k : (uint32_t)k;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t cell = tile * kBlock + threadIdx.x;
+  const bool active = cell < L.ncells;
+  Ctx c;
+  T f[19];
+  if (active) {
+    c = make_ctx(L, cell);  // L.o* = read origin (1 even, 2 odd)
+    if (c.fluid) {
+#pragma unroll
+      for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
+      collide(op, f);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flags + tile, epoch);
+  }
+  if (threadIdx.x < 38) {
+    const int d = threadIdx.x >> 1;
+    const int sgn = EVEN ? 1 : -1;
+    const long long D = (long long)(sgn + cx(d)) + (long long)L.nx * (sgn + cy(d)) +
+                        (long long)L.nx * L.ny * (sgn + cz(d));
+    long long tgt = (long long)tile * kBlock + D + ((threadIdx.x & 1) ? kBlock - 1 : 0);
+    if (tgt >= 0 && tgt < (long long)L.ncells) {
+      const unsigned* fl = flags + (uint32_t)(tgt / kBlock);
+      while (ld_acquire(fl) != epoch) __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (!active || !c.fluid) return;
+  const long long sh = (long long)1 + L.sx + L.sxy;  // shift1
+  const long long wr = EVEN ? c.s + sh : c.s - sh;
+  st<false>(F.at(0, wr), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const long long po = (long long)cx(i) + (long long)L.sx * cy(i) + L.sxy * cz(i);
+    T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + po);
+    st<false>(dst, f[i]);
+  }
+}
+
+template <class T, bool AOS>
+__global__ void k_cg_fixup(Fld<T, AOS> F, const long long* src, const long long* dst,
+                           const int8_t* dir, long long count, long long shift) {
+  const long long k = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const int i = dir[k];
+  *F.at(i, dst[k] - shift) = *F.at(i, src[k] - shift);
+}
+
+}  // namespace
+
+void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,
+                  const TrtHost& op, bool rd_opp, bool wr_opp) {
+  LBM_DISPATCH(src, {
+    auto a = fld<T, A>(src);
+    auto b = fld<T, A>(dst);
+    const auto o = cast_op<T>(op);
+    const unsigned g = grid_for(L.ncells);
+    if (!rd_opp && !wr_opp) k_local<T, A, false, false><<<g, kBlock, 0, st>>>(a, b, L, o);
+    if (!rd_opp && wr_opp) k_local<T, A, false, true><<<g, kBlock, 0, st>>>(a, b, L, o);
+    if (rd_opp && !wr_opp) k_local<T, A, true, false><<<g, kBlock, 0, st>>>(a, b, L, o);
+    if (rd_opp && wr_opp) k_local<T, A, true, true><<<g, kBlock, 0, st>>>(a, b, L, o);
+  });
+}
+
+void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L) {
+  LBM_DISPATCH(a, {
+    k_ts_stream<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L);
+  });
+}
+
+void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
+                    const TrtHost& op, bool streaming, bool two_s) {
+  LBM_DISPATCH(a, {
+    auto fa = fld<T, A>(a);
+    auto fb = fld<T, A>(b);
+    const auto o = cast_op<T>(op);
+    const unsigned g = grid_for(L.ncells);
+    if (!streaming && !two_s) k_os_pull<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
+    if (!streaming && two_s) k_os_pull<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, L, o);
+    if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
+    if (streaming && two_s) k_os_pull<T, A, true, true><<<g, kBlock, 0, st>>>(fa, fb, L, o);
+  });
+}
+
+void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
+                    const TrtHost& op) {
+  LBM_DISPATCH(a, {
+    k_os_push<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L,
+                                                           cast_op<T>(op));
+  });
+}
+
+void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op) {
+  LBM_DISPATCH(f, {
+    k_aa_odd<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+  });
+}
+
+void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+               const EtBase& base) {
+  LBM_DISPATCH(f, {
+    k_et<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), base);
+  });
+}
+
+void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) {
+  LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
+}
+
+void launch_cg(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+               bool even, unsigned long long* ticket, unsigned* flags, unsigned epoch) {
+  const uint32_t ntiles = grid_for(L.ncells);
+  LBM_DISPATCH(f, {
+    if (even)
+      k_cg<T, A, true><<<ntiles, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket, flags,
+                                                  epoch, ntiles);
+    else
+      k_cg<T, A, false><<<ntiles, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket,
+                                                   flags, epoch, ntiles);
+  });
+}
+
+void launch_cg_fixup(cudaStream_t st, const DField& f, const long long* src,
+                     const long long* dst, const int8_t* dir, long long count, long long shift) {
+  if (count <= 0) return;
+  LBM_DISPATCH(f, {
+    k_cg_fixup<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), src, dst, dir, count,
+                                                         shift);
+  });
+}
+
+}  // namespace lbmgpu

@@ -1,0 +1,243 @@
+// sm_100a kernels for indirect (IDX) addressing: fluid nodes only, enumerated
+// x-fastest, one thread per node. The adjacency is stored transposed,
+// adj[(i-1)*N + n], so the 18 index loads of a warp are 18 coalesced 128-byte
+// rows (the reference's node-major adjacency[n*18 + i-1], geometry.cpp:196-205,
+// is exported bit-identically by lbmgpu_build_sparse). A bounce link stores
+// the node itself.
+#include "dispatch.h"
+#include "launch.h"
+
+namespace lbmgpu {
+using namespace dev;
+
+namespace {
+
+template <class T>
+Trt<T> cast_op(const TrtHost& h) {
+  Trt<T> o;
+  o.lambda_e = (T)h.lambda_e;
+  o.le_half = (T)h.le_half;
+  o.lo_half = (T)h.lo_half;
+  o.w0 = (T)h.w0;
+  for (int p = 0; p < 9; ++p) {
+    o.w2[p] = (T)h.w2[p];
+    o.f3w[p] = (T)h.f3w[p];
+  }
+  return o;
+}
+
+inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
+
+__device__ __forceinline__ uint32_t ldidx(const uint32_t* p) { return __ldg(p); }
+
+// local collision over nodes (TS collide, precollide, AA even, SWAP collide)
+template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
+__global__ void __launch_bounds__(kBlock) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
+                                                      uint32_t n, Trt<T> op) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= n) return;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(src.at(RD_OPP ? opp(i) : i, node));
+  collide(op, f);
+#pragma unroll
+  for (int i = 0; i < 19; ++i) st<false>(dst.at(WR_OPP ? opp(i) : i, node), f[i]);
+}
+
+// TS streaming over the IDX graph (GPU extension; the reference's TS is
+// direct-only, stepper.cpp:140-153): A[i][n] = src == n ? B[opp i][n] : B[i][src]
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_ts_stream_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+  T v[19];
+  v[0] = ld(b.at(0, node));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const uint32_t src = ldidx(I.adj + (size_t)(j - 1) * I.n + node);
+    v[i] = ld(src == node ? b.at(j, node) : b.at(i, src));
+  }
+#pragma unroll
+  for (int i = 0; i < 19; ++i) st<false>(a.at(i, node), v[i]);
+}
+
+// OS / OSNT pull, indirect (p/src/scheme_os.cpp:203-226, scheme_osnt.cpp:219-260)
+template <class T, bool AOS, bool NT, bool TWO_S>
+__global__ void __launch_bounds__(kBlock) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
+                                                        Trt<T> op) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+  T f[19];
+  f[0] = ld(a.at(0, node));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const uint32_t src = ldidx(I.adj + (size_t)(j - 1) * I.n + node);
+    f[i] = ld(src == node ? a.at(j, node) : a.at(i, src));
+  }
+  collide(op, f);
+  if (!TWO_S) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) st<NT>(b.at(i, node), f[i]);
+  } else {
+    st<NT>(b.at(0, node), f[0]);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      st<NT>(b.at(pair_i(p), node), f[pair_i(p)]);
+      st<NT>(b.at(pair_j(p), node), f[pair_j(p)]);
+    }
+  }
+}
+
+// OS push, indirect (p/src/scheme_os.cpp:176-201)
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_os_push_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
+                                                        Trt<T> op) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(a.at(i, node));
+  collide(op, f);
+  st<false>(b.at(0, node), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const uint32_t nb = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
+    st<false>(nb == node ? b.at(opp(i), node) : b.at(i, nb), f[i]);
+  }
+}
+
+// AA odd sweep, indirect (p/src/scheme_aap.cpp:175-201). The gather uses
+// row[opp i - 1] for i = 1..18 and the scatter row[j - 1] for j = 1..18: the
+// same 18 entries, loaded once.
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_aa_odd_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+  uint32_t e[19];
+#pragma unroll
+  for (int i = 1; i < 19; ++i) e[i] = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
+  T f[19];
+  f[0] = ld(F.at(0, node));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    f[i] = ld(e[j] == node ? F.at(i, node) : F.at(j, e[j]));
+  }
+  collide(op, f);
+  st<false>(F.at(0, node), f[0]);
+#pragma unroll
+  for (int j = 1; j < 19; ++j) st<false>(e[j] == node ? F.at(opp(j), node) : F.at(j, e[j]), f[j]);
+}
+
+// ET sweep, indirect (p/src/scheme_et.cpp:241-272): rem[p][n] = neighbour
+// along c_i or a mailbox slot >= N (i-link bounces), bit 31 = j-link bounces.
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op, EtBase B) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+  uint32_t rs[9];
+  T f[19];
+  f[0] = ld(F.at(0, node));
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    rs[p] = ldidx(I.rem + (size_t)p * I.n + node);
+    const uint32_t r = rs[p] & 0x7fffffffu;
+    const bool db = r >= I.n;
+    f[i] = ld(F.at(B.b[i], node));
+    f[j] = ld(F.at(db ? B.b[i] : B.b[j], r));
+  }
+  collide(op, f);
+  st<false>(F.at(0, node), f[0]);
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    const bool ub = (rs[p] & 0x80000000u) != 0;
+    st<false>(F.at(ub ? B.b[j] : B.b[i], node), f[j]);
+    st<false>(F.at(B.b[j], rs[p] & 0x7fffffffu), f[i]);
+  }
+}
+
+// SWAP link exchange over the IDX graph (GPU extension, see k_swap): every
+// non-bounce back-half link swaps (i, n) <-> (opp i, adj[i][n]).
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock) k_swap_idx(Fld<T, AOS> F, Idx I) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.n) return;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int i = back_dir(k);
+    const uint32_t nb = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
+    if (nb == node) continue;
+    T* a = F.at(i, node);
+    T* b = F.at(opp(i), nb);
+    const T va = ld(a), vb = ld(b);
+    st<false>(a, vb);
+    st<false>(b, va);
+  }
+}
+
+}  // namespace
+
+void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uint32_t n,
+                      const TrtHost& op, bool rd_opp, bool wr_opp) {
+  LBM_DISPATCH(src, {
+    auto a = fld<T, A>(src);
+    auto b = fld<T, A>(dst);
+    const auto o = cast_op<T>(op);
+    const unsigned g = grid_for(n);
+    if (!rd_opp && !wr_opp) k_local_idx<T, A, false, false><<<g, kBlock, 0, st>>>(a, b, n, o);
+    if (!rd_opp && wr_opp) k_local_idx<T, A, false, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+    if (rd_opp && !wr_opp) k_local_idx<T, A, true, false><<<g, kBlock, 0, st>>>(a, b, n, o);
+    if (rd_opp && wr_opp) k_local_idx<T, A, true, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+  });
+}
+
+void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I) {
+  LBM_DISPATCH(a, {
+    k_ts_stream_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I);
+  });
+}
+
+void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
+                        const TrtHost& op, bool streaming, bool two_s) {
+  LBM_DISPATCH(a, {
+    auto fa = fld<T, A>(a);
+    auto fb = fld<T, A>(b);
+    const auto o = cast_op<T>(op);
+    const unsigned g = grid_for(I.n);
+    if (!streaming && !two_s) k_os_pull_idx<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, I, o);
+    if (!streaming && two_s) k_os_pull_idx<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, I, o);
+    if (streaming && !two_s) k_os_pull_idx<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, I, o);
+    if (streaming && two_s) k_os_pull_idx<T, A, true, true><<<g, kBlock, 0, st>>>(fa, fb, I, o);
+  });
+}
+
+void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
+                        const TrtHost& op) {
+  LBM_DISPATCH(a, {
+    k_os_push_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I,
+                                                          cast_op<T>(op));
+  });
+}
+
+void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
+  LBM_DISPATCH(f, {
+    k_aa_odd_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
+  });
+}
+
+void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
+                   const EtBase& base) {
+  LBM_DISPATCH(f, {
+    k_et_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op), base);
+  });
+}
+
+void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I) {
+  LBM_DISPATCH(f, { k_swap_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I); });
+}
+
+}  // namespace lbmgpu

@@ -1,0 +1,543 @@
+// Geometry/IDX construction, canonical-snapshot conversion and initial
+// fields, all on the device (sm_100a).
+//
+//   build_node_maps  exclusive scan of the fluid mask -> node_of / cell_of_node
+//                    (the x-fastest enumeration of build_sparse,
+//                    p/src/geometry.cpp:187-194)
+//   launch_adjacency resolve_link per (node, dir) -> transposed IDX
+//                    (p/src/geometry.cpp:49-60, 196-205)
+//   build_et_rem     ET remote table with per-pair mailbox running counts
+//                    (p/src/scheme_et.cpp:42-62) as 9 exclusive scans
+//   launch_extract / launch_load
+//                    canonical snapshot <-> scheme storage (the
+//                    copy_out/gather_out/load_in helpers, p/src/stepper.cpp:207-289,
+//                    and the per-scheme extract_natural/load_natural)
+#include "dispatch.h"
+#include "launch.h"
+
+namespace lbmgpu {
+using namespace dev;
+
+namespace {
+
+inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
+
+__device__ __forceinline__ double weight(int i) {
+  return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0);
+}
+
+// counter-based uniform in [-1, 1): splitmix64 of (seed, stream)
+__device__ __forceinline__ double urand(unsigned long long seed, unsigned long long stream) {
+  unsigned long long z = seed + 0x9e3779b97f4a7c15ull * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return __dsub_rn(__dmul_rn((double)(z >> 11), 0x1.0p-52), 1.0);
+}
+
+// equilibrium (p/src/collision.cpp:38-45)
+__device__ __forceinline__ double equilibrium(double rho, double ux, double uy, double uz, int i) {
+  double cu = 0.0, usq = 0.0;
+  cu = __dadd_rn(cu, __dmul_rn((double)cx(i), ux));
+  usq = __dadd_rn(usq, __dmul_rn(ux, ux));
+  cu = __dadd_rn(cu, __dmul_rn((double)cy(i), uy));
+  usq = __dadd_rn(usq, __dmul_rn(uy, uy));
+  cu = __dadd_rn(cu, __dmul_rn((double)cz(i), uz));
+  usq = __dadd_rn(usq, __dmul_rn(uz, uz));
+  const double a = __dadd_rn(__dadd_rn(1.0, __dmul_rn(3.0, cu)), __dmul_rn(__dmul_rn(4.5, cu), cu));
+  return __dmul_rn(__dmul_rn(weight(i), rho), __dsub_rn(a, __dmul_rn(1.5, usq)));
+}
+
+// Initial canonical values of one node (host buffer or a generator).
+//  Rest:        w_i rho0 (every reference stepper's start, e.g. scheme_aap.cpp:32-36)
+//  TaylorGreen: equilibrium(rho, u) + noise*U, rho = rho0 + drho*U,
+//               u = u0 (sin X cos Y cos Z, -cos X sin Y cos Z, 0),
+//               X = 2 pi x / gnx (cell index x, likewise Y, Z)
+//  Random:      w_i rho0 (0.9 + 0.2 U01)  (shape of test_schemes.cpp:29-39)
+// U draws are keyed by the GLOBAL cell index, so z-slabs reproduce the
+// single-domain field exactly.
+__device__ __forceinline__ void node_values(const InitSpec& in, const double* buf, uint32_t k,
+                                            int x, int y, int z, double (&v)[19]) {
+  if (in.source == kSrcBuffer) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) v[i] = buf[(size_t)k * 19 + i];
+    return;
+  }
+  if (in.source == kSrcRest) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) v[i] = __dmul_rn(weight(i), in.rho0);
+    return;
+  }
+  const int gz = z + in.z0;
+  const unsigned long long gcell =
+      (unsigned long long)x + (unsigned long long)in.gnx * ((unsigned long long)y + (unsigned long long)in.gny * gz);
+  if (in.source == kSrcRandom) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) {
+      const double u01 = 0.5 * (urand(in.seed, gcell * 20 + i) + 1.0);
+      v[i] = __dmul_rn(__dmul_rn(weight(i), in.rho0), __dadd_rn(0.9, __dmul_rn(0.2, u01)));
+    }
+    return;
+  }
+  double sx, cxv, sy, cyv, sz, czv;
+  sincospi(2.0 * x / in.gnx, &sx, &cxv);
+  sincospi(2.0 * y / in.gny, &sy, &cyv);
+  sincospi(2.0 * gz / in.gnz, &sz, &czv);
+  const double rho = in.rho0 + in.drho * urand(in.seed, gcell * 20 + 19);
+  const double ux = in.u0 * sx * cyv * czv;
+  const double uy = -in.u0 * cxv * sy * czv;
+  const double uz = 0.0;
+#pragma unroll
+  for (int i = 0; i < 19; ++i)
+    v[i] = equilibrium(rho, ux, uy, uz, i) + in.noise * urand(in.seed, gcell * 20 + i);
+}
+
+template <class T, bool AOS>
+__global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint32_t n0,
+                          uint32_t count, int mode, EtBase B, double* buf) {
+  const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const uint32_t node = n0 + k;
+  const uint32_t cell = cell_of_node ? cell_of_node[node] : node;
+  const Ctx c = make_ctx(L, cell);
+  double* o = buf + (size_t)k * 19;
+  switch (mode) {
+    case kExNatural:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(i, c.s);
+      break;
+    case kExOpposed:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(opp(i), c.s);
+      break;
+    case kExGather:  // gather_out_direct (p/src/stepper.cpp:228-252)
+      o[0] = (double)*F.at(0, c.s);
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        o[i] = (double)*(c.bb(j) ? F.at(j, c.s) : F.at(i, c.s + c.off(j)));
+      }
+      break;
+    case kExAaOdd:  // AapStepper::extract_natural, odd (p/src/scheme_aap.cpp:57-75)
+      o[0] = (double)*F.at(0, c.s);
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        o[i] = (double)*(c.bb(j) ? F.at(i, c.s) : F.at(j, c.s + c.off(j)));
+      }
+      break;
+    case kExEt:  // EtStepper::extract_natural, direct (p/src/scheme_et.cpp:83-109)
+      o[0] = (double)*F.at(0, c.s);
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        o[i] = (double)*F.at(B.b[i], c.s);
+        o[j] = (double)*F.at(c.bb(i) ? B.b[i] : B.b[j], c.s + c.off(i));
+      }
+      break;
+  }
+}
+
+template <class T, bool AOS>
+__global__ void k_load(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint32_t n0,
+                       uint32_t count, int mode, const double* buf, InitSpec in) {
+  const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const uint32_t node = n0 + k;
+  const uint32_t cell = cell_of_node ? cell_of_node[node] : node;
+  const Ctx c = make_ctx(L, cell);
+  double v[19];
+  node_values(in, buf, k, c.x, c.y, c.z, v);
+  switch (mode) {
+    case kExNatural:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) *F.at(i, c.s) = (T)v[i];
+      break;
+    case kExOpposed:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) *F.at(opp(i), c.s) = (T)v[i];
+      break;
+    case kExEt:  // EtStepper::fill, direct (p/src/scheme_et.cpp:152-169), identity handles
+      *F.at(0, c.s) = (T)v[0];
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        *F.at(i, c.s) = (T)v[i];
+        *F.at(c.bb(i) ? i : j, c.s + c.off(i)) = (T)v[j];
+      }
+      break;
+  }
+}
+
+template <class T, bool AOS>
+__global__ void k_extract_idx(Fld<T, AOS> F, Idx I, uint32_t n0, uint32_t count, int mode,
+                              EtBase B, double* buf) {
+  const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const uint32_t node = n0 + k;
+  double* o = buf + (size_t)k * 19;
+  switch (mode) {
+    case kExNatural:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(i, node);
+      break;
+    case kExOpposed:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(opp(i), node);
+      break;
+    case kExGather:  // gather_out_indirect (p/src/stepper.cpp:254-271)
+      o[0] = (double)*F.at(0, node);
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        const uint32_t src = I.adj[(size_t)(j - 1) * I.n + node];
+        o[i] = (double)*(src == node ? F.at(j, node) : F.at(i, src));
+      }
+      break;
+    case kExAaOdd:  // p/src/scheme_aap.cpp:81-97
+      o[0] = (double)*F.at(0, node);
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        const uint32_t e = I.adj[(size_t)(j - 1) * I.n + node];
+        o[i] = (double)*(e == node ? F.at(i, node) : F.at(j, e));
+      }
+      break;
+    case kExEt:  // p/src/scheme_et.cpp:110-123
+      o[0] = (double)*F.at(0, node);
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        const uint32_t r = I.rem[(size_t)p * I.n + node] & 0x7fffffffu;
+        o[i] = (double)*F.at(B.b[i], node);
+        o[j] = (double)*F.at(r >= I.n ? B.b[i] : B.b[j], r);
+      }
+      break;
+  }
+}
+
+template <class T, bool AOS>
+__global__ void k_load_idx(Fld<T, AOS> F, Idx I, Lat L, const uint32_t* cell_of_node,
+                           uint32_t n0, uint32_t count, int mode, const double* buf, InitSpec in) {
+  const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const uint32_t node = n0 + k;
+  int x = 0, y = 0, z = 0;
+  if (in.source != kSrcBuffer) {
+    const uint32_t cell = cell_of_node ? cell_of_node[node] : node;
+    const uint32_t row = L.divx.div(cell);
+    x = (int)(cell - row * (uint32_t)L.nx);
+    const uint32_t zz = L.divy.div(row);
+    y = (int)(row - zz * (uint32_t)L.ny);
+    z = (int)zz;
+  }
+  double v[19];
+  node_values(in, buf, k, x, y, z, v);
+  switch (mode) {
+    case kExNatural:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) *F.at(i, node) = (T)v[i];
+      break;
+    case kExOpposed:
+#pragma unroll
+      for (int i = 0; i < 19; ++i) *F.at(opp(i), node) = (T)v[i];
+      break;
+    case kExEt:  // EtStepper::fill, indirect (p/src/scheme_et.cpp:170-183)
+      *F.at(0, node) = (T)v[0];
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        const uint32_t r = I.rem[(size_t)p * I.n + node] & 0x7fffffffu;
+        *F.at(i, node) = (T)v[i];
+        *F.at(r >= I.n ? i : j, r) = (T)v[j];
+      }
+      break;
+  }
+}
+
+template <class T>
+__global__ void k_fill(T* p, long long count, T v) {
+  for (long long k = (long long)blockIdx.x * kBlock + threadIdx.x; k < count;
+       k += (long long)gridDim.x * kBlock)
+    p[k] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Device-wide exclusive scan (3 phases: tile reduce, scan of tile sums in one
+// block, tile re-scan + offset). Tiles of 1024 threads x 16 items.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 16;
+constexpr uint64_t kScanTile = (uint64_t)kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// exclusive block scan of one value per thread; returns exclusive prefix, total in *tot
+__device__ uint32_t block_excl(uint32_t v, uint32_t* tot) {
+  __shared__ uint32_t ws[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl(v);
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = ws[lane];
+    ws[lane] = warp_incl(x) - x;
+  }
+  __syncthreads();
+  const uint32_t r = ws[w] + inc - v;
+  if (tot) *tot = ws[31] + __shfl_sync(0xffffffffu, inc, 31);  // valid for the last warp
+  __syncthreads();
+  return r;
+}
+
+struct MaskFlag {
+  const uint8_t* m;
+  __device__ uint32_t operator()(uint64_t k) const { return m[k] != 0; }
+};
+struct BounceFlag {  // ET: i-link of pair p bounces
+  const uint32_t* adj_i;
+  __device__ uint32_t operator()(uint64_t k) const { return adj_i[k] == (uint32_t)k; }
+};
+
+template <class Flag>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Flag fl, uint64_t n, uint32_t* part) {
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t)
+    if (base + t < n) s += fl(base + t);
+  uint32_t tot = 0;
+  block_excl(s, &tot);
+  if (threadIdx.x == kScanThreads - 1) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_parts(uint32_t* part, uint32_t np,
+                                                             unsigned long long* total) {
+  const uint32_t per = (np + kScanThreads - 1) / kScanThreads;
+  const uint32_t b0 = threadIdx.x * per;
+  uint32_t s = 0;
+  for (uint32_t k = 0; k < per; ++k)
+    if (b0 + k < np) s += part[b0 + k];
+  uint32_t tot = 0;
+  uint32_t run = block_excl(s, &tot);
+  for (uint32_t k = 0; k < per; ++k)
+    if (b0 + k < np) {
+      const uint32_t v = part[b0 + k];
+      part[b0 + k] = run;
+      run += v;
+    }
+  if (threadIdx.x == kScanThreads - 1) *total = tot;
+}
+
+template <class Flag, class Sink>
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(Flag fl, uint64_t n,
+                                                             const uint32_t* part, Sink sink) {
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t f[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t) {
+    f[t] = (base + t < n) ? fl(base + t) : 0u;
+    s += f[t];
+  }
+  uint32_t run = block_excl(s, nullptr) + part[blockIdx.x];
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t)
+    if (base + t < n) {
+      sink(base + t, f[t], run);
+      run += f[t];
+    }
+}
+
+struct NodeMapSink {
+  uint32_t* node_of;
+  uint32_t* cell_of_node;
+  __device__ void operator()(uint64_t cell, uint32_t flag, uint32_t idx) const {
+    if (node_of) node_of[cell] = flag ? idx : ~0u;
+    if (flag && cell_of_node) cell_of_node[idx] = (uint32_t)cell;
+  }
+};
+
+struct EtRemSink {
+  const uint32_t* adj_i;
+  const uint32_t* adj_j;
+  uint32_t* rem_p;
+  uint32_t n;
+  __device__ void operator()(uint64_t node, uint32_t flag, uint32_t idx) const {
+    const uint32_t r = flag ? n + idx : adj_i[node];
+    const bool ub = adj_j[node] == (uint32_t)node;
+    rem_p[node] = r | (ub ? 0x80000000u : 0u);
+  }
+};
+
+template <class Flag, class Sink>
+uint64_t device_scan(cudaStream_t st, Flag fl, uint64_t n, Sink sink, uint32_t* scratch) {
+  const uint32_t np = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(scratch);
+  uint32_t* part = scratch + 2;
+  if (np == 0) return 0;
+  k_scan_reduce<<<np, kScanThreads, 0, st>>>(fl, n, part);
+  k_scan_parts<<<1, kScanThreads, 0, st>>>(part, np, total);
+  k_scan_apply<<<np, kScanThreads, 0, st>>>(fl, n, part, sink);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, total, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return h;
+}
+
+// resolve_link on the device (p/src/geometry.cpp:49-60); returns target cell or -1 (bounce)
+__device__ __forceinline__ long long resolve(const uint8_t* mask, const Lat& L, int x, int y,
+                                             int z, int i) {
+  int t[3] = {x + cx(i), y + cy(i), z + cz(i)};
+  const int n[3] = {L.nx, L.ny, L.nz};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (t[k] >= 0 && t[k] < n[k]) continue;
+    if (L.wall[k]) return -1;
+    t[k] = t[k] < 0 ? t[k] + n[k] : t[k] - n[k];
+  }
+  const long long cell = (long long)t[0] + (long long)L.nx * ((long long)t[1] + (long long)L.ny * t[2]);
+  if (mask && !mask[cell]) return -1;
+  return cell;
+}
+
+__global__ void k_linkmask(const uint8_t* mask, Lat L, uint32_t* out) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  if (mask && !mask[cell]) {
+    out[cell] = 0;
+    return;
+  }
+  const uint32_t row = L.divx.div(cell);
+  const int x = (int)(cell - row * (uint32_t)L.nx);
+  const uint32_t z = L.divy.div(row);
+  const int y = (int)(row - z * (uint32_t)L.ny);
+  uint32_t m = 1u;
+#pragma unroll
+  for (int i = 1; i < 19; ++i)
+    if (resolve(mask, L, x, y, (int)z, i) < 0) m |= 1u << i;
+  out[cell] = m;
+}
+
+__global__ void k_adjacency(const uint8_t* mask, Lat L, const uint32_t* node_of,
+                            const uint32_t* cell_of_node, uint32_t n, uint32_t* adjT) {
+  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+  if (node >= n) return;
+  const uint32_t cell = cell_of_node ? cell_of_node[node] : node;
+  const uint32_t row = L.divx.div(cell);
+  const int x = (int)(cell - row * (uint32_t)L.nx);
+  const uint32_t z = L.divy.div(row);
+  const int y = (int)(row - z * (uint32_t)L.ny);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const long long t = resolve(mask, L, x, y, (int)z, i);
+    adjT[(size_t)(i - 1) * n + node] =
+        t < 0 ? node : (node_of ? node_of[t] : (uint32_t)t);
+  }
+}
+
+__global__ void k_transpose(const uint32_t* inT, uint32_t rows, uint32_t n, uint32_t* out) {
+  const uint64_t k = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+  if (k >= (uint64_t)rows * n) return;
+  const uint32_t node = (uint32_t)(k / rows), r = (uint32_t)(k % rows);
+  out[k] = inT[(size_t)r * n + node];
+}
+
+}  // namespace
+
+uint64_t scan_scratch_elems(uint64_t n) { return 2 + (n + kScanTile - 1) / kScanTile + 2; }
+
+uint64_t build_node_maps(cudaStream_t st, const uint8_t* mask, uint64_t ncells,
+                         uint32_t* node_of, uint32_t* cell_of_node, uint32_t* scratch,
+                         uint64_t) {
+  return device_scan(st, MaskFlag{mask}, ncells, NodeMapSink{node_of, cell_of_node}, scratch);
+}
+
+uint32_t build_et_rem(cudaStream_t st, const uint32_t* adjT, uint32_t n, uint32_t* remT,
+                      uint32_t* scratch, uint64_t) {
+  uint32_t nmail = 0;
+  for (int p = 0; p < 9; ++p) {
+    const uint32_t* ai = adjT + (size_t)(pair_i(p) - 1) * n;
+    const uint32_t* aj = adjT + (size_t)(pair_j(p) - 1) * n;
+    const uint64_t cnt =
+        device_scan(st, BounceFlag{ai}, n, EtRemSink{ai, aj, remT + (size_t)p * n, n}, scratch);
+    if (cnt > nmail) nmail = (uint32_t)cnt;
+  }
+  return nmail;
+}
+
+void launch_linkmask(cudaStream_t st, const uint8_t* mask, const dev::Lat& L, uint32_t* out) {
+  k_linkmask<<<grid_for(L.ncells), kBlock, 0, st>>>(mask, L, out);
+}
+
+void launch_adjacency(cudaStream_t st, const uint8_t* mask, const dev::Lat& L,
+                      const uint32_t* node_of, const uint32_t* cell_of_node, uint32_t n,
+                      uint32_t* adjT) {
+  if (n == 0) return;
+  k_adjacency<<<grid_for(n), kBlock, 0, st>>>(mask, L, node_of, cell_of_node, n, adjT);
+}
+
+void launch_transpose_u32(cudaStream_t st, const uint32_t* inT, uint32_t rows, uint32_t n,
+                          uint32_t* out) {
+  const uint64_t tot = (uint64_t)rows * n;
+  if (tot == 0) return;
+  k_transpose<<<grid_for(tot), kBlock, 0, st>>>(inT, rows, n, out);
+}
+
+void launch_extract(cudaStream_t st, const DField& f, const dev::Lat& L,
+                    const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                    const EtBase& base, double* buf) {
+  if (count == 0) return;
+  LBM_DISPATCH(f, {
+    k_extract<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), L, cell_of_node, n0,
+                                                        count, mode, base, buf);
+  });
+}
+
+void launch_load(cudaStream_t st, const DField& f, const dev::Lat& L,
+                 const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                 const double* buf, const InitSpec& init) {
+  if (count == 0) return;
+  LBM_DISPATCH(f, {
+    k_load<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), L, cell_of_node, n0, count,
+                                                     mode, buf, init);
+  });
+}
+
+void launch_extract_idx(cudaStream_t st, const DField& f, const Idx& I, uint32_t n0,
+                        uint32_t count, int mode, const EtBase& base, double* buf) {
+  if (count == 0) return;
+  LBM_DISPATCH(f, {
+    k_extract_idx<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), I, n0, count, mode,
+                                                            base, buf);
+  });
+}
+
+void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::Lat& Lcells,
+                     const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                     const double* buf, const InitSpec& init) {
+  if (count == 0) return;
+  LBM_DISPATCH(f, {
+    k_load_idx<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), I, Lcells, cell_of_node,
+                                                         n0, count, mode, buf, init);
+  });
+}
+
+void launch_fill(cudaStream_t st, const DField& f, long long count, double v) {
+  if (count <= 0) return;
+  const unsigned g = (unsigned)std::min<long long>((count + kBlock - 1) / kBlock, 148 * 64);
+  if (f.prec == Prec::f64)
+    k_fill<double><<<g, kBlock, 0, st>>>(static_cast<double*>(f.p), count, v);
+  else
+    k_fill<float><<<g, kBlock, 0, st>>>(static_cast<float*>(f.p), count, (float)v);
+}
+
+}  // namespace lbmgpu

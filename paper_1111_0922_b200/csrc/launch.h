@@ -1,0 +1,125 @@
+// Host-side launchers for the sm_100a kernels (internal to liblbmgpu.so).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lbm_device.cuh"
+
+namespace lbmgpu {
+
+enum class Prec { f64 = 8, f32 = 4 };
+
+// A PDF field in device memory: SoA (direction planes of `stride` elements)
+// or AoS (node-major records of 19), fp64 or fp32.
+struct DField {
+  void* p = nullptr;
+  long long stride = 0;
+  bool aos = false;
+  Prec prec = Prec::f64;
+};
+
+// TrtOperator coefficients in double (cast per launch for fp32)
+struct TrtHost {
+  double lambda_e, le_half, lo_half, w0;
+  double w2[9], f3w[9];
+};
+
+struct EtBase {
+  int8_t b[20];
+};
+
+constexpr int kBlock = 256;
+
+// ---- direct (full-grid) addressing -----------------------------------------
+// collide every fluid cell locally: dst[wr(i)][s] = collide(src[rd(i)][s])
+void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,
+                  const TrtHost& op, bool rd_opp, bool wr_opp);
+// TS streaming sweep: A[i][s] = B[i][s - c_i] (bounce: B[opp i][s])
+void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L);
+// OS / OSNT pull: gather from a, collide, store local into b
+void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
+                    const TrtHost& op, bool streaming, bool two_s);
+// OS push: read local from a, collide, scatter into b
+void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
+                    const TrtHost& op);
+// AA-pattern odd sweep (the even sweep is launch_local(rd natural, wr opposed))
+void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op);
+// Esoteric twist sweep with the current handle table
+void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+               const EtBase& base);
+// SWAP link exchange: mode 0 all links, 1 only non-wrapped, 2 only wrapped
+void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode);
+// Compressed grid sweep (ticketed tiles); L carries the +3 padded storage
+void launch_cg(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+               bool even, unsigned long long* ticket, unsigned* flags, unsigned epoch);
+void launch_cg_fixup(cudaStream_t st, const DField& f, const long long* src,
+                     const long long* dst, const int8_t* dir, long long count, long long shift);
+
+// ---- indirect (IDX) addressing ---------------------------------------------
+struct Idx {
+  const uint32_t* adj;  // transposed [18][n]: adj[(i-1)*n + node]
+  const uint32_t* rem;  // ET: transposed [9][n] (bit 31 = j-link bounces)
+  uint32_t n;
+};
+void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uint32_t n,
+                      const TrtHost& op, bool rd_opp, bool wr_opp);
+void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I);
+void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
+                        const TrtHost& op, bool streaming, bool two_s);
+void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
+                        const TrtHost& op);
+void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op);
+void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
+                   const EtBase& base);
+void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I);
+
+// ---- canonical snapshot <-> scheme storage ---------------------------------
+enum ExMode : int {
+  kExNatural = 0,   // o[i] = F[i][s]
+  kExOpposed = 1,   // o[i] = F[opp i][s]
+  kExGather = 2,    // o[i] = F[i][s - c_i] (bounce F[opp i][s]): stream the stored post-collision state
+  kExAaOdd = 3,     // o[i] = F[opp i][s - c_i] (bounce F[i][s])
+  kExEt = 4,        // twisted handles
+};
+enum LdSource : int { kSrcBuffer = 0, kSrcRest = 1, kSrcTaylorGreen = 2, kSrcRandom = 3 };
+struct InitSpec {
+  int source = kSrcBuffer;
+  double rho0 = 1.0;
+  unsigned long long seed = 0;
+  double u0 = 0.01, drho = 1e-3, noise = 1e-4;
+  int gnx = 0, gny = 0, gnz = 0;  // global box for Taylor-Green phase
+  int z0 = 0;                     // global z of local plane 0 (slabs)
+};
+// nodes [n0, n0+count) of the canonical order; buf[(n-n0)*19 + i] (fp64)
+void launch_extract(cudaStream_t st, const DField& f, const dev::Lat& L,
+                    const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                    const EtBase& base, double* buf);
+void launch_load(cudaStream_t st, const DField& f, const dev::Lat& L,
+                 const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                 const double* buf, const InitSpec& init);
+void launch_extract_idx(cudaStream_t st, const DField& f, const Idx& I, uint32_t n0,
+                        uint32_t count, int mode, const EtBase& base, double* buf);
+void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::Lat& Lcells,
+                     const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
+                     const double* buf, const InitSpec& init);
+void launch_fill(cudaStream_t st, const DField& f, long long count, double v);
+
+// ---- geometry / IDX construction -------------------------------------------
+// exclusive scan of (mask != 0) over ncells -> node_of (~0u for solids),
+// cell_of_node; returns the fluid count (synchronises)
+uint64_t build_node_maps(cudaStream_t st, const uint8_t* mask, uint64_t ncells,
+                         uint32_t* node_of, uint32_t* cell_of_node, uint32_t* scratch,
+                         uint64_t scratch_elems);
+uint64_t scan_scratch_elems(uint64_t n);
+void launch_linkmask(cudaStream_t st, const uint8_t* mask, const dev::Lat& L, uint32_t* out);
+void launch_adjacency(cudaStream_t st, const uint8_t* mask, const dev::Lat& L,
+                      const uint32_t* node_of, const uint32_t* cell_of_node, uint32_t n,
+                      uint32_t* adjT);
+// ET remote table: returns max mailbox count (synchronises)
+uint32_t build_et_rem(cudaStream_t st, const uint32_t* adjT, uint32_t n, uint32_t* remT,
+                      uint32_t* scratch, uint64_t scratch_elems);
+void launch_transpose_u32(cudaStream_t st, const uint32_t* inT, uint32_t rows, uint32_t n,
+                          uint32_t* out_nodemajor);
+
+}  // namespace lbmgpu

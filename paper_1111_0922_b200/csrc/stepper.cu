@@ -1,0 +1,1361 @@
+// Host runtime of liblbmgpu.so: one C++ class per propagation scheme, each
+// owning its device storage, index tables and CUDA stream, plus the C ABI of
+// include/lbmgpu.h. Mirrors the reference's Stepper hierarchy
+// (p/include/lbmlab/stepper.hpp:70-106, p/src/scheme_*.cpp): same state
+// machine (time step, fresh/pending flags, ET handle table, layout phases),
+// with every sweep a sm_100a kernel launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lbmgpu.h"
+#include "launch.h"
+
+namespace lbmgpu {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+static void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw std::bad_alloc();
+  }
+  throw CudaError(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+static void ck_launch() { ck(cudaGetLastError(), "kernel launch"); }
+
+// ---------------------------------------------------------------------------
+// device memory
+// ---------------------------------------------------------------------------
+class DevMem {
+ public:
+  DevMem() = default;
+  explicit DevMem(size_t bytes) { alloc(bytes); }
+  ~DevMem() { release(); }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DevMem& operator=(DevMem&& o) noexcept {
+    release();
+    p_ = o.p_, n_ = o.n_;
+    o.p_ = nullptr, o.n_ = 0;
+    return *this;
+  }
+  void alloc(size_t bytes) {
+    release();
+    if (bytes == 0) bytes = 256;
+    CK(cudaMalloc(&p_, bytes));
+    n_ = bytes;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  template <class T = void>
+  T* get() const {
+    return static_cast<T*>(p_);
+  }
+  size_t bytes() const { return n_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// ---------------------------------------------------------------------------
+// host-side restatements used to set up kernels
+// ---------------------------------------------------------------------------
+static constexpr int kC[19][3] = {
+    {0, 0, 0},   {1, 0, 0},   {-1, 0, 0}, {0, 1, 0},   {0, -1, 0}, {0, 0, 1},  {0, 0, -1},
+    {-1, -1, 0}, {-1, 0, -1}, {-1, 0, 1}, {-1, 1, 0},  {0, -1, -1}, {0, -1, 1}, {0, 1, -1},
+    {0, 1, 1},   {1, -1, 0},  {1, 0, -1}, {1, 0, 1},   {1, 1, 0}};
+static constexpr int kPi[9] = {1, 3, 5, 7, 8, 9, 10, 11, 12};
+static constexpr int kPj[9] = {2, 4, 6, 18, 17, 16, 15, 14, 13};
+static double w_of(int i) { return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0); }
+
+// TrtOperator ctor/build (p/src/collision.cpp:50-93), including the
+// zero-collision identity operator (p/src/stepper_common.hpp:104-108).
+static TrtHost make_trt(const lbmgpu_flow& p, bool zero_collision) {
+  const double le = zero_collision ? 0.0 : p.lambda_even;
+  const double lo = zero_collision ? 0.0 : p.lambda_odd;
+  const double g[3] = {zero_collision ? 0.0 : p.body_force[0],
+                       zero_collision ? 0.0 : p.body_force[1],
+                       zero_collision ? 0.0 : p.body_force[2]};
+  TrtHost t{};
+  t.lambda_e = le;
+  t.le_half = 0.5 * le;
+  t.lo_half = 0.5 * lo;
+  t.w0 = w_of(0);
+  for (int q = 0; q < 9; ++q) {
+    const int i = kPi[q];
+    double cg = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int ck_ = kC[i][k];
+      if (ck_ == 0) continue;
+      cg += ck_ * g[k];
+    }
+    t.w2[q] = 2.0 * w_of(i);
+    t.f3w[q] = 3.0 * w_of(i) * cg;
+  }
+  return t;
+}
+
+struct HostGeo {
+  int nx = 0, ny = 0, nz = 0;
+  uint8_t policy[3] = {0, 0, 0};
+  std::vector<uint8_t> mask;  // empty = all fluid
+  bool solids = false;
+  uint64_t cells() const { return (uint64_t)nx * ny * nz; }
+  bool fluid(uint64_t c) const { return mask.empty() || mask[c]; }
+  uint64_t idx(int x, int y, int z) const {
+    return (uint64_t)x + (uint64_t)nx * ((uint64_t)y + (uint64_t)ny * z);
+  }
+  // resolve_link (p/src/geometry.cpp:49-60); returns false on bounce
+  bool link(int x, int y, int z, int i, int* t) const {
+    const int n[3] = {nx, ny, nz};
+    int p[3] = {x + kC[i][0], y + kC[i][1], z + kC[i][2]};
+    for (int k = 0; k < 3; ++k) {
+      if (p[k] >= 0 && p[k] < n[k]) continue;
+      if (policy[k] == 1) return false;
+      p[k] = p[k] < 0 ? p[k] + n[k] : p[k] - n[k];
+    }
+    if (!fluid(idx(p[0], p[1], p[2]))) return false;
+    t[0] = p[0], t[1] = p[1], t[2] = p[2];
+    return true;
+  }
+};
+
+static HostGeo copy_geo(const lbmgpu_geometry* g) {
+  if (!g) throw std::invalid_argument("null geometry");
+  if (g->nx < 1 || g->ny < 1 || g->nz < 1) throw std::invalid_argument("zero dimension");
+  for (int k = 0; k < 3; ++k)
+    if (g->axis_policy[k] > 1) throw std::invalid_argument("unknown axis policy");
+  HostGeo h;
+  h.nx = g->nx, h.ny = g->ny, h.nz = g->nz;
+  for (int k = 0; k < 3; ++k) h.policy[k] = g->axis_policy[k];
+  if (h.cells() >= (uint64_t{1} << 32))
+    throw std::runtime_error("grid exceeds 32-bit cell index range");
+  if (g->mask) {
+    h.mask.assign(g->mask, g->mask + h.cells());
+    for (auto& m : h.mask) m = m != 0;
+    h.solids = std::find(h.mask.begin(), h.mask.end(), 0) != h.mask.end();
+    if (!h.solids) h.mask.clear();
+  }
+  return h;
+}
+
+static dev::Lat make_lat(const HostGeo& g, const uint32_t* linkmask, int hx, int hy, int hz,
+                         int origin) {
+  dev::Lat L{};
+  L.nx = g.nx, L.ny = g.ny, L.nz = g.nz;
+  L.sx = g.nx + 2 * hx;
+  L.sy = g.ny + 2 * hy;
+  L.sxy = (long long)L.sx * L.sy;
+  L.ox = hx + origin, L.oy = hy + origin, L.oz = hz + origin;
+  L.ncells = (uint32_t)g.cells();
+  for (int k = 0; k < 3; ++k) L.wall[k] = g.policy[k];
+  L.zghost = 0;
+  L.linkmask = linkmask;
+  L.divx.init((uint32_t)g.nx);
+  L.divy.init((uint32_t)g.ny);
+  return L;
+}
+
+// kernel availability (p/src/stepper.cpp:140-153)
+static bool available(int s, int a, bool ext) {
+  if (s < 0 || s > 9 || a < 0 || a > 1) return false;
+  if (a == LBMGPU_DIRECT) return true;
+  switch (s) {
+    case LBMGPU_OS_PUSH:
+    case LBMGPU_OS_PULL:
+    case LBMGPU_OSNT_PULL_1S:
+    case LBMGPU_OSNT_PULL_2S:
+    case LBMGPU_AAP:
+    case LBMGPU_ET:
+      return true;
+    case LBMGPU_TS:
+    case LBMGPU_SWAP_PUSH:
+    case LBMGPU_SWAP_PULL:
+      return ext;
+    default:
+      return false;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stepper base: geometry on the device, node maps, canonical conversion
+// ---------------------------------------------------------------------------
+class Stepper {
+ public:
+  Stepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : geo_(g), opt_(o), op_(make_trt(p, o.zero_collision != 0)), rho0_(p.rho0) {
+    prec_ = o.precision == 4 ? Prec::f32 : Prec::f64;
+    aos_ = o.layout == LBMGPU_AOS;
+    CK(cudaSetDevice(o.device));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    setup_nodes();
+  }
+  virtual ~Stepper() {
+    if (stream_) {
+      cudaStreamSynchronize(stream_);
+      cudaStreamDestroy(stream_);
+    }
+  }
+
+  virtual void step_one() = 0;
+  virtual int launches_per_step() const { return 1; }
+  virtual void extract_range(uint32_t n0, uint32_t cnt, double* dbuf) = 0;
+  virtual void load_range(uint32_t n0, uint32_t cnt, const double* dbuf, const InitSpec& in) = 0;
+  virtual void after_load() { t_ = 0; }
+  virtual void before_extract() {}
+  virtual void after_extract() {}
+  virtual int layout_phase() const { return LBMGPU_NATURAL; }
+  virtual bool exchange_opposite_handles() { return false; }
+  virtual uint64_t pdf_bytes() const = 0;
+  virtual uint64_t idx_bytes() const { return 0; }
+
+  void step(long long n) {
+    CK(cudaSetDevice(opt_.device));
+    for (long long k = 0; k < n; ++k) {
+      if (nodes_ > 0) step_one();
+      ++t_;
+    }
+    ck_launch();
+  }
+
+  void sync() { CK(cudaStreamSynchronize(stream_)); }
+
+  // canonical snapshot <-> storage, in chunks through a device staging buffer
+  void extract(double* out, bool out_on_device) {
+    CK(cudaSetDevice(opt_.device));
+    before_extract();
+    for_chunks([&](uint32_t n0, uint32_t cnt) {
+      double* d = out_on_device ? out + (size_t)n0 * 19 : stage();
+      extract_range(n0, cnt, d);
+      ck_launch();
+      if (!out_on_device)
+        CK(cudaMemcpyAsync(out + (size_t)n0 * 19, d, (size_t)cnt * 19 * sizeof(double),
+                           cudaMemcpyDeviceToHost, stream_));
+      if (!out_on_device) sync();
+    });
+    after_extract();
+    sync();
+  }
+
+  void load(const double* in, bool in_on_device) {
+    CK(cudaSetDevice(opt_.device));
+    InitSpec spec;
+    spec.source = kSrcBuffer;
+    for_chunks([&](uint32_t n0, uint32_t cnt) {
+      const double* d = in + (size_t)n0 * 19;
+      if (!in_on_device) {
+        double* s = stage();
+        CK(cudaMemcpyAsync(s, d, (size_t)cnt * 19 * sizeof(double), cudaMemcpyHostToDevice,
+                           stream_));
+        d = s;
+      }
+      load_range(n0, cnt, d, spec);
+      ck_launch();
+      if (!in_on_device) sync();
+    });
+    after_load();
+    sync();
+  }
+
+  void init(const InitSpec& spec) {
+    CK(cudaSetDevice(opt_.device));
+    for_chunks([&](uint32_t n0, uint32_t cnt) {
+      load_range(n0, cnt, nullptr, spec);
+      ck_launch();
+    });
+    after_load();
+    sync();
+  }
+
+  InitSpec base_init(int source) const {
+    InitSpec s;
+    s.source = source;
+    s.rho0 = rho0_;
+    s.gnx = geo_.nx, s.gny = geo_.ny, s.gnz = geo_.nz;
+    s.z0 = 0;
+    return s;
+  }
+
+  long long t_ = 0;
+  uint64_t nodes_ = 0;
+  cudaStream_t stream_ = nullptr;
+  lbmgpu_options opt_;
+
+ protected:
+  DField field(DevMem& m, long long stride) const {
+    DField f;
+    f.p = m.get();
+    f.stride = stride;
+    f.aos = aos_;
+    f.prec = prec_;
+    return f;
+  }
+  size_t esize() const { return prec_ == Prec::f64 ? 8 : 4; }
+  long long soa_stride(uint64_t storage) const {
+    return (long long)((storage + 31) & ~uint64_t{31});
+  }
+  uint64_t field_elems(uint64_t storage) const {
+    return aos_ ? storage * 19 + 32 : (uint64_t)soa_stride(storage) * 19;
+  }
+  void alloc_field(DevMem& m, uint64_t storage) {
+    m.alloc(field_elems(storage) * esize());
+    CK(cudaMemsetAsync(m.get(), 0, m.bytes(), stream_));
+  }
+
+  double* stage() {
+    if (!stage_.get()) stage_.alloc((size_t)chunk_nodes() * 19 * sizeof(double));
+    return stage_.get<double>();
+  }
+  uint32_t chunk_nodes() const {
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nodes_, uint64_t{1} << 20));
+  }
+  template <class F>
+  void for_chunks(F&& f) {
+    const uint32_t ch = chunk_nodes();
+    for (uint64_t n0 = 0; n0 < nodes_; n0 += ch)
+      f((uint32_t)n0, (uint32_t)std::min<uint64_t>(ch, nodes_ - n0));
+  }
+
+  // fluid enumeration x-fastest (build_sparse, p/src/geometry.cpp:187-194)
+  void setup_nodes() {
+    const uint64_t cells = geo_.cells();
+    if (!geo_.solids) {
+      nodes_ = cells;
+      return;
+    }
+    mask_d_.alloc(cells);
+    CK(cudaMemcpyAsync(mask_d_.get(), geo_.mask.data(), cells, cudaMemcpyHostToDevice, stream_));
+    cell_of_node_.alloc(cells * sizeof(uint32_t));
+    node_of_.alloc(cells * sizeof(uint32_t));
+    DevMem scratch(scan_scratch_elems(cells) * sizeof(uint32_t));
+    nodes_ = build_node_maps(stream_, mask_d_.get<uint8_t>(), cells, node_of_.get<uint32_t>(),
+                             cell_of_node_.get<uint32_t>(), scratch.get<uint32_t>(), 0);
+    ck_launch();
+  }
+  void setup_linkmask() {
+    if (!geo_.solids) return;
+    linkmask_.alloc(geo_.cells() * sizeof(uint32_t));
+    const dev::Lat L = make_lat(geo_, nullptr, 0, 0, 0, 0);
+    launch_linkmask(stream_, mask_d_.get<uint8_t>(), L, linkmask_.get<uint32_t>());
+    ck_launch();
+  }
+  const uint32_t* linkmask() const { return geo_.solids ? linkmask_.get<uint32_t>() : nullptr; }
+  const uint32_t* cell_of_node() const {
+    return geo_.solids ? cell_of_node_.get<uint32_t>() : nullptr;
+  }
+
+  HostGeo geo_;
+  TrtHost op_;
+  double rho0_;
+  Prec prec_ = Prec::f64;
+  bool aos_ = false;
+  DevMem mask_d_, cell_of_node_, node_of_, linkmask_, stage_;
+};
+
+// ---------------------------------------------------------------------------
+// direct schemes
+// ---------------------------------------------------------------------------
+class DirectStepper : public Stepper {
+ public:
+  DirectStepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : Stepper(g, p, o) {
+    setup_linkmask();
+    L_ = make_lat(geo_, linkmask(), 0, 0, 0, 0);
+  }
+
+ protected:
+  void ex(const DField& f, const dev::Lat& L, int mode, uint32_t n0, uint32_t cnt, double* d,
+          const EtBase& b = EtBase{}) {
+    launch_extract(stream_, f, L, cell_of_node(), n0, cnt, mode, b, d);
+  }
+  void ld(const DField& f, const dev::Lat& L, int mode, uint32_t n0, uint32_t cnt,
+          const double* d, const InitSpec& in) {
+    launch_load(stream_, f, L, cell_of_node(), n0, cnt, mode, d, in);
+  }
+  dev::Lat L_;
+};
+
+// TS: collide A -> B, stream B -> A (p/src/scheme_ts.cpp)
+class TsDirect final : public DirectStepper {
+ public:
+  TsDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o) : DirectStepper(g, p, o) {
+    alloc_field(a_, g.cells());
+    alloc_field(b_, g.cells());
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const long long s = soa_stride(geo_.cells());
+    launch_local(stream_, field(a_, s), field(b_, s), L_, op_, false, false);
+    launch_ts_stream(stream_, field(a_, s), field(b_, s), L_);
+  }
+  int launches_per_step() const override { return 2; }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(a_, soa_stride(geo_.cells())), L_, kExNatural, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(a_, soa_stride(geo_.cells())), L_, kExNatural, n0, c, d, in);
+  }
+  uint64_t pdf_bytes() const override { return a_.bytes() + b_.bytes(); }
+
+ private:
+  DevMem a_, b_;
+};
+
+// OS push/pull and OSNT pull (p/src/scheme_os.cpp, p/src/scheme_osnt.cpp)
+class OsDirect final : public DirectStepper {
+ public:
+  OsDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : DirectStepper(g, p, o) {
+    const int s = o.scheme;
+    pull_ = s != LBMGPU_OS_PUSH;
+    nt_ = (s == LBMGPU_OSNT_PULL_1S || s == LBMGPU_OSNT_PULL_2S) && o.streaming_stores;
+    two_s_ = s == LBMGPU_OSNT_PULL_2S;
+    alloc_field(g_[0], g.cells());
+    alloc_field(g_[1], g.cells());
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const long long s = soa_stride(geo_.cells());
+    DField a = field(g_[active_], s), b = field(g_[active_ ^ 1], s);
+    if (pull_ && fresh_) {
+      launch_local(stream_, a, a, L_, op_, false, false);
+      fresh_ = false;
+    }
+    if (pull_)
+      launch_os_pull(stream_, a, b, L_, op_, nt_, two_s_);
+    else
+      launch_os_push(stream_, a, b, L_, op_);
+    active_ ^= 1;
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    const long long s = soa_stride(geo_.cells());
+    if (!pull_ || fresh_)
+      ex(field(g_[active_], s), L_, kExNatural, n0, c, d);
+    else
+      ex(field(g_[active_ ^ 1], s), L_, kExGather, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(g_[active_], soa_stride(geo_.cells())), L_, kExNatural, n0, c, d, in);
+  }
+  void after_load() override {
+    t_ = 0;
+    fresh_ = pull_;
+  }
+  uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
+
+ private:
+  bool pull_, nt_, two_s_;
+  bool fresh_ = false;
+  int active_ = 0;
+  DevMem g_[2];
+};
+
+// AA pattern (p/src/scheme_aap.cpp)
+class AaDirect final : public DirectStepper {
+ public:
+  AaDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : DirectStepper(g, p, o) {
+    alloc_field(f_, g.cells());
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(geo_.cells()));
+    if ((t_ & 1) == 0)
+      launch_local(stream_, f, f, L_, op_, false, true);
+    else
+      launch_aa_odd(stream_, f, L_, op_);
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(f_, soa_stride(geo_.cells())), L_, (t_ & 1) ? kExAaOdd : kExNatural, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(f_, soa_stride(geo_.cells())), L_, kExNatural, n0, c, d, in);
+  }
+  int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+ private:
+  DevMem f_;
+};
+
+// ET (p/src/scheme_et.cpp): extended grid with a halo plane on wall axes
+class EtDirect final : public DirectStepper {
+ public:
+  EtDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : DirectStepper(g, p, o) {
+    for (int k = 0; k < 3; ++k) halo_[k] = g.policy[k] == 1 ? 1 : 0;
+    Le_ = make_lat(geo_, linkmask(), halo_[0], halo_[1], halo_[2], 0);
+    ext_ = (uint64_t)(g.nx + 2 * halo_[0]) * (g.ny + 2 * halo_[1]) * (g.nz + 2 * halo_[2]);
+    alloc_field(f_, ext_);
+    reset_base();
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    launch_et(stream_, field(f_, soa_stride(ext_)), Le_, op_, base_);
+    swap_base();
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(f_, soa_stride(ext_)), Le_, kExEt, n0, c, d, base_);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    reset_base();
+    ld(field(f_, soa_stride(ext_)), Le_, kExEt, n0, c, d, in);
+  }
+  bool exchange_opposite_handles() override {
+    swap_base();
+    return true;
+  }
+  int layout_phase() const override {
+    for (int i = 0; i < 19; ++i)
+      if (base_.b[i] != i) return LBMGPU_TWISTED;
+    return LBMGPU_NATURAL;
+  }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+ private:
+  void reset_base() {
+    for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
+  }
+  void swap_base() {
+    for (int q = 0; q < 9; ++q) std::swap(base_.b[kPi[q]], base_.b[kPj[q]]);
+  }
+  int halo_[3];
+  uint64_t ext_ = 0;
+  dev::Lat Le_;
+  EtBase base_;
+  DevMem f_;
+};
+
+// periodic-seam links (targets wrapped by resolve_link), from fluid cells
+// along `dirs` (CG: all 18, p/src/scheme_cg.cpp:31-41; SWAP: back half,
+// p/src/scheme_swap.cpp:48-65)
+struct SeamLink {
+  int x, y, z, tx, ty, tz, lx, ly, lz, dir;
+};
+static std::vector<SeamLink> seam_links(const HostGeo& g, const int* dirs, int ndirs) {
+  std::vector<SeamLink> out;
+  for (int z = 0; z < g.nz; ++z)
+    for (int y = 0; y < g.ny; ++y)
+      for (int x = 0; x < g.nx; ++x) {
+        if (x > 0 && x < g.nx - 1 && y > 0 && y < g.ny - 1 && z > 0 && z < g.nz - 1) continue;
+        if (!g.fluid(g.idx(x, y, z))) continue;
+        for (int k = 0; k < ndirs; ++k) {
+          const int i = dirs[k];
+          int t[3];
+          if (!g.link(x, y, z, i, t)) continue;
+          const int tx = x + kC[i][0], ty = y + kC[i][1], tz = z + kC[i][2];
+          if (tx == t[0] && ty == t[1] && tz == t[2]) continue;
+          out.push_back({x, y, z, tx, ty, tz, t[0], t[1], t[2], i});
+        }
+      }
+  return out;
+}
+
+// CG (p/src/scheme_cg.cpp): one grid padded by 3 per axis; sweeps alternate
+// read origin +1 / +2 (shift1 = 1 + px + px*py)
+class CgDirect final : public DirectStepper {
+ public:
+  CgDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : DirectStepper(g, p, o) {
+    px_ = g.nx + 3, py_ = g.ny + 3, pz_ = g.nz + 3;
+    padded_ = (uint64_t)px_ * py_ * pz_;
+    if (padded_ >= (uint64_t{1} << 32)) throw std::runtime_error("grid exceeds 32-bit cell index range");
+    L1_ = make_lat(geo_, linkmask(), 0, 0, 0, 0);
+    L1_.sx = px_, L1_.sy = py_, L1_.sxy = (long long)px_ * py_;
+    L2_ = L1_;
+    L1_.ox = L1_.oy = L1_.oz = 1;
+    L2_.ox = L2_.oy = L2_.oz = 2;
+    shift1_ = 1 + (long long)px_ + (long long)px_ * py_;
+    alloc_field(f_, padded_);
+    static const int all[18] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18};
+    const auto links = seam_links(geo_, all, 18);
+    nfix_ = (long long)links.size();
+    if (nfix_) {
+      std::vector<long long> src(nfix_), dst(nfix_);
+      std::vector<int8_t> dir(nfix_);
+      for (long long k = 0; k < nfix_; ++k) {
+        const SeamLink& s = links[k];
+        src[k] = pidx(s.tx + 2, s.ty + 2, s.tz + 2);
+        dst[k] = pidx(s.lx + 2, s.ly + 2, s.lz + 2);
+        dir[k] = (int8_t)s.dir;
+      }
+      fsrc_.alloc(nfix_ * 8), fdst_.alloc(nfix_ * 8), fdir_.alloc(nfix_);
+      CK(cudaMemcpyAsync(fsrc_.get(), src.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
+      CK(cudaMemcpyAsync(fdst_.get(), dst.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
+      CK(cudaMemcpyAsync(fdir_.get(), dir.data(), nfix_, cudaMemcpyHostToDevice, stream_));
+    }
+    const uint64_t ntiles = (geo_.cells() + kBlock - 1) / kBlock;
+    flags_.alloc(ntiles * sizeof(unsigned));
+    ticket_.alloc(sizeof(unsigned long long));
+    CK(cudaMemsetAsync(flags_.get(), 0, flags_.bytes(), stream_));
+    CK(cudaMemsetAsync(ticket_.get(), 0, ticket_.bytes(), stream_));
+    init(base_init(kSrcRest));
+    sync();
+  }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(padded_));
+    const bool even = (t_ & 1) == 0;
+    ++epoch_;
+    launch_cg(stream_, f, even ? L1_ : L2_, op_, even, ticket_.get<unsigned long long>(),
+              flags_.get<unsigned>(), epoch_);
+    launch_cg_fixup(stream_, f, fsrc_.get<long long>(), fdst_.get<long long>(),
+                    fdir_.get<int8_t>(), nfix_, even ? 0 : shift1_);
+  }
+  int launches_per_step() const override { return nfix_ ? 2 : 1; }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(f_, soa_stride(padded_)), (t_ & 1) ? L2_ : L1_, kExNatural, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(f_, soa_stride(padded_)), L1_, kExNatural, n0, c, d, in);
+  }
+  int layout_phase() const override {
+    return (t_ & 1) ? LBMGPU_SHIFTED_EVEN : LBMGPU_SHIFTED_ODD;
+  }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  uint64_t idx_bytes() const override { return flags_.bytes(); }
+
+ private:
+  long long pidx(int x, int y, int z) const {
+    return ((long long)z * py_ + y) * px_ + x;
+  }
+  int px_, py_, pz_;
+  uint64_t padded_;
+  long long shift1_;
+  long long nfix_ = 0;
+  unsigned epoch_ = 0;
+  dev::Lat L1_, L2_;
+  DevMem f_, fsrc_, fdst_, fdir_, flags_, ticket_;
+};
+
+// SWAP push/pull (p/src/scheme_swap.cpp): collide + link exchange
+class SwapDirect final : public DirectStepper {
+ public:
+  SwapDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : DirectStepper(g, p, o) {
+    pull_ = o.scheme == LBMGPU_SWAP_PULL;
+    defer_ = o.swap_deferred_fixup != 0;
+    static const int back[9] = {2, 4, 6, 7, 8, 11, 13, 15, 16};
+    has_wrapped_ = !seam_links(geo_, back, 9).empty();
+    alloc_field(f_, g.cells());
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(geo_.cells()));
+    if (pull_) {
+      if (fresh_) {
+        launch_local(stream_, f, f, L_, op_, false, false);
+        fresh_ = false;
+      } else {
+        launch_swap(stream_, f, L_, 0);
+        launch_local(stream_, f, f, L_, op_, true, false);
+      }
+    } else {
+      if (pending_) {
+        launch_swap(stream_, f, L_, 2);
+        pending_ = false;
+      }
+      launch_local(stream_, f, f, L_, op_, true, false);
+      launch_swap(stream_, f, L_, defer_ ? 1 : 0);
+      pending_ = defer_ && has_wrapped_;
+    }
+  }
+  int launches_per_step() const override { return 2; }
+  void before_extract() override {
+    if (!pull_ && pending_) launch_swap(stream_, field(f_, soa_stride(geo_.cells())), L_, 2);
+  }
+  void after_extract() override {
+    if (!pull_ && pending_) launch_swap(stream_, field(f_, soa_stride(geo_.cells())), L_, 2);
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    const DField f = field(f_, soa_stride(geo_.cells()));
+    if (pull_)
+      ex(f, L_, fresh_ ? kExNatural : kExGather, n0, c, d);
+    else
+      ex(f, L_, kExOpposed, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(f_, soa_stride(geo_.cells())), L_, pull_ ? kExNatural : kExOpposed, n0, c, d, in);
+  }
+  void after_load() override {
+    t_ = 0;
+    fresh_ = pull_;
+    pending_ = false;
+  }
+  int layout_phase() const override {
+    if (pull_) return LBMGPU_NATURAL;
+    return pending_ ? LBMGPU_SWAP_PARTIAL : LBMGPU_OPPOSED;
+  }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+ private:
+  bool pull_, defer_, has_wrapped_;
+  bool fresh_ = false, pending_ = false;
+  DevMem f_;
+};
+
+// ---------------------------------------------------------------------------
+// indirect schemes: IDX built on the device (build_sparse restated)
+// ---------------------------------------------------------------------------
+class IndirectStepper : public Stepper {
+ public:
+  IndirectStepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : Stepper(g, p, o) {
+    if (nodes_ >= (uint64_t{1} << 31))
+      throw std::runtime_error("fluid count exceeds 32-bit index range");
+    adj_.alloc((size_t)nodes_ * 18 * sizeof(uint32_t));
+    const dev::Lat L = make_lat(geo_, nullptr, 0, 0, 0, 0);
+    Lcells_ = L;
+    launch_adjacency(stream_, geo_.solids ? mask_d_.get<uint8_t>() : nullptr, L,
+                     geo_.solids ? node_of_.get<uint32_t>() : nullptr, cell_of_node(),
+                     (uint32_t)nodes_, adj_.get<uint32_t>());
+    ck_launch();
+    I_.adj = adj_.get<uint32_t>();
+    I_.rem = nullptr;
+    I_.n = (uint32_t)nodes_;
+  }
+
+ protected:
+  void ex(const DField& f, int mode, uint32_t n0, uint32_t cnt, double* d,
+          const EtBase& b = EtBase{}) {
+    launch_extract_idx(stream_, f, I_, n0, cnt, mode, b, d);
+  }
+  void ld(const DField& f, int mode, uint32_t n0, uint32_t cnt, const double* d,
+          const InitSpec& in) {
+    launch_load_idx(stream_, f, I_, Lcells_, cell_of_node(), n0, cnt, mode, d, in);
+  }
+  uint64_t idx_bytes() const override { return adj_.bytes(); }
+  DevMem adj_;
+  Idx I_;
+  dev::Lat Lcells_;
+};
+
+class TsIndirect final : public IndirectStepper {
+ public:
+  TsIndirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : IndirectStepper(g, p, o) {
+    alloc_field(a_, nodes_);
+    alloc_field(b_, nodes_);
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const long long s = soa_stride(nodes_);
+    launch_local_idx(stream_, field(a_, s), field(b_, s), I_.n, op_, false, false);
+    launch_ts_stream_idx(stream_, field(a_, s), field(b_, s), I_);
+  }
+  int launches_per_step() const override { return 2; }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(a_, soa_stride(nodes_)), kExNatural, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(a_, soa_stride(nodes_)), kExNatural, n0, c, d, in);
+  }
+  uint64_t pdf_bytes() const override { return a_.bytes() + b_.bytes(); }
+
+ private:
+  DevMem a_, b_;
+};
+
+class OsIndirect final : public IndirectStepper {
+ public:
+  OsIndirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : IndirectStepper(g, p, o) {
+    const int s = o.scheme;
+    pull_ = s != LBMGPU_OS_PUSH;
+    nt_ = (s == LBMGPU_OSNT_PULL_1S || s == LBMGPU_OSNT_PULL_2S) && o.streaming_stores;
+    two_s_ = s == LBMGPU_OSNT_PULL_2S;
+    alloc_field(g_[0], nodes_);
+    alloc_field(g_[1], nodes_);
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const long long s = soa_stride(nodes_);
+    DField a = field(g_[active_], s), b = field(g_[active_ ^ 1], s);
+    if (pull_ && fresh_) {
+      launch_local_idx(stream_, a, a, I_.n, op_, false, false);
+      fresh_ = false;
+    }
+    if (pull_)
+      launch_os_pull_idx(stream_, a, b, I_, op_, nt_, two_s_);
+    else
+      launch_os_push_idx(stream_, a, b, I_, op_);
+    active_ ^= 1;
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    const long long s = soa_stride(nodes_);
+    if (!pull_ || fresh_)
+      ex(field(g_[active_], s), kExNatural, n0, c, d);
+    else
+      ex(field(g_[active_ ^ 1], s), kExGather, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(g_[active_], soa_stride(nodes_)), kExNatural, n0, c, d, in);
+  }
+  void after_load() override {
+    t_ = 0;
+    fresh_ = pull_;
+  }
+  uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
+
+ private:
+  bool pull_, nt_, two_s_;
+  bool fresh_ = false;
+  int active_ = 0;
+  DevMem g_[2];
+};
+
+class AaIndirect final : public IndirectStepper {
+ public:
+  AaIndirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : IndirectStepper(g, p, o) {
+    alloc_field(f_, nodes_);
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(nodes_));
+    if ((t_ & 1) == 0)
+      launch_local_idx(stream_, f, f, I_.n, op_, false, true);
+    else
+      launch_aa_odd_idx(stream_, f, I_, op_);
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(f_, soa_stride(nodes_)), (t_ & 1) ? kExAaOdd : kExNatural, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(f_, soa_stride(nodes_)), kExNatural, n0, c, d, in);
+  }
+  int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+ private:
+  DevMem f_;
+};
+
+class EtIndirect final : public IndirectStepper {
+ public:
+  EtIndirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : IndirectStepper(g, p, o) {
+    rem_.alloc((size_t)nodes_ * 9 * sizeof(uint32_t));
+    {
+      DevMem scratch(scan_scratch_elems(nodes_) * sizeof(uint32_t));
+      nmail_ = build_et_rem(stream_, adj_.get<uint32_t>(), (uint32_t)nodes_, rem_.get<uint32_t>(),
+                            scratch.get<uint32_t>(), 0);
+    }
+    I_.rem = rem_.get<uint32_t>();
+    storage_ = nodes_ + nmail_;
+    alloc_field(f_, storage_);
+    reset_base();
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    launch_et_idx(stream_, field(f_, soa_stride(storage_)), I_, op_, base_);
+    swap_base();
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    ex(field(f_, soa_stride(storage_)), kExEt, n0, c, d, base_);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    reset_base();
+    ld(field(f_, soa_stride(storage_)), kExEt, n0, c, d, in);
+  }
+  bool exchange_opposite_handles() override {
+    swap_base();
+    return true;
+  }
+  int layout_phase() const override {
+    for (int i = 0; i < 19; ++i)
+      if (base_.b[i] != i) return LBMGPU_TWISTED;
+    return LBMGPU_NATURAL;
+  }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  uint64_t idx_bytes() const override { return adj_.bytes() + rem_.bytes(); }
+
+ private:
+  void reset_base() {
+    for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
+  }
+  void swap_base() {
+    for (int q = 0; q < 9; ++q) std::swap(base_.b[kPi[q]], base_.b[kPj[q]]);
+  }
+  uint32_t nmail_ = 0;
+  uint64_t storage_ = 0;
+  EtBase base_;
+  DevMem rem_, f_;
+};
+
+class SwapIndirect final : public IndirectStepper {
+ public:
+  SwapIndirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : IndirectStepper(g, p, o) {
+    pull_ = o.scheme == LBMGPU_SWAP_PULL;
+    alloc_field(f_, nodes_);
+    init(base_init(kSrcRest));
+  }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(nodes_));
+    if (pull_) {
+      if (fresh_) {
+        launch_local_idx(stream_, f, f, I_.n, op_, false, false);
+        fresh_ = false;
+      } else {
+        launch_swap_idx(stream_, f, I_);
+        launch_local_idx(stream_, f, f, I_.n, op_, true, false);
+      }
+    } else {
+      launch_local_idx(stream_, f, f, I_.n, op_, true, false);
+      launch_swap_idx(stream_, f, I_);
+    }
+  }
+  int launches_per_step() const override { return 2; }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    const DField f = field(f_, soa_stride(nodes_));
+    if (pull_)
+      ex(f, fresh_ ? kExNatural : kExGather, n0, c, d);
+    else
+      ex(f, kExOpposed, n0, c, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    ld(field(f_, soa_stride(nodes_)), pull_ ? kExNatural : kExOpposed, n0, c, d, in);
+  }
+  void after_load() override {
+    t_ = 0;
+    fresh_ = pull_;
+  }
+  int layout_phase() const override { return pull_ ? LBMGPU_NATURAL : LBMGPU_OPPOSED; }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+ private:
+  bool pull_;
+  bool fresh_ = false;
+  DevMem f_;
+};
+
+// create_stepper (p/src/stepper.cpp:155-180)
+static std::unique_ptr<Stepper> create(const lbmgpu_geometry* gg, const lbmgpu_flow* p,
+                                       const lbmgpu_options* o) {
+  if (!p || !o) throw std::invalid_argument("null argument");
+  if (!available(o->scheme, o->addressing, o->extensions != 0))
+    throw std::invalid_argument("kernel not implemented; traffic model only");
+  if (o->workers < 0) throw std::invalid_argument("workers must be >= 0");
+  if (o->chunk_length < 1) throw std::invalid_argument("chunk_length must be >= 1");
+  if (o->precision != 8 && o->precision != 4)
+    throw std::invalid_argument("precision must be 8 (fp64) or 4 (fp32)");
+  if (o->layout != LBMGPU_SOA && o->layout != LBMGPU_AOS)
+    throw std::invalid_argument("unknown layout");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (o->device < 0 || o->device >= ndev) throw std::invalid_argument("no such CUDA device");
+  if (o->z_end != 0 || o->z_begin != 0)
+    throw std::invalid_argument("z-slab decomposition requires lbmgpu_create_slab");
+  const HostGeo g = copy_geo(gg);
+  if (o->addressing == LBMGPU_DIRECT) {
+    switch (o->scheme) {
+      case LBMGPU_TS: return std::make_unique<TsDirect>(g, *p, *o);
+      case LBMGPU_OS_PUSH:
+      case LBMGPU_OS_PULL:
+      case LBMGPU_OSNT_PULL_1S:
+      case LBMGPU_OSNT_PULL_2S: return std::make_unique<OsDirect>(g, *p, *o);
+      case LBMGPU_CG: return std::make_unique<CgDirect>(g, *p, *o);
+      case LBMGPU_SWAP_PUSH:
+      case LBMGPU_SWAP_PULL: return std::make_unique<SwapDirect>(g, *p, *o);
+      case LBMGPU_AAP: return std::make_unique<AaDirect>(g, *p, *o);
+      case LBMGPU_ET: return std::make_unique<EtDirect>(g, *p, *o);
+    }
+  } else {
+    switch (o->scheme) {
+      case LBMGPU_TS: return std::make_unique<TsIndirect>(g, *p, *o);
+      case LBMGPU_OS_PUSH:
+      case LBMGPU_OS_PULL:
+      case LBMGPU_OSNT_PULL_1S:
+      case LBMGPU_OSNT_PULL_2S: return std::make_unique<OsIndirect>(g, *p, *o);
+      case LBMGPU_SWAP_PUSH:
+      case LBMGPU_SWAP_PULL: return std::make_unique<SwapIndirect>(g, *p, *o);
+      case LBMGPU_AAP: return std::make_unique<AaIndirect>(g, *p, *o);
+      case LBMGPU_ET: return std::make_unique<EtIndirect>(g, *p, *o);
+    }
+  }
+  throw std::invalid_argument("unknown scheme");
+}
+
+// ---------------------------------------------------------------------------
+// standalone IDX construction (build_sparse on the device)
+// ---------------------------------------------------------------------------
+struct IdxBuild {
+  uint32_t n = 0;
+  DevMem adj, node_of, rem;
+  uint32_t nmail = 0;
+};
+
+static void build_idx(const lbmgpu_geometry* gg, int device, bool want_node_of, bool want_rem,
+                      IdxBuild& out, cudaStream_t st) {
+  const HostGeo g = copy_geo(gg);
+  CK(cudaSetDevice(device));
+  const uint64_t cells = g.cells();
+  DevMem mask, cofn;
+  uint64_t n = cells;
+  if (g.solids || want_node_of) {
+    mask.alloc(cells);
+    if (g.solids)
+      CK(cudaMemcpyAsync(mask.get(), g.mask.data(), cells, cudaMemcpyHostToDevice, st));
+    else
+      CK(cudaMemsetAsync(mask.get(), 1, cells, st));
+    out.node_of.alloc(cells * 4);
+    cofn.alloc(cells * 4);
+    DevMem scratch(scan_scratch_elems(cells) * sizeof(uint32_t));
+    n = build_node_maps(st, mask.get<uint8_t>(), cells, out.node_of.get<uint32_t>(),
+                        cofn.get<uint32_t>(), scratch.get<uint32_t>(), 0);
+    ck_launch();
+  }
+  // guard of build_sparse (p/src/geometry.cpp:177-179)
+  if (n >= (uint64_t{1} << 31)) throw std::runtime_error("fluid count exceeds 32-bit index range");
+  out.n = (uint32_t)n;
+  out.adj.alloc(n * 18 * 4);
+  launch_adjacency(st, g.solids ? mask.get<uint8_t>() : nullptr, make_lat(g, nullptr, 0, 0, 0, 0),
+                   g.solids ? out.node_of.get<uint32_t>() : nullptr,
+                   g.solids ? cofn.get<uint32_t>() : nullptr, out.n, out.adj.get<uint32_t>());
+  ck_launch();
+  if (want_rem) {
+    out.rem.alloc(n * 9 * 4);
+    DevMem scratch(scan_scratch_elems(n) * sizeof(uint32_t));
+    out.nmail = build_et_rem(st, out.adj.get<uint32_t>(), out.n, out.rem.get<uint32_t>(),
+                             scratch.get<uint32_t>(), 0);
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace lbmgpu
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace lbmgpu;
+
+struct lbmgpu_stepper {
+  std::unique_ptr<Stepper> s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return LBMGPU_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return LBMGPU_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return LBMGPU_DOMAIN_ERROR;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return LBMGPU_BAD_ALLOC;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return LBMGPU_CUDA_ERROR;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return LBMGPU_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LBMGPU_RUNTIME_ERROR;
+  }
+}
+
+Stepper& S(lbmgpu_stepper* h) {
+  if (!h || !h->s) throw std::invalid_argument("null stepper");
+  return *h->s;
+}
+}  // namespace
+
+extern "C" {
+
+void lbmgpu_default_options(lbmgpu_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->scheme = LBMGPU_AAP;
+  o->addressing = LBMGPU_DIRECT;
+  o->layout = LBMGPU_SOA;
+  o->precision = 8;
+  o->device = 0;
+  o->workers = 1;
+  o->chunk_length = 150;
+  o->streaming_stores = 1;
+}
+
+int lbmgpu_create(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgpu_options* o,
+                  lbmgpu_stepper** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output handle");
+    auto h = std::make_unique<lbmgpu_stepper>();
+    h->s = create(g, p, o);
+    *out = h.release();
+  });
+}
+
+int lbmgpu_destroy(lbmgpu_stepper* h) {
+  return guard([&] {
+    if (h) {
+      if (h->s) cudaSetDevice(h->s->opt_.device);
+      delete h;
+    }
+  });
+}
+
+int lbmgpu_step(lbmgpu_stepper* h, int64_t n) {
+  return guard([&] {
+    if (n < 0) throw std::invalid_argument("steps must be >= 0");
+    S(h).step(n);
+  });
+}
+
+int lbmgpu_synchronize(lbmgpu_stepper* h) { return guard([&] { S(h).sync(); }); }
+
+int lbmgpu_step_timed(lbmgpu_stepper* h, int64_t n, double* ms) {
+  return guard([&] {
+    if (n < 0) throw std::invalid_argument("steps must be >= 0");
+    Stepper& s = S(h);
+    CK(cudaSetDevice(s.opt_.device));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    struct EvGuard {
+      cudaEvent_t a, b;
+      ~EvGuard() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } eg{e0, e1};
+    s.sync();
+    CK(cudaEventRecord(e0, s.stream_));
+    s.step(n);
+    CK(cudaEventRecord(e1, s.stream_));
+    CK(cudaEventSynchronize(e1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, e0, e1));
+    *ms = (double)f;
+  });
+}
+
+int lbmgpu_extract_natural(lbmgpu_stepper* h, double* out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output buffer");
+    S(h).extract(out, false);
+  });
+}
+int lbmgpu_load_natural(lbmgpu_stepper* h, const double* in) {
+  return guard([&] {
+    if (!in) throw std::invalid_argument("null input buffer");
+    S(h).load(in, false);
+  });
+}
+int lbmgpu_extract_natural_device(lbmgpu_stepper* h, double* out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output buffer");
+    S(h).extract(out, true);
+  });
+}
+int lbmgpu_load_natural_device(lbmgpu_stepper* h, const double* in) {
+  return guard([&] {
+    if (!in) throw std::invalid_argument("null input buffer");
+    S(h).load(in, true);
+  });
+}
+
+int lbmgpu_init_field(lbmgpu_stepper* h, int32_t kind, uint64_t seed, double u0, double drho,
+                      double noise) {
+  return guard([&] {
+    Stepper& s = S(h);
+    InitSpec in;
+    switch (kind) {
+      case 0: in = s.base_init(kSrcRest); break;
+      case 1: in = s.base_init(kSrcTaylorGreen); break;
+      case 2: in = s.base_init(kSrcRandom); break;
+      default: throw std::invalid_argument("unknown init kind");
+    }
+    in.seed = seed, in.u0 = u0, in.drho = drho, in.noise = noise;
+    s.init(in);
+  });
+}
+
+int lbmgpu_layout_phase(lbmgpu_stepper* h, int32_t* phase) {
+  return guard([&] { *phase = S(h).layout_phase(); });
+}
+int lbmgpu_exchange_opposite_handles(lbmgpu_stepper* h, int32_t* had) {
+  return guard([&] { *had = S(h).exchange_opposite_handles() ? 1 : 0; });
+}
+int lbmgpu_time_step(lbmgpu_stepper* h, int64_t* t) {
+  return guard([&] { *t = S(h).t_; });
+}
+int lbmgpu_node_count(lbmgpu_stepper* h, uint64_t* n) {
+  return guard([&] { *n = S(h).nodes_; });
+}
+int lbmgpu_storage_bytes(lbmgpu_stepper* h, uint64_t* pdf, uint64_t* idx) {
+  return guard([&] {
+    *pdf = S(h).pdf_bytes();
+    *idx = S(h).idx_bytes();
+  });
+}
+int lbmgpu_stream(lbmgpu_stepper* h, void** st) {
+  return guard([&] { *st = (void*)S(h).stream_; });
+}
+int lbmgpu_launches_per_step(lbmgpu_stepper* h, int32_t* n) {
+  return guard([&] { *n = S(h).launches_per_step(); });
+}
+
+int lbmgpu_kernel_available(int32_t s, int32_t a) { return available(s, a, false) ? 1 : 0; }
+int lbmgpu_kernel_available_ext(int32_t s, int32_t a) { return available(s, a, true) ? 1 : 0; }
+
+int lbmgpu_build_sparse(const lbmgpu_geometry* g, int32_t device, uint32_t* fluid_count,
+                        uint32_t* adjacency, uint32_t* node_of) {
+  return guard([&] {
+    cudaStream_t st;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    IdxBuild b;
+    build_idx(g, device, node_of != nullptr, false, b, st);
+    if (fluid_count) *fluid_count = b.n;
+    if (adjacency && b.n) {
+      DevMem nm((size_t)b.n * 18 * 4);
+      launch_transpose_u32(st, b.adj.get<uint32_t>(), 18, b.n, nm.get<uint32_t>());
+      ck_launch();
+      CK(cudaMemcpyAsync(adjacency, nm.get(), (size_t)b.n * 18 * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (node_of)
+      CK(cudaMemcpyAsync(node_of, b.node_of.get(), (size_t)g->nx * g->ny * g->nz * 4,
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int lbmgpu_build_et_rem(const lbmgpu_geometry* g, int32_t device, uint32_t* fluid_count,
+                        uint32_t* rem, uint32_t* mailboxes) {
+  return guard([&] {
+    cudaStream_t st;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    IdxBuild b;
+    build_idx(g, device, false, true, b, st);
+    if (fluid_count) *fluid_count = b.n;
+    if (mailboxes) *mailboxes = b.nmail;
+    if (rem && b.n) {
+      DevMem nm((size_t)b.n * 9 * 4);
+      launch_transpose_u32(st, b.rem.get<uint32_t>(), 9, b.n, nm.get<uint32_t>());
+      ck_launch();
+      CK(cudaMemcpyAsync(rem, nm.get(), (size_t)b.n * 9 * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+// traffic() restated (p/src/perfmodel.cpp:12-75)
+int lbmgpu_traffic(int32_t family, int32_t addressing, int32_t pdf_bytes, int32_t* out,
+                   double* bytes_per_lup) {
+  return guard([&] {
+    const int q = 19;
+    int loads = 0, wa = 0, stores = 0, idx = 0, halves = 0;
+    switch (family) {
+      case 0: loads = 2 * q, wa = 2 * q, stores = 2 * q, idx = 2 * (q - 1); break;
+      case 1: loads = q, wa = q, stores = q, idx = q - 1; break;
+      case 2: loads = q, wa = 0, stores = q, idx = q - 1; break;
+      case 3: loads = q, wa = q - 1, stores = q, idx = q - 1; break;
+      case 4: loads = (3 * q - 1) / 2, wa = 0, stores = (3 * q - 1) / 2, idx = (q - 1) / 2; break;
+      case 5: loads = q, wa = 0, stores = q, idx = 0, halves = addressing ? q - 1 : 0; break;
+      case 6: loads = q, wa = 0, stores = q, idx = (q + 1) / 2; break;
+      default: throw std::invalid_argument("unknown scheme");
+    }
+    if (family != 5 && addressing) halves = 2 * idx;
+    if (pdf_bytes != 8 && pdf_bytes != 4) throw std::invalid_argument("pdf_bytes must be 8 or 4");
+    if (out) {
+      out[0] = loads, out[1] = wa, out[2] = stores, out[3] = halves, out[4] = pdf_bytes,
+      out[5] = 4;
+    }
+    *bytes_per_lup = (double)(loads + wa + stores) * pdf_bytes + (double)halves * 4 / 2.0;
+  });
+}
+
+// compulsory DRAM bytes per fluid-node update:
+// PDF loads + stores + IDX, no write-allocate.
+int lbmgpu_gpu_bytes_per_lup(int32_t scheme, int32_t addressing, int32_t pdf_bytes,
+                             double* bytes_per_lup) {
+  return guard([&] {
+    if (scheme < 0 || scheme > 9) throw std::invalid_argument("unknown scheme");
+    if (pdf_bytes != 8 && pdf_bytes != 4) throw std::invalid_argument("pdf_bytes must be 8 or 4");
+    const int pdfs = scheme == LBMGPU_TS ? 4 * 19 : 2 * 19;
+    double idx = 0;
+    if (addressing) {
+      switch (scheme) {
+        case LBMGPU_TS: idx = 18; break;
+        case LBMGPU_OS_PUSH:
+        case LBMGPU_OS_PULL:
+        case LBMGPU_OSNT_PULL_1S:
+        case LBMGPU_OSNT_PULL_2S:
+        case LBMGPU_CG: idx = 18; break;
+        default: idx = 9; break;  // SWAP, AA (odd steps only), ET rem
+      }
+    }
+    *bytes_per_lup = (double)pdfs * pdf_bytes + idx * 4;
+  });
+}
+
+double lbmgpu_lambda_odd(double lambda_even, double magic) {
+  const double tau_e_m = 1.0 / lambda_even - 0.5;
+  return 1.0 / (magic / tau_e_m + 0.5);
+}
+
+int lbmgpu_host_alloc(uint64_t bytes, void** p) {
+  return guard([&] {
+    if (!p) throw std::invalid_argument("null output pointer");
+    CK(cudaHostAlloc(p, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+int lbmgpu_host_free(void* p) {
+  return guard([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
+const char* lbmgpu_last_error(void) { return g_err.c_str(); }
+
+int lbmgpu_device_count(int32_t* count) {
+  return guard([&] {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+const char* lbmgpu_version(void) { return "lbmgpu 0.1 (sm_100a)"; }
+
+}  // extern "C"

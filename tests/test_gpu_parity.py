@@ -1,0 +1,240 @@
+"""GPU parity: every (scheme, addressing, layout, precision) of liblbmgpu.so,
+driven through the C ABI (paper_1111_0922_b200 -> include/lbmgpu.h), against
+the reference's own results (tests/golden/, made by make_golden.py from the
+compiled reference) and against the C oracle at larger sizes.
+
+Bar: fp64 bit-for-bit (memcmp), like the reference's cross-scheme check
+(p/src/bench.cpp:314-329); fp32 max relative error <= 1e-5 (north_star).
+"""
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal, load_case, max_rel
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["ts", "os-push", "os-pull", "osnt-pull-1s", "osnt-pull-2s", "cg", "swap-push",
+           "swap-pull", "aap", "et"]
+PAIRS = [(s, "direct") for s in SCHEMES] + [
+    (s, "indirect") for s in ["os-push", "os-pull", "osnt-pull-1s", "osnt-pull-2s", "aap", "et"]]
+EXT_PAIRS = [("ts", "indirect"), ("swap-push", "indirect"), ("swap-pull", "indirect")]
+CASES = ["seeded42", "channel_c1", "periodic_c0", "porous_c2", "closed_box"]
+FP32_TOL = 1e-5
+
+
+def geometry(L, c):
+    pol = ["wall" if p else "periodic" for p in c["policy"]]
+    mask = c["mask"] if not c["mask"].all() else None
+    return L.GridGeometry(*[int(v) for v in c["dims"]], pol, mask)
+
+
+def make(L, c, scheme, addr, layout="soa", precision=8, **kw):
+    flow = L.FlowParams(float(c["lambda_even"]), float(c["magic"]), tuple(c["force"]), 1.0)
+    opts = L.StepperOptions(layout=layout, precision=precision,
+                            extensions=(scheme, addr) in EXT_PAIRS, **kw)
+    return L.create_stepper(scheme, addr, geometry(L, c), flow, opts)
+
+
+def check(got, want, precision):
+    if precision == 8:
+        assert bitwise_equal(got, want), f"max rel {max_rel(got, want):.3e}"
+    else:
+        assert max_rel(got, want) <= FP32_TOL
+
+
+@pytest.mark.parametrize("precision", [8, 4])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("scheme,addr", PAIRS + EXT_PAIRS)
+@pytest.mark.parametrize("case", CASES)
+def test_scheme_matches_reference(gpu, case, scheme, addr, layout, precision):
+    c = load_case(case)
+    st = make(gpu, c, scheme, addr, layout, precision)
+    assert st.node_count() == c["f0"].size // 19
+    st.load_natural(c["f0"])
+    assert st.time_step() == 0
+    st.step()
+    check(st.extract_natural(), c["f1"], precision)
+    steps = int(c["steps"])
+    st.step_n(steps - 1)
+    st.synchronize()
+    assert st.time_step() == steps
+    check(st.extract_natural(), c[f"f{steps}"], precision)
+
+
+@pytest.mark.parametrize("scheme,addr", PAIRS)
+def test_every_step_tracks_reference_seeded42(gpu, scheme, addr):
+    """the reference's equivalence test: extract after EVERY step
+    (p/tests/test_schemes.cpp:145-183) — here against steps 1,2,3,10."""
+    c = load_case("seeded42")
+    st = make(gpu, c, scheme, addr)
+    st.load_natural(c["f0"])
+    for t in range(1, 11):
+        st.step()
+        if f"f{t}" in c:
+            assert bitwise_equal(st.extract_natural(), c[f"f{t}"]), t
+
+
+@pytest.mark.parametrize("scheme,addr", PAIRS + EXT_PAIRS)
+def test_load_then_extract_is_identity(gpu, scheme, addr):
+    """p/tests/test_schemes.cpp:210-224"""
+    c = load_case("seeded42")
+    st = make(gpu, c, scheme, addr)
+    st.step()
+    st.load_natural(c["f0"])
+    assert st.time_step() == 0
+    assert bitwise_equal(st.extract_natural(), c["f0"])
+
+
+@pytest.mark.parametrize("scheme,addr", PAIRS + EXT_PAIRS)
+def test_equilibrium_start_agrees(gpu, scheme, addr):
+    """p/tests/test_schemes.cpp:185-208: the default start is w_i*rho0"""
+    c = load_case("seeded42")
+    st = make(gpu, c, scheme, addr)
+    n = st.node_count()
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    assert bitwise_equal(st.extract_natural(), np.tile(w, n))
+
+
+def test_pure_streaming_is_a_permutation(gpu):
+    """p/tests/test_schemes.cpp:226-245"""
+    c = load_case("seeded42")
+    for scheme, addr in PAIRS:
+        st = make(gpu, c, scheme, addr, zero_collision=True)
+        st.load_natural(c["f0"])
+        s0 = np.sort(c["f0"])
+        for _ in range(4):
+            st.step()
+            assert bitwise_equal(np.sort(st.extract_natural()), s0), scheme
+
+
+def test_two_zero_collision_aa_steps_equal_double_streaming(gpu):
+    """p/tests/test_schemes.cpp:247-266"""
+    c = load_case("seeded42")
+    for addr in ("direct", "indirect"):
+        aa = make(gpu, c, "aap", addr, zero_collision=True)
+        ts = make(gpu, c, "ts", "direct", zero_collision=True)
+        aa.load_natural(c["f0"])
+        ts.load_natural(c["f0"])
+        aa.step(), aa.step(), ts.step(), ts.step()
+        assert bitwise_equal(aa.extract_natural(), ts.extract_natural())
+
+
+def test_chunk_length_and_streaming_stores_do_not_change_results(gpu):
+    """p/tests/test_schemes.cpp:268-307"""
+    c = load_case("seeded42")
+    for scheme in ("osnt-pull-1s", "osnt-pull-2s"):
+        for addr in ("direct", "indirect"):
+            outs = []
+            for chunk, nt in ((1, True), (150, True), (922, False)):
+                st = make(gpu, c, scheme, addr, chunk_length=chunk, streaming_stores=nt)
+                st.load_natural(c["f0"])
+                st.step_n(5)
+                outs.append(st.extract_natural())
+            assert bitwise_equal(outs[0], outs[1]) and bitwise_equal(outs[0], outs[2])
+
+
+def test_swap_fixup_timing_does_not_change_state(gpu):
+    """p/tests/test_schemes.cpp:309-330"""
+    c = load_case("seeded42")
+    for scheme in ("swap-push", "swap-pull"):
+        x = make(gpu, c, scheme, "direct", swap_deferred_fixup=False)
+        y = make(gpu, c, scheme, "direct", swap_deferred_fixup=True)
+        x.load_natural(c["f0"])
+        y.load_natural(c["f0"])
+        for _ in range(6):
+            x.step(), y.step()
+            assert bitwise_equal(x.extract_natural(), y.extract_natural())
+
+
+def test_layout_phases(gpu):
+    """p/tests/test_schemes.cpp:358-396"""
+    L = gpu
+    g = L.gen_channel(8, 4, 4)
+
+    def phase(scheme, steps, deferred=False):
+        st = L.create_stepper(scheme, "direct", g, L.FlowParams(),
+                              L.StepperOptions(swap_deferred_fixup=deferred))
+        for _ in range(steps):
+            st.step()
+        return st.layout_phase()
+
+    for s in ("ts", "os-push", "os-pull", "osnt-pull-1s"):
+        assert all(phase(s, t) == "natural" for t in (0, 1, 2))
+    assert [phase("aap", t) for t in (0, 1, 2)] == ["natural", "opposed", "natural"]
+    assert phase("cg", 1) == "shifted_even" and phase("cg", 2) == "shifted_odd"
+    assert phase("swap-push", 1) == "opposed"
+    assert phase("swap-push", 1, True) == "swap_partial"
+    assert phase("swap-pull", 2) == "natural"
+    assert [phase("et", t) for t in (0, 1, 2)] == ["natural", "twisted", "natural"]
+
+
+def test_et_handle_exchange_is_an_involution(gpu):
+    """p/tests/test_schemes.cpp:398-414"""
+    L = gpu
+    g = L.gen_channel(8, 4, 4)
+    for addr in ("direct", "indirect"):
+        et = L.create_stepper("et", addr, g)
+        before = et.extract_natural()
+        assert et.layout_phase() == "natural"
+        assert et.exchange_opposite_handles()
+        assert et.layout_phase() == "twisted"
+        assert et.exchange_opposite_handles()
+        assert bitwise_equal(et.extract_natural(), before)
+    assert not L.create_stepper("ts", "direct", g).exchange_opposite_handles()
+
+
+@pytest.mark.parametrize("scheme,addr", PAIRS + EXT_PAIRS)
+def test_closed_box_conserves_mass(gpu, scheme, addr):
+    """p/tests/test_schemes.cpp:416-436 (100 steps, 1e-12)"""
+    c = load_case("closed_box")
+    st = make(gpu, c, scheme, addr)
+    st.load_natural(c["f0"])
+    m0 = c["f0"].sum()
+    st.step_n(100)
+    assert abs(st.extract_natural().sum() - m0) / m0 <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [1, 42, 1234])
+def test_build_sparse_bitwise(gpu, seed):
+    z = load_case("idx")
+    L = gpu
+    g = L.GridGeometry(16, 8, 8, ("periodic", "wall", "periodic"), z[f"seed{seed}_mask"])
+    n, adj, node_of = L.build_sparse(g, node_of=True)
+    assert n == int(z[f"seed{seed}_mask"].sum())
+    assert np.array_equal(adj, z[f"seed{seed}_adjacency"])
+    assert np.array_equal(node_of, z[f"seed{seed}_node_of"])
+
+
+def test_build_sparse_porous_and_et_rem(gpu):
+    z = load_case("idx")
+    c = load_case("porous_c2")
+    L = gpu
+    g = geometry(L, c)
+    n, adj, _ = L.build_sparse(g)
+    assert np.array_equal(adj, z["porous_adjacency"])
+    rem, nmail = L.build_et_rem(g)
+    assert np.array_equal(rem, z["porous_et_rem"]) and nmail == int(z["porous_et_mail"])
+
+
+def test_build_sparse_edge_cases(gpu):
+    L = gpu
+    n, adj, _ = L.build_sparse(L.GridGeometry(4, 4, 4))
+    assert n == 64 and (adj != np.arange(64)[:, None]).all()
+    n, adj, _ = L.build_sparse(L.GridGeometry(1, 1, 1, ("wall",) * 3))
+    assert n == 1 and (adj == 0).all()
+    n, adj, _ = L.build_sparse(L.GridGeometry(3, 3, 3, mask=np.zeros(27, np.uint8)))
+    assert n == 0 and adj.size == 0
+
+
+def test_unsupported_pairs_and_option_errors(gpu):
+    L = gpu
+    g = L.gen_channel(4, 4, 4)
+    for s in ("ts", "cg", "swap-push", "swap-pull"):
+        with pytest.raises(ValueError, match="kernel not implemented; traffic model only"):
+            L.create_stepper(s, "indirect", g)
+    with pytest.raises(ValueError, match="kernel not implemented; traffic model only"):
+        L.create_stepper("cg", "indirect", g, options=L.StepperOptions(extensions=True))
+    with pytest.raises(ValueError, match="workers must be >= 0"):
+        L.create_stepper("aap", "direct", g, options=L.StepperOptions(workers=-1))
+    with pytest.raises(ValueError, match="chunk_length must be >= 1"):
+        L.create_stepper("osnt-pull-1s", "direct", g, options=L.StepperOptions(chunk_length=0))
