@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIBRARY_PATH = os.path.join(_HERE, "liblbmgpu.so")
+LIBRARY_PATH = os.environ.get("LBMGPU_LIBRARY") or os.path.join(_HERE, "liblbmgpu.so")
 
 if not os.path.exists(LIBRARY_PATH):
     raise ImportError(

@@ -37,7 +37,7 @@ inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlo
 //   SWAP collide from opposed slots     (p/src/scheme_swap.cpp:187-190, 228-231)
 // ---------------------------------------------------------------------------
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
-__global__ void __launch_bounds__(kBlock) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
                                                   Trt<T> op) {
   const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
@@ -52,41 +52,43 @@ __global__ void __launch_bounds__(kBlock) k_local(Fld<T, AOS> src, Fld<T, AOS> d
 }
 
 // TS stream_sweep: pull B -> A with bounce B[opp i][cell] (p/src/scheme_ts.cpp:82-112)
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
-  if (cell >= L.ncells) return;
-  const Ctx c = make_ctx(L, cell);
-  if (!c.fluid) return;
+template <bool BB, class T, bool AOS>
+__device__ __forceinline__ void ts_stream_body(const Fld<T, AOS>& a, const Fld<T, AOS>& b,
+                                               const Ctx& c) {
   T v[19];
   v[0] = ld(b.at(0, c.s));
 #pragma unroll
   for (int i = 1; i < 19; ++i) {
     const int j = opp(i);
-    const T* src = c.bb(j) ? b.at(j, c.s) : b.at(i, c.s + c.off(j));
-    v[i] = ld(src);
+    v[i] = ld((BB && c.bb(j)) ? b.at(j, c.s) : b.at(i, c.nb(j)));
   }
 #pragma unroll
   for (int i = 0; i < 19; ++i) st<false>(a.at(i, c.s), v[i]);
+}
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    ts_stream_body<false>(a, b, c);
+  else
+    ts_stream_body<true>(a, b, c);
 }
 
 // OS pull (p/src/scheme_os.cpp:141-174) and OSNT pull with streaming stores
 // (p/src/scheme_osnt.cpp:131-173, 175-217: 1S = one store loop per direction,
 // 2S = rest then one per opposing pair; st.global.cs replaces _mm_stream_si64).
-template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
-                                                    Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
-  if (cell >= L.ncells) return;
-  const Ctx c = make_ctx(L, cell);
-  if (!c.fluid) return;
+template <bool BB, bool NT, bool TWO_S, class T, bool AOS>
+__device__ __forceinline__ void os_pull_body(const Fld<T, AOS>& a, const Fld<T, AOS>& b,
+                                             const Ctx& c, const Trt<T>& op) {
   T f[19];
   f[0] = ld(a.at(0, c.s));
 #pragma unroll
   for (int i = 1; i < 19; ++i) {
     const int j = opp(i);
-    const T* src = c.bb(j) ? a.at(j, c.s) : a.at(i, c.s + c.off(j));
-    f[i] = ld(src);
+    f[i] = ld((BB && c.bb(j)) ? a.at(j, c.s) : a.at(i, c.nb(j)));
   }
   collide(op, f);
   if (!TWO_S) {
@@ -101,81 +103,110 @@ __global__ void __launch_bounds__(kBlock) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b
     }
   }
 }
-
-// OS push (p/src/scheme_os.cpp:104-139)
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+template <class T, bool AOS, bool NT, bool TWO_S>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
                                                     Trt<T> op) {
   const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
+  if (warp_interior(c))
+    os_pull_body<false, NT, TWO_S>(a, b, c, op);
+  else
+    os_pull_body<true, NT, TWO_S>(a, b, c, op);
+}
+
+// OS push (p/src/scheme_os.cpp:104-139)
+template <bool BB, class T, bool AOS>
+__device__ __forceinline__ void os_push_body(const Fld<T, AOS>& a, const Fld<T, AOS>& b,
+                                             const Ctx& c, const Trt<T>& op) {
   T f[19];
 #pragma unroll
   for (int i = 0; i < 19; ++i) f[i] = ld(a.at(i, c.s));
   collide(op, f);
   st<false>(b.at(0, c.s), f[0]);
 #pragma unroll
-  for (int i = 1; i < 19; ++i) {
-    T* dst = c.bb(i) ? b.at(opp(i), c.s) : b.at(i, c.s + c.off(i));
-    st<false>(dst, f[i]);
-  }
+  for (int i = 1; i < 19; ++i)
+    st<false>((BB && c.bb(i)) ? b.at(opp(i), c.s) : b.at_off(i, c.s, c.off(i)), f[i]);
+}
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+                                                    Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    os_push_body<false>(a, b, c, op);
+  else
+    os_push_body<true>(a, b, c, op);
 }
 
 // AA pattern odd sweep (p/src/scheme_aap.cpp:133-173): gather
 // f[opp i][x - c_i] (bounce: f[i][x]), collide, scatter f[j][x + c_j]
 // (bounce: f[opp j][x]). Every slot is read and rewritten by one thread.
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
-  if (cell >= L.ncells) return;
-  const Ctx c = make_ctx(L, cell);
-  if (!c.fluid) return;
+template <bool BB, class T, bool AOS>
+__device__ __forceinline__ void aa_odd_body(const Fld<T, AOS>& F, const Ctx& c,
+                                            const Trt<T>& op) {
   T f[19];
   f[0] = ld(F.at(0, c.s));
 #pragma unroll
   for (int i = 1; i < 19; ++i) {
     const int j = opp(i);
-    const T* src = c.bb(j) ? F.at(i, c.s) : F.at(j, c.s + c.off(j));
-    f[i] = ld(src);
+    f[i] = ld((BB && c.bb(j)) ? F.at(i, c.s) : F.at(j, c.nb(j)));
   }
   collide(op, f);
   st<false>(F.at(0, c.s), f[0]);
 #pragma unroll
-  for (int j = 1; j < 19; ++j) {
-    T* dst = c.bb(j) ? F.at(opp(j), c.s) : F.at(j, c.s + c.off(j));
-    st<false>(dst, f[j]);
-  }
+  for (int j = 1; j < 19; ++j)
+    st<false>((BB && c.bb(j)) ? F.at(opp(j), c.s) : F.at_off(j, c.s, c.off(j)), f[j]);
+}
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    aa_odd_body<false>(F, c, op);
+  else
+    aa_odd_body<true>(F, c, op);
 }
 
 // Esoteric twist sweep (p/src/scheme_et.cpp:191-239). For pair (i, j):
 // tmp_i = F[b_i][X], tmp_j = F[b_(db?i:j)][X + c_i]; collide;
 // F[b_(ub?j:i)][X] = tmp_j, F[b_j][X + c_i] = tmp_i. Wall axes carry a halo
 // plane, solid cells act as mailboxes, so X + c_i is always a storage slot.
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, EtBase B) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
-  if (cell >= L.ncells) return;
-  const Ctx c = make_ctx(L, cell);
-  if (!c.fluid) return;
+template <bool BB, class T, bool AOS>
+__device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, const Trt<T>& op,
+                                        const EtBase& B) {
   T f[19];
   f[0] = ld(F.at(0, c.s));
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    const long long rs = c.s + c.off(i);
     f[i] = ld(F.at(B.b[i], c.s));
-    f[j] = ld(F.at(c.bb(i) ? B.b[i] : B.b[j], rs));
+    f[j] = ld(F.at((BB && c.bb(i)) ? B.b[i] : B.b[j], c.nb(i)));
   }
   collide(op, f);
   st<false>(F.at(0, c.s), f[0]);
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    const long long rs = c.s + c.off(i);
-    st<false>(F.at(c.bb(j) ? B.b[j] : B.b[i], c.s), f[j]);
-    st<false>(F.at(B.b[j], rs), f[i]);
+    st<false>(F.at((BB && c.bb(j)) ? B.b[j] : B.b[i], c.s), f[j]);
+    st<false>(F.at_off(B.b[j], c.s, c.off(i)), f[i]);
   }
+}
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, EtBase B) {
+  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    et_body<false>(F, c, op, B);
+  else
+    et_body<true>(F, c, op, B);
 }
 
 // SWAP link exchange (p/src/scheme_swap.cpp:172-235, fix-ups :127-131).
@@ -185,7 +216,7 @@ __global__ void __launch_bounds__(kBlock) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, 
 // sweep equals "all collisions, then all swaps" (push) or "all swaps, then all
 // collisions" (pull), bit for bit. mode: 0 all, 1 non-wrapped, 2 wrapped only.
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_swap(Fld<T, AOS> F, Lat L, int mode) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap(Fld<T, AOS> F, Lat L, int mode) {
   const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -197,7 +228,7 @@ __global__ void __launch_bounds__(kBlock) k_swap(Fld<T, AOS> F, Lat L, int mode)
     const bool w = c.wrapped(L, i);
     if ((mode == 1 && w) || (mode == 2 && !w)) continue;
     T* a = F.at(i, c.s);
-    T* b = F.at(opp(i), c.s + c.off(i));
+    T* b = F.at(opp(i), c.nb(i));
     const T va = ld(a), vb = ld(b);
     st<false>(a, vb);
     st<false>(b, va);
@@ -224,7 +255,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // wait on it — and only then stores. Values crossing a periodic seam land
 // unwrapped in the padding and are copied by k_cg_fixup after the sweep.
 template <class T, bool AOS, bool EVEN>
-__global__ void __launch_bounds__(kBlock) k_cg(Fld<T, AOS> F, Lat L, Trt<T> op,
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_cg(Fld<T, AOS> F, Lat L, Trt<T> op,
                                                unsigned long long* ticket, unsigned* flags,
                                                unsigned epoch, uint32_t ntiles) {
   __shared__ uint32_t s_tile;
@@ -264,13 +295,13 @@ __global__ void __launch_bounds__(kBlock) k_cg(Fld<T, AOS> F, Lat L, Trt<T> op,
   }
   __syncthreads();
   if (!active || !c.fluid) return;
-  const long long sh = (long long)1 + L.sx + L.sxy;  // shift1
-  const long long wr = EVEN ? c.s + sh : c.s - sh;
+  const uint32_t sh = 1u + (uint32_t)L.sx + (uint32_t)L.sxy;  // shift1
+  const uint32_t wr = EVEN ? c.s + sh : c.s - sh;
   st<false>(F.at(0, wr), f[0]);
 #pragma unroll
   for (int i = 1; i < 19; ++i) {
-    const long long po = (long long)cx(i) + (long long)L.sx * cy(i) + L.sxy * cz(i);
-    T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + po);
+    const int po = cx(i) + L.sx * cy(i) + (int)L.sxy * cz(i);
+    T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + (uint32_t)po);
     st<false>(dst, f[i]);
   }
 }
@@ -281,7 +312,7 @@ __global__ void k_cg_fixup(Fld<T, AOS> F, const long long* src, const long long*
   const long long k = (long long)blockIdx.x * kBlock + threadIdx.x;
   if (k >= count) return;
   const int i = dir[k];
-  *F.at(i, dst[k] - shift) = *F.at(i, src[k] - shift);
+  *F.at(i, (uint32_t)(dst[k] - shift)) = *F.at(i, (uint32_t)(src[k] - shift));
 }
 
 }  // namespace

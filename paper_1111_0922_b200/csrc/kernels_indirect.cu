@@ -32,7 +32,7 @@ __device__ __forceinline__ uint32_t ldidx(const uint32_t* p) { return __ldg(p); 
 
 // local collision over nodes (TS collide, precollide, AA even, SWAP collide)
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
-__global__ void __launch_bounds__(kBlock) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
                                                       uint32_t n, Trt<T> op) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= n) return;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kBlock) k_local_idx(Fld<T, AOS> src, Fld<T, AO
 // TS streaming over the IDX graph (GPU extension; the reference's TS is
 // direct-only, stepper.cpp:140-153): A[i][n] = src == n ? B[opp i][n] : B[i][src]
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_ts_stream_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
   T v[19];
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kBlock) k_ts_stream_idx(Fld<T, AOS> a, Fld<T, 
 
 // OS / OSNT pull, indirect (p/src/scheme_os.cpp:203-226, scheme_osnt.cpp:219-260)
 template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
                                                         Trt<T> op) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kBlock) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AO
 
 // OS push, indirect (p/src/scheme_os.cpp:176-201)
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_os_push_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
                                                         Trt<T> op) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kBlock) k_os_push_idx(Fld<T, AOS> a, Fld<T, AO
 // row[opp i - 1] for i = 1..18 and the scatter row[j - 1] for j = 1..18: the
 // same 18 entries, loaded once.
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_aa_odd_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
   uint32_t e[19];
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kBlock) k_aa_odd_idx(Fld<T, AOS> F, Idx I, Trt
 // ET sweep, indirect (p/src/scheme_et.cpp:241-272): rem[p][n] = neighbour
 // along c_i or a mailbox slot >= N (i-link bounces), bit 31 = j-link bounces.
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op, EtBase B) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op, EtBase B) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
   uint32_t rs[9];
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kBlock) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> 
 // SWAP link exchange over the IDX graph (GPU extension, see k_swap): every
 // non-bounce back-half link swaps (i, n) <-> (opp i, adj[i][n]).
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock) k_swap_idx(Fld<T, AOS> F, Idx I) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap_idx(Fld<T, AOS> F, Idx I) {
   const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.n) return;
 #pragma unroll

@@ -115,7 +115,7 @@ __global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, ui
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
-        o[i] = (double)*(c.bb(j) ? F.at(j, c.s) : F.at(i, c.s + c.off(j)));
+        o[i] = (double)*(c.bb(j) ? F.at(j, c.s) : F.at(i, c.nb(j)));
       }
       break;
     case kExAaOdd:  // AapStepper::extract_natural, odd (p/src/scheme_aap.cpp:57-75)
@@ -123,7 +123,7 @@ __global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, ui
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
-        o[i] = (double)*(c.bb(j) ? F.at(i, c.s) : F.at(j, c.s + c.off(j)));
+        o[i] = (double)*(c.bb(j) ? F.at(i, c.s) : F.at(j, c.nb(j)));
       }
       break;
     case kExEt:  // EtStepper::extract_natural, direct (p/src/scheme_et.cpp:83-109)
@@ -132,7 +132,7 @@ __global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, ui
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
         o[i] = (double)*F.at(B.b[i], c.s);
-        o[j] = (double)*F.at(c.bb(i) ? B.b[i] : B.b[j], c.s + c.off(i));
+        o[j] = (double)*F.at(c.bb(i) ? B.b[i] : B.b[j], c.nb(i));
       }
       break;
   }
@@ -163,7 +163,7 @@ __global__ void k_load(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint3
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
         *F.at(i, c.s) = (T)v[i];
-        *F.at(c.bb(i) ? i : j, c.s + c.off(i)) = (T)v[j];
+        *F.at(c.bb(i) ? i : j, c.nb(i)) = (T)v[j];
       }
       break;
   }

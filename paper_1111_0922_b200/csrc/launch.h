@@ -30,6 +30,20 @@ struct EtBase {
 };
 
 constexpr int kBlock = 256;
+// Resident 256-thread blocks per SM that the register budget must allow
+// (__launch_bounds__ min blocks): fp64 kernels 2 (<= 128 registers, no
+// spills), fp32 kernels 4 (<= 64). Measured on B200: tools/sweep.py c1,
+// profiles/r01_variants.md.
+#ifndef LBM_MIN_BLOCKS_F64
+#define LBM_MIN_BLOCKS_F64 2
+#endif
+#ifndef LBM_MIN_BLOCKS_F32
+#define LBM_MIN_BLOCKS_F32 4
+#endif
+template <class T>
+struct MinBlocks {
+  static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_MIN_BLOCKS_F32;
+};
 
 // ---- direct (full-grid) addressing -----------------------------------------
 // collide every fluid cell locally: dst[wr(i)][s] = collide(src[rd(i)][s])
