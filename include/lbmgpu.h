@@ -180,6 +180,25 @@ int lbmgpu_gpu_bytes_per_lup(int32_t scheme, int32_t addressing, int32_t pdf_byt
 /* lambda_odd (p/src/collision.cpp:8-11) */
 double lbmgpu_lambda_odd(double lambda_even, double magic_lambda);
 
+/* ---- multi-GPU z-slabs (AA pattern, direct, SoA; options.z_begin/z_end) ----
+ * A slab stepper owns global planes [z_begin, z_end) of the geometry's box
+ * (periodic z). Its canonical snapshot is that contiguous range of the global
+ * one. Exchanges follow one plan: phase 0 (before each odd sweep) copies the
+ * owners' face slots into the neighbours' ghost planes, phase 1 (after it)
+ * copies them back; ops[k*5 + {phase, send, peer(-1 lower/+1 upper), plane
+ * (-1 lower ghost .. nzl upper ghost), slot}], posted in this order. */
+int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count);
+#define LBMGPU_NCCL_ID_BYTES 128
+int lbmgpu_nccl_unique_id(uint8_t* id);
+/* one rank per GPU: ring over ranks, rank r owns the r-th slab; collective */
+int lbmgpu_slab_connect_nccl(lbmgpu_stepper* h, const uint8_t* id, int32_t nranks, int32_t rank);
+/* ghosts <- owners (phase 0), needed before extract_natural at odd t; collective */
+int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h);
+/* several slabs in ONE process (any devices): step them in lockstep, the
+ * exchanges as device-to-device copies following the same plan */
+int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps);
+int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n);
+
 /* page-locked host memory (cudaHostAlloc) for the canonical snapshot, so
  * extract/load run at full host-link bandwidth */
 int lbmgpu_host_alloc(uint64_t bytes, void** p);

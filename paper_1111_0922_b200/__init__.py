@@ -91,6 +91,12 @@ _sig = {
                                            C.POINTER(C.c_double)]),
     "lbmgpu_lambda_odd": (C.c_double, [C.c_double, C.c_double]),
     "lbmgpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    "lbmgpu_halo_plan": (C.c_int, [C.c_int32, _P, C.POINTER(C.c_int32)]),
+    "lbmgpu_nccl_unique_id": (C.c_int, [_P]),
+    "lbmgpu_slab_connect_nccl": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
+    "lbmgpu_slab_sync_ghosts": (C.c_int, [_P]),
+    "lbmgpu_slab_group_step": (C.c_int, [_P, C.c_int32, C.c_int64]),
+    "lbmgpu_slab_group_sync_ghosts": (C.c_int, [_P, C.c_int32]),
     "lbmgpu_host_free": (C.c_int, [_P]),
     "lbmgpu_last_error": (C.c_char_p, []),
     "lbmgpu_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
@@ -204,6 +210,8 @@ class StepperOptions:
     precision: int = 8         # 8 fp64 | 4 fp32
     device: int = 0
     extensions: bool = False   # allow TS/SWAP indirect (GPU-only kernels)
+    z_begin: int = 0           # z-slab [z_begin, z_end) of a multi-GPU decomposition
+    z_end: int = 0             # (AA, direct, SoA); 0 = whole box
 
 
 # ---------------------------------------------------------------------------
@@ -315,6 +323,14 @@ class Stepper:
         _check(_L.lbmgpu_launches_per_step(self._h, C.byref(v)))
         return int(v.value)
 
+    # -- multi-GPU z-slabs ------------------------------------------------------
+    def slab_connect_nccl(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(_L.lbmgpu_slab_connect_nccl(self._h, buf, nranks, rank))
+
+    def slab_sync_ghosts(self) -> None:
+        _check(_L.lbmgpu_slab_sync_ghosts(self._h))
+
     def cuda_stream(self) -> int:
         v = C.c_void_p()
         _check(_L.lbmgpu_stream(self._h, C.byref(v)))
@@ -341,6 +357,8 @@ def create_stepper(scheme, addressing, geometry: GridGeometry, flow: FlowParams 
     o.swap_deferred_fixup = int(bool(options.swap_deferred_fixup))
     o.zero_collision = int(bool(options.zero_collision))
     o.extensions = int(bool(options.extensions))
+    o.z_begin = int(options.z_begin)
+    o.z_end = int(options.z_end)
     h = C.c_void_p()
     _check(_L.lbmgpu_create(C.byref(g), C.byref(fl), C.byref(o), C.byref(h)))
     del keep
@@ -393,6 +411,33 @@ def gpu_bytes_per_lup(scheme, addressing, pdf_bytes: int = 8) -> float:
     _check(_L.lbmgpu_gpu_bytes_per_lup(_scheme_id(scheme), _addr_id(addressing), pdf_bytes,
                                        C.byref(b)))
     return b.value
+
+
+def halo_plan(nzl: int):
+    """The z-slab exchange plan (lbmgpu_halo_plan): rows of (phase, send,
+    peer, plane, slot) in posting order."""
+    n = C.c_int32()
+    _check(_L.lbmgpu_halo_plan(nzl, None, C.byref(n)))
+    ops = np.zeros(n.value * 5, np.int32)
+    _check(_L.lbmgpu_halo_plan(nzl, ops.ctypes.data, C.byref(n)))
+    return ops.reshape(-1, 5)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_L.lbmgpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def slab_group_step(steppers, steps: int) -> None:
+    """Step in-process z-slabs in lockstep (exchanges as device copies)."""
+    arr = (C.c_void_p * len(steppers))(*[s._h for s in steppers])
+    _check(_L.lbmgpu_slab_group_step(arr, len(steppers), int(steps)))
+
+
+def slab_group_sync_ghosts(steppers) -> None:
+    arr = (C.c_void_p * len(steppers))(*[s._h for s in steppers])
+    _check(_L.lbmgpu_slab_group_sync_ghosts(arr, len(steppers)))
 
 
 class PinnedArray:

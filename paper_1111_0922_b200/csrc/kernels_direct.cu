@@ -39,7 +39,7 @@ inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlo
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
                                                   Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -67,7 +67,7 @@ __device__ __forceinline__ void ts_stream_body(const Fld<T, AOS>& a, const Fld<T
 }
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -106,7 +106,7 @@ __device__ __forceinline__ void os_pull_body(const Fld<T, AOS>& a, const Fld<T, 
 template <class T, bool AOS, bool NT, bool TWO_S>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
                                                     Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -132,7 +132,7 @@ __device__ __forceinline__ void os_push_body(const Fld<T, AOS>& a, const Fld<T, 
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
                                                     Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -163,7 +163,7 @@ __device__ __forceinline__ void aa_odd_body(const Fld<T, AOS>& F, const Ctx& c,
 }
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -199,7 +199,7 @@ __device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, cons
 }
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, EtBase B) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et(Fld<T, AOS> 
 // collisions" (pull), bit for bit. mode: 0 all, 1 non-wrapped, 2 wrapped only.
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap(Fld<T, AOS> F, Lat L, int mode) {
-  const uint32_t cell = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
@@ -319,11 +319,12 @@ __global__ void k_cg_fixup(Fld<T, AOS> F, const long long* src, const long long*
 
 void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,
                   const TrtHost& op, bool rd_opp, bool wr_opp) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(src, {
     auto a = fld<T, A>(src);
     auto b = fld<T, A>(dst);
     const auto o = cast_op<T>(op);
-    const unsigned g = grid_for(L.ncells);
+    const unsigned g = grid_for(L.ncells - L.cell_begin);
     if (!rd_opp && !wr_opp) k_local<T, A, false, false><<<g, kBlock, 0, st>>>(a, b, L, o);
     if (!rd_opp && wr_opp) k_local<T, A, false, true><<<g, kBlock, 0, st>>>(a, b, L, o);
     if (rd_opp && !wr_opp) k_local<T, A, true, false><<<g, kBlock, 0, st>>>(a, b, L, o);
@@ -332,18 +333,20 @@ void launch_local(cudaStream_t st, const DField& src, const DField& dst, const d
 }
 
 void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(a, {
-    k_ts_stream<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L);
+    k_ts_stream<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L);
   });
 }
 
 void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op, bool streaming, bool two_s) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(a, {
     auto fa = fld<T, A>(a);
     auto fb = fld<T, A>(b);
     const auto o = cast_op<T>(op);
-    const unsigned g = grid_for(L.ncells);
+    const unsigned g = grid_for(L.ncells - L.cell_begin);
     if (!streaming && !two_s) k_os_pull<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
     if (!streaming && two_s) k_os_pull<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, L, o);
     if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
@@ -353,32 +356,37 @@ void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev
 
 void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(a, {
-    k_os_push<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L,
+    k_os_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L,
                                                            cast_op<T>(op));
   });
 }
 
 void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(f, {
-    k_aa_odd<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+    k_aa_odd<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
   });
 }
 
 void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                const EtBase& base) {
+  if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(f, {
-    k_et<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), base);
+    k_et<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), base);
   });
 }
 
 void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) {
-  LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
+  if (L.ncells <= L.cell_begin) return;
+  LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
 }
 
 void launch_cg(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                bool even, unsigned long long* ticket, unsigned* flags, unsigned epoch) {
-  const uint32_t ntiles = grid_for(L.ncells);
+  if (L.ncells <= L.cell_begin) return;
+  const uint32_t ntiles = grid_for(L.ncells - L.cell_begin);
   LBM_DISPATCH(f, {
     if (even)
       k_cg<T, A, true><<<ntiles, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket, flags,

@@ -223,6 +223,7 @@ class Stepper {
   virtual void load_range(uint32_t n0, uint32_t cnt, const double* dbuf, const InitSpec& in) = 0;
   virtual void after_load() { t_ = 0; }
   virtual void before_extract() {}
+  virtual void finish() {}  // join side streams into stream_ after a step() batch
   virtual void after_extract() {}
   virtual int layout_phase() const { return LBMGPU_NATURAL; }
   virtual bool exchange_opposite_handles() { return false; }
@@ -235,6 +236,7 @@ class Stepper {
       if (nodes_ > 0) step_one();
       ++t_;
     }
+    finish();
     ck_launch();
   }
 
@@ -949,6 +951,316 @@ class SwapIndirect final : public IndirectStepper {
   DevMem f_;
 };
 
+
+// ---------------------------------------------------------------------------
+// Multi-GPU z-slab decomposition of the AA pattern.
+//
+// A slab owns global planes [z0, z1) plus one ghost plane below and above
+// (storage plane 0 and nzl+1). The even sweep is node-local. The odd sweep
+// of a bottom-plane cell reads and rewrites exactly the cz = -1 slots
+// {6,8,11,13,16} of the plane below it, and a top-plane cell the cz = +1
+// slots {5,9,12,14,17} of the plane above (p/src/scheme_aap.cpp:133-173
+// with X - c_i / X + c_j crossing the slab face). Within an odd sweep no one
+// else touches those slots, so the exchange is: before the sweep copy the
+// owners' face slots into the neighbours' ghosts, after it copy them back.
+// The plan (order included) is one table used by every transport: NCCL
+// (ncclSend/ncclRecv in one group per phase, over NVLink/NVSwitch), an
+// in-process device-to-device transport (several slabs on one or more
+// devices of one process), and the CPU gloo test (tests/test_slab_plan.py).
+// ---------------------------------------------------------------------------
+static constexpr int kZm[5] = {6, 8, 11, 13, 16};  // cz = -1
+static constexpr int kZp[5] = {5, 9, 12, 14, 17};  // cz = +1
+
+struct HaloOp {
+  int phase;  // 0: before the odd sweep (owner -> ghost); 1: after it (ghost -> owner)
+  int send;   // 1 send, 0 recv
+  int peer;   // -1 lower neighbour (rank - 1), +1 upper neighbour (rank + 1), periodic ring
+  int plane;  // local plane: -1 lower ghost, 0 bottom, nzl-1 top, nzl upper ghost
+  int slot;   // direction slot (a whole nx*ny slot plane)
+};
+
+static std::vector<HaloOp> halo_plan(int nzl) {
+  std::vector<HaloOp> v;
+  // phase 0: sends [up: top cz-] [down: bottom cz+]; recvs [down: lower ghost cz-] [up: upper ghost cz+]
+  for (int s : kZm) v.push_back({0, 1, +1, nzl - 1, s});
+  for (int s : kZp) v.push_back({0, 1, -1, 0, s});
+  for (int s : kZm) v.push_back({0, 0, -1, -1, s});
+  for (int s : kZp) v.push_back({0, 0, +1, nzl, s});
+  // phase 1: sends [down: lower ghost cz-] [up: upper ghost cz+]; recvs [up: top cz-] [down: bottom cz+]
+  for (int s : kZm) v.push_back({1, 1, -1, -1, s});
+  for (int s : kZp) v.push_back({1, 1, +1, nzl, s});
+  for (int s : kZm) v.push_back({1, 0, +1, nzl - 1, s});
+  for (int s : kZp) v.push_back({1, 0, -1, 0, s});
+  return v;
+}
+
+// NCCL, loaded on first use (dlopen) so processes that never decompose do not
+// map it; inside a torch process this resolves to torch's libnccl.so.2.
+#include <dlfcn.h>
+#include <nccl.h>
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  static Nccl& get() {
+    static Nccl n;
+    if (!n.h) {
+      n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!n.h) n.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!n.h) throw std::runtime_error(std::string("cannot load NCCL: ") + dlerror());
+#define LBM_SYM(f, name)                                                    \
+  n.f = reinterpret_cast<decltype(n.f)>(dlsym(n.h, name));                  \
+  if (!n.f) throw std::runtime_error("NCCL symbol missing: " name);
+      LBM_SYM(getUniqueId, "ncclGetUniqueId")
+      LBM_SYM(commInitRank, "ncclCommInitRank")
+      LBM_SYM(commDestroy, "ncclCommDestroy")
+      LBM_SYM(send, "ncclSend")
+      LBM_SYM(recv, "ncclRecv")
+      LBM_SYM(groupStart, "ncclGroupStart")
+      LBM_SYM(groupEnd, "ncclGroupEnd")
+      LBM_SYM(errStr, "ncclGetErrorString")
+#undef LBM_SYM
+    }
+    return n;
+  }
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw CudaError(std::string("nccl: ") + what + ": " + errStr(r));
+  }
+};
+
+class AaSlab final : public Stepper {
+ public:
+  AaSlab(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+      : Stepper(slab_geo(g, o), p, o), gnz_(g.nz), z0_(o.z_begin), z1_(o.z_end) {
+    nzl_ = z1_ - z0_;
+    plane_ = (uint64_t)g.nx * g.ny;
+    L_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
+    L_.zghost = 1;
+    L_.oz = 1;
+    L_.wall[2] = 0;
+    storage_ = plane_ * (nzl_ + 2);
+    alloc_field(f_, storage_);
+    CK(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
+    for (auto* e : {&ev_c_, &ev_halo_, &ev_odd_, &ev_back_})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    InitSpec r = base_init(kSrcRest);
+    init(r);
+  }
+  ~AaSlab() override {
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (comm_) {
+      cudaStreamSynchronize(comm_);
+      cudaStreamDestroy(comm_);
+    }
+    for (auto e : {ev_c_, ev_halo_, ev_odd_, ev_back_})
+      if (e) cudaEventDestroy(e);
+    if (nccl_) Nccl::get().commDestroy(nccl_);
+  }
+
+  static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
+    if (o.scheme != LBMGPU_AAP || o.addressing != LBMGPU_DIRECT || o.layout != LBMGPU_SOA)
+      throw std::invalid_argument("z-slab decomposition supports the AA pattern, direct, SoA");
+    if (g.solids) throw std::invalid_argument("z-slab decomposition needs an all-fluid box");
+    if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
+    if (o.z_begin < 0 || o.z_end > g.nz || o.z_end <= o.z_begin)
+      throw std::invalid_argument("z-slab range must satisfy 0 <= z_begin < z_end <= nz");
+    HostGeo s = g;
+    s.nz = o.z_end - o.z_begin;
+    return s;
+  }
+
+  InitSpec slab_init(int source) const {
+    InitSpec s = base_init(source);
+    s.gnz = gnz_;
+    s.z0 = z0_;
+    return s;
+  }
+
+  // ---- transports ----------------------------------------------------------
+  void connect_nccl(const ncclUniqueId& id, int nranks, int rank) {
+    CK(cudaSetDevice(opt_.device));
+    Nccl& N = Nccl::get();
+    if (nccl_) N.commDestroy(nccl_), nccl_ = nullptr;
+    N.check(N.commInitRank(&nccl_, nranks, id, rank), "ncclCommInitRank");
+    nranks_ = nranks, rank_ = rank;
+    transport_ = kNccl;
+  }
+  void set_local(int transport) { transport_ = transport; }
+
+  double* slot_ptr(int slot, int plane) const {
+    // storage plane = local plane + 1 (ghost below is storage plane 0)
+    return static_cast<double*>(f_.get()) + (size_t)slot * soa_stride(storage_) +
+           (size_t)(plane + 1) * plane_;
+  }
+  size_t plane_bytes() const { return plane_ * esize(); }
+
+  // NCCL phase: the plan's sends and receives in plan order, one group
+  void nccl_phase(int phase) {
+    Nccl& N = Nccl::get();
+    const ncclDataType_t ty = prec_ == Prec::f64 ? ncclDouble : ncclFloat;
+    N.check(N.groupStart(), "ncclGroupStart");
+    for (const HaloOp& op : halo_plan(nzl_)) {
+      if (op.phase != phase) continue;
+      const int peer = (rank_ + op.peer + nranks_) % nranks_;
+      void* p = slot_ptr(op.slot, op.plane);
+      if (op.send)
+        N.check(N.send(p, plane_, ty, peer, nccl_, comm_), "ncclSend");
+      else
+        N.check(N.recv(p, plane_, ty, peer, nccl_, comm_), "ncclRecv");
+    }
+    N.check(N.groupEnd(), "ncclGroupEnd");
+  }
+
+  dev::Lat planes(int za, int zb) const {  // local planes [za, zb)
+    dev::Lat L = L_;
+    L.cell_begin = (uint32_t)(za * plane_);
+    L.ncells = (uint32_t)(zb * plane_);
+    return L;
+  }
+
+  void step_one() override {
+    const DField f = field(f_, soa_stride(storage_));
+    const bool even = (t_ & 1) == 0;
+    if (transport_ == kNccl) {
+      // overlapped: interior planes never touch ghost or exchanged face slots
+      const int zi0 = 1, zi1 = std::max(1, nzl_ - 1);
+      if (even) {
+        launch_local(stream_, f, f, planes(zi0, zi1), op_, false, true);
+        CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
+        launch_local(stream_, f, f, planes(0, 1), op_, false, true);
+        if (nzl_ > 1) launch_local(stream_, f, f, planes(nzl_ - 1, nzl_), op_, false, true);
+      } else {
+        CK(cudaEventRecord(ev_c_, stream_));
+        CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
+        nccl_phase(0);
+        CK(cudaEventRecord(ev_halo_, comm_));
+        launch_aa_odd(stream_, f, planes(zi0, zi1), op_);
+        CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+        launch_aa_odd(stream_, f, planes(0, 1), op_);
+        if (nzl_ > 1) launch_aa_odd(stream_, f, planes(nzl_ - 1, nzl_), op_);
+        CK(cudaEventRecord(ev_odd_, stream_));
+        CK(cudaStreamWaitEvent(comm_, ev_odd_, 0));
+        nccl_phase(1);
+        CK(cudaEventRecord(ev_back_, comm_));
+      }
+      ghosts_fresh_ = false;
+      return;
+    }
+    if (transport_ != kLocalGroup)
+      throw std::runtime_error("slab stepper has no transport: connect NCCL or step as a group");
+    // in-process group: the driver (group_step) runs the exchanges between phases
+    if (even)
+      launch_local(stream_, f, f, L_, op_, false, true);
+    else
+      launch_aa_odd(stream_, f, L_, op_);
+  }
+  int launches_per_step() const override {
+    if (transport_ != kNccl) return 1;
+    return (t_ & 1) == 0 ? (nzl_ > 2 ? 3 : nzl_) : (nzl_ > 2 ? 3 : nzl_);
+  }
+
+  void finish() override {
+    if (transport_ == kNccl) CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
+  }
+
+  void sync_ghosts_nccl() {
+    if (transport_ != kNccl) throw std::runtime_error("slab stepper is not connected to NCCL");
+    CK(cudaEventRecord(ev_c_, stream_));
+    CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
+    nccl_phase(0);
+    CK(cudaEventRecord(ev_halo_, comm_));
+    CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+    ghosts_fresh_ = true;
+  }
+
+  void before_extract() override {
+    if ((t_ & 1) && !ghosts_fresh_)
+      throw std::runtime_error(
+          "slab extract at an odd time step reads the ghost planes: call "
+          "lbmgpu_slab_sync_ghosts (or the group variant) first");
+  }
+  void extract_range(uint32_t n0, uint32_t c, double* d) override {
+    launch_extract(stream_, field(f_, soa_stride(storage_)), L_, nullptr, n0, c,
+                   (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
+  }
+  void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
+    InitSpec s = in;
+    if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
+    launch_load(stream_, field(f_, soa_stride(storage_)), L_, nullptr, n0, c, kExNatural, d, s);
+  }
+  void after_load() override {
+    t_ = 0;
+    ghosts_fresh_ = false;
+  }
+  int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
+  uint64_t pdf_bytes() const override { return f_.bytes(); }
+
+  enum { kNone = 0, kLocalGroup = 1, kNccl = 2 };
+  int transport_ = kNone;
+  int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
+  bool ghosts_fresh_ = false;
+  uint64_t plane_ = 0, storage_ = 0;
+  dev::Lat L_;
+  DevMem f_;
+  cudaStream_t comm_ = nullptr;
+  cudaEvent_t ev_c_ = nullptr, ev_halo_ = nullptr, ev_odd_ = nullptr, ev_back_ = nullptr;
+  ncclComm_t nccl_ = nullptr;
+  int nranks_ = 1, rank_ = 0;
+};
+
+// In-process transport: executes one plan phase for a ring of slabs (rank k
+// = slab k) by matching each rank's sends with its peer's receives in plan
+// order — NCCL's point-to-point matching rule — as device-to-device copies.
+static void local_phase(std::vector<AaSlab*>& S, int phase) {
+  const int n = (int)S.size();
+  for (auto* s : S) s->sync();
+  std::vector<std::vector<HaloOp>> plans(n);
+  for (int k = 0; k < n; ++k) plans[k] = halo_plan(S[k]->nzl_);
+  for (int k = 0; k < n; ++k) {
+    std::vector<size_t> cursor(n, 0);
+    for (const HaloOp& op : plans[k]) {
+      if (op.phase != phase || !op.send) continue;
+      const int peer = (k + op.peer + n) % n;
+      // the next receive the peer posts from rank k in this phase
+      size_t& c = cursor[peer];
+      const std::vector<HaloOp>& pp = plans[peer];
+      for (; c < pp.size(); ++c) {
+        const HaloOp& r = pp[c];
+        if (r.phase == phase && !r.send && (peer + r.peer + n) % n == k) break;
+      }
+      if (c == pp.size()) throw std::runtime_error("halo plan: unmatched send");
+      const HaloOp& r = pp[c++];
+      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(r.slot, r.plane), S[peer]->opt_.device,
+                             S[k]->slot_ptr(op.slot, op.plane), S[k]->opt_.device,
+                             S[k]->plane_bytes(), S[k]->stream_));
+    }
+  }
+  for (auto* s : S) s->sync();
+}
+
+static void group_step(std::vector<AaSlab*>& S, long long steps) {
+  for (auto* s : S) {
+    if (s->transport_ == AaSlab::kNccl) throw std::invalid_argument("slab is NCCL-connected");
+    s->set_local(AaSlab::kLocalGroup);
+  }
+  for (long long k = 0; k < steps; ++k) {
+    const bool odd = (S[0]->t_ & 1) != 0;
+    for (auto* s : S)
+      if (((s->t_ & 1) != 0) != odd) throw std::invalid_argument("slabs out of step");
+    if (odd) local_phase(S, 0);
+    for (auto* s : S) s->step(1);
+    if (odd) local_phase(S, 1);
+    for (auto* s : S) s->ghosts_fresh_ = false;
+  }
+  for (auto* s : S) s->sync();
+}
+
 // create_stepper (p/src/stepper.cpp:155-180)
 static std::unique_ptr<Stepper> create(const lbmgpu_geometry* gg, const lbmgpu_flow* p,
                                        const lbmgpu_options* o) {
@@ -964,9 +1276,8 @@ static std::unique_ptr<Stepper> create(const lbmgpu_geometry* gg, const lbmgpu_f
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (o->device < 0 || o->device >= ndev) throw std::invalid_argument("no such CUDA device");
-  if (o->z_end != 0 || o->z_begin != 0)
-    throw std::invalid_argument("z-slab decomposition requires lbmgpu_create_slab");
   const HostGeo g = copy_geo(gg);
+  if (o->z_end != 0 || o->z_begin != 0) return std::make_unique<AaSlab>(g, *p, *o);
   if (o->addressing == LBMGPU_DIRECT) {
     switch (o->scheme) {
       case LBMGPU_TS: return std::make_unique<TsDirect>(g, *p, *o);
@@ -1192,6 +1503,10 @@ int lbmgpu_init_field(lbmgpu_stepper* h, int32_t kind, uint64_t seed, double u0,
       case 2: in = s.base_init(kSrcRandom); break;
       default: throw std::invalid_argument("unknown init kind");
     }
+    if (auto* sl = dynamic_cast<AaSlab*>(&s)) {
+      const int src = in.source;
+      in = sl->slab_init(src);
+    }
     in.seed = seed, in.u0 = u0, in.drho = drho, in.noise = noise;
     s.init(in);
   });
@@ -1220,6 +1535,71 @@ int lbmgpu_stream(lbmgpu_stepper* h, void** st) {
 }
 int lbmgpu_launches_per_step(lbmgpu_stepper* h, int32_t* n) {
   return guard([&] { *n = S(h).launches_per_step(); });
+}
+
+int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count) {
+  return guard([&] {
+    if (nzl < 1) throw std::invalid_argument("slab needs at least one plane");
+    const auto plan = halo_plan(nzl);
+    if (count) *count = (int32_t)plan.size();
+    if (ops)
+      for (size_t k = 0; k < plan.size(); ++k) {
+        ops[k * 5 + 0] = plan[k].phase;
+        ops[k * 5 + 1] = plan[k].send;
+        ops[k * 5 + 2] = plan[k].peer;
+        ops[k * 5 + 3] = plan[k].plane;
+        ops[k * 5 + 4] = plan[k].slot;
+      }
+  });
+}
+
+int lbmgpu_nccl_unique_id(uint8_t* id) {
+  return guard([&] {
+    ncclUniqueId u;
+    Nccl& N = Nccl::get();
+    N.check(N.getUniqueId(&u), "ncclGetUniqueId");
+    static_assert(sizeof(u) == LBMGPU_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+static AaSlab& slab(lbmgpu_stepper* h) {
+  auto* s = dynamic_cast<AaSlab*>(&S(h));
+  if (!s) throw std::invalid_argument("not a z-slab stepper");
+  return *s;
+}
+
+int lbmgpu_slab_connect_nccl(lbmgpu_stepper* h, const uint8_t* id, int32_t nranks,
+                             int32_t rank) {
+  return guard([&] {
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank");
+    slab(h).connect_nccl(u, nranks, rank);
+  });
+}
+
+int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h) {
+  return guard([&] { slab(h).sync_ghosts_nccl(); });
+}
+
+int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps) {
+  return guard([&] {
+    if (n < 1 || !hs) throw std::invalid_argument("empty slab group");
+    std::vector<AaSlab*> S;
+    for (int k = 0; k < n; ++k) S.push_back(&slab(hs[k]));
+    group_step(S, steps);
+  });
+}
+
+int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n) {
+  return guard([&] {
+    if (n < 1 || !hs) throw std::invalid_argument("empty slab group");
+    std::vector<AaSlab*> S;
+    for (int k = 0; k < n; ++k) S.push_back(&slab(hs[k]));
+    local_phase(S, 0);
+    for (auto* s : S) s->ghosts_fresh_ = true;
+  });
 }
 
 int lbmgpu_kernel_available(int32_t s, int32_t a) { return available(s, a, false) ? 1 : 0; }

@@ -1,0 +1,122 @@
+"""CPU, multi-process (gloo, world_size 2): the z-slab halo plan that
+liblbmgpu.so's NCCL transport executes (lbmgpu_halo_plan) drives a numpy AA
+restatement on two ranks; the gathered state must equal the single-domain
+two-step oracle bit for bit, at even and odd steps."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+DIMS = (6, 4, 8)  # nx, ny, nz (periodic); two slabs of 4 planes
+STEPS = 7
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _initial(nodes):
+    import oracle
+    return oracle.Oracle().random_field(20251019, nodes)
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from oracle.aa_numpy import AaSlab, trt
+    import paper_1111_0922_b200 as L
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny, nz = DIMS
+    nzl = nz // world
+    op = trt(1.3, 1.3, (1e-4, -2e-5, 3e-5))
+    slab = AaSlab(nx, ny, nzl, op)
+    f0 = _initial(nx * ny * nz)
+    per = nx * ny * nzl * 19
+    slab.load(f0[rank * per:(rank + 1) * per])
+    plan = L.halo_plan(nzl)
+
+    def phase(ph):
+        reqs = []
+        for (p, send, peer, plane, slot) in plan:
+            if p != ph or not send:
+                continue
+            dst = (rank + peer) % world
+            t = torch.from_numpy(np.ascontiguousarray(slab.plane(slot, plane)))
+            reqs.append(dist.isend(t, dst=dst, tag=int(slot) + 32 * ph))
+        for (p, send, peer, plane, slot) in plan:
+            if p != ph or send:
+                continue
+            src = (rank + peer) % world
+            t = torch.empty(ny, nx, dtype=torch.float64)
+            dist.recv(t, src=src, tag=int(slot) + 32 * ph)
+            slab.plane(slot, plane)[...] = t.numpy()
+        for r in reqs:
+            r.wait()
+
+    results = {}
+    for t in range(1, STEPS + 1):
+        odd = slab.t % 2 == 1
+        if odd:
+            phase(0)
+        slab.step_local()
+        if odd:
+            phase(1)
+        if t in (STEPS - 1, STEPS):
+            if slab.t % 2 == 1:
+                phase(0)  # fresh ghosts for the odd-time gather
+            results[t] = slab.extract()
+    out = {}
+    for t, v in results.items():
+        parts = [torch.zeros(per, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(v))
+        out[t] = np.concatenate([p.numpy() for p in parts])
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_halo_plan_shape():
+    import paper_1111_0922_b200 as L
+    plan = L.halo_plan(5)
+    assert plan.shape == (40, 5)
+    for ph in (0, 1):
+        rows = plan[plan[:, 0] == ph]
+        assert (rows[:, 1] == 1).sum() == 10 and (rows[:, 1] == 0).sum() == 10
+    # crossing slot sets: cz=-1 {6,8,11,13,16}, cz=+1 {5,9,12,14,17}
+    assert set(plan[(plan[:, 3] == -1)][:, 4]) == {6, 8, 11, 13, 16}
+    assert set(plan[(plan[:, 3] == 5)][:, 4]) == {5, 9, 12, 14, 17}
+
+
+def test_two_rank_gloo_slabs_match_single_domain():
+    import torch.multiprocessing as mp
+    import oracle
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    nx, ny, nz = DIMS
+    f0 = _initial(nx * ny * nz)
+    O = oracle.Oracle()
+    for t in (STEPS - 1, STEPS):
+        want = O.ts_run(nx, ny, nz, [0, 0, 0], None, 1.3, 1.3, (1e-4, -2e-5, 3e-5), f0, t)
+        assert np.array_equal(out[t].view(np.uint64), want.view(np.uint64)), t
