@@ -315,11 +315,144 @@ __global__ void k_cg_fixup(Fld<T, AOS> F, const long long* src, const long long*
   *F.at(i, (uint32_t)(dst[k] - shift)) = *F.at(i, (uint32_t)(src[k] - shift));
 }
 
+
+// ---------------------------------------------------------------------------
+// AoS variants with shared-memory staging of the record-contiguous (local)
+// side: the block's 256 records are read and/or written as one coalesced
+// 16-byte-vector run. Used when storage index = cell + soff (no x/y halo).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool cell_fluid(const Lat& L, uint32_t cell) {
+  return L.linkmask ? (L.linkmask[cell] & 1u) != 0 : true;
+}
+
+template <class T, bool RD_OPP, bool WR_OPP>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_local_aos(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, uint32_t soff) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t c0 = L.cell_begin + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, L.ncells - c0);
+  aos_stage_in(sm, src.p + (size_t)(c0 + soff) * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k < nrec && cell_fluid(L, c0 + k)) {
+    T f[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = sm[k * 19 + (RD_OPP ? opp(i) : i)];
+    collide(op, f);
+#pragma unroll
+    for (int i = 0; i < 19; ++i) sm[k * 19 + (WR_OPP ? opp(i) : i)] = f[i];
+  }
+  __syncthreads();
+  aos_stage_out(dst.p + (size_t)(c0 + soff) * 19, sm, nrec);
+}
+
+// OS/OSNT pull, AoS: gather per field (neighbour records), staged local store
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_os_pull_aos(Fld<T, true> a, Fld<T, true> b, Lat L, Trt<T> op, uint32_t soff) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t c0 = L.cell_begin + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, L.ncells - c0);
+  const uint32_t k = threadIdx.x;
+  T f[19];
+  bool live = false;
+  if (k < nrec) {
+    const Ctx c = make_ctx(L, c0 + k);
+    live = c.fluid;
+    if (live) {
+      f[0] = ld(a.at(0, c.s));
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        f[i] = ld(c.bb(j) ? a.at(j, c.s) : a.at(i, c.nb(j)));
+      }
+      collide(op, f);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 19; ++i)
+    if (k < nrec) sm[k * 19 + i] = live ? f[i] : T(0);
+  __syncthreads();
+  aos_stage_out(b.p + (size_t)(c0 + soff) * 19, sm, nrec);
+}
+
+// OS push, AoS: staged local load, scatter per field
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_os_push_aos(Fld<T, true> a, Fld<T, true> b, Lat L, Trt<T> op, uint32_t soff) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t c0 = L.cell_begin + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, L.ncells - c0);
+  aos_stage_in(sm, a.p + (size_t)(c0 + soff) * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k >= nrec) return;
+  const Ctx c = make_ctx(L, c0 + k);
+  if (!c.fluid) return;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = sm[k * 19 + i];
+  collide(op, f);
+  st<false>(b.at(0, c.s), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i)
+    st<false>(c.bb(i) ? b.at(opp(i), c.s) : b.at_off(i, c.s, c.off(i)), f[i]);
+}
+
+// TS stream, AoS: gather per field, staged local store
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_ts_stream_aos(Fld<T, true> a, Fld<T, true> b, Lat L, uint32_t soff) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t c0 = L.cell_begin + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, L.ncells - c0);
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    const Ctx c = make_ctx(L, c0 + k);
+    if (c.fluid) {
+      sm[k * 19] = ld(b.at(0, c.s));
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        sm[k * 19 + i] = ld(c.bb(j) ? b.at(j, c.s) : b.at(i, c.nb(j)));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 19; ++i) sm[k * 19 + i] = T(0);
+    }
+  }
+  __syncthreads();
+  aos_stage_out(a.p + (size_t)(c0 + soff) * 19, sm, nrec);
+}
+
+// storage index = cell + soff for every cell (no x/y halo or padding)?
+inline bool aos_contiguous(const DField& f, const dev::Lat& L, uint32_t* soff) {
+  if (!f.aos || L.sx != L.nx || L.sy != L.ny || L.ox != 0 || L.oy != 0) return false;
+  *soff = (uint32_t)(L.oz * L.sxy);
+  return true;
+}
+
 }  // namespace
 
 void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,
                   const TrtHost& op, bool rd_opp, bool wr_opp) {
   if (L.ncells <= L.cell_begin) return;
+  uint32_t soff = 0;
+  if (aos_contiguous(src, L, &soff)) {
+    const unsigned g = grid_for(L.ncells - L.cell_begin);
+    LBM_DISPATCH(src, {
+      if constexpr (A) {
+        auto a = fld<T, true>(src);
+        auto b = fld<T, true>(dst);
+        const auto o = cast_op<T>(op);
+        if (!rd_opp && !wr_opp) k_local_aos<T, false, false><<<g, kBlock, 0, st>>>(a, b, L, o, soff);
+        if (!rd_opp && wr_opp) k_local_aos<T, false, true><<<g, kBlock, 0, st>>>(a, b, L, o, soff);
+        if (rd_opp && !wr_opp) k_local_aos<T, true, false><<<g, kBlock, 0, st>>>(a, b, L, o, soff);
+        if (rd_opp && wr_opp) k_local_aos<T, true, true><<<g, kBlock, 0, st>>>(a, b, L, o, soff);
+      }
+    });
+    return;
+  }
   LBM_DISPATCH(src, {
     auto a = fld<T, A>(src);
     auto b = fld<T, A>(dst);
@@ -334,6 +467,15 @@ void launch_local(cudaStream_t st, const DField& src, const DField& dst, const d
 
 void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L) {
   if (L.ncells <= L.cell_begin) return;
+  uint32_t soff = 0;
+  if (aos_contiguous(a, L, &soff)) {
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_ts_stream_aos<T><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+            fld<T, true>(a), fld<T, true>(b), L, soff);
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     k_ts_stream<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L);
   });
@@ -342,6 +484,17 @@ void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const d
 void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op, bool streaming, bool two_s) {
   if (L.ncells <= L.cell_begin) return;
+  uint32_t soff = 0;
+  if (aos_contiguous(a, L, &soff)) {
+    // the staged store writes whole 16-byte vectors: store order (1S/2S) and
+    // streaming hints are properties of the record run, not of single slots
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_os_pull_aos<T><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+            fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), soff);
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     auto fa = fld<T, A>(a);
     auto fb = fld<T, A>(b);
@@ -357,6 +510,15 @@ void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev
 void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op) {
   if (L.ncells <= L.cell_begin) return;
+  uint32_t soff = 0;
+  if (aos_contiguous(a, L, &soff)) {
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_os_push_aos<T><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+            fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), soff);
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     k_os_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L,
                                                            cast_op<T>(op));

@@ -179,10 +179,121 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap_idx(Fld<T,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// AoS variants: the node-contiguous (local) side is staged through shared
+// memory as coalesced 16-byte vectors (see aos_stage_in / aos_stage_out).
+// ---------------------------------------------------------------------------
+template <class T, bool RD_OPP, bool WR_OPP>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_local_idx_aos(Fld<T, true> src, Fld<T, true> dst, uint32_t n, Trt<T> op) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t n0 = blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, n - n0);
+  aos_stage_in(sm, src.p + (size_t)n0 * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    T f[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = sm[k * 19 + (RD_OPP ? opp(i) : i)];
+    collide(op, f);
+#pragma unroll
+    for (int i = 0; i < 19; ++i) sm[k * 19 + (WR_OPP ? opp(i) : i)] = f[i];
+  }
+  __syncthreads();
+  aos_stage_out(dst.p + (size_t)n0 * 19, sm, nrec);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_os_pull_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I, Trt<T> op) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t n0 = blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    const uint32_t node = n0 + k;
+    T f[19];
+    f[0] = ld(a.at(0, node));
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      const uint32_t src = ldidx(I.adj + (size_t)(j - 1) * I.n + node);
+      f[i] = ld(src == node ? a.at(j, node) : a.at(i, src));
+    }
+    collide(op, f);
+#pragma unroll
+    for (int i = 0; i < 19; ++i) sm[k * 19 + i] = f[i];
+  }
+  __syncthreads();
+  aos_stage_out(b.p + (size_t)n0 * 19, sm, nrec);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_os_push_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I, Trt<T> op) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t n0 = blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  aos_stage_in(sm, a.p + (size_t)n0 * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k >= nrec) return;
+  const uint32_t node = n0 + k;
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = sm[k * 19 + i];
+  collide(op, f);
+  st<false>(b.at(0, node), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const uint32_t nb = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
+    st<false>(nb == node ? b.at(opp(i), node) : b.at(i, nb), f[i]);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t n0 = blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    const uint32_t node = n0 + k;
+    sm[k * 19] = ld(b.at(0, node));
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      const uint32_t src = ldidx(I.adj + (size_t)(j - 1) * I.n + node);
+      sm[k * 19 + i] = ld(src == node ? b.at(j, node) : b.at(i, src));
+    }
+  }
+  __syncthreads();
+  aos_stage_out(a.p + (size_t)n0 * 19, sm, nrec);
+}
+
 }  // namespace
 
 void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uint32_t n,
                       const TrtHost& op, bool rd_opp, bool wr_opp) {
+  if (n == 0) return;
+  if (src.aos) {
+    const unsigned g = grid_for(n);
+    LBM_DISPATCH(src, {
+      if constexpr (A) {
+        auto a = fld<T, true>(src);
+        auto b = fld<T, true>(dst);
+        const auto o = cast_op<T>(op);
+        if (!rd_opp && !wr_opp) k_local_idx_aos<T, false, false><<<g, kBlock, 0, st>>>(a, b, n, o);
+        if (!rd_opp && wr_opp) k_local_idx_aos<T, false, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+        if (rd_opp && !wr_opp) k_local_idx_aos<T, true, false><<<g, kBlock, 0, st>>>(a, b, n, o);
+        if (rd_opp && wr_opp) k_local_idx_aos<T, true, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+      }
+    });
+    return;
+  }
   LBM_DISPATCH(src, {
     auto a = fld<T, A>(src);
     auto b = fld<T, A>(dst);
@@ -196,6 +307,14 @@ void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uin
 }
 
 void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I) {
+  if (I.n == 0) return;
+  if (a.aos) {
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_ts_stream_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I);
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     k_ts_stream_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I);
   });
@@ -203,6 +322,15 @@ void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, con
 
 void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
                         const TrtHost& op, bool streaming, bool two_s) {
+  if (I.n == 0) return;
+  if (a.aos) {
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_os_pull_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
+                                                               cast_op<T>(op));
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     auto fa = fld<T, A>(a);
     auto fb = fld<T, A>(b);
@@ -217,6 +345,15 @@ void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const
 
 void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
                         const TrtHost& op) {
+  if (I.n == 0) return;
+  if (a.aos) {
+    LBM_DISPATCH(a, {
+      if constexpr (A)
+        k_os_push_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
+                                                               cast_op<T>(op));
+    });
+    return;
+  }
   LBM_DISPATCH(a, {
     k_os_push_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I,
                                                           cast_op<T>(op));
@@ -224,6 +361,7 @@ void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const
 }
 
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
+  if (I.n == 0) return;
   LBM_DISPATCH(f, {
     k_aa_odd_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
   });
@@ -231,12 +369,14 @@ void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const Trt
 
 void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
                    const EtBase& base) {
+  if (I.n == 0) return;
   LBM_DISPATCH(f, {
     k_et_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op), base);
   });
 }
 
 void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I) {
+  if (I.n == 0) return;
   LBM_DISPATCH(f, { k_swap_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I); });
 }
 
