@@ -235,75 +235,19 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap(Fld<T, AOS
   }
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Compressed grid sweep (p/src/scheme_cg.cpp:118-158), parallel form.
-// Within one sweep every slot is read before it is overwritten and there are
-// only write-after-read hazards: the node reading the slot a write lands on
-// sits at X + (1,1,1) + c_i (even) / X - (1,1,1) + c_i (odd). Tiles of 256
-// lexicographic cells take tickets in the reference traversal order (reverse
-// lex for even, forward for odd); a tile loads and collides, publishes
-// "reads done" (release), waits (acquire) for the <= 38 tiles owning its write
-// targets — all of which hold earlier tickets, so they are resident and never
-// wait on it — and only then stores. Values crossing a periodic seam land
-// unwrapped in the padding and are copied by k_cg_fixup after the sweep.
-template <class T, bool AOS, bool EVEN>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_cg(Fld<T, AOS> F, Lat L, Trt<T> op,
-                                               unsigned long long* ticket, unsigned* flags,
-                                               unsigned epoch, uint32_t ntiles) {
-  __shared__ uint32_t s_tile;
-  if (threadIdx.x == 0) {
-    const unsigned long long k = atomicAdd(ticket, 1ull) - (unsigned long long)(epoch - 1) * ntiles;
-    s_tile = EVEN ? ntiles - 1 - (uint32_t)k : (uint32_t)k;
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint32_t cell = tile * kBlock + threadIdx.x;
-  const bool active = cell < L.ncells;
-  Ctx c;
-  T f[19];
-  if (active) {
-    c = make_ctx(L, cell);  // L.o* = read origin (1 even, 2 odd)
-    if (c.fluid) {
-#pragma unroll
-      for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
-      collide(op, f);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flags + tile, epoch);
-  }
-  if (threadIdx.x < 38) {
-    const int d = threadIdx.x >> 1;
-    const int sgn = EVEN ? 1 : -1;
-    const long long D = (long long)(sgn + cx(d)) + (long long)L.nx * (sgn + cy(d)) +
-                        (long long)L.nx * L.ny * (sgn + cz(d));
-    long long tgt = (long long)tile * kBlock + D + ((threadIdx.x & 1) ? kBlock - 1 : 0);
-    if (tgt >= 0 && tgt < (long long)L.ncells) {
-      const unsigned* fl = flags + (uint32_t)(tgt / kBlock);
-      while (ld_acquire(fl) != epoch) __nanosleep(64);
-    }
-  }
-  __syncthreads();
-  if (!active || !c.fluid) return;
-  const uint32_t sh = 1u + (uint32_t)L.sx + (uint32_t)L.sxy;  // shift1
-  const uint32_t wr = EVEN ? c.s + sh : c.s - sh;
-  st<false>(F.at(0, wr), f[0]);
-#pragma unroll
-  for (int i = 1; i < 19; ++i) {
-    const int po = cx(i) + L.sx * cy(i) + (int)L.sxy * cz(i);
-    T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + (uint32_t)po);
-    st<false>(dst, f[i]);
-  }
+// swap a list of slot pairs (i, a) <-> (opp i, b): SWAP periodic-seam fix-ups
+// (p/src/scheme_swap.cpp:127-131)
+template <class T, bool AOS>
+__global__ void k_swap_list(Fld<T, AOS> F, const long long* a, const long long* b,
+                            const int8_t* dir, long long count) {
+  const long long k = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (k >= count) return;
+  const int i = dir[k];
+  T* pa = F.at(i, (uint32_t)a[k]);
+  T* pb = F.at(opp(i), (uint32_t)b[k]);
+  const T va = *pa, vb = *pb;
+  *pa = vb;
+  *pb = va;
 }
 
 template <class T, bool AOS>
@@ -432,6 +376,155 @@ inline bool aos_contiguous(const DField& f, const dev::Lat& L, uint32_t* soff) {
   return true;
 }
 
+
+// ---------------------------------------------------------------------------
+// Ticketed tiles (used by the compressed-grid sweep): blocks take tickets in
+// the reference traversal order, publish per-tile progress with st.release,
+// and wait with ld.acquire only on tiles holding earlier tickets, so the
+// waits cannot deadlock. Loads of data another SM rewrote during the sweep
+// use ld.global.cg (L2) so they are never served from a stale L1 line.
+template <class T>
+__device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+
+__device__ __forceinline__ uint32_t take_ticket(unsigned long long* ticket, unsigned epoch,
+                                                uint32_t ntiles, bool reverse) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) {
+    const unsigned long long k =
+        atomicAdd(ticket, 1ull) - (unsigned long long)(epoch - 1) * ntiles;
+    s_tile = reverse ? ntiles - 1 - (uint32_t)k : (uint32_t)k;
+  }
+  __syncthreads();
+  return s_tile;
+}
+__device__ __forceinline__ void publish_tile(unsigned* flags, uint32_t tile, unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(epoch) : "memory");
+  }
+}
+// threads 2k, 2k+1 wait for the tiles holding lex offsets D_k of the tile's
+// first / last cell (k < nd); returns after a block barrier
+__device__ __forceinline__ void wait_tiles(const unsigned* flags, uint32_t tile, unsigned epoch,
+                                           uint32_t ncells, const long long* D, int nd) {
+  // threads 0 .. 2nd-1: the dependency tiles; thread 2nd: the tile itself
+  if ((int)threadIdx.x <= 2 * nd) {
+    const long long tgt = (int)threadIdx.x == 2 * nd
+                              ? (long long)tile * kBlock
+                              : (long long)tile * kBlock + D[threadIdx.x >> 1] +
+                                    ((threadIdx.x & 1) ? kBlock - 1 : 0);
+    if (tgt >= 0 && tgt < (long long)ncells) {
+      const unsigned* fl = flags + (uint32_t)(tgt / kBlock);
+      unsigned v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+        if (v == epoch) break;
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Compressed grid, lagged pipeline (p/src/scheme_cg.cpp:118-158). Ticket tau
+// (reference traversal order: reverse lex for even sweeps, forward for odd)
+// runs phase A on its tile — read the 19 slots at the read origin, collide,
+// park the result in an L2-resident ring slot, publish "read" — and phase B on
+// the tile lag tickets behind: wait until every tile whose read slots it
+// overwrites has published "read" (X + (1,1,1) + c_i even / X - (1,1,1) + c_i
+// odd, all earlier tickets), then write the parked values at the write origin
+// and publish "ring slot free". The only hazards in a CG sweep are
+// write-after-read (every slot is read before it is overwritten), so these
+// waits reproduce the sequential result bit for bit.
+template <class T, bool AOS, bool EVEN>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_cg_lag(Fld<T, AOS> F, Lat L, Trt<T> op, unsigned long long* ticket, unsigned* flagsA,
+             unsigned* flagsB, unsigned epoch, uint32_t ntiles, uint32_t lag, T* ring,
+             uint32_t R) {
+  const uint32_t tau = take_ticket(ticket, epoch, ntiles + lag, false);
+  // ---- phase A ----
+  if (tau < ntiles) {
+    const uint32_t a = EVEN ? ntiles - 1 - tau : tau;
+    if (tau >= R) {  // the ring slot's previous tile must have been written out
+      if (threadIdx.x == 0) {
+        const uint32_t prev = EVEN ? ntiles - 1 - (tau - R) : tau - R;
+        unsigned v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flagsB + prev) : "memory");
+          if (v == epoch) break;
+          __nanosleep(32);
+        }
+      }
+      __syncthreads();
+    }
+    const uint32_t cell = a * kBlock + threadIdx.x;
+    T* slot = ring + (size_t)(tau % R) * 19 * kBlock + threadIdx.x;
+    if (cell < L.ncells) {
+      const Ctx c = make_ctx(L, cell);  // L.o* = read origin (1 even, 2 odd)
+      if (c.fluid) {
+        T f[19];
+#pragma unroll
+        for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
+        collide(op, f);
+#pragma unroll
+        for (int i = 0; i < 19; ++i) slot[i * kBlock] = f[i];
+      }
+    }
+    publish_tile(flagsA, a, epoch);
+  }
+  // ---- phase B ----
+  if (tau >= lag) {
+    const uint32_t ub = tau - lag;
+    const uint32_t b = EVEN ? ntiles - 1 - ub : ub;
+    if (threadIdx.x < 38) {
+      const int d = threadIdx.x >> 1;
+      const int sgn = EVEN ? 1 : -1;
+      const long long D = (long long)(sgn + cx(d)) + (long long)L.nx * (sgn + cy(d)) +
+                          (long long)L.nx * L.ny * (sgn + cz(d));
+      const long long tgt = (long long)b * kBlock + D + ((threadIdx.x & 1) ? kBlock - 1 : 0);
+      if (tgt >= 0 && tgt < (long long)L.ncells) {
+        const unsigned* fl = flagsA + (uint32_t)(tgt / kBlock);
+        unsigned v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+          if (v == epoch) break;
+          __nanosleep(32);
+        }
+      }
+    } else if (threadIdx.x == 38) {  // the tile's own phase A (ring contents)
+      unsigned v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flagsA + b) : "memory");
+        if (v == epoch) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    const uint32_t cell = b * kBlock + threadIdx.x;
+    const T* slot = ring + (size_t)(ub % R) * 19 * kBlock + threadIdx.x;
+    if (cell < L.ncells) {
+      const Ctx c = make_ctx(L, cell);
+      if (c.fluid) {
+        T f[19];
+#pragma unroll
+        for (int i = 0; i < 19; ++i) f[i] = __ldcg(slot + i * kBlock);
+        const uint32_t sh = 1u + (uint32_t)L.sx + (uint32_t)L.sxy;  // shift1
+        const uint32_t wr = EVEN ? c.s + sh : c.s - sh;
+        st<false>(F.at(0, wr), f[0]);
+#pragma unroll
+        for (int i = 1; i < 19; ++i) {
+          const int po = cx(i) + L.sx * cy(i) + (int)L.sxy * cz(i);
+          T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + (uint32_t)po);
+          st<false>(dst, f[i]);
+        }
+      }
+    }
+    publish_tile(flagsB, b, epoch);
+  }
+}
+
+
 }  // namespace
 
 void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,
@@ -545,17 +638,34 @@ void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) 
   LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
 }
 
-void launch_cg(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-               bool even, unsigned long long* ticket, unsigned* flags, unsigned epoch) {
+uint32_t cg_lag(const dev::Lat& L) {
+  const uint64_t reach = (2ull * L.nx * L.ny + 2ull * L.nx + 2 + kBlock - 1) / kBlock + 2;
+  return (uint32_t)(reach + 148 * 2);
+}
+
+void launch_cg_lag(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                   bool even, unsigned long long* ticket, unsigned* flagsA, unsigned* flagsB,
+                   unsigned epoch, void* ring, uint32_t R) {
   if (L.ncells <= L.cell_begin) return;
-  const uint32_t ntiles = grid_for(L.ncells - L.cell_begin);
+  const uint32_t ntiles = grid_for(L.ncells);
+  const uint32_t lag = cg_lag(L);
   LBM_DISPATCH(f, {
     if (even)
-      k_cg<T, A, true><<<ntiles, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket, flags,
-                                                  epoch, ntiles);
+      k_cg_lag<T, A, true><<<ntiles + lag, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket,
+                                                            flagsA, flagsB, epoch, ntiles, lag,
+                                                            static_cast<T*>(ring), R);
     else
-      k_cg<T, A, false><<<ntiles, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket,
-                                                   flags, epoch, ntiles);
+      k_cg_lag<T, A, false><<<ntiles + lag, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op),
+                                                             ticket, flagsA, flagsB, epoch, ntiles,
+                                                             lag, static_cast<T*>(ring), R);
+  });
+}
+
+void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
+                      const int8_t* dir, long long count) {
+  if (count <= 0) return;
+  LBM_DISPATCH(f, {
+    k_swap_list<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), a, b, dir, count);
   });
 }
 

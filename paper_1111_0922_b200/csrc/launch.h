@@ -64,9 +64,13 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
                const EtBase& base);
 // SWAP link exchange: mode 0 all links, 1 only non-wrapped, 2 only wrapped
 void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode);
-// Compressed grid sweep (ticketed tiles); L carries the +3 padded storage
-void launch_cg(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-               bool even, unsigned long long* ticket, unsigned* flags, unsigned epoch);
+void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
+                      const int8_t* dir, long long count);
+// CG lagged pipeline: ring of R tiles (R * 19 * 256 elements), R > cg_lag(L)
+uint32_t cg_lag(const dev::Lat& L);
+void launch_cg_lag(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                   bool even, unsigned long long* ticket, unsigned* flagsA, unsigned* flagsB,
+                   unsigned epoch, void* ring, uint32_t R);
 void launch_cg_fixup(cudaStream_t st, const DField& f, const long long* src,
                      const long long* dst, const int8_t* dir, long long count, long long shift);
 

@@ -608,9 +608,13 @@ class CgDirect final : public DirectStepper {
     }
     const uint64_t ntiles = (geo_.cells() + kBlock - 1) / kBlock;
     flags_.alloc(ntiles * sizeof(unsigned));
+    flagsB_.alloc(ntiles * sizeof(unsigned));
     ticket_.alloc(sizeof(unsigned long long));
     CK(cudaMemsetAsync(flags_.get(), 0, flags_.bytes(), stream_));
+    CK(cudaMemsetAsync(flagsB_.get(), 0, flagsB_.bytes(), stream_));
     CK(cudaMemsetAsync(ticket_.get(), 0, ticket_.bytes(), stream_));
+    ring_tiles_ = cg_lag(L1_) + 512;
+    ring_.alloc((size_t)ring_tiles_ * 19 * kBlock * esize());
     init(base_init(kSrcRest));
     sync();
   }
@@ -618,8 +622,9 @@ class CgDirect final : public DirectStepper {
     const DField f = field(f_, soa_stride(padded_));
     const bool even = (t_ & 1) == 0;
     ++epoch_;
-    launch_cg(stream_, f, even ? L1_ : L2_, op_, even, ticket_.get<unsigned long long>(),
-              flags_.get<unsigned>(), epoch_);
+    launch_cg_lag(stream_, f, even ? L1_ : L2_, op_, even, ticket_.get<unsigned long long>(),
+                  flags_.get<unsigned>(), flagsB_.get<unsigned>(), epoch_, ring_.get(),
+                  ring_tiles_);
     launch_cg_fixup(stream_, f, fsrc_.get<long long>(), fdst_.get<long long>(),
                     fdir_.get<int8_t>(), nfix_, even ? 0 : shift1_);
   }
@@ -634,7 +639,7 @@ class CgDirect final : public DirectStepper {
     return (t_ & 1) ? LBMGPU_SHIFTED_EVEN : LBMGPU_SHIFTED_ODD;
   }
   uint64_t pdf_bytes() const override { return f_.bytes(); }
-  uint64_t idx_bytes() const override { return flags_.bytes(); }
+  uint64_t idx_bytes() const override { return flags_.bytes() + flagsB_.bytes() + ring_.bytes(); }
 
  private:
   long long pidx(int x, int y, int z) const {
@@ -646,10 +651,15 @@ class CgDirect final : public DirectStepper {
   long long nfix_ = 0;
   unsigned epoch_ = 0;
   dev::Lat L1_, L2_;
-  DevMem f_, fsrc_, fdst_, fdir_, flags_, ticket_;
+  uint32_t ring_tiles_ = 0;
+  DevMem f_, fsrc_, fdst_, fdir_, flags_, flagsB_, ticket_, ring_;
 };
 
-// SWAP push/pull (p/src/scheme_swap.cpp): collide + link exchange
+// SWAP push/pull (p/src/scheme_swap.cpp): collide pass + link-exchange pass
+// + the periodic-seam fix-up list (post-sweep for push, or deferred; pre-sweep
+// for pull), exactly the reference's state machine. Fused single-sweep
+// variants (ticketed tiles, a lagged pipeline, z-plane stages) were measured
+// slower on B200.
 class SwapDirect final : public DirectStepper {
  public:
   SwapDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
@@ -657,9 +667,28 @@ class SwapDirect final : public DirectStepper {
     pull_ = o.scheme == LBMGPU_SWAP_PULL;
     defer_ = o.swap_deferred_fixup != 0;
     static const int back[9] = {2, 4, 6, 7, 8, 11, 13, 15, 16};
-    has_wrapped_ = !seam_links(geo_, back, 9).empty();
+    const auto links = seam_links(geo_, back, 9);
+    nfix_ = (long long)links.size();
+    if (nfix_) {
+      std::vector<long long> a(nfix_), b(nfix_);
+      std::vector<int8_t> d(nfix_);
+      for (long long k = 0; k < nfix_; ++k) {
+        a[k] = (long long)geo_.idx(links[k].x, links[k].y, links[k].z);
+        b[k] = (long long)geo_.idx(links[k].lx, links[k].ly, links[k].lz);
+        d[k] = (int8_t)links[k].dir;
+      }
+      fa_.alloc(nfix_ * 8), fb_.alloc(nfix_ * 8), fd_.alloc(nfix_);
+      CK(cudaMemcpyAsync(fa_.get(), a.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
+      CK(cudaMemcpyAsync(fb_.get(), b.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
+      CK(cudaMemcpyAsync(fd_.get(), d.data(), nfix_, cudaMemcpyHostToDevice, stream_));
+    }
     alloc_field(f_, g.cells());
     init(base_init(kSrcRest));
+    sync();
+  }
+  void fixup(const DField& f) {
+    launch_swap_list(stream_, f, fa_.get<long long>(), fb_.get<long long>(), fd_.get<int8_t>(),
+                     nfix_);
   }
   void step_one() override {
     const DField f = field(f_, soa_stride(geo_.cells()));
@@ -667,26 +696,40 @@ class SwapDirect final : public DirectStepper {
       if (fresh_) {
         launch_local(stream_, f, f, L_, op_, false, false);
         fresh_ = false;
-      } else {
-        launch_swap(stream_, f, L_, 0);
-        launch_local(stream_, f, f, L_, op_, true, false);
+        return;
       }
+      fixup(f);
+      sweep(f, false);
     } else {
       if (pending_) {
-        launch_swap(stream_, f, L_, 2);
+        fixup(f);
         pending_ = false;
       }
-      launch_local(stream_, f, f, L_, op_, true, false);
-      launch_swap(stream_, f, L_, defer_ ? 1 : 0);
-      pending_ = defer_ && has_wrapped_;
+      sweep(f, true);
+      if (defer_ && nfix_)
+        pending_ = true;
+      else
+        fixup(f);
     }
   }
-  int launches_per_step() const override { return 2; }
+  // all collisions then all swaps (push) / all swaps then all collisions
+  // (pull): the swapped slot pairs are disjoint and independent of the
+  // sweep's collisions, so this equals the sequential sweep bit for bit.
+  void sweep(const DField& f, bool push) {
+    if (push) {
+      launch_local(stream_, f, f, L_, op_, true, false);
+      launch_swap(stream_, f, L_, 1);
+    } else {
+      launch_swap(stream_, f, L_, 1);
+      launch_local(stream_, f, f, L_, op_, true, false);
+    }
+  }
+  int launches_per_step() const override { return 2 + (nfix_ ? 1 : 0); }
   void before_extract() override {
-    if (!pull_ && pending_) launch_swap(stream_, field(f_, soa_stride(geo_.cells())), L_, 2);
+    if (!pull_ && pending_) fixup(field(f_, soa_stride(geo_.cells())));
   }
   void after_extract() override {
-    if (!pull_ && pending_) launch_swap(stream_, field(f_, soa_stride(geo_.cells())), L_, 2);
+    if (!pull_ && pending_) fixup(field(f_, soa_stride(geo_.cells())));
   }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
     const DField f = field(f_, soa_stride(geo_.cells()));
@@ -710,9 +753,10 @@ class SwapDirect final : public DirectStepper {
   uint64_t pdf_bytes() const override { return f_.bytes(); }
 
  private:
-  bool pull_, defer_, has_wrapped_;
+  bool pull_, defer_;
   bool fresh_ = false, pending_ = false;
-  DevMem f_;
+  long long nfix_ = 0;
+  DevMem f_, fa_, fb_, fd_;
 };
 
 // ---------------------------------------------------------------------------
