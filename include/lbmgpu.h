@@ -126,6 +126,10 @@ int lbmgpu_step_timed(lbmgpu_stepper* h, int64_t n, double* ms);
  * memory of node_count*19 doubles. Both synchronise; load resets t to 0. */
 int lbmgpu_extract_natural(lbmgpu_stepper* h, double* out);
 int lbmgpu_load_natural(lbmgpu_stepper* h, const double* in);
+/* nodes [first, first + count) of the canonical snapshot only (count*19
+ * doubles, host or device memory): extract a large lattice in pieces */
+int lbmgpu_extract_natural_range(lbmgpu_stepper* h, uint64_t first, uint64_t count, double* out,
+                                 int32_t out_on_device);
 /* the same with a device pointer (node_count*19 doubles on the stepper's device) */
 int lbmgpu_extract_natural_device(lbmgpu_stepper* h, double* dev_out);
 int lbmgpu_load_natural_device(lbmgpu_stepper* h, const double* dev_in);

@@ -68,6 +68,7 @@ _sig = {
     "lbmgpu_synchronize": (C.c_int, [_P]),
     "lbmgpu_extract_natural": (C.c_int, [_P, _P]),
     "lbmgpu_load_natural": (C.c_int, [_P, _P]),
+    "lbmgpu_extract_natural_range": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_int32]),
     "lbmgpu_extract_natural_device": (C.c_int, [_P, _P]),
     "lbmgpu_load_natural_device": (C.c_int, [_P, _P]),
     "lbmgpu_init_field": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_double, C.c_double,
@@ -263,6 +264,12 @@ class Stepper:
         if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != self.values():
             raise ValueError("out must be a contiguous float64 array of node_count*19")
         _check(_L.lbmgpu_extract_natural(self._h, out.ctypes.data))
+        return out
+
+    def extract_natural_range(self, first: int, count: int) -> np.ndarray:
+        """nodes [first, first + count) of the canonical snapshot"""
+        out = np.empty(int(count) * Q, dtype=np.float64)
+        _check(_L.lbmgpu_extract_natural_range(self._h, int(first), int(count), out.ctypes.data, 0))
         return out
 
     def load_natural(self, f: np.ndarray) -> None:

@@ -404,29 +404,6 @@ __device__ __forceinline__ void publish_tile(unsigned* flags, uint32_t tile, uns
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(epoch) : "memory");
   }
 }
-// threads 2k, 2k+1 wait for the tiles holding lex offsets D_k of the tile's
-// first / last cell (k < nd); returns after a block barrier
-__device__ __forceinline__ void wait_tiles(const unsigned* flags, uint32_t tile, unsigned epoch,
-                                           uint32_t ncells, const long long* D, int nd) {
-  // threads 0 .. 2nd-1: the dependency tiles; thread 2nd: the tile itself
-  if ((int)threadIdx.x <= 2 * nd) {
-    const long long tgt = (int)threadIdx.x == 2 * nd
-                              ? (long long)tile * kBlock
-                              : (long long)tile * kBlock + D[threadIdx.x >> 1] +
-                                    ((threadIdx.x & 1) ? kBlock - 1 : 0);
-    if (tgt >= 0 && tgt < (long long)ncells) {
-      const unsigned* fl = flags + (uint32_t)(tgt / kBlock);
-      unsigned v;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
-        if (v == epoch) break;
-        __nanosleep(32);
-      }
-    }
-  }
-  __syncthreads();
-}
-
 // Compressed grid, lagged pipeline (p/src/scheme_cg.cpp:118-158). Ticket tau
 // (reference traversal order: reverse lex for even sweeps, forward for odd)
 // runs phase A on its tile — read the 19 slots at the read origin, collide,

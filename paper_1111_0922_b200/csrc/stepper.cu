@@ -242,19 +242,27 @@ class Stepper {
 
   void sync() { CK(cudaStreamSynchronize(stream_)); }
 
-  // canonical snapshot <-> storage, in chunks through a device staging buffer
-  void extract(double* out, bool out_on_device) {
+  // canonical snapshot <-> storage, in chunks through a device staging buffer;
+  // [first, first + count) selects a node range (out holds count*19 values)
+  void extract(double* out, bool out_on_device, uint64_t first = 0, uint64_t count = ~0ull) {
     CK(cudaSetDevice(opt_.device));
+    if (count == ~0ull) count = nodes_ - std::min(first, nodes_);
+    if (first > nodes_ || count > nodes_ - first)
+      throw std::invalid_argument("node range outside the snapshot");
     before_extract();
-    for_chunks([&](uint32_t n0, uint32_t cnt) {
-      double* d = out_on_device ? out + (size_t)n0 * 19 : stage();
+    const uint64_t ch = chunk_nodes();
+    for (uint64_t k = 0; k < count; k += ch) {
+      const uint32_t n0 = (uint32_t)(first + k);
+      const uint32_t cnt = (uint32_t)std::min<uint64_t>(ch, count - k);
+      double* d = out_on_device ? out + (size_t)k * 19 : stage();
       extract_range(n0, cnt, d);
       ck_launch();
-      if (!out_on_device)
-        CK(cudaMemcpyAsync(out + (size_t)n0 * 19, d, (size_t)cnt * 19 * sizeof(double),
+      if (!out_on_device) {
+        CK(cudaMemcpyAsync(out + (size_t)k * 19, d, (size_t)cnt * 19 * sizeof(double),
                            cudaMemcpyDeviceToHost, stream_));
-      if (!out_on_device) sync();
-    });
+        sync();
+      }
+    }
     after_extract();
     sync();
   }
@@ -1517,6 +1525,14 @@ int lbmgpu_extract_natural(lbmgpu_stepper* h, double* out) {
     S(h).extract(out, false);
   });
 }
+int lbmgpu_extract_natural_range(lbmgpu_stepper* h, uint64_t first, uint64_t count, double* out,
+                                 int32_t out_on_device) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output buffer");
+    S(h).extract(out, out_on_device != 0, first, count);
+  });
+}
+
 int lbmgpu_load_natural(lbmgpu_stepper* h, const double* in) {
   return guard([&] {
     if (!in) throw std::invalid_argument("null input buffer");
