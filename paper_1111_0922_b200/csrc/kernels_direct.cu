@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
 }
 
 
+
 }  // namespace
 
 void launch_local(cudaStream_t st, const DField& src, const DField& dst, const dev::Lat& L,

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -666,8 +667,8 @@ class CgDirect final : public DirectStepper {
 // SWAP push/pull (p/src/scheme_swap.cpp): collide pass + link-exchange pass
 // + the periodic-seam fix-up list (post-sweep for push, or deferred; pre-sweep
 // for pull), exactly the reference's state machine. Fused single-sweep
-// variants (ticketed tiles, a lagged pipeline, z-plane stages) were measured
-// slower on B200.
+// variants (ticketed tiles, a lagged pipeline, z-plane stage launches, a
+// cooperative persistent sweep) were measured slower on B200.
 class SwapDirect final : public DirectStepper {
  public:
   SwapDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
