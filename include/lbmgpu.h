@@ -155,6 +155,36 @@ int lbmgpu_stream(lbmgpu_stepper* h, void** cuda_stream);
 /* kernels enqueued by one step() at the current parity */
 int lbmgpu_launches_per_step(lbmgpu_stepper* h, int32_t* launches);
 
+/* ---- harness (p/src/bench.cpp) ---------------------------------------------
+ * run_bench (bench.cpp:155-198): rest start, warmup steps, then timed_runs x
+ * steps, median device time (CUDA events on the stepper's stream).
+ * MLUPs = fluid * steps / s / 1e6 (bench.cpp:184); bytes_per_lup = the paper's
+ * traffic(); gpu_bytes_per_lup = compulsory bytes; predicted = hbm_gbs /
+ * gpu_bytes_per_lup (hbm_gbs <= 0: no prediction). */
+typedef struct {
+  int32_t scheme, addressing, layout, precision;
+  uint64_t fluid_count;
+  int32_t steps;
+  double seconds, mlups, bytes_per_lup, gpu_bytes_per_lup, predicted_mlups, model_fraction,
+      achieved_gbs;
+} lbmgpu_bench_result;
+int lbmgpu_run_bench(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgpu_options* o,
+                     int32_t steps, int32_t warmup, int32_t timed_runs, double hbm_gbs,
+                     lbmgpu_bench_result* result);
+
+/* verify_suite (bench.cpp:275-341): make_seeded_geometry(seed), seeded start,
+ * every implemented pair (all_variants: x {SoA, AoS} x {fp64, fp32}) against
+ * the GPU two-step reference after every step. fp64 passes bitwise (or
+ * max_rel <= 1e-13, the reference's fallback), fp32 at max_rel <= 1e-5. */
+typedef struct {
+  int32_t scheme, addressing, layout, precision;
+  int32_t bitwise, pass;
+  double max_rel_linf;
+} lbmgpu_verify_entry;
+int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t all_variants,
+                        lbmgpu_verify_entry* entries, int32_t capacity, int32_t* count,
+                        int32_t* all_pass);
+
 /* kernel_available (p/src/stepper.cpp:140-153): 10 direct + 6 indirect */
 int lbmgpu_kernel_available(int32_t scheme, int32_t addressing);
 /* the same including the GPU extensions (TS / SWAP indirect) */

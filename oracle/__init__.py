@@ -208,6 +208,7 @@ class RefLib:
         L.ref_verify_suite.argtypes = [C.c_ulonglong, C.c_int, _i32p, _f64p,
                                        C.POINTER(C.c_int)]
         L.ref_flops_per_update.restype = C.c_int
+        L.ref_save_geo.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, C.c_void_p, C.c_char_p]
         L.ref_kernel_available.argtypes = [C.c_int, C.c_int]
 
     def error(self):
@@ -261,6 +262,12 @@ class RefLib:
         pol = np.zeros(3, np.uint8)
         self.L.ref_make_seeded_geometry(seed, mask, pol)
         return (16, 8, 8), pol, mask
+
+    def save_geo(self, dims, policy, mask, path):
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        if self.L.ref_save_geo(dims[0], dims[1], dims[2], np.asarray(policy, np.uint8),
+                               None if m is None else m.ctypes.data, path.encode()) != 0:
+            raise RuntimeError(self.error())
 
     def traffic(self, family, addressing):
         out = np.zeros(6, np.int32)

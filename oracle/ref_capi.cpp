@@ -167,6 +167,19 @@ int ref_exchange_opposite_handles(void* h) {
 }
 void ref_destroy(void* h) { delete static_cast<Handle*>(h); }
 
+// save_geo / load_geo (p/src/geometry.cpp:123-171)
+int ref_save_geo(int nx, int ny, int nz, const std::uint8_t* policy, const std::uint8_t* mask,
+                 const char* path) {
+  return guard([&] { save_geo(make_geo(nx, ny, nz, policy, mask), path); });
+}
+int ref_load_geo_dims(const char* path, int* dims, std::uint8_t* policy) {
+  return guard([&] {
+    const GridGeometry g = load_geo(path);
+    dims[0] = g.nx, dims[1] = g.ny, dims[2] = g.nz;
+    for (int k = 0; k < 3; ++k) policy[k] = static_cast<std::uint8_t>(g.axis_policy[k]);
+  });
+}
+
 int ref_kernel_available(int scheme, int addressing) {
   return kernel_available(static_cast<SchemeId>(scheme), static_cast<Addressing>(addressing))
              ? 1

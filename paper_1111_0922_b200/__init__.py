@@ -50,6 +50,18 @@ class _Flow(C.Structure):
                 ("body_force", C.c_double * 3), ("rho0", C.c_double)]
 
 
+class _BenchResult(C.Structure):
+    _fields_ = [("scheme", C.c_int32), ("addressing", C.c_int32), ("layout", C.c_int32),
+                ("precision", C.c_int32), ("fluid_count", C.c_uint64), ("steps", C.c_int32)] + \
+               [(n, C.c_double) for n in ("seconds", "mlups", "bytes_per_lup", "gpu_bytes_per_lup",
+                                          "predicted_mlups", "model_fraction", "achieved_gbs")]
+
+
+class _VerifyEntry(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("scheme", "addressing", "layout", "precision", "bitwise",
+                                         "pass_")] + [("max_rel_linf", C.c_double)]
+
+
 class _Options(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "scheme", "addressing", "layout", "precision", "device", "workers", "chunk_length",
@@ -99,6 +111,10 @@ _sig = {
     "lbmgpu_slab_group_step": (C.c_int, [_P, C.c_int32, C.c_int64]),
     "lbmgpu_slab_group_sync_ghosts": (C.c_int, [_P, C.c_int32]),
     "lbmgpu_host_free": (C.c_int, [_P]),
+    "lbmgpu_run_bench": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
+                                   C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
+    "lbmgpu_verify_suite": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "lbmgpu_last_error": (C.c_char_p, []),
     "lbmgpu_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "lbmgpu_version": (C.c_char_p, []),
@@ -344,14 +360,7 @@ class Stepper:
         return int(v.value or 0)
 
 
-def create_stepper(scheme, addressing, geometry: GridGeometry, flow: FlowParams = None,
-                   options: StepperOptions = None) -> Stepper:
-    """create_stepper (p/src/stepper.cpp:155-180)."""
-    flow = flow or FlowParams()
-    options = options or StepperOptions()
-    sid, aid = _scheme_id(scheme), _addr_id(addressing)
-    g, keep = geometry._c()
-    fl = _Flow(flow.lambda_even, lambda_odd(flow), (C.c_double * 3)(*flow.body_force), flow.rho0)
+def _c_options(sid, aid, options):
     o = _Options()
     _L.lbmgpu_default_options(C.byref(o))
     o.scheme, o.addressing = sid, aid
@@ -366,10 +375,125 @@ def create_stepper(scheme, addressing, geometry: GridGeometry, flow: FlowParams 
     o.extensions = int(bool(options.extensions))
     o.z_begin = int(options.z_begin)
     o.z_end = int(options.z_end)
+    return o
+
+
+def _c_flow(flow):
+    return _Flow(flow.lambda_even, lambda_odd(flow), (C.c_double * 3)(*flow.body_force), flow.rho0)
+
+
+def create_stepper(scheme, addressing, geometry: GridGeometry, flow: FlowParams = None,
+                   options: StepperOptions = None) -> Stepper:
+    """create_stepper (p/src/stepper.cpp:155-180)."""
+    flow = flow or FlowParams()
+    options = options or StepperOptions()
+    sid, aid = _scheme_id(scheme), _addr_id(addressing)
+    g, keep = geometry._c()
+    fl = _c_flow(flow)
+    o = _c_options(sid, aid, options)
     h = C.c_void_p()
     _check(_L.lbmgpu_create(C.byref(g), C.byref(fl), C.byref(o), C.byref(h)))
     del keep
     return Stepper(h, sid, aid, options)
+
+
+@dataclass
+class BenchResult:
+    """lbmlab::BenchResult (p/include/lbmlab/bench.hpp:49-62) + B200 columns."""
+    scheme: str
+    addressing: str
+    layout: str
+    dtype: str
+    geometry: str
+    fluid_count: int
+    steps: int
+    seconds: float
+    mlups: float
+    bytes_per_lup: float        # the paper's traffic() model
+    gpu_bytes_per_lup: float    # compulsory DRAM bytes of these kernels
+    predicted_mlups: float      # hbm_gbs / gpu_bytes_per_lup
+    model_fraction: float
+    achieved_gbs: float
+    model_violated: bool
+
+
+CSV_COLUMNS = ("scheme,addressing,layout,dtype,geometry,fluid_count,steps,seconds,mlups,"
+               "bytes_per_lup,gpu_bytes_per_lup,predicted_mlups,model_fraction,achieved_gbs")
+
+
+def run_bench(scheme, addressing, geometry: GridGeometry, flow: FlowParams = None, steps: int = 10,
+              warmup: int = 3, timed_runs: int = 3, options: StepperOptions = None,
+              hbm_gbs: float = 0.0, geometry_name: str = "custom") -> BenchResult:
+    """run_bench (p/src/bench.cpp:155-198) on the GPU: median device time of
+    timed_runs x steps; model_violated when model_fraction > 1.1 (bench.cpp:196)."""
+    flow = flow or FlowParams()
+    options = options or StepperOptions()
+    sid, aid = _scheme_id(scheme), _addr_id(addressing)
+    g, keep = geometry._c()
+    r = _BenchResult()
+    _check(_L.lbmgpu_run_bench(C.byref(g), C.byref(_c_flow(flow)),
+                               C.byref(_c_options(sid, aid, options)), steps, warmup, timed_runs,
+                               hbm_gbs, C.byref(r)))
+    del keep
+    return BenchResult(SCHEMES[sid], ADDRESSINGS[aid], options.layout,
+                       "f64" if options.precision == 8 else "f32", geometry_name,
+                       int(r.fluid_count), r.steps, r.seconds, r.mlups, r.bytes_per_lup,
+                       r.gpu_bytes_per_lup, r.predicted_mlups, r.model_fraction, r.achieved_gbs,
+                       r.model_fraction > 1.1)
+
+
+def to_csv(results) -> str:
+    """to_csv (p/src/bench.cpp:210-241) with the B200 columns"""
+    out = CSV_COLUMNS + "\n"
+    for r in results:
+        out += ",".join([r.scheme, r.addressing, r.layout, r.dtype, r.geometry,
+                         str(r.fluid_count), str(r.steps)] +
+                        [f"{v:.6g}" for v in (r.seconds, r.mlups, r.bytes_per_lup,
+                                              r.gpu_bytes_per_lup, r.predicted_mlups,
+                                              r.model_fraction, r.achieved_gbs)]) + "\n"
+    return out
+
+
+@dataclass
+class VerifyEntry:
+    scheme: str
+    addressing: str
+    layout: str
+    dtype: str
+    bitwise: bool
+    passed: bool
+    max_rel_linf: float
+
+
+def verify_suite(seed: int = 42, steps: int = 10, device: int = 0, all_variants: bool = False):
+    """verify_suite (p/src/bench.cpp:275-341) on the GPU. Returns (entries, all_pass)."""
+    cap = 128
+    arr = (_VerifyEntry * cap)()
+    n, ap = C.c_int32(), C.c_int32()
+    _check(_L.lbmgpu_verify_suite(seed, steps, device, int(all_variants), arr, cap, C.byref(n),
+                                  C.byref(ap)))
+    ents = [VerifyEntry(SCHEMES[e.scheme], ADDRESSINGS[e.addressing], ("soa", "aos")[e.layout],
+                        "f64" if e.precision == 8 else "f32", bool(e.bitwise), bool(e.pass_),
+                        e.max_rel_linf) for e in arr[:n.value]]
+    return ents, bool(ap.value)
+
+
+def macroscopic_fields(stepper: Stepper, flow: FlowParams):
+    """macroscopic_fields (p/src/stepper.cpp:182-193): per fluid node rho and
+    u = (sum f c) / rho + g / 2 (moments, p/src/collision.cpp:24-36); host-side
+    diagnostic over the extracted snapshot. Raises ArithmeticError on vacuum."""
+    from .geometry import C_VECTORS
+    f = stepper.extract_natural().reshape(-1, Q)
+    rho = np.zeros(f.shape[0])
+    m = np.zeros((f.shape[0], 3))
+    for i in range(Q):
+        rho = rho + f[:, i]
+        for k in range(3):
+            m[:, k] = m[:, k] + f[:, i] * C_VECTORS[i][k]
+    if not np.all(rho > 0.0):
+        raise ArithmeticError("vacuum node")
+    u = m / rho[:, None] + 0.5 * np.asarray(flow.body_force)[None, :]
+    return rho, u
 
 
 def kernel_available(scheme, addressing, extensions: bool = False) -> bool:

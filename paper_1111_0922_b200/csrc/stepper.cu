@@ -8,7 +8,9 @@
 
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdlib>
+#include <random>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -1406,6 +1408,34 @@ static void build_idx(const lbmgpu_geometry* gg, int device, bool want_node_of, 
   CK(cudaStreamSynchronize(st));
 }
 
+
+// ---------------------------------------------------------------------------
+// Harness (p/src/bench.cpp): run_bench and verify_suite on the GPU.
+// ---------------------------------------------------------------------------
+// make_seeded_geometry (p/src/bench.cpp:259-273): 16x8x8, periodic x/z, wall y
+static HostGeo seeded_geometry(uint64_t seed) {
+  HostGeo g;
+  g.nx = 16, g.ny = 8, g.nz = 8;
+  g.policy[0] = 0, g.policy[1] = 1, g.policy[2] = 0;
+  g.mask.assign(g.cells(), 1);
+  std::mt19937_64 rng(seed);
+  for (int z = 0; z < g.nz; ++z)
+    for (int y = 1; y < g.ny - 1; ++y)
+      for (int x = 0; x < g.nx; ++x)
+        if (rng() % 100 < 12) g.mask[g.idx(x, y, z)] = 0;
+  g.solids = std::find(g.mask.begin(), g.mask.end(), 0) != g.mask.end();
+  if (!g.solids) g.mask.clear();
+  return g;
+}
+
+static lbmgpu_geometry c_geo(const HostGeo& g) {
+  lbmgpu_geometry c{};
+  c.nx = g.nx, c.ny = g.ny, c.nz = g.nz;
+  for (int k = 0; k < 3; ++k) c.axis_policy[k] = g.policy[k];
+  c.mask = g.mask.empty() ? nullptr : g.mask.data();
+  return c;
+}
+
 }  // namespace lbmgpu
 
 // ===========================================================================
@@ -1444,6 +1474,10 @@ int guard(F&& f) {
     g_err = e.what();
     return LBMGPU_RUNTIME_ERROR;
   }
+}
+
+void check_ok(int rc) {
+  if (rc != LBMGPU_OK) throw std::runtime_error(g_err);
 }
 
 Stepper& S(lbmgpu_stepper* h) {
@@ -1660,6 +1694,133 @@ int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n) {
     for (int k = 0; k < n; ++k) S.push_back(&slab(hs[k]));
     local_phase(S, 0);
     for (auto* s : S) s->ghosts_fresh_ = true;
+  });
+}
+
+int lbmgpu_run_bench(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgpu_options* o,
+                     int32_t steps, int32_t warmup, int32_t timed_runs, double hbm_gbs,
+                     lbmgpu_bench_result* r) {
+  return guard([&] {
+    if (steps < 1) throw std::invalid_argument("steps must be at least 1");
+    if (!r) throw std::invalid_argument("null result");
+    auto st = create(g, p, o);
+    st->init(st->base_init(kSrcRest));
+    st->step(warmup);
+    st->sync();
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    std::vector<double> times;
+    for (int k = 0; k < std::max(1, timed_runs); ++k) {
+      CK(cudaEventRecord(e0, st->stream_));
+      st->step(steps);
+      CK(cudaEventRecord(e1, st->stream_));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      times.push_back(ms * 1e-3);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::sort(times.begin(), times.end());
+    const size_t n = times.size();
+    const double sec = n % 2 ? times[n / 2] : 0.5 * (times[n / 2 - 1] + times[n / 2]);
+    std::memset(r, 0, sizeof(*r));
+    r->scheme = o->scheme, r->addressing = o->addressing, r->layout = o->layout;
+    r->precision = o->precision;
+    r->fluid_count = st->nodes_;
+    r->steps = steps;
+    r->seconds = sec;
+    r->mlups = (double)st->nodes_ * steps / sec / 1.0e6;  // p/src/bench.cpp:184
+    static const int fam[10] = {0, 1, 1, 2, 2, 3, 4, 4, 5, 6};
+    int32_t cnt[6];
+    double bpl = 0, gbpl = 0;
+    check_ok(lbmgpu_traffic(fam[o->scheme], o->addressing, o->precision, cnt, &bpl));
+    check_ok(lbmgpu_gpu_bytes_per_lup(o->scheme, o->addressing, o->precision, &gbpl));
+    r->bytes_per_lup = bpl;
+    r->gpu_bytes_per_lup = gbpl;
+    r->predicted_mlups = hbm_gbs > 0 ? hbm_gbs * 1e9 / gbpl / 1e6 : 0;
+    r->model_fraction = r->predicted_mlups > 0 ? r->mlups / r->predicted_mlups : 0;
+    r->achieved_gbs = r->mlups * 1e6 * gbpl / 1e9;
+  });
+}
+
+// verify_suite (p/src/bench.cpp:275-341) on the GPU: every implemented pair
+// (optionally also AoS and fp32) against the GPU two-step reference on the
+// seeded geometry, compared after every step; fp64 must be bitwise (1e-13
+// relative is the reference's recorded fallback), fp32 within 1e-5.
+int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t all_variants,
+                        lbmgpu_verify_entry* entries, int32_t capacity, int32_t* count,
+                        int32_t* all_pass) {
+  return guard([&] {
+    const HostGeo hg = seeded_geometry(seed);
+    const lbmgpu_geometry g = c_geo(hg);
+    lbmgpu_flow p{};
+    p.lambda_even = 1.0 / 0.9;
+    p.lambda_odd = lbmgpu_lambda_odd(p.lambda_even, 3.0 / 16.0);
+    p.body_force[0] = 1e-5;
+    p.rho0 = 1.0;
+    lbmgpu_options o;
+    lbmgpu_default_options(&o);
+    o.device = device;
+    o.scheme = LBMGPU_TS;
+    auto ref = create(&g, &p, &o);
+    const uint64_t nodes = ref->nodes_;
+    const size_t nv = nodes * 19;
+    std::vector<double> f0(nv), want(nv), got(nv);
+    std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ull);
+    for (uint64_t n = 0; n < nodes; ++n)
+      for (int i = 0; i < 19; ++i) {
+        const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+        f0[n * 19 + i] = w_of(i) * p.rho0 * (0.9 + 0.2 * u);
+      }
+    ref->load(f0.data(), false);
+    struct Probe {
+      lbmgpu_verify_entry e;
+      std::unique_ptr<Stepper> st;
+    };
+    std::vector<Probe> probes;
+    for (int sc = 0; sc < 10; ++sc)
+      for (int ad = 0; ad < 2; ++ad)
+        for (int lay = 0; lay < (all_variants ? 2 : 1); ++lay)
+          for (int pr : {8, 4}) {
+            if (pr == 4 && !all_variants) continue;
+            if (!available(sc, ad, false)) continue;
+            if (sc == LBMGPU_TS && ad == 0 && lay == 0 && pr == 8) continue;  // the reference
+            lbmgpu_options q = o;
+            q.scheme = sc, q.addressing = ad, q.layout = lay, q.precision = pr;
+            Probe pb{};
+            pb.e.scheme = sc, pb.e.addressing = ad, pb.e.layout = lay, pb.e.precision = pr;
+            pb.e.bitwise = 1, pb.e.pass = 1;
+            pb.st = create(&g, &p, &q);
+            pb.st->load(f0.data(), false);
+            probes.push_back(std::move(pb));
+          }
+    for (int k = 0; k < steps; ++k) {
+      ref->step(1);
+      ref->extract(want.data(), false);
+      for (Probe& pb : probes) {
+        pb.st->step(1);
+        pb.st->extract(got.data(), false);
+        if (std::memcmp(want.data(), got.data(), nv * sizeof(double)) == 0) continue;
+        pb.e.bitwise = 0;
+        for (size_t v = 0; v < nv; ++v) {
+          const double d = std::fabs(got[v] - want[v]) / std::max(std::fabs(want[v]), 1e-300);
+          pb.e.max_rel_linf = std::max(pb.e.max_rel_linf, d);
+        }
+      }
+    }
+    int ap = 1;
+    int n = 0;
+    for (Probe& pb : probes) {
+      const double tol = pb.e.precision == 8 ? 1e-13 : 1e-5;
+      pb.e.pass = pb.e.bitwise || pb.e.max_rel_linf <= tol;
+      ap &= pb.e.pass;
+      if (entries && n < capacity) entries[n] = pb.e;
+      ++n;
+    }
+    if (count) *count = n;
+    if (all_pass) *all_pass = ap;
   });
 }
 

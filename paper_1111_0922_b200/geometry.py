@@ -10,10 +10,60 @@
 from __future__ import annotations
 
 import math
+import struct
 
 import numpy as np
 
 from . import GridGeometry
+
+# D3Q19 lattice vectors in canonical order (p/src/stencil.cpp:18-57)
+C_VECTORS = ((0, 0, 0), (1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1),
+             (-1, -1, 0), (-1, 0, -1), (-1, 0, 1), (-1, 1, 0), (0, -1, -1), (0, -1, 1),
+             (0, 1, -1), (0, 1, 1), (1, -1, 0), (1, 0, -1), (1, 0, 1), (1, 1, 0))
+
+_MAGIC = b"LBMGEO1\0"
+
+
+def save_geo(g: GridGeometry, path: str) -> None:
+    """save_geo (p/src/geometry.cpp:123-135): 8-byte magic, u32 nx/ny/nz
+    little-endian, 3 axis-policy bytes, nx*ny*nz mask bytes (x-fastest)."""
+    mask = np.ones(g.cells(), np.uint8) if g.mask is None else np.asarray(g.mask, np.uint8)
+    pol = [{"periodic": 0, "wall": 1, 0: 0, 1: 1}[p] for p in g.axis_policy]
+    try:
+        fh = open(path, "wb")
+    except OSError:
+        raise RuntimeError(f"cannot open {path}")
+    with fh:
+        fh.write(_MAGIC + struct.pack("<III", g.nx, g.ny, g.nz) + bytes(pol) + mask.tobytes())
+
+
+def load_geo(path: str) -> GridGeometry:
+    """load_geo (p/src/geometry.cpp:137-171), same checks and messages."""
+    try:
+        fh = open(path, "rb")
+    except OSError:
+        raise RuntimeError(f"cannot open {path}")
+    with fh:
+        magic = fh.read(8)
+        if len(magic) != 8 or magic != _MAGIC:
+            raise RuntimeError("not a geometry file")
+        dims = fh.read(12)
+        if len(dims) != 12:
+            raise RuntimeError("short read")
+        nx, ny, nz = struct.unpack("<III", dims)
+        if (nx == 0 or ny == 0 or nz == 0 or max(nx, ny, nz) > 0x7FFFFFFF
+                or nx * ny * nz > (1 << 40)):
+            raise RuntimeError("dimension overflow")
+        pol = fh.read(3)
+        if len(pol) != 3:
+            raise RuntimeError("short read")
+        if any(p > 1 for p in pol):
+            raise RuntimeError("not a geometry file")
+        mask = np.frombuffer(fh.read(nx * ny * nz), np.uint8)
+        if mask.size != nx * ny * nz:
+            raise RuntimeError("short read")
+    policy = tuple("wall" if p else "periodic" for p in pol)
+    return GridGeometry(nx, ny, nz, policy, (mask != 0).astype(np.uint8))
 
 
 def gen_random_spheres(nx: int, ny: int, nz: int, radius: float = 8.0, porosity: float = 0.40,

@@ -145,12 +145,18 @@ def main():
     col["verify_max_rel"] = mr
     np.savez_compressed(os.path.join(HERE, "collision_traffic.npz"), **col)
 
+    # LBMGEO1 file written by the reference's save_geo (p/src/geometry.cpp:123-135)
+    dims, pol, mask = R.make_seeded_geometry(42)
+    R.save_geo(dims, pol, mask, os.path.join(HERE, "seeded42.lbmgeo"))
+
     with open(os.path.join(HERE, "SHA256SUMS"), "w") as fh:
         for name in sorted(os.listdir(HERE)):
             if name.endswith(".npz"):
                 with np.load(os.path.join(HERE, name)) as z:
                     for k in sorted(z.files):
                         fh.write(f"{name}:{k} {sha(z[k])}\n")
+        with open(os.path.join(HERE, "seeded42.lbmgeo"), "rb") as g:
+            fh.write(f"seeded42.lbmgeo:bytes {hashlib.sha256(g.read()).hexdigest()}\n")
     print("golden fixtures written to", HERE)
 
 
