@@ -211,7 +211,7 @@ def run_ours(args):
     import paper_1111_0922_b200 as L
     if L.device_count() < 1:
         raise SystemExit("no CUDA device visible")
-    if ws > 1:
+    if ws > 1 or args.slabs:
         return run_slabs(args, ws, rank, local, dist, L)
 
     cfg = CONFIGS[args.config]
@@ -316,7 +316,8 @@ def run_slabs(args, ws, rank, local, dist, L):
     st = L.create_stepper("aap", "direct", geo, flow,
                           L.StepperOptions(device=local, z_begin=z0, z_end=z1))
     uid = [L.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
+    if dist is not None:
+        dist.broadcast_object_list(uid, src=0)
     st.slab_connect_nccl(uid[0], ws, rank)
     st.init_field(cfg["init"], seed=2011)
     nodes_local = st.node_count()
@@ -370,11 +371,13 @@ def main():
     ap.add_argument("--precision", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="run the z-slab/NCCL path even at N=1 (one rank, ring to itself)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.config is None:
-        args.config = "c1" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c3"
+        args.config = "c1" if int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.slabs else "c3"
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

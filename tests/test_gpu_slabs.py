@@ -73,3 +73,26 @@ def test_slab_errors(gpu):
     s = L.create_stepper("aap", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(RuntimeError, match="no transport"):
         s.step()
+
+
+def test_nccl_transport_single_rank_ring(gpu):
+    """The NCCL transport itself (liblbmgpu.so dlopens libnccl): one rank whose
+    ring neighbours are itself, the overlapped interior/boundary schedule, the
+    phase-0/phase-1 groups — bitwise equal to the periodic single domain."""
+    L = gpu
+    dims = (32, 24, 20)
+    flow = L.bgk(1.0)
+    ref = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow)
+    ref.init_field("taylor_green", seed=9, u0=0.05)
+    s = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow,
+                         L.StepperOptions(z_begin=0, z_end=dims[2]))
+    s.slab_connect_nccl(L.nccl_unique_id(), 1, 0)
+    s.init_field("taylor_green", seed=9, u0=0.05)
+    for steps in (6, 3):
+        ref.step_n(steps)
+        ref.synchronize()
+        s.step_n(steps)
+        s.synchronize()
+        if s.time_step() % 2:
+            s.slab_sync_ghosts()
+        assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
