@@ -250,14 +250,6 @@ __global__ void k_swap_list(Fld<T, AOS> F, const long long* a, const long long* 
   *pb = va;
 }
 
-template <class T, bool AOS>
-__global__ void k_cg_fixup(Fld<T, AOS> F, const long long* src, const long long* dst,
-                           const int8_t* dir, long long count, long long shift) {
-  const long long k = (long long)blockIdx.x * kBlock + threadIdx.x;
-  if (k >= count) return;
-  const int i = dir[k];
-  *F.at(i, (uint32_t)(dst[k] - shift)) = *F.at(i, (uint32_t)(src[k] - shift));
-}
 
 
 // ---------------------------------------------------------------------------
@@ -378,130 +370,69 @@ inline bool aos_contiguous(const DField& f, const dev::Lat& L, uint32_t* soff) {
 
 
 // ---------------------------------------------------------------------------
-// Ticketed tiles (used by the compressed-grid sweep): blocks take tickets in
-// the reference traversal order, publish per-tile progress with st.release,
-// and wait with ld.acquire only on tiles holding earlier tickets, so the
-// waits cannot deadlock. Loads of data another SM rewrote during the sweep
-// use ld.global.cg (L2) so they are never served from a stale L1 line.
-template <class T>
-__device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
-
-__device__ __forceinline__ uint32_t take_ticket(unsigned long long* ticket, unsigned epoch,
-                                                uint32_t ntiles, bool reverse) {
-  __shared__ uint32_t s_tile;
-  if (threadIdx.x == 0) {
-    const unsigned long long k =
-        atomicAdd(ticket, 1ull) - (unsigned long long)(epoch - 1) * ntiles;
-    s_tile = reverse ? ntiles - 1 - (uint32_t)k : (uint32_t)k;
-  }
-  __syncthreads();
-  return s_tile;
+// Compressed grid (p/src/scheme_cg.cpp:118-158) as plane-group push
+// launches. The reference shifts the write origin by (1,1,1) cells from the
+// read origin and relies on a sequential traversal; here the shift is S whole
+// z-planes and a launch covers P < S planes, so no write of a launch lands in
+// a slot a node of the same launch still has to read (the readers of every
+// written slot lie in earlier launches) and each launch is a plain push
+// sweep. x/y links wrap directly; z-seam values land in a padding plane and
+// are copied to their wrapped plane after the sweep (the reference's fix-up).
+template <bool BB, class T, bool AOS>
+__device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c, const Trt<T>& op,
+                                             int delta) {
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
+  collide(op, f);
+  const uint32_t w = c.s + (uint32_t)delta;
+  st<false>(F.at(0, w), f[0]);
+#pragma unroll
+  for (int i = 1; i < 19; ++i)
+    st<false>((BB && c.bb(i)) ? F.at(opp(i), w) : F.at_off(i, w, c.off(i)), f[i]);
 }
-__device__ __forceinline__ void publish_tile(unsigned* flags, uint32_t tile, unsigned epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(epoch) : "memory");
-  }
-}
-// Compressed grid, lagged pipeline (p/src/scheme_cg.cpp:118-158). Ticket tau
-// (reference traversal order: reverse lex for even sweeps, forward for odd)
-// runs phase A on its tile — read the 19 slots at the read origin, collide,
-// park the result in an L2-resident ring slot, publish "read" — and phase B on
-// the tile lag tickets behind: wait until every tile whose read slots it
-// overwrites has published "read" (X + (1,1,1) + c_i even / X - (1,1,1) + c_i
-// odd, all earlier tickets), then write the parked values at the write origin
-// and publish "ring slot free". The only hazards in a CG sweep are
-// write-after-read (every slot is read before it is overwritten), so these
-// waits reproduce the sequential result bit for bit.
-template <class T, bool AOS, bool EVEN>
+template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
-    k_cg_lag(Fld<T, AOS> F, Lat L, Trt<T> op, unsigned long long* ticket, unsigned* flagsA,
-             unsigned* flagsB, unsigned epoch, uint32_t ntiles, uint32_t lag, T* ring,
-             uint32_t R) {
-  const uint32_t tau = take_ticket(ticket, epoch, ntiles + lag, false);
-  // ---- phase A ----
-  if (tau < ntiles) {
-    const uint32_t a = EVEN ? ntiles - 1 - tau : tau;
-    if (tau >= R) {  // the ring slot's previous tile must have been written out
-      if (threadIdx.x == 0) {
-        const uint32_t prev = EVEN ? ntiles - 1 - (tau - R) : tau - R;
-        unsigned v;
-        while (true) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flagsB + prev) : "memory");
-          if (v == epoch) break;
-          __nanosleep(32);
-        }
-      }
-      __syncthreads();
-    }
-    const uint32_t cell = a * kBlock + threadIdx.x;
-    T* slot = ring + (size_t)(tau % R) * 19 * kBlock + threadIdx.x;
-    if (cell < L.ncells) {
-      const Ctx c = make_ctx(L, cell);  // L.o* = read origin (1 even, 2 odd)
-      if (c.fluid) {
-        T f[19];
-#pragma unroll
-        for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
-        collide(op, f);
-#pragma unroll
-        for (int i = 0; i < 19; ++i) slot[i * kBlock] = f[i];
-      }
-    }
-    publish_tile(flagsA, a, epoch);
-  }
-  // ---- phase B ----
-  if (tau >= lag) {
-    const uint32_t ub = tau - lag;
-    const uint32_t b = EVEN ? ntiles - 1 - ub : ub;
-    if (threadIdx.x < 38) {
-      const int d = threadIdx.x >> 1;
-      const int sgn = EVEN ? 1 : -1;
-      const long long D = (long long)(sgn + cx(d)) + (long long)L.nx * (sgn + cy(d)) +
-                          (long long)L.nx * L.ny * (sgn + cz(d));
-      const long long tgt = (long long)b * kBlock + D + ((threadIdx.x & 1) ? kBlock - 1 : 0);
-      if (tgt >= 0 && tgt < (long long)L.ncells) {
-        const unsigned* fl = flagsA + (uint32_t)(tgt / kBlock);
-        unsigned v;
-        while (true) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
-          if (v == epoch) break;
-          __nanosleep(32);
-        }
-      }
-    } else if (threadIdx.x == 38) {  // the tile's own phase A (ring contents)
-      unsigned v;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flagsA + b) : "memory");
-        if (v == epoch) break;
-        __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    const uint32_t cell = b * kBlock + threadIdx.x;
-    const T* slot = ring + (size_t)(ub % R) * 19 * kBlock + threadIdx.x;
-    if (cell < L.ncells) {
-      const Ctx c = make_ctx(L, cell);
-      if (c.fluid) {
-        T f[19];
-#pragma unroll
-        for (int i = 0; i < 19; ++i) f[i] = __ldcg(slot + i * kBlock);
-        const uint32_t sh = 1u + (uint32_t)L.sx + (uint32_t)L.sxy;  // shift1
-        const uint32_t wr = EVEN ? c.s + sh : c.s - sh;
-        st<false>(F.at(0, wr), f[0]);
-#pragma unroll
-        for (int i = 1; i < 19; ++i) {
-          const int po = cx(i) + L.sx * cy(i) + (int)L.sxy * cz(i);
-          T* dst = c.bb(i) ? F.at(opp(i), wr) : F.at(i, wr + (uint32_t)po);
-          st<false>(dst, f[i]);
-        }
-      }
-    }
-    publish_tile(flagsB, b, epoch);
-  }
+    k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    cg_push_body<false>(F, c, op, delta);
+  else
+    cg_push_body<true>(F, c, op, delta);
 }
 
-
+// z-seam fix-up: copy the 5 slot planes of one padding plane to the wrapped
+// plane, for the links that were actually written there — i.e. whose writer
+// (the node one link back, on plane writer_z) is fluid and did not bounce
+template <class T, bool AOS>
+__global__ void k_plane_copy(Fld<T, AOS> F, Lat L, int8_t d0, int8_t d1, int8_t d2, int8_t d3,
+                             int8_t d4, uint32_t src, uint32_t dst, int writer_z) {
+  const uint32_t plane = (uint32_t)L.nx * L.ny;
+  const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= plane) return;
+  const int x = (int)(k % L.nx), y = (int)(k / L.nx);
+  const int8_t d[5] = {d0, d1, d2, d3, d4};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    int xw = x - cx(d[q]), yw = y - cy(d[q]);
+    if (xw < 0 || xw >= L.nx) {
+      if (L.wall[0]) continue;
+      xw = xw < 0 ? xw + L.nx : xw - L.nx;
+    }
+    if (yw < 0 || yw >= L.ny) {
+      if (L.wall[1]) continue;
+      yw = yw < 0 ? yw + L.ny : yw - L.ny;
+    }
+    if (L.linkmask) {
+      const uint32_t lm = L.linkmask[(uint32_t)xw + (uint32_t)L.nx * ((uint32_t)yw + (uint32_t)L.ny * writer_z)];
+      if (!(lm & 1u) || ((lm >> d[q]) & 1u)) continue;
+    }
+    *F.at(d[q], dst + k) = *F.at(d[q], src + k);
+  }
+}
 
 }  // namespace
 
@@ -616,43 +547,11 @@ void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) 
   LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
 }
 
-uint32_t cg_lag(const dev::Lat& L) {
-  const uint64_t reach = (2ull * L.nx * L.ny + 2ull * L.nx + 2 + kBlock - 1) / kBlock + 2;
-  return (uint32_t)(reach + 148 * 2);
-}
-
-void launch_cg_lag(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-                   bool even, unsigned long long* ticket, unsigned* flagsA, unsigned* flagsB,
-                   unsigned epoch, void* ring, uint32_t R) {
-  if (L.ncells <= L.cell_begin) return;
-  const uint32_t ntiles = grid_for(L.ncells);
-  const uint32_t lag = cg_lag(L);
-  LBM_DISPATCH(f, {
-    if (even)
-      k_cg_lag<T, A, true><<<ntiles + lag, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), ticket,
-                                                            flagsA, flagsB, epoch, ntiles, lag,
-                                                            static_cast<T*>(ring), R);
-    else
-      k_cg_lag<T, A, false><<<ntiles + lag, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op),
-                                                             ticket, flagsA, flagsB, epoch, ntiles,
-                                                             lag, static_cast<T*>(ring), R);
-  });
-}
-
 void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
                       const int8_t* dir, long long count) {
   if (count <= 0) return;
   LBM_DISPATCH(f, {
     k_swap_list<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), a, b, dir, count);
-  });
-}
-
-void launch_cg_fixup(cudaStream_t st, const DField& f, const long long* src,
-                     const long long* dst, const int8_t* dir, long long count, long long shift) {
-  if (count <= 0) return;
-  LBM_DISPATCH(f, {
-    k_cg_fixup<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), src, dst, dir, count,
-                                                         shift);
   });
 }
 

@@ -66,14 +66,12 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
 void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode);
 void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
                       const int8_t* dir, long long count);
-// CG lagged pipeline: ring of R tiles (R * 19 * 256 elements), R > cg_lag(L)
-uint32_t cg_lag(const dev::Lat& L);
-void launch_cg_lag(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-                   bool even, unsigned long long* ticket, unsigned* flagsA, unsigned* flagsB,
-                   unsigned epoch, void* ring, uint32_t R);
-void launch_cg_fixup(cudaStream_t st, const DField& f, const long long* src,
-                     const long long* dst, const int8_t* dir, long long count, long long shift);
-
+// CG as a plane-group push launch: read at the cell's storage index, write at
+// + delta (the other origin); copy of 5 slot planes src -> dst (seam fix-up)
+void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                    int delta);
+void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, const int* dirs,
+                       uint32_t src, uint32_t dst, int writer_z);
 // ---- indirect (IDX) addressing ---------------------------------------------
 struct Idx {
   const uint32_t* adj;  // transposed [18][n]: adj[(i-1)*n + node]

@@ -584,86 +584,72 @@ static std::vector<SeamLink> seam_links(const HostGeo& g, const int* dirs, int n
   return out;
 }
 
-// CG (p/src/scheme_cg.cpp): one grid padded by 3 per axis; sweeps alternate
-// read origin +1 / +2 (shift1 = 1 + px + px*py)
+// CG (p/src/scheme_cg.cpp): one grid, two origins S planes apart, sweeps
+// alternate the read origin (even: read S, write 0, ascending plane groups;
+// odd: read 0, write S, descending), each plane group of P < S planes one
+// push launch; z-periodic seam values land in padding planes and are copied
+// to their wrapped planes after the sweep. Storage: nz + S + 2 planes
+// (planes 0 and nz+S+1 pad; origin o's plane z at storage z + 1 + o).
 class CgDirect final : public DirectStepper {
  public:
   CgDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
       : DirectStepper(g, p, o) {
-    px_ = g.nx + 3, py_ = g.ny + 3, pz_ = g.nz + 3;
-    padded_ = (uint64_t)px_ * py_ * pz_;
-    if (padded_ >= (uint64_t{1} << 32)) throw std::runtime_error("grid exceeds 32-bit cell index range");
-    L1_ = make_lat(geo_, linkmask(), 0, 0, 0, 0);
-    L1_.sx = px_, L1_.sy = py_, L1_.sxy = (long long)px_ * py_;
-    L2_ = L1_;
-    L1_.ox = L1_.oy = L1_.oz = 1;
-    L2_.ox = L2_.oy = L2_.oz = 2;
-    shift1_ = 1 + (long long)px_ + (long long)px_ * py_;
-    alloc_field(f_, padded_);
-    static const int all[18] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18};
-    const auto links = seam_links(geo_, all, 18);
-    nfix_ = (long long)links.size();
-    if (nfix_) {
-      std::vector<long long> src(nfix_), dst(nfix_);
-      std::vector<int8_t> dir(nfix_);
-      for (long long k = 0; k < nfix_; ++k) {
-        const SeamLink& s = links[k];
-        src[k] = pidx(s.tx + 2, s.ty + 2, s.tz + 2);
-        dst[k] = pidx(s.lx + 2, s.ly + 2, s.lz + 2);
-        dir[k] = (int8_t)s.dir;
-      }
-      fsrc_.alloc(nfix_ * 8), fdst_.alloc(nfix_ * 8), fdir_.alloc(nfix_);
-      CK(cudaMemcpyAsync(fsrc_.get(), src.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
-      CK(cudaMemcpyAsync(fdst_.get(), dst.data(), nfix_ * 8, cudaMemcpyHostToDevice, stream_));
-      CK(cudaMemcpyAsync(fdir_.get(), dir.data(), nfix_, cudaMemcpyHostToDevice, stream_));
-    }
-    const uint64_t ntiles = (geo_.cells() + kBlock - 1) / kBlock;
-    flags_.alloc(ntiles * sizeof(unsigned));
-    flagsB_.alloc(ntiles * sizeof(unsigned));
-    ticket_.alloc(sizeof(unsigned long long));
-    CK(cudaMemsetAsync(flags_.get(), 0, flags_.bytes(), stream_));
-    CK(cudaMemsetAsync(flagsB_.get(), 0, flagsB_.bytes(), stream_));
-    CK(cudaMemsetAsync(ticket_.get(), 0, ticket_.bytes(), stream_));
-    ring_tiles_ = cg_lag(L1_) + 512;
-    ring_.alloc((size_t)ring_tiles_ * 19 * kBlock * esize());
+    P_ = std::min(16, g.nz);
+    S_ = P_ + 1;
+    plane_ = (uint64_t)g.nx * g.ny;
+    storage_ = plane_ * (uint64_t)(g.nz + S_ + 2);
+    if (storage_ >= (uint64_t{1} << 32))
+      throw std::runtime_error("grid exceeds 32-bit cell index range");
+    alloc_field(f_, storage_);
     init(base_init(kSrcRest));
     sync();
   }
-  void step_one() override {
-    const DField f = field(f_, soa_stride(padded_));
-    const bool even = (t_ & 1) == 0;
-    ++epoch_;
-    launch_cg_lag(stream_, f, even ? L1_ : L2_, op_, even, ticket_.get<unsigned long long>(),
-                  flags_.get<unsigned>(), flagsB_.get<unsigned>(), epoch_, ring_.get(),
-                  ring_tiles_);
-    launch_cg_fixup(stream_, f, fsrc_.get<long long>(), fdst_.get<long long>(),
-                    fdir_.get<int8_t>(), nfix_, even ? 0 : shift1_);
+  dev::Lat frame(int origin) const {
+    dev::Lat L = L_;
+    L.oz = 1 + origin;
+    L.znowrap = 1;
+    return L;
   }
-  int launches_per_step() const override { return nfix_ ? 2 : 1; }
+  void step_one() override {
+    const DField f = field(f_, soa_stride(storage_));
+    const bool even = (t_ & 1) == 0;
+    const int R = even ? S_ : 0, W = even ? 0 : S_;
+    const int delta = (W - R) * (int)plane_;
+    const dev::Lat Lr = frame(R);
+    const int ngroups = (geo_.nz + P_ - 1) / P_;
+    for (int k = 0; k < ngroups; ++k) {
+      const int gi = even ? k : ngroups - 1 - k;
+      dev::Lat L = Lr;
+      L.cell_begin = (uint32_t)(gi * P_ * plane_);
+      L.ncells = (uint32_t)(std::min(geo_.nz, (gi + 1) * P_) * plane_);
+      launch_cg_push(stream_, f, L, op_, delta);
+    }
+    if (geo_.policy[2] == 0) {  // z-periodic seam fix-up
+      static const int zm[5] = {6, 8, 11, 13, 16}, zp[5] = {5, 9, 12, 14, 17};
+      const uint32_t pl = (uint32_t)plane_;
+      launch_plane_copy(stream_, f, L_, zm, (uint32_t)W * pl, (uint32_t)(geo_.nz + W) * pl, 0);
+      launch_plane_copy(stream_, f, L_, zp, (uint32_t)(geo_.nz + 1 + W) * pl,
+                        (uint32_t)(1 + W) * pl, geo_.nz - 1);
+    }
+  }
+  int launches_per_step() const override {
+    return (geo_.nz + P_ - 1) / P_ + (geo_.policy[2] == 0 ? 2 : 0);
+  }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
-    ex(field(f_, soa_stride(padded_)), (t_ & 1) ? L2_ : L1_, kExNatural, n0, c, d);
+    ex(field(f_, soa_stride(storage_)), frame((t_ & 1) ? 0 : S_), kExNatural, n0, c, d);
   }
   void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
-    ld(field(f_, soa_stride(padded_)), L1_, kExNatural, n0, c, d, in);
+    ld(field(f_, soa_stride(storage_)), frame(S_), kExNatural, n0, c, d, in);
   }
   int layout_phase() const override {
     return (t_ & 1) ? LBMGPU_SHIFTED_EVEN : LBMGPU_SHIFTED_ODD;
   }
   uint64_t pdf_bytes() const override { return f_.bytes(); }
-  uint64_t idx_bytes() const override { return flags_.bytes() + flagsB_.bytes() + ring_.bytes(); }
 
  private:
-  long long pidx(int x, int y, int z) const {
-    return ((long long)z * py_ + y) * px_ + x;
-  }
-  int px_, py_, pz_;
-  uint64_t padded_;
-  long long shift1_;
-  long long nfix_ = 0;
-  unsigned epoch_ = 0;
-  dev::Lat L1_, L2_;
-  uint32_t ring_tiles_ = 0;
-  DevMem f_, fsrc_, fdst_, fdir_, flags_, flagsB_, ticket_, ring_;
+  int P_, S_;
+  uint64_t plane_, storage_;
+  DevMem f_;
 };
 
 // SWAP push/pull (p/src/scheme_swap.cpp): collide pass + link-exchange pass
