@@ -78,7 +78,7 @@ def main():
     elif args.config == "c1":
         geo = L.GridGeometry(256, 256, 256, ("periodic", "periodic", "wall"))
         flow, init = L.bgk(1.7, (1e-6, 0, 0)), "rest"
-        pairs = [("aap", "direct"), ("et", "direct"), ("os-pull", "direct"), ("os-push", "direct")]
+        pairs = [(s, "direct") for s in SCHEMES]
     else:
         geo = gen_random_spheres(256, 256, 256, 8.0, 0.40, seed=2011)
         flow, init = L.bgk(1.7, (1e-6, 0, 0)), "rest"
