@@ -547,6 +547,25 @@ void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) 
   LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
 }
 
+void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                    int delta) {
+  if (L.ncells <= L.cell_begin) return;
+  LBM_DISPATCH(f, {
+    k_cg_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L,
+                                                                          cast_op<T>(op), delta);
+  });
+}
+
+void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, const int* dirs,
+                       uint32_t src, uint32_t dst, int writer_z) {
+  const uint32_t plane = (uint32_t)L.nx * L.ny;
+  LBM_DISPATCH(f, {
+    k_plane_copy<T, A><<<grid_for(plane), kBlock, 0, st>>>(
+        fld<T, A>(f), L, (int8_t)dirs[0], (int8_t)dirs[1], (int8_t)dirs[2], (int8_t)dirs[3],
+        (int8_t)dirs[4], src, dst, writer_z);
+  });
+}
+
 void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
                       const int8_t* dir, long long count) {
   if (count <= 0) return;
