@@ -19,7 +19,8 @@ def _declared():
 def test_library_exports_every_declared_symbol(lbm):
     names = _declared()
     assert len(names) >= 30
-    lib = ctypes.CDLL(lbm.LIBRARY_PATH)
+    # RTLD_NOW: every symbol the library references must resolve at load time
+    lib = ctypes.CDLL(lbm.LIBRARY_PATH, mode=os.RTLD_NOW | os.RTLD_LOCAL)
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
 
