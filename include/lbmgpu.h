@@ -214,7 +214,7 @@ int lbmgpu_gpu_bytes_per_lup(int32_t scheme, int32_t addressing, int32_t pdf_byt
 /* lambda_odd (p/src/collision.cpp:8-11) */
 double lbmgpu_lambda_odd(double lambda_even, double magic_lambda);
 
-/* ---- multi-GPU z-slabs (AA pattern, direct, SoA; options.z_begin/z_end) ----
+/* ---- multi-GPU z-slabs (AA, OS push/pull, OSNT; direct, SoA; options.z_begin/z_end) ----
  * A slab stepper owns global planes [z_begin, z_end) of the geometry's box
  * (periodic z). Its canonical snapshot is that contiguous range of the global
  * one. Exchanges follow one plan: phase 0 (before each odd sweep) copies the
@@ -222,6 +222,10 @@ double lbmgpu_lambda_odd(double lambda_even, double magic_lambda);
  * copies them back; ops[k*5 + {phase, send, peer(-1 lower/+1 upper), plane
  * (-1 lower ghost .. nzl upper ghost), slot}], posted in this order. */
 int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count);
+/* the plan of any decomposable scheme: AA (phases around odd sweeps), OS/OSNT
+ * pull (phase 0 before every sweep, on the active grid), OS push (phase 1
+ * after every sweep, on the grid just written) */
+int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* count);
 #define LBMGPU_NCCL_ID_BYTES 128
 int lbmgpu_nccl_unique_id(uint8_t* id);
 /* one rank per GPU: ring over ranks, rank r owns the r-th slab; collective */

@@ -1,5 +1,6 @@
-"""TEST INFRASTRUCTURE ONLY — a numpy restatement of the AA pattern on one
-z-slab with ghost planes, used to check the multi-GPU halo plan on CPU.
+"""TEST INFRASTRUCTURE ONLY — numpy restatements of the AA pattern and the
+one-step push/pull scheme on one z-slab with ghost planes, used to check the
+multi-GPU halo plans on CPU.
 
 Vectorised over cells with the reference's exact operation order (numpy
 float64 ufuncs round like the -ffp-contract=off C code), so it is bitwise equal
@@ -131,4 +132,68 @@ class AaSlab:
                 cx, cy, cz = C[i]
                 rolled = np.roll(self.F[OPP[i]], (cy, cx), axis=(1, 2))
                 out[..., i] = rolled[1 - cz:n + 1 - cz]
+        return out.ravel()
+
+
+class OsSlab:
+    """One-step two-grid scheme on a slab (p/src/scheme_os.cpp): pull gathers
+    A[i][X - c_i] (after a first precollide, :79-102, 141-174), push scatters
+    to B[i][X + c_i] (:104-139); x/y periodic, z through ghost planes."""
+
+    def __init__(self, nx, ny, nzl, op, pull):
+        self.nx, self.ny, self.nzl, self.op, self.pull = nx, ny, nzl, op, pull
+        self.G = [np.zeros((19, nzl + 2, ny, nx)), np.zeros((19, nzl + 2, ny, nx))]
+        self.active = 0
+        self.fresh = pull
+        self.t = 0
+
+    def load(self, snap):
+        s = snap.reshape(self.nzl, self.ny, self.nx, 19)
+        for i in range(19):
+            self.G[self.active][i, 1:-1] = s[..., i]
+        self.t = 0
+        self.fresh = self.pull
+
+    def plane(self, grid, slot, plane):
+        return self.G[grid][slot, plane + 1]
+
+    def precollide(self):
+        if self.pull and self.fresh:
+            n, A = self.nzl, self.G[self.active]
+            tmp = collide(self.op, [A[i, 1:n + 1] for i in range(19)])
+            for i in range(19):
+                A[i, 1:n + 1] = tmp[i]
+            self.fresh = False
+
+    def step_local(self):
+        n, A, B = self.nzl, self.G[self.active], self.G[self.active ^ 1]
+        if self.pull:
+            src = [A[0, 1:n + 1]]
+            for i in range(1, 19):
+                cx, cy, cz = C[i]
+                src.append(np.roll(A[i], (cy, cx), axis=(1, 2))[1 - cz:n + 1 - cz])
+            tmp = collide(self.op, src)
+            for i in range(19):
+                B[i, 1:n + 1] = tmp[i]
+        else:
+            tmp = collide(self.op, [A[i, 1:n + 1] for i in range(19)])
+            B[0, 1:n + 1] = tmp[0]
+            for i in range(1, 19):
+                cx, cy, cz = C[i]
+                B[i, 1 + cz:n + 1 + cz] = np.roll(tmp[i], (cy, cx), axis=(1, 2))
+        self.active ^= 1
+        self.t += 1
+
+    def extract(self):
+        n = self.nzl
+        out = np.zeros((n, self.ny, self.nx, 19))
+        if not self.pull or self.fresh:
+            for i in range(19):
+                out[..., i] = self.G[self.active][i, 1:n + 1]
+        else:  # gather_out_direct from the idle grid (p/src/stepper.cpp:228-252)
+            I = self.G[self.active ^ 1]
+            out[..., 0] = I[0, 1:n + 1]
+            for i in range(1, 19):
+                cx, cy, cz = C[i]
+                out[..., i] = np.roll(I[i], (cy, cx), axis=(1, 2))[1 - cz:n + 1 - cz]
         return out.ravel()

@@ -105,6 +105,7 @@ _sig = {
     "lbmgpu_lambda_odd": (C.c_double, [C.c_double, C.c_double]),
     "lbmgpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "lbmgpu_halo_plan": (C.c_int, [C.c_int32, _P, C.POINTER(C.c_int32)]),
+    "lbmgpu_scheme_halo_plan": (C.c_int, [C.c_int32, C.c_int32, _P, C.POINTER(C.c_int32)]),
     "lbmgpu_nccl_unique_id": (C.c_int, [_P]),
     "lbmgpu_slab_connect_nccl": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
     "lbmgpu_slab_sync_ghosts": (C.c_int, [_P]),
@@ -544,13 +545,14 @@ def gpu_bytes_per_lup(scheme, addressing, pdf_bytes: int = 8) -> float:
     return b.value
 
 
-def halo_plan(nzl: int):
-    """The z-slab exchange plan (lbmgpu_halo_plan): rows of (phase, send,
-    peer, plane, slot) in posting order."""
+def halo_plan(nzl: int, scheme="aap"):
+    """The z-slab exchange plan (lbmgpu_scheme_halo_plan): rows of (phase,
+    send, peer, plane, slot) in posting order."""
     n = C.c_int32()
-    _check(_L.lbmgpu_halo_plan(nzl, None, C.byref(n)))
+    sid = _scheme_id(scheme)
+    _check(_L.lbmgpu_scheme_halo_plan(sid, nzl, None, C.byref(n)))
     ops = np.zeros(n.value * 5, np.int32)
-    _check(_L.lbmgpu_halo_plan(nzl, ops.ctypes.data, C.byref(n)))
+    _check(_L.lbmgpu_scheme_halo_plan(sid, nzl, ops.ctypes.data, C.byref(n)))
     return ops.reshape(-1, 5)
 
 

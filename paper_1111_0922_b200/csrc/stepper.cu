@@ -1020,20 +1020,44 @@ struct HaloOp {
   int slot;   // direction slot (a whole nx*ny slot plane)
 };
 
-static std::vector<HaloOp> halo_plan(int nzl) {
+enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2 };
+
+// Exchange plan per scheme. phase 0 runs before a sweep, phase 1 after it.
+//  AA (odd sweeps only): 0 = owners' face slots -> neighbours' ghosts (the
+//     opposed slots the odd gather reads), 1 = ghosts -> owners
+//  OS pull (every step, active grid): 0 = the slots the pull gathers across
+//     the face (bottom cells read cz=+1 slots below, top cells cz=-1 above)
+//  OS push (every step, destination grid): 1 = the slots pushed into the
+//     ghosts (top cells push cz=+1 up, bottom cells cz=-1 down) -> owners
+static std::vector<HaloOp> halo_plan(int kind, int nzl) {
   std::vector<HaloOp> v;
-  // phase 0: sends [up: top cz-] [down: bottom cz+]; recvs [down: lower ghost cz-] [up: upper ghost cz+]
-  for (int s : kZm) v.push_back({0, 1, +1, nzl - 1, s});
-  for (int s : kZp) v.push_back({0, 1, -1, 0, s});
-  for (int s : kZm) v.push_back({0, 0, -1, -1, s});
-  for (int s : kZp) v.push_back({0, 0, +1, nzl, s});
-  // phase 1: sends [down: lower ghost cz-] [up: upper ghost cz+]; recvs [up: top cz-] [down: bottom cz+]
-  for (int s : kZm) v.push_back({1, 1, -1, -1, s});
-  for (int s : kZp) v.push_back({1, 1, +1, nzl, s});
-  for (int s : kZm) v.push_back({1, 0, +1, nzl - 1, s});
-  for (int s : kZp) v.push_back({1, 0, -1, 0, s});
+  auto add = [&](int ph, int send, int peer, int plane, const int* slots) {
+    for (int k = 0; k < 5; ++k) v.push_back({ph, send, peer, plane, slots[k]});
+  };
+  if (kind == kSlabAA) {
+    // phase 0: sends [up: top cz-] [down: bottom cz+]; recvs [down: lower ghost cz-] [up: upper ghost cz+]
+    add(0, 1, +1, nzl - 1, kZm);
+    add(0, 1, -1, 0, kZp);
+    add(0, 0, -1, -1, kZm);
+    add(0, 0, +1, nzl, kZp);
+  }
+  if (kind == kSlabOsPull) {
+    // phase 0: sends [up: top cz+] [down: bottom cz-]; recvs [down: lower ghost cz+] [up: upper ghost cz-]
+    add(0, 1, +1, nzl - 1, kZp);
+    add(0, 1, -1, 0, kZm);
+    add(0, 0, -1, -1, kZp);
+    add(0, 0, +1, nzl, kZm);
+  }
+  if (kind == kSlabAA || kind == kSlabOsPush) {
+    // phase 1: sends [down: lower ghost cz-] [up: upper ghost cz+]; recvs [up: top cz-] [down: bottom cz+]
+    add(1, 1, -1, -1, kZm);
+    add(1, 1, +1, nzl, kZp);
+    add(1, 0, +1, nzl - 1, kZm);
+    add(1, 0, -1, 0, kZp);
+  }
   return v;
 }
+static std::vector<HaloOp> halo_plan(int nzl) { return halo_plan(kSlabAA, nzl); }
 
 // NCCL, loaded on first use (dlopen) so processes that never decompose do not
 // map it; inside a torch process this resolves to torch's libnccl.so.2.
@@ -1075,10 +1099,13 @@ struct Nccl {
   }
 };
 
-class AaSlab final : public Stepper {
+class SlabStepper final : public Stepper {
  public:
-  AaSlab(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
+  SlabStepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
       : Stepper(slab_geo(g, o), p, o), gnz_(g.nz), z0_(o.z_begin), z1_(o.z_end) {
+    kind_ = o.scheme == LBMGPU_AAP ? kSlabAA : (o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush : kSlabOsPull);
+    nt_ = (o.scheme == LBMGPU_OSNT_PULL_1S || o.scheme == LBMGPU_OSNT_PULL_2S) && o.streaming_stores;
+    two_s_ = o.scheme == LBMGPU_OSNT_PULL_2S;
     nzl_ = z1_ - z0_;
     plane_ = (uint64_t)g.nx * g.ny;
     L_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
@@ -1086,14 +1113,15 @@ class AaSlab final : public Stepper {
     L_.oz = 1;
     L_.wall[2] = 0;
     storage_ = plane_ * (nzl_ + 2);
-    alloc_field(f_, storage_);
+    ngrids_ = kind_ == kSlabAA ? 1 : 2;
+    for (int k = 0; k < ngrids_; ++k) alloc_field(g_[k], storage_);
     CK(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
     for (auto* e : {&ev_c_, &ev_halo_, &ev_odd_, &ev_back_})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    InitSpec r = base_init(kSrcRest);
-    init(r);
+    CK(cudaEventRecord(ev_back_, comm_));
+    init(base_init(kSrcRest));
   }
-  ~AaSlab() override {
+  ~SlabStepper() override {
     if (stream_) cudaStreamSynchronize(stream_);
     if (comm_) {
       cudaStreamSynchronize(comm_);
@@ -1105,8 +1133,12 @@ class AaSlab final : public Stepper {
   }
 
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
-    if (o.scheme != LBMGPU_AAP || o.addressing != LBMGPU_DIRECT || o.layout != LBMGPU_SOA)
-      throw std::invalid_argument("z-slab decomposition supports the AA pattern, direct, SoA");
+    const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_OS_PUSH ||
+                           o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
+                           o.scheme == LBMGPU_OSNT_PULL_2S;
+    if (!ok_scheme || o.addressing != LBMGPU_DIRECT || o.layout != LBMGPU_SOA)
+      throw std::invalid_argument(
+          "z-slab decomposition supports the AA pattern and OS/OSNT, direct, SoA");
     if (g.solids) throw std::invalid_argument("z-slab decomposition needs an all-fluid box");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
     if (o.z_begin < 0 || o.z_end > g.nz || o.z_end <= o.z_begin)
@@ -1134,28 +1166,42 @@ class AaSlab final : public Stepper {
   }
   void set_local(int transport) { transport_ = transport; }
 
-  double* slot_ptr(int slot, int plane) const {
+  // the grid an exchange phase applies to: AA its one grid; OS pull the
+  // active grid (read by the coming pull); OS push the grid just written
+  int phase_grid(int phase) const {
+    if (kind_ == kSlabAA) return 0;
+    if (kind_ == kSlabOsPull) return active_;
+    return phase == 1 ? active_ ^ 1 : active_;
+  }
+  void* slot_ptr(int grid, int slot, int plane) const {
     // storage plane = local plane + 1 (ghost below is storage plane 0)
-    return static_cast<double*>(f_.get()) + (size_t)slot * soa_stride(storage_) +
-           (size_t)(plane + 1) * plane_;
+    return static_cast<char*>(g_[grid].get()) +
+           ((size_t)slot * soa_stride(storage_) + (size_t)(plane + 1) * plane_) * esize();
   }
   size_t plane_bytes() const { return plane_ * esize(); }
 
   // NCCL phase: the plan's sends and receives in plan order, one group
-  void nccl_phase(int phase) {
+  void nccl_phase(int phase, int grid) {
     Nccl& N = Nccl::get();
     const ncclDataType_t ty = prec_ == Prec::f64 ? ncclDouble : ncclFloat;
     N.check(N.groupStart(), "ncclGroupStart");
-    for (const HaloOp& op : halo_plan(nzl_)) {
+    for (const HaloOp& op : halo_plan(kind_, nzl_)) {
       if (op.phase != phase) continue;
       const int peer = (rank_ + op.peer + nranks_) % nranks_;
-      void* p = slot_ptr(op.slot, op.plane);
+      void* p = slot_ptr(grid, op.slot, op.plane);
       if (op.send)
         N.check(N.send(p, plane_, ty, peer, nccl_, comm_), "ncclSend");
       else
         N.check(N.recv(p, plane_, ty, peer, nccl_, comm_), "ncclRecv");
     }
     N.check(N.groupEnd(), "ncclGroupEnd");
+  }
+  // comm stream runs `phase` after everything enqueued on stream_ so far
+  void enqueue_phase(int phase, int grid, cudaEvent_t done) {
+    CK(cudaEventRecord(ev_c_, stream_));
+    CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
+    nccl_phase(phase, grid);
+    CK(cudaEventRecord(done, comm_));
   }
 
   dev::Lat planes(int za, int zb) const {  // local planes [za, zb)
@@ -1165,90 +1211,140 @@ class AaSlab final : public Stepper {
     return L;
   }
 
+  // one sweep of the scheme's kernel over local planes [za, zb)
+  void sweep(int za, int zb) {
+    if (zb <= za) return;
+    const long long st = soa_stride(storage_);
+    const dev::Lat L = planes(za, zb);
+    if (kind_ == kSlabAA) {
+      const DField f = field(g_[0], st);
+      if ((t_ & 1) == 0)
+        launch_local(stream_, f, f, L, op_, false, true);
+      else
+        launch_aa_odd(stream_, f, L, op_);
+    } else {
+      const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
+      if (kind_ == kSlabOsPull)
+        launch_os_pull(stream_, a, b, L, op_, nt_, two_s_);
+      else
+        launch_os_push(stream_, a, b, L, op_);
+    }
+  }
+  // the interior planes never touch ghost planes or exchanged face slots
+  void sweep_split(cudaEvent_t wait_before_boundary) {
+    const int zi0 = 1, zi1 = std::max(1, nzl_ - 1);
+    sweep(zi0, zi1);
+    CK(cudaStreamWaitEvent(stream_, wait_before_boundary, 0));
+    sweep(0, 1);
+    if (nzl_ > 1) sweep(nzl_ - 1, nzl_);
+  }
+
+  void precollide_if_fresh() {
+    if (kind_ == kSlabOsPull && fresh_) {
+      const DField a = field(g_[active_], soa_stride(storage_));
+      launch_local(stream_, a, a, planes(0, nzl_), op_, false, false);
+      fresh_ = false;
+    }
+  }
+
   void step_one() override {
-    const DField f = field(f_, soa_stride(storage_));
-    const bool even = (t_ & 1) == 0;
     if (transport_ == kNccl) {
-      // overlapped: interior planes never touch ghost or exchanged face slots
-      const int zi0 = 1, zi1 = std::max(1, nzl_ - 1);
-      if (even) {
-        launch_local(stream_, f, f, planes(zi0, zi1), op_, false, true);
-        CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
-        launch_local(stream_, f, f, planes(0, 1), op_, false, true);
-        if (nzl_ > 1) launch_local(stream_, f, f, planes(nzl_ - 1, nzl_), op_, false, true);
-      } else {
-        CK(cudaEventRecord(ev_c_, stream_));
-        CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
-        nccl_phase(0);
-        CK(cudaEventRecord(ev_halo_, comm_));
-        launch_aa_odd(stream_, f, planes(zi0, zi1), op_);
-        CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
-        launch_aa_odd(stream_, f, planes(0, 1), op_);
-        if (nzl_ > 1) launch_aa_odd(stream_, f, planes(nzl_ - 1, nzl_), op_);
-        CK(cudaEventRecord(ev_odd_, stream_));
-        CK(cudaStreamWaitEvent(comm_, ev_odd_, 0));
-        nccl_phase(1);
-        CK(cudaEventRecord(ev_back_, comm_));
+      if (kind_ == kSlabAA) {
+        if ((t_ & 1) == 0) {
+          sweep_split(ev_back_);
+        } else {
+          enqueue_phase(0, 0, ev_halo_);
+          sweep_split(ev_halo_);
+          enqueue_phase(1, 0, ev_back_);
+        }
+      } else if (kind_ == kSlabOsPull) {
+        precollide_if_fresh();
+        enqueue_phase(0, active_, ev_halo_);
+        sweep_split(ev_halo_);
+        active_ ^= 1;
+      } else {  // push: interior and boundary, then ghosts -> owners of the new grid
+        sweep_split(ev_back_);
+        enqueue_phase(1, active_ ^ 1, ev_back_);
+        active_ ^= 1;
       }
       ghosts_fresh_ = false;
       return;
     }
     if (transport_ != kLocalGroup)
       throw std::runtime_error("slab stepper has no transport: connect NCCL or step as a group");
-    // in-process group: the driver (group_step) runs the exchanges between phases
-    if (even)
-      launch_local(stream_, f, f, L_, op_, false, true);
-    else
-      launch_aa_odd(stream_, f, L_, op_);
+    // in-process group: group_step runs the exchange phases around the sweep
+    sweep(0, nzl_);
+    if (kind_ != kSlabAA) active_ ^= 1;
   }
   int launches_per_step() const override {
     if (transport_ != kNccl) return 1;
-    return (t_ & 1) == 0 ? (nzl_ > 2 ? 3 : nzl_) : (nzl_ > 2 ? 3 : nzl_);
+    return nzl_ > 2 ? 3 : nzl_;
   }
 
   void finish() override {
     if (transport_ == kNccl) CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
   }
 
+  // ghost planes the extraction gathers from: AA at odd t, OS pull once it
+  // streams the idle grid (phase-0 slot set applied to that grid)
+  bool extract_needs_ghosts() const {
+    if (kind_ == kSlabAA) return (t_ & 1) != 0;
+    if (kind_ == kSlabOsPull) return !fresh_;
+    return false;
+  }
+  int ghost_grid() const { return kind_ == kSlabOsPull ? active_ ^ 1 : 0; }
+
   void sync_ghosts_nccl() {
     if (transport_ != kNccl) throw std::runtime_error("slab stepper is not connected to NCCL");
-    CK(cudaEventRecord(ev_c_, stream_));
-    CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
-    nccl_phase(0);
-    CK(cudaEventRecord(ev_halo_, comm_));
+    enqueue_phase(0, ghost_grid(), ev_halo_);
     CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
     ghosts_fresh_ = true;
   }
 
   void before_extract() override {
-    if ((t_ & 1) && !ghosts_fresh_)
+    if (extract_needs_ghosts() && !ghosts_fresh_)
       throw std::runtime_error(
-          "slab extract at an odd time step reads the ghost planes: call "
+          "slab extract reads the ghost planes at this time step: call "
           "lbmgpu_slab_sync_ghosts (or the group variant) first");
   }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
-    launch_extract(stream_, field(f_, soa_stride(storage_)), L_, nullptr, n0, c,
-                   (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
+    const long long st = soa_stride(storage_);
+    if (kind_ == kSlabAA)
+      launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
+                     (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
+    else if (kind_ == kSlabOsPull && !fresh_)
+      launch_extract(stream_, field(g_[active_ ^ 1], st), L_, nullptr, n0, c, kExGather,
+                     EtBase{}, d);
+    else
+      launch_extract(stream_, field(g_[active_], st), L_, nullptr, n0, c, kExNatural,
+                     EtBase{}, d);
   }
   void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
     InitSpec s = in;
     if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
-    launch_load(stream_, field(f_, soa_stride(storage_)), L_, nullptr, n0, c, kExNatural, d, s);
+    launch_load(stream_, field(g_[active_], soa_stride(storage_)), L_, nullptr, n0, c,
+                kExNatural, d, s);
   }
   void after_load() override {
     t_ = 0;
     ghosts_fresh_ = false;
+    fresh_ = kind_ == kSlabOsPull;
   }
-  int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
-  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  int layout_phase() const override {
+    return (kind_ == kSlabAA && (t_ & 1)) ? LBMGPU_OPPOSED : LBMGPU_NATURAL;
+  }
+  uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
 
   enum { kNone = 0, kLocalGroup = 1, kNccl = 2 };
+  int kind_ = kSlabAA;
   int transport_ = kNone;
   int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
+  int ngrids_ = 1, active_ = 0;
+  bool nt_ = false, two_s_ = false, fresh_ = false;
   bool ghosts_fresh_ = false;
   uint64_t plane_ = 0, storage_ = 0;
   dev::Lat L_;
-  DevMem f_;
+  DevMem g_[2];
   cudaStream_t comm_ = nullptr;
   cudaEvent_t ev_c_ = nullptr, ev_halo_ = nullptr, ev_odd_ = nullptr, ev_back_ = nullptr;
   ncclComm_t nccl_ = nullptr;
@@ -1258,13 +1354,14 @@ class AaSlab final : public Stepper {
 // In-process transport: executes one plan phase for a ring of slabs (rank k
 // = slab k) by matching each rank's sends with its peer's receives in plan
 // order — NCCL's point-to-point matching rule — as device-to-device copies.
-static void local_phase(std::vector<AaSlab*>& S, int phase) {
+static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_grid = false) {
   const int n = (int)S.size();
   for (auto* s : S) s->sync();
   std::vector<std::vector<HaloOp>> plans(n);
-  for (int k = 0; k < n; ++k) plans[k] = halo_plan(S[k]->nzl_);
+  for (int k = 0; k < n; ++k) plans[k] = halo_plan(S[k]->kind_, S[k]->nzl_);
   for (int k = 0; k < n; ++k) {
     std::vector<size_t> cursor(n, 0);
+    const int gk = use_ghost_grid ? S[k]->ghost_grid() : S[k]->phase_grid(phase);
     for (const HaloOp& op : plans[k]) {
       if (op.phase != phase || !op.send) continue;
       const int peer = (k + op.peer + n) % n;
@@ -1277,26 +1374,41 @@ static void local_phase(std::vector<AaSlab*>& S, int phase) {
       }
       if (c == pp.size()) throw std::runtime_error("halo plan: unmatched send");
       const HaloOp& r = pp[c++];
-      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(r.slot, r.plane), S[peer]->opt_.device,
-                             S[k]->slot_ptr(op.slot, op.plane), S[k]->opt_.device,
+      const int gp = use_ghost_grid ? S[peer]->ghost_grid() : S[peer]->phase_grid(phase);
+      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(gp, r.slot, r.plane), S[peer]->opt_.device,
+                             S[k]->slot_ptr(gk, op.slot, op.plane), S[k]->opt_.device,
                              S[k]->plane_bytes(), S[k]->stream_));
     }
   }
   for (auto* s : S) s->sync();
 }
 
-static void group_step(std::vector<AaSlab*>& S, long long steps) {
+static void group_step(std::vector<SlabStepper*>& S, long long steps) {
   for (auto* s : S) {
-    if (s->transport_ == AaSlab::kNccl) throw std::invalid_argument("slab is NCCL-connected");
-    s->set_local(AaSlab::kLocalGroup);
+    if (s->transport_ == SlabStepper::kNccl) throw std::invalid_argument("slab is NCCL-connected");
+    if (s->kind_ != S[0]->kind_) throw std::invalid_argument("slabs of different schemes");
+    s->set_local(SlabStepper::kLocalGroup);
   }
+  const int kind = S[0]->kind_;
   for (long long k = 0; k < steps; ++k) {
     const bool odd = (S[0]->t_ & 1) != 0;
     for (auto* s : S)
       if (((s->t_ & 1) != 0) != odd) throw std::invalid_argument("slabs out of step");
-    if (odd) local_phase(S, 0);
+    if (kind == kSlabOsPull) {
+      for (auto* s : S) s->precollide_if_fresh();
+    }
+    const bool pre = (kind == kSlabAA && odd) || kind == kSlabOsPull;
+    const bool post = (kind == kSlabAA && odd) || kind == kSlabOsPush;
+    if (pre) local_phase(S, 0);
     for (auto* s : S) s->step(1);
-    if (odd) local_phase(S, 1);
+    // phase 1 of push applies to the grid just written (now active)
+    if (post) {
+      if (kind == kSlabOsPush)
+        for (auto* s : S) s->active_ ^= 1;  // phase_grid(1) = active ^ 1 = written grid
+      local_phase(S, 1);
+      if (kind == kSlabOsPush)
+        for (auto* s : S) s->active_ ^= 1;
+    }
     for (auto* s : S) s->ghosts_fresh_ = false;
   }
   for (auto* s : S) s->sync();
@@ -1318,7 +1430,7 @@ static std::unique_ptr<Stepper> create(const lbmgpu_geometry* gg, const lbmgpu_f
   CK(cudaGetDeviceCount(&ndev));
   if (o->device < 0 || o->device >= ndev) throw std::invalid_argument("no such CUDA device");
   const HostGeo g = copy_geo(gg);
-  if (o->z_end != 0 || o->z_begin != 0) return std::make_unique<AaSlab>(g, *p, *o);
+  if (o->z_end != 0 || o->z_begin != 0) return std::make_unique<SlabStepper>(g, *p, *o);
   if (o->addressing == LBMGPU_DIRECT) {
     switch (o->scheme) {
       case LBMGPU_TS: return std::make_unique<TsDirect>(g, *p, *o);
@@ -1584,7 +1696,7 @@ int lbmgpu_init_field(lbmgpu_stepper* h, int32_t kind, uint64_t seed, double u0,
       case 2: in = s.base_init(kSrcRandom); break;
       default: throw std::invalid_argument("unknown init kind");
     }
-    if (auto* sl = dynamic_cast<AaSlab*>(&s)) {
+    if (auto* sl = dynamic_cast<SlabStepper*>(&s)) {
       const int src = in.source;
       in = sl->slab_init(src);
     }
@@ -1618,10 +1730,19 @@ int lbmgpu_launches_per_step(lbmgpu_stepper* h, int32_t* n) {
   return guard([&] { *n = S(h).launches_per_step(); });
 }
 
-int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count) {
+int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* count) {
   return guard([&] {
     if (nzl < 1) throw std::invalid_argument("slab needs at least one plane");
-    const auto plan = halo_plan(nzl);
+    int kind;
+    switch (scheme) {
+      case LBMGPU_AAP: kind = kSlabAA; break;
+      case LBMGPU_OS_PUSH: kind = kSlabOsPush; break;
+      case LBMGPU_OS_PULL:
+      case LBMGPU_OSNT_PULL_1S:
+      case LBMGPU_OSNT_PULL_2S: kind = kSlabOsPull; break;
+      default: throw std::invalid_argument("no z-slab decomposition for this scheme");
+    }
+    const auto plan = halo_plan(kind, nzl);
     if (count) *count = (int32_t)plan.size();
     if (ops)
       for (size_t k = 0; k < plan.size(); ++k) {
@@ -1634,6 +1755,10 @@ int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count) {
   });
 }
 
+int lbmgpu_halo_plan(int32_t nzl, int32_t* ops, int32_t* count) {
+  return lbmgpu_scheme_halo_plan(LBMGPU_AAP, nzl, ops, count);
+}
+
 int lbmgpu_nccl_unique_id(uint8_t* id) {
   return guard([&] {
     ncclUniqueId u;
@@ -1644,8 +1769,8 @@ int lbmgpu_nccl_unique_id(uint8_t* id) {
   });
 }
 
-static AaSlab& slab(lbmgpu_stepper* h) {
-  auto* s = dynamic_cast<AaSlab*>(&S(h));
+static SlabStepper& slab(lbmgpu_stepper* h) {
+  auto* s = dynamic_cast<SlabStepper*>(&S(h));
   if (!s) throw std::invalid_argument("not a z-slab stepper");
   return *s;
 }
@@ -1667,7 +1792,7 @@ int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h) {
 int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps) {
   return guard([&] {
     if (n < 1 || !hs) throw std::invalid_argument("empty slab group");
-    std::vector<AaSlab*> S;
+    std::vector<SlabStepper*> S;
     for (int k = 0; k < n; ++k) S.push_back(&slab(hs[k]));
     group_step(S, steps);
   });
@@ -1676,9 +1801,9 @@ int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps) {
 int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n) {
   return guard([&] {
     if (n < 1 || !hs) throw std::invalid_argument("empty slab group");
-    std::vector<AaSlab*> S;
+    std::vector<SlabStepper*> S;
     for (int k = 0; k < n; ++k) S.push_back(&slab(hs[k]));
-    local_phase(S, 0);
+    local_phase(S, 0, true);
     for (auto* s : S) s->ghosts_fresh_ = true;
   });
 }

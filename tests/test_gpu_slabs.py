@@ -10,24 +10,29 @@ from conftest import bitwise_equal
 pytestmark = pytest.mark.gpu
 
 
-def _slabs(L, dims, flow, bounds, precision=8):
+def _slabs(L, dims, flow, bounds, precision=8, scheme="aap"):
     geo = L.GridGeometry(*dims, ("periodic", "periodic", "periodic"))
-    return [L.create_stepper("aap", "direct", geo, flow,
+    return [L.create_stepper(scheme, "direct", geo, flow,
                              L.StepperOptions(z_begin=a, z_end=b, precision=precision))
             for a, b in bounds]
 
 
+def _needs_ghosts(scheme, t):
+    return (scheme == "aap" and t % 2 == 1) or (scheme.endswith("pull") or "pull" in scheme)
+
+
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s"])
 @pytest.mark.parametrize("nslab", [1, 2, 3, 4])
-def test_slabs_match_single_domain(gpu, nslab):
+def test_slabs_match_single_domain(gpu, nslab, scheme):
     L = gpu
     dims = (24, 20, 16)
     nz = dims[2]
     cuts = np.linspace(0, nz, nslab + 1).astype(int)
     bounds = list(zip(cuts[:-1], cuts[1:]))
     flow = L.bgk(1.0)
-    ref = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow)
+    ref = L.create_stepper(scheme, "direct", L.GridGeometry(*dims), flow)
     ref.init_field("taylor_green", seed=11, u0=0.05)
-    slabs = _slabs(L, dims, flow, bounds)
+    slabs = _slabs(L, dims, flow, bounds, scheme=scheme)
     for s in slabs:
         s.init_field("taylor_green", seed=11, u0=0.05)
     # device-side init is keyed by the global cell: the slabs start identical
@@ -37,7 +42,7 @@ def test_slabs_match_single_domain(gpu, nslab):
         ref.step_n(steps)
         ref.synchronize()
         L.slab_group_step(slabs, steps)
-        if ref.time_step() % 2:
+        if _needs_ghosts(scheme, ref.time_step()):
             L.slab_group_sync_ghosts(slabs)
         got = np.concatenate([s.extract_natural() for s in slabs])
         assert bitwise_equal(got, ref.extract_natural()), (nslab, ref.time_step())
@@ -65,7 +70,7 @@ def test_slab_load_and_uneven_split(gpu):
 def test_slab_errors(gpu):
     L = gpu
     geo = L.GridGeometry(8, 8, 8)
-    with pytest.raises(ValueError, match="AA pattern"):
+    with pytest.raises(ValueError, match="supports the AA pattern and OS/OSNT"):
         L.create_stepper("et", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(ValueError, match="periodic z"):
         L.create_stepper("aap", "direct", L.gen_channel(8, 8, 8),
@@ -75,16 +80,17 @@ def test_slab_errors(gpu):
         s.step()
 
 
-def test_nccl_transport_single_rank_ring(gpu):
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push"])
+def test_nccl_transport_single_rank_ring(gpu, scheme):
     """The NCCL transport itself (liblbmgpu.so dlopens libnccl): one rank whose
     ring neighbours are itself, the overlapped interior/boundary schedule, the
     phase-0/phase-1 groups — bitwise equal to the periodic single domain."""
     L = gpu
     dims = (32, 24, 20)
     flow = L.bgk(1.0)
-    ref = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow)
+    ref = L.create_stepper(scheme, "direct", L.GridGeometry(*dims), flow)
     ref.init_field("taylor_green", seed=9, u0=0.05)
-    s = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow,
+    s = L.create_stepper(scheme, "direct", L.GridGeometry(*dims), flow,
                          L.StepperOptions(z_begin=0, z_end=dims[2]))
     s.slab_connect_nccl(L.nccl_unique_id(), 1, 0)
     s.init_field("taylor_green", seed=9, u0=0.05)
@@ -93,6 +99,6 @@ def test_nccl_transport_single_rank_ring(gpu):
         ref.synchronize()
         s.step_n(steps)
         s.synchronize()
-        if s.time_step() % 2:
+        if _needs_ghosts(scheme, s.time_step()):
             s.slab_sync_ghosts()
         assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
