@@ -313,7 +313,7 @@ def run_slabs(args, ws, rank, local, dist, L):
     z0, z1 = rank * nz // ws, (rank + 1) * nz // ws
     geo = L.GridGeometry(nx, ny, nz, cfg["policy"])
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
-    st = L.create_stepper("aap", "direct", geo, flow,
+    st = L.create_stepper(args.scheme, "direct", geo, flow,
                           L.StepperOptions(device=local, z_begin=z0, z_end=z1))
     uid = [L.nccl_unique_id() if rank == 0 else None]
     if dist is not None:
@@ -330,22 +330,22 @@ def run_slabs(args, ws, rank, local, dist, L):
     ms = reduce_max(dist, ms_local)
     value = nodes * args.steps / (ms * 1e-3) / 1e6
     peak, peak_src = load_peaks()
-    bpl = L.gpu_bytes_per_lup("aap", "direct", 8)
+    bpl = L.gpu_bytes_per_lup(args.scheme, "direct", 8)
     achieved = bpl * nodes_local / (ms / args.steps * 1e-3) / 1e9
-    launches = 3 if (z1 - z0) > 2 else (z1 - z0)
+    launches = st.launches_per_step()
     halo = 2 * 2 * 5 * nx * ny * 8  # bytes per rank per odd step, each direction
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MFLUP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json configs[3]; seeded device-side Taylor-Green init)",
-        "config": {"workload": cfg["desc"], "scheme": "aap", "addressing": "direct",
+        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": "direct",
                    "layout": "soa", "dims": [nx, ny, nz], "fluid_nodes": nodes,
                    "parallelism": f"z-slabs x{ws} (NCCL halo, 5 slot planes/face)",
                    "l2": "inputs larger than L2, no flush needed"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "algorithmic_bytes_per_flup": bpl, "kernel": "k_local+k_aa_odd (per rank)",
+                     "algorithmic_bytes_per_flup": bpl, "kernel": f"{args.scheme} sweep (per rank)",
                      "peak_source": peak_src,
                      "halo_bytes_per_odd_step_per_rank": halo},
         "gpu_launches": args.steps * launches,
