@@ -197,3 +197,71 @@ class OsSlab:
                 cx, cy, cz = C[i]
                 out[..., i] = np.roll(I[i], (cy, cx), axis=(1, 2))[1 - cz:n + 1 - cz]
         return out.ravel()
+
+
+class EtSlab:
+    """Esoteric twist on a slab (p/src/scheme_et.cpp): one grid, handle table
+    b[] swapped pairwise after every sweep (:191-239), fill with identity
+    handles (:152-169), natural extraction (:83-109); x/y periodic, z through
+    ghost planes. plane(slot, plane) maps the logical slot through b[]."""
+
+    def __init__(self, nx, ny, nzl, op):
+        self.nx, self.ny, self.nzl, self.op = nx, ny, nzl, op
+        self.F = np.zeros((19, nzl + 2, ny, nx))
+        self.b = list(range(19))
+        self.t = 0
+
+    def _remote(self, slot, i):  # F[slot][X + c_i] over the local planes
+        cx, cy, cz = C[i]
+        n = self.nzl
+        return np.roll(self.F[slot], (-cy, -cx), axis=(1, 2))[1 + cz:n + 1 + cz]
+
+    def _put_remote(self, slot, i, v):
+        cx, cy, cz = C[i]
+        n = self.nzl
+        self.F[slot, 1 + cz:n + 1 + cz] = np.roll(v, (cy, cx), axis=(1, 2))
+
+    def load(self, snap):
+        s = snap.reshape(self.nzl, self.ny, self.nx, 19)
+        self.b = list(range(19))
+        self.F[0, 1:-1] = s[..., 0]
+        for p in range(9):
+            i, j = PI[p], PJ[p]
+            self.F[i, 1:-1] = s[..., i]
+            self._put_remote(j, i, s[..., j])
+        self.t = 0
+
+    def plane(self, slot, plane):
+        return self.F[self.b[slot], plane + 1]
+
+    def step_local(self):
+        """one sweep with the current handles; swap_handles() afterwards"""
+        n, b = self.nzl, self.b
+        f = [None] * 19
+        f[0] = self.F[0, 1:n + 1].copy()
+        for p in range(9):
+            i, j = PI[p], PJ[p]
+            f[i] = self.F[b[i], 1:n + 1].copy()
+            f[j] = self._remote(b[j], i).copy()
+        f = collide(self.op, f)
+        self.F[0, 1:n + 1] = f[0]
+        for p in range(9):
+            i, j = PI[p], PJ[p]
+            self.F[b[i], 1:n + 1] = f[j]
+            self._put_remote(b[j], i, f[i])
+        self.t += 1
+
+    def swap_handles(self):
+        for p in range(9):
+            i, j = PI[p], PJ[p]
+            self.b[i], self.b[j] = self.b[j], self.b[i]
+
+    def extract(self):
+        n, b = self.nzl, self.b
+        out = np.zeros((n, self.ny, self.nx, 19))
+        out[..., 0] = self.F[0, 1:n + 1]
+        for p in range(9):
+            i, j = PI[p], PJ[p]
+            out[..., i] = self.F[b[i], 1:n + 1]
+            out[..., j] = self._remote(b[j], i)
+        return out.ravel()

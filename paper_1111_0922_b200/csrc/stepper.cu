@@ -1020,7 +1020,13 @@ struct HaloOp {
   int slot;   // direction slot (a whole nx*ny slot plane)
 };
 
-enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2 };
+enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3 };
+// ET remote slots crossing a face (logical directions, mapped through the
+// handle table base[] when executed): a top cell reads and rewrites the second
+// members j of the pairs whose first member points up (5,9,12 -> 6,16,13) one
+// plane above; a bottom cell those of the pairs pointing down (8,11 -> 17,14)
+static constexpr int kEtUp[3] = {6, 16, 13};
+static constexpr int kEtDown[2] = {17, 14};
 
 // Exchange plan per scheme. phase 0 runs before a sweep, phase 1 after it.
 //  AA (odd sweeps only): 0 = owners' face slots -> neighbours' ghosts (the
@@ -1047,6 +1053,21 @@ static std::vector<HaloOp> halo_plan(int kind, int nzl) {
     add(0, 1, -1, 0, kZm);
     add(0, 0, -1, -1, kZp);
     add(0, 0, +1, nzl, kZm);
+  }
+  if (kind == kSlabEt) {
+    // every sweep. phase 0: sends [up: top {17,14}] [down: bottom {6,16,13}];
+    // recvs [down: lower ghost {17,14}] [up: upper ghost {6,16,13}]; phase 1 back
+    auto addn = [&](int ph, int send, int peer, int plane, const int* slots, int n) {
+      for (int k = 0; k < n; ++k) v.push_back({ph, send, peer, plane, slots[k]});
+    };
+    addn(0, 1, +1, nzl - 1, kEtDown, 2);
+    addn(0, 1, -1, 0, kEtUp, 3);
+    addn(0, 0, -1, -1, kEtDown, 2);
+    addn(0, 0, +1, nzl, kEtUp, 3);
+    addn(1, 1, -1, -1, kEtDown, 2);
+    addn(1, 1, +1, nzl, kEtUp, 3);
+    addn(1, 0, +1, nzl - 1, kEtDown, 2);
+    addn(1, 0, -1, 0, kEtUp, 3);
   }
   if (kind == kSlabAA || kind == kSlabOsPush) {
     // phase 1: sends [down: lower ghost cz-] [up: upper ghost cz+]; recvs [up: top cz-] [down: bottom cz+]
@@ -1103,7 +1124,11 @@ class SlabStepper final : public Stepper {
  public:
   SlabStepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
       : Stepper(slab_geo(g, o), p, o), gnz_(g.nz), z0_(o.z_begin), z1_(o.z_end) {
-    kind_ = o.scheme == LBMGPU_AAP ? kSlabAA : (o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush : kSlabOsPull);
+    kind_ = o.scheme == LBMGPU_AAP    ? kSlabAA
+            : o.scheme == LBMGPU_ET   ? kSlabEt
+            : o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush
+                                         : kSlabOsPull;
+    for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
     nt_ = (o.scheme == LBMGPU_OSNT_PULL_1S || o.scheme == LBMGPU_OSNT_PULL_2S) && o.streaming_stores;
     two_s_ = o.scheme == LBMGPU_OSNT_PULL_2S;
     nzl_ = z1_ - z0_;
@@ -1113,7 +1138,7 @@ class SlabStepper final : public Stepper {
     L_.oz = 1;
     L_.wall[2] = 0;
     storage_ = plane_ * (nzl_ + 2);
-    ngrids_ = kind_ == kSlabAA ? 1 : 2;
+    ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt) ? 1 : 2;
     for (int k = 0; k < ngrids_; ++k) alloc_field(g_[k], storage_);
     CK(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
     for (auto* e : {&ev_c_, &ev_halo_, &ev_odd_, &ev_back_})
@@ -1133,12 +1158,12 @@ class SlabStepper final : public Stepper {
   }
 
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
-    const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_OS_PUSH ||
+    const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_OS_PUSH ||
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
     if (!ok_scheme || o.addressing != LBMGPU_DIRECT || o.layout != LBMGPU_SOA)
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern and OS/OSNT, direct, SoA");
+          "z-slab decomposition supports the AA pattern, ET and OS/OSNT, direct, SoA");
     if (g.solids) throw std::invalid_argument("z-slab decomposition needs an all-fluid box");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
     if (o.z_begin < 0 || o.z_end > g.nz || o.z_end <= o.z_begin)
@@ -1169,7 +1194,7 @@ class SlabStepper final : public Stepper {
   // the grid an exchange phase applies to: AA its one grid; OS pull the
   // active grid (read by the coming pull); OS push the grid just written
   int phase_grid(int phase) const {
-    if (kind_ == kSlabAA) return 0;
+    if (kind_ == kSlabAA || kind_ == kSlabEt) return 0;
     if (kind_ == kSlabOsPull) return active_;
     return phase == 1 ? active_ ^ 1 : active_;
   }
@@ -1179,6 +1204,11 @@ class SlabStepper final : public Stepper {
            ((size_t)slot * soa_stride(storage_) + (size_t)(plane + 1) * plane_) * esize();
   }
   size_t plane_bytes() const { return plane_ * esize(); }
+  // storage plane of a logical slot (ET: through the handle table)
+  int phys_slot(int slot) const { return kind_ == kSlabEt ? base_.b[slot] : slot; }
+  void swap_base() {
+    for (int q = 0; q < 9; ++q) std::swap(base_.b[kPi[q]], base_.b[kPj[q]]);
+  }
 
   // NCCL phase: the plan's sends and receives in plan order, one group
   void nccl_phase(int phase, int grid) {
@@ -1188,7 +1218,7 @@ class SlabStepper final : public Stepper {
     for (const HaloOp& op : halo_plan(kind_, nzl_)) {
       if (op.phase != phase) continue;
       const int peer = (rank_ + op.peer + nranks_) % nranks_;
-      void* p = slot_ptr(grid, op.slot, op.plane);
+      void* p = slot_ptr(grid, phys_slot(op.slot), op.plane);
       if (op.send)
         N.check(N.send(p, plane_, ty, peer, nccl_, comm_), "ncclSend");
       else
@@ -1222,6 +1252,8 @@ class SlabStepper final : public Stepper {
         launch_local(stream_, f, f, L, op_, false, true);
       else
         launch_aa_odd(stream_, f, L, op_);
+    } else if (kind_ == kSlabEt) {
+      launch_et(stream_, field(g_[0], st), L, op_, base_);
     } else {
       const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
       if (kind_ == kSlabOsPull)
@@ -1249,7 +1281,16 @@ class SlabStepper final : public Stepper {
 
   void step_one() override {
     if (transport_ == kNccl) {
-      if (kind_ == kSlabAA) {
+      if (kind_ == kSlabEt) {
+        if (owners_stale_) {  // values a load parked in the ghosts -> owners
+          enqueue_phase(1, 0, ev_back_);
+          owners_stale_ = false;
+        }
+        enqueue_phase(0, 0, ev_halo_);
+        sweep_split(ev_halo_);
+        enqueue_phase(1, 0, ev_back_);
+        swap_base();
+      } else if (kind_ == kSlabAA) {
         if ((t_ & 1) == 0) {
           sweep_split(ev_back_);
         } else {
@@ -1274,7 +1315,10 @@ class SlabStepper final : public Stepper {
       throw std::runtime_error("slab stepper has no transport: connect NCCL or step as a group");
     // in-process group: group_step runs the exchange phases around the sweep
     sweep(0, nzl_);
-    if (kind_ != kSlabAA) active_ ^= 1;
+    if (kind_ == kSlabEt)
+      swap_base();
+    else if (kind_ != kSlabAA)
+      active_ ^= 1;
   }
   int launches_per_step() const override {
     if (transport_ != kNccl) return 1;
@@ -1289,6 +1333,7 @@ class SlabStepper final : public Stepper {
   // streams the idle grid (phase-0 slot set applied to that grid)
   bool extract_needs_ghosts() const {
     if (kind_ == kSlabAA) return (t_ & 1) != 0;
+    if (kind_ == kSlabEt) return true;
     if (kind_ == kSlabOsPull) return !fresh_;
     return false;
   }
@@ -1312,6 +1357,8 @@ class SlabStepper final : public Stepper {
     if (kind_ == kSlabAA)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
                      (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
+    else if (kind_ == kSlabEt)
+      launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c, kExEt, base_, d);
     else if (kind_ == kSlabOsPull && !fresh_)
       launch_extract(stream_, field(g_[active_ ^ 1], st), L_, nullptr, n0, c, kExGather,
                      EtBase{}, d);
@@ -1322,15 +1369,33 @@ class SlabStepper final : public Stepper {
   void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
     InitSpec s = in;
     if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
+    if (kind_ == kSlabEt) {
+      for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
+      launch_load(stream_, field(g_[0], soa_stride(storage_)), L_, nullptr, n0, c, kExEt, d, s);
+      return;
+    }
     launch_load(stream_, field(g_[active_], soa_stride(storage_)), L_, nullptr, n0, c,
                 kExNatural, d, s);
   }
   void after_load() override {
     t_ = 0;
-    ghosts_fresh_ = false;
     fresh_ = kind_ == kSlabOsPull;
+    // ET's load writes the remote slots of the boundary cells into the ghost
+    // planes: they are fresh, and their owners get them before the first sweep
+    ghosts_fresh_ = kind_ == kSlabEt;
+    owners_stale_ = kind_ == kSlabEt;
+  }
+  bool exchange_opposite_handles() override {
+    if (kind_ != kSlabEt) return false;
+    swap_base();
+    return true;
   }
   int layout_phase() const override {
+    if (kind_ == kSlabEt) {
+      for (int i = 0; i < 19; ++i)
+        if (base_.b[i] != i) return LBMGPU_TWISTED;
+      return LBMGPU_NATURAL;
+    }
     return (kind_ == kSlabAA && (t_ & 1)) ? LBMGPU_OPPOSED : LBMGPU_NATURAL;
   }
   uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
@@ -1341,7 +1406,8 @@ class SlabStepper final : public Stepper {
   int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
   int ngrids_ = 1, active_ = 0;
   bool nt_ = false, two_s_ = false, fresh_ = false;
-  bool ghosts_fresh_ = false;
+  bool ghosts_fresh_ = false, owners_stale_ = false;
+  EtBase base_;
   uint64_t plane_ = 0, storage_ = 0;
   dev::Lat L_;
   DevMem g_[2];
@@ -1375,9 +1441,10 @@ static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_
       if (c == pp.size()) throw std::runtime_error("halo plan: unmatched send");
       const HaloOp& r = pp[c++];
       const int gp = use_ghost_grid ? S[peer]->ghost_grid() : S[peer]->phase_grid(phase);
-      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(gp, r.slot, r.plane), S[peer]->opt_.device,
-                             S[k]->slot_ptr(gk, op.slot, op.plane), S[k]->opt_.device,
-                             S[k]->plane_bytes(), S[k]->stream_));
+      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(gp, S[peer]->phys_slot(r.slot), r.plane),
+                             S[peer]->opt_.device,
+                             S[k]->slot_ptr(gk, S[k]->phys_slot(op.slot), op.plane),
+                             S[k]->opt_.device, S[k]->plane_bytes(), S[k]->stream_));
     }
   }
   for (auto* s : S) s->sync();
@@ -1397,17 +1464,25 @@ static void group_step(std::vector<SlabStepper*>& S, long long steps) {
     if (kind == kSlabOsPull) {
       for (auto* s : S) s->precollide_if_fresh();
     }
-    const bool pre = (kind == kSlabAA && odd) || kind == kSlabOsPull;
-    const bool post = (kind == kSlabAA && odd) || kind == kSlabOsPush;
+    if (kind == kSlabEt && S[0]->owners_stale_) {
+      local_phase(S, 1);
+      for (auto* s : S) s->owners_stale_ = false;
+    }
+    const bool pre = (kind == kSlabAA && odd) || kind == kSlabOsPull || kind == kSlabEt;
+    const bool post = (kind == kSlabAA && odd) || kind == kSlabOsPush || kind == kSlabEt;
     if (pre) local_phase(S, 0);
     for (auto* s : S) s->step(1);
     // phase 1 of push applies to the grid just written (now active)
     if (post) {
       if (kind == kSlabOsPush)
         for (auto* s : S) s->active_ ^= 1;  // phase_grid(1) = active ^ 1 = written grid
+      if (kind == kSlabEt)  // the sweep's handle table (step() already swapped it)
+        for (auto* s : S) s->swap_base();
       local_phase(S, 1);
       if (kind == kSlabOsPush)
         for (auto* s : S) s->active_ ^= 1;
+      if (kind == kSlabEt)
+        for (auto* s : S) s->swap_base();
     }
     for (auto* s : S) s->ghosts_fresh_ = false;
   }
@@ -1740,6 +1815,7 @@ int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* 
       case LBMGPU_OS_PULL:
       case LBMGPU_OSNT_PULL_1S:
       case LBMGPU_OSNT_PULL_2S: kind = kSlabOsPull; break;
+      case LBMGPU_ET: kind = kSlabEt; break;
       default: throw std::invalid_argument("no z-slab decomposition for this scheme");
     }
     const auto plan = halo_plan(kind, nzl);

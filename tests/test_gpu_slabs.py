@@ -1,7 +1,8 @@
-"""GPU: z-slab AA steppers (the multi-GPU decomposition) driven in one process
-with the in-process transport (same halo plan as the NCCL transport). P slabs
-must reproduce the single-domain AA stepper bit for bit, at even and odd
-steps; the slab snapshots are contiguous ranges of the global one."""
+"""GPU: z-slab steppers (the multi-GPU decomposition: AA, ET, OS push/pull,
+OSNT) driven in one process with the in-process transport (same halo plan as
+the NCCL transport). P slabs must reproduce the single-domain stepper of the
+same scheme bit for bit, at even and odd steps; the slab snapshots are
+contiguous ranges of the global one."""
 import numpy as np
 import pytest
 
@@ -18,10 +19,10 @@ def _slabs(L, dims, flow, bounds, precision=8, scheme="aap"):
 
 
 def _needs_ghosts(scheme, t):
-    return (scheme == "aap" and t % 2 == 1) or (scheme.endswith("pull") or "pull" in scheme)
+    return (scheme == "aap" and t % 2 == 1) or "pull" in scheme or scheme == "et"
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "et"])
 @pytest.mark.parametrize("nslab", [1, 2, 3, 4])
 def test_slabs_match_single_domain(gpu, nslab, scheme):
     L = gpu
@@ -48,21 +49,24 @@ def test_slabs_match_single_domain(gpu, nslab, scheme):
         assert bitwise_equal(got, ref.extract_natural()), (nslab, ref.time_step())
 
 
-def test_slab_load_and_uneven_split(gpu):
+@pytest.mark.parametrize("scheme", ["aap", "et", "os-pull"])
+def test_slab_load_and_uneven_split(gpu, scheme):
     L = gpu
     dims = (16, 12, 10)
     flow = L.bgk(1.7, (1e-6, 0, 0))
-    ref = L.create_stepper("aap", "direct", L.GridGeometry(*dims), flow)
+    ref = L.create_stepper(scheme, "direct", L.GridGeometry(*dims), flow)
     ref.init_field("random", seed=3)
     f0 = ref.extract_natural()
     bounds = [(0, 1), (1, 4), (4, 10)]
-    slabs = _slabs(L, dims, flow, bounds)
+    slabs = _slabs(L, dims, flow, bounds, scheme=scheme)
     per = dims[0] * dims[1] * 19
     for s, (a, b) in zip(slabs, bounds):
         s.load_natural(f0[a * per:b * per])
     ref.step_n(6)
     ref.synchronize()
     L.slab_group_step(slabs, 6)
+    if _needs_ghosts(scheme, 6):
+        L.slab_group_sync_ghosts(slabs)
     assert bitwise_equal(np.concatenate([s.extract_natural() for s in slabs]),
                          ref.extract_natural())
 
@@ -70,8 +74,8 @@ def test_slab_load_and_uneven_split(gpu):
 def test_slab_errors(gpu):
     L = gpu
     geo = L.GridGeometry(8, 8, 8)
-    with pytest.raises(ValueError, match="supports the AA pattern and OS/OSNT"):
-        L.create_stepper("et", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="supports the AA pattern, ET and OS/OSNT"):
+        L.create_stepper("swap-pull", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(ValueError, match="periodic z"):
         L.create_stepper("aap", "direct", L.gen_channel(8, 8, 8),
                          options=L.StepperOptions(z_begin=0, z_end=4))
@@ -80,7 +84,7 @@ def test_slab_errors(gpu):
         s.step()
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et"])
 def test_nccl_transport_single_rank_ring(gpu, scheme):
     """The NCCL transport itself (liblbmgpu.so dlopens libnccl): one rank whose
     ring neighbours are itself, the overlapped interior/boundary schedule, the

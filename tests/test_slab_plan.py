@@ -1,7 +1,7 @@
 """CPU, multi-process (gloo, world_size 2): the z-slab halo plans that
 liblbmgpu.so's NCCL transport executes (lbmgpu_scheme_halo_plan) drive numpy
-restatements of the AA pattern and of the one-step push/pull scheme on two
-ranks; the gathered state must equal the single-domain two-step oracle bit
+restatements of the AA pattern, the one-step push/pull scheme and the
+esoteric twist on two ranks; the gathered state must equal the single-domain two-step oracle bit
 for bit, at even and odd steps."""
 import os
 import socket
@@ -34,7 +34,7 @@ def _worker(rank, world, port, scheme, q):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
-    from oracle.aa_numpy import AaSlab, OsSlab, trt
+    from oracle.aa_numpy import AaSlab, EtSlab, OsSlab, trt
     import paper_1111_0922_b200 as L
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -45,6 +45,9 @@ def _worker(rank, world, port, scheme, q):
     op = trt(1.3, 1.3, FORCE)
     if scheme == "aap":
         slab = AaSlab(nx, ny, nzl, op)
+        plane_of = lambda grid, slot, plane: slab.plane(slot, plane)  # noqa: E731
+    elif scheme == "et":
+        slab = EtSlab(nx, ny, nzl, op)
         plane_of = lambda grid, slot, plane: slab.plane(slot, plane)  # noqa: E731
     else:
         slab = OsSlab(nx, ny, nzl, op, pull=scheme == "os-pull")
@@ -73,8 +76,15 @@ def _worker(rank, world, port, scheme, q):
             r.wait()
 
     results = {}
+    if scheme == "et":
+        phase(1, 0)  # the fill parks boundary cells' remote slots in the ghosts
     for t in range(1, STEPS + 1):
-        if scheme == "aap":
+        if scheme == "et":
+            phase(0, 0)
+            slab.step_local()
+            phase(1, 0)  # with the sweep's handles
+            slab.swap_handles()
+        elif scheme == "aap":
             odd = slab.t % 2 == 1
             if odd:
                 phase(0, 0)
@@ -91,6 +101,8 @@ def _worker(rank, world, port, scheme, q):
         if t in (STEPS - 1, STEPS):
             if scheme == "aap" and slab.t % 2 == 1:
                 phase(0, 0)  # fresh ghosts for the odd-time gather
+            if scheme == "et":
+                phase(0, 0)  # the gather reads remote slots under the new handles
             if scheme == "os-pull":
                 phase(0, slab.active ^ 1)  # the idle grid the extraction streams
             results[t] = slab.extract()
@@ -121,11 +133,15 @@ def test_halo_plan_shape():
     push = L.halo_plan(5, "os-push")
     assert push.shape == (20, 5) and (push[:, 0] == 1).all()
     assert np.array_equal(L.halo_plan(5, "osnt-pull-2s"), pull)
+    et = L.halo_plan(5, "et")
+    assert et.shape == (20, 5)
+    assert set(et[et[:, 3] == 5][:, 4]) == {6, 16, 13}  # upper ghost
+    assert set(et[et[:, 3] == -1][:, 4]) == {17, 14}  # lower ghost
     with pytest.raises(ValueError):
-        L.halo_plan(5, "et")
+        L.halo_plan(5, "swap-pull")
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et"])
 def test_two_rank_gloo_slabs_match_single_domain(scheme):
     import torch.multiprocessing as mp
     import oracle
