@@ -10,6 +10,21 @@ inline dev::Fld<T, AOS> fld(const DField& f) {
   return dev::Fld<T, AOS>{static_cast<T*>(f.p), f.stride};
 }
 
+// TrtOperator coefficients in the kernel's precision (fp32 casts the fp64 ones)
+template <class T>
+inline dev::Trt<T> cast_op(const TrtHost& h) {
+  dev::Trt<T> o;
+  o.lambda_e = (T)h.lambda_e;
+  o.le_half = (T)h.le_half;
+  o.lo_half = (T)h.lo_half;
+  o.w0 = (T)h.w0;
+  for (int p = 0; p < 9; ++p) {
+    o.w2[p] = (T)h.w2[p];
+    o.f3w[p] = (T)h.f3w[p];
+  }
+  return o;
+}
+
 // Expands BODY with `T` (double|float) and `A` (AoS?) bound to F's type.
 #define LBM_DISPATCH(F, ...)                     \
   do {                                           \

@@ -1,0 +1,595 @@
+// AoS "window" kernels (direct addressing, record layout f[s*19 + i]).
+//
+// The per-thread AoS kernels in kernels_direct.cu read or write one field of
+// 32 different 152-byte records per warp instruction: every gather/scatter
+// moves a 32-byte L2 sector for 8 useful bytes, so the streamed side runs at
+// a quarter of the sector rate (profiles/r01_sweep_c1_final2.jsonl: OS pull
+// 0.45, OS push 0.23, AA 0.32 of the HBM roofline). Here a block owns a
+// 32 x 8 x-y tile and marches through a chunk of z planes. Each plane of the
+// tile plus a one-cell halo (34 x 10 records) is copied whole into a 4-plane
+// shared-memory ring with cp.async (16-byte chunks, the row phase in shared
+// memory matches the record's global byte phase); all neighbour accesses are
+// shared-memory accesses, and the tile's output records leave as contiguous
+// 16-byte stores. DRAM sees each record once per sweep (the halo rows/planes
+// are L2 hits of the neighbouring tiles), L2 sees 1.33x the record bytes.
+//
+// Modes (bitwise the same arithmetic as the per-thread kernels):
+//   kWinPull   OS / OSNT pull: gather A[X - c_i][i] (bounce A[X][opp i]),
+//              collide, store B[X]                  (p/src/scheme_os.cpp:141-174)
+//   kWinStream TS stream: B[X][i] = A[X - c_i][i]   (p/src/scheme_ts.cpp:82-112)
+//   kWinPush   OS push: collide every window record in place, then
+//              B[X][i] = bounce(opp i) ? post(X)[opp i] : post(X - c_i)[i],
+//              the same values the scatter B[i][Y + c_i] = post(Y)[i] writes
+//              (p/src/scheme_os.cpp:104-139); halo records are collided
+//              redundantly by both tiles (deterministic, identical)
+//   kWinAaOdd  AA odd sweep in place (p/src/scheme_aap.cpp:133-173). Node X
+//              reads and rewrites the slot set {(opp i, X - c_i)} (bounce:
+//              (i, X)); those sets partition the grid, so the owner of slot
+//              (k, R) is R if link opp k of R bounces, else R - c_k. A record
+//              whose 19 owners all lie in this block's tile and z chunk is
+//              written back whole; the others (tile rim, halo ring, chunk
+//              faces) slot by slot, only the owned slots.
+#include "dispatch.h"
+#include "launch.h"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace lbmgpu {
+using namespace dev;
+
+namespace {
+
+constexpr int kTX = 32, kTY = 8;             // tile: one warp per x-row
+constexpr int kWC = kTX + 2, kWR = kTY + 2;  // window columns / rows (1-cell halo)
+constexpr int kNB = 4;                       // plane buffers in the ring
+constexpr int kWinThreads = kTX * kTY;
+
+enum WinMode : int { kWinPull = 0, kWinStream = 1, kWinPush = 2, kWinAaOdd = 3 };
+
+template <class T>
+struct WinSz {
+  static constexpr int V = 16 / (int)sizeof(T);                    // elements per 16 B
+  static constexpr int ROW = ((kWC * 19 + V + V - 1) / V) * V;     // + phase slack
+  static constexpr int BUF = kWR * ROW;
+  static constexpr size_t kBytes = (size_t)kNB * BUF * sizeof(T);
+};
+static_assert(WinSz<double>::kBytes <= 227 * 1024 - 256, "fp64 ring exceeds shared memory");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <int N>
+__device__ __forceinline__ void cp_async(void* s, const void* g) {
+  if constexpr (N == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(s)), "l"(g),
+                 "n"(N)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// one warp copies n elements global -> shared; s and g congruent mod 16 bytes
+template <class T>
+__device__ __forceinline__ void copy_in(T* s, const T* g, int n, int lane) {
+  constexpr int V = 16 / (int)sizeof(T);
+  int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
+  if (head > n) head = n;
+  const int nv = (n - head) / V;
+  if (lane < head) cp_async<sizeof(T)>(s + lane, g + lane);
+  uint32_t sa = smem_u32(s + head) + 16u * (uint32_t)lane;
+  const char* ga = reinterpret_cast<const char*>(g + head) + 16 * lane;
+  for (int c = lane; c < nv; c += 32, sa += 512u, ga += 512)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(ga) : "memory");
+  const int t0 = head + nv * V;
+  if (t0 + lane < n) cp_async<sizeof(T)>(s + t0 + lane, g + t0 + lane);
+}
+// one record from another phase (a wrapped halo column)
+template <class T>
+__device__ __forceinline__ void copy_in_rec(T* s, const T* g, int lane) {
+  if (lane < 19) cp_async<sizeof(T)>(s + lane, g + lane);
+}
+// one warp copies n elements shared -> global; congruent mod 16 bytes
+template <class T>
+__device__ __forceinline__ void copy_out(T* g, const T* s, int n, int lane) {
+  constexpr int V = 16 / (int)sizeof(T);
+  int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
+  if (head > n) head = n;
+  const int nv = (n - head) / V;
+  if (lane < head) g[lane] = s[lane];
+  const float4* sv = reinterpret_cast<const float4*>(s + head) + lane;
+  float4* gv = reinterpret_cast<float4*>(g + head) + lane;
+  for (int c = lane; c < nv; c += 32, sv += 32, gv += 32) *gv = *sv;
+  const int t0 = head + nv * V;
+  if (t0 + lane < n) g[t0 + lane] = s[t0 + lane];
+}
+
+// storage index of cell (0, y, z) after periodic wrap; false if beyond a wall
+__device__ __forceinline__ bool row_base(const Lat& L, int y, int z, uint32_t& rb) {
+  if (y < 0 || y >= L.ny) {
+    if (L.wall[1]) return false;
+    y = y < 0 ? y + L.ny : y - L.ny;
+  }
+  if (z < 0 || z >= L.nz) {
+    if (L.wall[2]) return false;
+    z = z < 0 ? z + L.nz : z - L.nz;
+  }
+  rb = (uint32_t)L.nx * ((uint32_t)y + (uint32_t)L.ny * (uint32_t)z);
+  return true;
+}
+// wrapped x of window column rx; false if beyond a wall
+__device__ __forceinline__ bool col_x(const Lat& L, int x0, int rx, int& x) {
+  x = x0 - 1 + rx;
+  if (x < 0 || x >= L.nx) {
+    if (L.wall[0]) return false;
+    x = x < 0 ? x + L.nx : x - L.nx;
+  }
+  return true;
+}
+// links of an in-range cell (resolve_link, p/src/geometry.cpp:49-60)
+__device__ __forceinline__ bool cell_links(const Lat& L, int x, int y, int z, uint32_t& bounce) {
+  if (L.linkmask) {
+    const uint32_t lm = L.linkmask[(uint32_t)x + (uint32_t)L.nx * ((uint32_t)y + (uint32_t)L.ny * (uint32_t)z)];
+    bounce = lm & ~1u;
+    return lm & 1u;
+  }
+  uint32_t b = 0;
+  if (L.wall[0]) b |= (x == 0 ? kMxm : 0u) | (x == L.nx - 1 ? kMxp : 0u);
+  if (L.wall[1]) b |= (y == 0 ? kMym : 0u) | (y == L.ny - 1 ? kMyp : 0u);
+  if (L.wall[2]) b |= (z == 0 ? kMzm : 0u) | (z == L.nz - 1 ? kMzp : 0u);
+  bounce = b;
+  return true;
+}
+
+struct Tile {
+  int x0, y0, txv, tyv, zb, ze;
+};
+
+// issue the cp.async copies of window plane z (cell z, may be -1 / nz)
+template <class T>
+__device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
+                                           int* ph, const Tile& t, int z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < t.tyv + 2; r += kTY) {
+    uint32_t rb;
+    int phase = 0;
+    if (row_base(L, t.y0 - 1 + r, z, rb)) {
+      const long long v0 = (long long)rb + t.x0 - 1;  // record under window column 0
+      phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
+      T* srow = buf + r * WinSz<T>::ROW + phase;
+      const int xa = max(t.x0 - 1, 0), xb = min(t.x0 + t.txv, L.nx - 1);
+      copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)xa) * 19, (xb - xa + 1) * 19,
+              lane);
+      if (!L.wall[0]) {
+        if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
+        if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
+      }
+    }
+    if (lane == 0) ph[r] = phase;
+  }
+}
+
+// OS push: collide every fluid record of a window plane in place
+template <class T>
+__device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T* buf,
+                                              const int* ph, const Tile& t, int z) {
+  if ((z < 0 || z >= L.nz) && L.wall[2]) return;
+  const int zw = z < 0 ? z + L.nz : (z >= L.nz ? z - L.nz : z);
+  const int w = t.txv + 2, n = w * (t.tyv + 2);
+  for (int q = threadIdx.x; q < n; q += kWinThreads) {
+    const int r = q / w, rx = q - r * w;
+    int x, y = t.y0 - 1 + r;
+    if (y < 0 || y >= L.ny) {
+      if (L.wall[1]) continue;
+      y = y < 0 ? y + L.ny : y - L.ny;
+    }
+    if (!col_x(L, t.x0, rx, x)) continue;
+    uint32_t bounce;
+    if (!cell_links(L, x, y, zw, bounce)) continue;
+    T* rec = buf + r * WinSz<T>::ROW + ph[r] + rx * 19;
+    T f[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = rec[i];
+    collide(op, f);
+#pragma unroll
+    for (int i = 0; i < 19; ++i) rec[i] = f[i];
+  }
+}
+
+// AA odd: write back window plane z of the in-place field (owned slots only).
+// Work items, round-robin over the 8 warps: the halves (by column) of the
+// rows that are written slot by slot throughout, then the rows whose interior
+// records are owned whole (one 16-byte vector run plus the 4 rim columns
+// 0, 1, txv, txv+1 slot by slot). Lanes first compute the 19-bit ownership
+// mask of each of the item's columns (into msk), then store element-parallel
+// (coalesced, with holes).
+template <class T>
+__device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
+                                                const int* ph, uint32_t* msk, const Tile& t,
+                                                int z) {
+  if ((z < 0 || z >= L.nz) && L.wall[2]) return;
+  const int zw = z < 0 ? z + L.nz : (z >= L.nz ? z - L.nz : z);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
+  const int w = t.txv + 2, rows = t.tyv + 2;
+  const bool can_run = zin && t.txv >= 3;
+  // rows with a run: r in [2, tyv-1] when can_run; the others are split in two
+  const int nrun = can_run ? max(0, t.tyv - 2) : 0;
+  const int nfull = rows - nrun;
+  const int nitems = 2 * nfull + nrun;
+  for (int it = warp; it < nitems; it += kTY) {
+    int r, c0, c1;  // row, column range [c0, c1) for the slot-by-slot pass
+    bool run;
+    if (it < 2 * nfull) {
+      const int fr = it >> 1;  // fr-th row without a run
+      r = (!can_run || fr < 2) ? fr : fr + nrun;
+      const int half = (w + 1) / 2;
+      c0 = (it & 1) ? half : 0;
+      c1 = (it & 1) ? w : half;
+      run = false;
+    } else {
+      r = 2 + (it - 2 * nfull);
+      c0 = 0;
+      c1 = 4;
+      run = true;
+    }
+    uint32_t rb;
+    if (!row_base(L, t.y0 - 1 + r, z, rb)) continue;
+    int y = t.y0 - 1 + r;
+    y = y < 0 ? y + L.ny : (y >= L.ny ? y - L.ny : y);
+    const T* srow = buf + r * WinSz<T>::ROW + ph[r];
+    // column q of the item: [c0, c1) directly, or the rim list of a run row
+    auto col_of = [&](int q) { return run ? (q < 2 ? q : t.txv + q - 2) : q; };
+    uint32_t* mk = msk + warp * kWC;
+    for (int q = c0 + lane; q < c1; q += 32) {
+      const int rx = col_of(q);
+      uint32_t m = 0;
+      int x;
+      uint32_t bounce;
+      if (col_x(L, t.x0, rx, x) && cell_links(L, x, y, zw, bounce)) {
+        const bool self_in =
+            rx >= 1 && rx <= t.txv && r >= 1 && r <= t.tyv && z >= t.zb && z < t.ze;
+        m = self_in ? 1u : 0u;
+#pragma unroll
+        for (int k = 1; k < 19; ++k) {
+          bool own;
+          if ((bounce >> opp(k)) & 1u) {
+            own = self_in;
+          } else {
+            const int ox = rx - cx(k), oy = r - cy(k), oz = z - cz(k);
+            own = ox >= 1 && ox <= t.txv && oy >= 1 && oy <= t.tyv && oz >= t.zb && oz < t.ze;
+          }
+          m |= own ? (1u << k) : 0u;
+        }
+      }  // beyond a wall or solid: never written
+      mk[q - c0] = m;
+    }
+    __syncwarp();
+    if (run)
+      copy_out(g + ((size_t)rb + (size_t)(t.x0 + 1)) * 19, srow + 2 * 19, (t.txv - 2) * 19, lane);
+    const int n = (c1 - c0) * 19;
+    for (int e = lane; e < n; e += 32) {
+      const int qq = e / 19, k = e - qq * 19;
+      if (!((mk[qq] >> k) & 1u)) continue;
+      const int rx = col_of(c0 + qq);
+      int x = t.x0 - 1 + rx;
+      x = x < 0 ? x + L.nx : (x >= L.nx ? x - L.nx : x);
+      g[((size_t)rb + (size_t)x) * 19 + k] = srow[rx * 19 + k];
+    }
+    __syncwarp();
+  }
+}
+
+// per-node body: gather (pull form) or in-place AA odd, BB = some lane of the
+// warp has a bounce link
+template <int MODE, bool BB, class T, class At>
+__device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&f)[19], At at) {
+  if constexpr (MODE == kWinAaOdd) {
+    f[0] = at(0, 0);
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      f[i] = (BB && ((bounce >> j) & 1u)) ? at(0, i) : at(j, j);
+    }
+    collide(op, f);
+    at(0, 0) = f[0];
+#pragma unroll
+    for (int j = 1; j < 19; ++j) {
+      if (BB && ((bounce >> j) & 1u))
+        at(0, opp(j)) = f[j];
+      else
+        at(j, j) = f[j];
+    }
+  } else {
+    f[0] = at(0, 0);
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      f[i] = (BB && ((bounce >> j) & 1u)) ? at(0, j) : at(j, i);
+    }
+    if constexpr (MODE == kWinPull) collide(op, f);
+  }
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(kWinThreads, sizeof(T) == 8 ? 1 : 2)
+    k_win(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
+  extern __shared__ __align__(16) unsigned char win_smem[];
+  T* sm = reinterpret_cast<T*>(win_smem);
+  __shared__ int ph[kNB][kWR];
+  __shared__ uint32_t msk[MODE == kWinAaOdd ? kTY * kWC : 1];
+  constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
+
+  const int ntile = tiles_x * tiles_y;
+  const int tile = (int)blockIdx.x % ntile, chunk = (int)blockIdx.x / ntile;
+  Tile t;
+  t.x0 = (tile % tiles_x) * kTX;
+  t.y0 = (tile / tiles_x) * kTY;
+  t.txv = min(kTX, L.nx - t.x0);
+  t.tyv = min(kTY, L.ny - t.y0);
+  t.zb = chunk * zc;
+  t.ze = min(L.nz, t.zb + zc);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const bool valid = tx < t.txv && ty < t.tyv;
+  const T* gin = src.p;
+  // ring slot of window plane z (z in [zb - 1, ze])
+  auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
+  auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z); };
+
+  // Schedule per plane z: wait for plane z + 1, barrier (every warp has also
+  // finished plane z - 1, so slot(z + 2) = slot(z - 2) is free), prefetch
+  // plane z + 2, compute, barrier (plane z - 1 fully read), then each warp
+  // stages / writes back its rows of plane z - 1's slot.
+  load(t.zb - 1);
+  load(t.zb);
+  cp_commit();
+  for (int z = t.zb; z < t.ze; ++z) {
+    if (z == t.zb) load(z + 1);
+    cp_commit();
+    if (z == t.zb) cp_wait1(); else cp_wait0();
+    __syncthreads();
+    if (z == t.zb) {
+      cp_wait0();  // plane z + 1 of the prologue
+      __syncthreads();
+    }
+    if (z + 2 <= t.ze) load(z + 2);
+    if constexpr (MODE == kWinPush) {
+      if (z == t.zb) {
+        collide_plane(L, op, sm + slot(z - 1) * BUF, ph[slot(z - 1)], t, z - 1);
+        collide_plane(L, op, sm + slot(z) * BUF, ph[slot(z)], t, z);
+      }
+      collide_plane(L, op, sm + slot(z + 1) * BUF, ph[slot(z + 1)], t, z + 1);
+      __syncthreads();
+    }
+    // element offsets of the 3 x 3 (z, y) neighbourhood at this thread's column
+    int rp[3][3];
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+        const int s = slot(z - 1 + dz), r = ty + dy;
+        rp[dz][dy] = s * BUF + r * ROW + ph[s][r] + (tx + 1) * 19;
+      }
+    auto at = [&](int i, int k) -> T& {  // slot k of the record at X + c_i
+      return sm[rp[1 + cz(i)][1 + cy(i)] + cx(i) * 19 + k];
+    };
+    T f[19];
+    bool live = false;
+    uint32_t bounce = 0;
+    if (valid) live = cell_links(L, t.x0 + tx, t.y0 + ty, z, bounce);
+    const bool interior = __all_sync(0xffffffffu, bounce == 0u);
+    if (live) {
+      if (interior)
+        win_node<MODE, false>(op, bounce, f, at);
+      else
+        win_node<MODE, true>(op, bounce, f, at);
+    }
+    __syncthreads();  // every read of plane z - 1 is done
+    if constexpr (MODE == kWinAaOdd) {
+      writeback_plane(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, t, z - 1);
+    } else if (ty < t.tyv) {
+      // stage the tile row in plane z - 1's slot with the phase of dst's row
+      uint32_t rb;
+      row_base(L, t.y0 + ty, z, rb);
+      const long long v0 = (long long)rb + t.x0;
+      const int phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
+      T* srow = sm + slot(z - 1) * BUF + ty * ROW + phase;
+      if (tx < t.txv) {
+#pragma unroll
+        for (int i = 0; i < 19; ++i) srow[tx * 19 + i] = live ? f[i] : T(0);
+      }
+      __syncwarp();
+      copy_out(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
+    }
+  }
+  if constexpr (MODE == kWinAaOdd) {
+    __syncthreads();
+    writeback_plane(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, t, t.ze - 1);
+    writeback_plane(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, t, t.ze);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Local AoS sweep (AA even, TS collide, OS precollide, SWAP collide) as a
+// persistent stream: each block walks 256-record runs with a two-slot
+// cp.async ring, so the next run's loads are in flight while this run
+// collides in shared memory and leaves as 16-byte vector stores.
+// ---------------------------------------------------------------------------
+constexpr int kRun = 256;
+template <class T>
+struct RunSz {
+  static constexpr int V = 16 / (int)sizeof(T);
+  static constexpr int SLOT = ((kRun * 19 + V + V - 1) / V) * V;
+  static constexpr size_t kBytes = 2 * (size_t)SLOT * sizeof(T);
+};
+
+template <class T, bool RD_OPP, bool WR_OPP>
+__global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
+    k_local_stream(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, uint32_t soff,
+                   uint32_t nruns) {
+  extern __shared__ __align__(16) unsigned char run_smem[];
+  T* sm = reinterpret_cast<T*>(run_smem);
+  constexpr int SLOT = RunSz<T>::SLOT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto phase_of = [&](uint32_t c0) {
+    return (int)((((unsigned long long)(c0 + soff) * 19ull * sizeof(T)) & 15ull) / sizeof(T));
+  };
+  // the block's k-th run and its record count
+  auto run_c0 = [&](uint32_t k) { return L.cell_begin + (blockIdx.x + k * gridDim.x) * kRun; };
+  auto issue = [&](uint32_t k) {
+    const uint32_t c0 = run_c0(k);
+    const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
+    // 8 warps split the contiguous run into 8 pieces
+    const uint32_t nel = nrec * 19, per = (nel + 7) / 8;
+    const uint32_t e0 = min(nel, (uint32_t)warp * per), e1 = min(nel, e0 + per);
+    T* s = sm + (k & 1) * SLOT + phase_of(c0);
+    if (e1 > e0) copy_in(s + e0, src.p + (size_t)(c0 + soff) * 19 + e0, (int)(e1 - e0), lane);
+  };
+  uint32_t nmine = 0;
+  while (blockIdx.x + nmine * gridDim.x < nruns) ++nmine;
+  if (nmine == 0) return;
+  issue(0);
+  cp_commit();
+  for (uint32_t k = 0; k < nmine; ++k) {
+    if (k + 1 < nmine) issue(k + 1);
+    cp_commit();
+    cp_wait1();
+    __syncthreads();
+    const uint32_t c0 = run_c0(k);
+    const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
+    T* s = sm + (k & 1) * SLOT + phase_of(c0);
+    const uint32_t r = threadIdx.x;
+    if (r < nrec && (L.linkmask ? (L.linkmask[c0 + r] & 1u) != 0 : true)) {
+      T f[19];
+#pragma unroll
+      for (int i = 0; i < 19; ++i) f[i] = s[r * 19 + (RD_OPP ? opp(i) : i)];
+      collide(op, f);
+#pragma unroll
+      for (int i = 0; i < 19; ++i) s[r * 19 + (WR_OPP ? opp(i) : i)] = f[i];
+    }
+    __syncthreads();
+    const uint32_t nel = nrec * 19, per = (nel + 7) / 8;
+    const uint32_t e0 = min(nel, (uint32_t)warp * per), e1 = min(nel, e0 + per);
+    if (e1 > e0) copy_out(dst.p + (size_t)(c0 + soff) * 19 + e0, s + e0, (int)(e1 - e0), lane);
+    __syncthreads();  // the slot is refilled two runs later
+  }
+}
+
+bool window_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_AOS_WINDOW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class T, int MODE>
+void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
+                const TrtHost& op, int zc) {
+  static bool attr = [] {
+    return cudaFuncSetAttribute(k_win<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)WinSz<T>::kBytes) == cudaSuccess;
+  }();
+  (void)attr;
+  const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTY - 1) / kTY;
+  const int nzc = (L.nz + zc - 1) / zc;
+  const unsigned grid = (unsigned)(tiles_x * tiles_y * nzc);
+  k_win<T, MODE><<<grid, kWinThreads, WinSz<T>::kBytes, st>>>(fld<T, true>(a), fld<T, true>(b), L,
+                                                             cast_op<T>(op), tiles_x, tiles_y, zc);
+}
+
+}  // namespace
+
+// z planes per block: enough blocks for ~7 waves of resident blocks (one
+// fp64 / two fp32 per SM), at most 64 planes, and for the in-place mode at
+// least two chunks on a periodic z axis (a chunk's halo plane must not be
+// one of its own planes)
+static int window_chunk(const Lat& L, bool fp64, bool inplace) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long tiles = (long long)((L.nx + kTX - 1) / kTX) * ((L.ny + kTY - 1) / kTY);
+  const long long resident = (long long)sms * (fp64 ? 1 : 2);
+  long long zc = (L.nz * tiles + resident * 7 - 1) / (resident * 7);
+  zc = std::max(4LL, std::min(64LL, zc));
+  if (inplace && !L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
+  return (int)std::max(1LL, std::min<long long>(zc, L.nz));
+}
+
+// Applicability: AoS, plain x-fastest storage (no halo/padding/ghost planes),
+// the whole lattice in one launch. In place additionally needs every window
+// position to be a distinct record (periodic nx >= 34, ny >= 10, nz >= 3).
+bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField& b,
+                       const Lat& L, const TrtHost& op) {
+  if (!a.aos || !window_enabled()) return false;
+  if (L.sx != L.nx || L.sy != L.ny || L.ox || L.oy || L.oz || L.zghost || L.znowrap) return false;
+  if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
+    return false;
+  const bool inplace = mode == kWinAaOdd;
+  if (inplace && ((!L.wall[0] && L.nx < kTX + 2) || (!L.wall[1] && L.ny < kTY + 2) ||
+                  (!L.wall[2] && L.nz < 3)))
+    return false;
+  const bool f64 = a.prec == Prec::f64;
+  const int zc = window_chunk(L, f64, inplace);
+  if (f64) {
+    switch (mode) {
+      case kWinPull: launch_win<double, kWinPull>(st, a, b, L, op, zc); break;
+      case kWinStream: launch_win<double, kWinStream>(st, a, b, L, op, zc); break;
+      case kWinPush: launch_win<double, kWinPush>(st, a, b, L, op, zc); break;
+      default: launch_win<double, kWinAaOdd>(st, a, b, L, op, zc); break;
+    }
+  } else {
+    switch (mode) {
+      case kWinPull: launch_win<float, kWinPull>(st, a, b, L, op, zc); break;
+      case kWinStream: launch_win<float, kWinStream>(st, a, b, L, op, zc); break;
+      case kWinPush: launch_win<float, kWinPush>(st, a, b, L, op, zc); break;
+      default: launch_win<float, kWinAaOdd>(st, a, b, L, op, zc); break;
+    }
+  }
+  return true;
+}
+
+template <class T, bool RD, bool WR>
+static void launch_stream_t(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
+                            const TrtHost& op, uint32_t soff) {
+  static int per_sm = [] {
+    cudaFuncSetAttribute(k_local_stream<T, RD, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)RunSz<T>::kBytes);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_local_stream<T, RD, WR>, kRun,
+                                                      RunSz<T>::kBytes) != cudaSuccess || n < 1)
+      n = 1;
+    return n;
+  }();
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t nruns = (L.ncells - L.cell_begin + kRun - 1) / kRun;
+  const uint32_t grid = std::min<uint32_t>(nruns, (uint32_t)(sms * per_sm));
+  k_local_stream<T, RD, WR><<<grid, kRun, RunSz<T>::kBytes, st>>>(
+      fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), soff, nruns);
+}
+
+// contiguous AoS local sweep: storage index = cell + soff for every cell
+bool launch_aos_local_stream(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
+                             const TrtHost& op, bool rd_opp, bool wr_opp, uint32_t soff) {
+  if (!a.aos || !window_enabled()) return false;
+  if (a.prec == Prec::f64) {
+    if (!rd_opp && !wr_opp) launch_stream_t<double, false, false>(st, a, b, L, op, soff);
+    if (!rd_opp && wr_opp) launch_stream_t<double, false, true>(st, a, b, L, op, soff);
+    if (rd_opp && !wr_opp) launch_stream_t<double, true, false>(st, a, b, L, op, soff);
+    if (rd_opp && wr_opp) launch_stream_t<double, true, true>(st, a, b, L, op, soff);
+  } else {
+    if (!rd_opp && !wr_opp) launch_stream_t<float, false, false>(st, a, b, L, op, soff);
+    if (!rd_opp && wr_opp) launch_stream_t<float, false, true>(st, a, b, L, op, soff);
+    if (rd_opp && !wr_opp) launch_stream_t<float, true, false>(st, a, b, L, op, soff);
+    if (rd_opp && wr_opp) launch_stream_t<float, true, true>(st, a, b, L, op, soff);
+  }
+  return true;
+}
+
+}  // namespace lbmgpu

@@ -13,20 +13,6 @@ using namespace dev;
 
 namespace {
 
-template <class T>
-Trt<T> cast_op(const TrtHost& h) {
-  Trt<T> o;
-  o.lambda_e = (T)h.lambda_e;
-  o.le_half = (T)h.le_half;
-  o.lo_half = (T)h.lo_half;
-  o.w0 = (T)h.w0;
-  for (int p = 0; p < 9; ++p) {
-    o.w2[p] = (T)h.w2[p];
-    o.f3w[p] = (T)h.f3w[p];
-  }
-  return o;
-}
-
 inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
 
 // ---------------------------------------------------------------------------
@@ -180,13 +166,14 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, A
 template <bool BB, class T, bool AOS>
 __device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, const Trt<T>& op,
                                         const EtBase& B) {
+  constexpr bool NC = sizeof(T) == 4 && !AOS;
   T f[19];
-  f[0] = ld(F.at(0, c.s));
+  f[0] = ldsel<NC>(F.at(0, c.s));
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    f[i] = ld(F.at(B.b[i], c.s));
-    f[j] = ld(F.at((BB && c.bb(i)) ? B.b[i] : B.b[j], c.nb(i)));
+    f[i] = ldsel<NC>(F.at(B.b[i], c.s));
+    f[j] = ldsel<NC>(F.at((BB && c.bb(i)) ? B.b[i] : B.b[j], c.nb(i)));
   }
   collide(op, f);
   st<false>(F.at(0, c.s), f[0]);
@@ -441,6 +428,7 @@ void launch_local(cudaStream_t st, const DField& src, const DField& dst, const d
   if (L.ncells <= L.cell_begin) return;
   uint32_t soff = 0;
   if (aos_contiguous(src, L, &soff)) {
+    if (launch_aos_local_stream(st, src, dst, L, op, rd_opp, wr_opp, soff)) return;
     const unsigned g = grid_for(L.ncells - L.cell_begin);
     LBM_DISPATCH(src, {
       if constexpr (A) {
@@ -469,6 +457,7 @@ void launch_local(cudaStream_t st, const DField& src, const DField& dst, const d
 
 void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L) {
   if (L.ncells <= L.cell_begin) return;
+  if (launch_aos_window(st, kWinModeStream, b, a, L, TrtHost{})) return;
   uint32_t soff = 0;
   if (aos_contiguous(a, L, &soff)) {
     LBM_DISPATCH(a, {
@@ -486,6 +475,7 @@ void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const d
 void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op, bool streaming, bool two_s) {
   if (L.ncells <= L.cell_begin) return;
+  if (launch_aos_window(st, kWinModePull, a, b, L, op)) return;
   uint32_t soff = 0;
   if (aos_contiguous(a, L, &soff)) {
     // the staged store writes whole 16-byte vectors: store order (1S/2S) and
@@ -512,6 +502,7 @@ void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev
 void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev::Lat& L,
                     const TrtHost& op) {
   if (L.ncells <= L.cell_begin) return;
+  if (launch_aos_window(st, kWinModePush, a, b, L, op)) return;
   uint32_t soff = 0;
   if (aos_contiguous(a, L, &soff)) {
     LBM_DISPATCH(a, {
@@ -529,6 +520,7 @@ void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev
 
 void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op) {
   if (L.ncells <= L.cell_begin) return;
+  if (launch_aos_window(st, kWinModeAaOdd, f, f, L, op)) return;
   LBM_DISPATCH(f, {
     k_aa_odd<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
   });

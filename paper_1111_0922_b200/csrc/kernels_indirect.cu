@@ -12,20 +12,6 @@ using namespace dev;
 
 namespace {
 
-template <class T>
-Trt<T> cast_op(const TrtHost& h) {
-  Trt<T> o;
-  o.lambda_e = (T)h.lambda_e;
-  o.le_half = (T)h.le_half;
-  o.lo_half = (T)h.lo_half;
-  o.w0 = (T)h.w0;
-  for (int p = 0; p < 9; ++p) {
-    o.w2[p] = (T)h.w2[p];
-    o.f3w[p] = (T)h.f3w[p];
-  }
-  return o;
-}
-
 inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
 
 __device__ __forceinline__ uint32_t ldidx(const uint32_t* p) { return __ldg(p); }

@@ -72,6 +72,15 @@ void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const T
                     int delta);
 void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, const int* dirs,
                        uint32_t src, uint32_t dst, int writer_z);
+// AoS window kernels (kernels_aos.cu): tile + halo planes staged in shared
+// memory. Returns false (nothing launched) where they do not apply.
+enum WinModeId : int { kWinModePull = 0, kWinModeStream = 1, kWinModePush = 2, kWinModeAaOdd = 3 };
+bool launch_aos_window(cudaStream_t st, int mode, const DField& src, const DField& dst,
+                       const dev::Lat& L, const TrtHost& op);
+// local AoS sweep over contiguous records (storage index = cell + soff)
+bool launch_aos_local_stream(cudaStream_t st, const DField& src, const DField& dst,
+                             const dev::Lat& L, const TrtHost& op, bool rd_opp, bool wr_opp,
+                             uint32_t soff);
 // ---- indirect (IDX) addressing ---------------------------------------------
 struct Idx {
   const uint32_t* adj;  // transposed [18][n]: adj[(i-1)*n + node]
