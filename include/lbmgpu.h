@@ -185,6 +185,12 @@ int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t al
                         lbmgpu_verify_entry* entries, int32_t capacity, int32_t* count,
                         int32_t* all_pass);
 
+/* Device self-test of the collision's shared-reciprocal division against
+ * __ddiv_rn: n seeded inputs (random bit patterns, collision-like ranges,
+ * signed zeros, denormals, infinities, NaNs); *mismatches = results whose
+ * bit patterns differ. */
+int lbmgpu_selftest_division(uint64_t n, uint64_t seed, int32_t device, uint64_t* mismatches);
+
 /* kernel_available (p/src/stepper.cpp:140-153): 10 direct + 6 indirect */
 int lbmgpu_kernel_available(int32_t scheme, int32_t addressing);
 /* the same including the GPU extensions (TS / SWAP indirect) */

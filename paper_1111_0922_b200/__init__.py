@@ -114,6 +114,8 @@ _sig = {
     "lbmgpu_host_free": (C.c_int, [_P]),
     "lbmgpu_run_bench": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
+    "lbmgpu_selftest_division": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int32,
+                                           C.POINTER(C.c_uint64)]),
     "lbmgpu_verify_suite": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32,
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "lbmgpu_last_error": (C.c_char_p, []),
@@ -464,6 +466,14 @@ class VerifyEntry:
     bitwise: bool
     passed: bool
     max_rel_linf: float
+
+
+def selftest_division(n: int = 1 << 26, seed: int = 1, device: int = 0) -> int:
+    """Mismatching bit patterns of the collision's shared-reciprocal division
+    against __ddiv_rn over n seeded inputs (lbmgpu_selftest_division)."""
+    m = C.c_uint64()
+    _check(_L.lbmgpu_selftest_division(n, seed, device, C.byref(m)))
+    return m.value
 
 
 def verify_suite(seed: int = 42, steps: int = 10, device: int = 0, all_variants: bool = False):

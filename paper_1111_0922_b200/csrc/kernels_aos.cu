@@ -108,26 +108,37 @@ __device__ __forceinline__ void copy_out(T* g, const T* s, int n, int lane) {
   if (t0 + lane < n) g[t0 + lane] = s[t0 + lane];
 }
 
-// storage index of cell (0, y, z) after periodic wrap; false if beyond a wall
-__device__ __forceinline__ bool row_base(const Lat& L, int y, int z, uint32_t& rb) {
-  if (y < 0 || y >= L.ny) {
-    if (L.wall[1]) return false;
-    y = y < 0 ? y + L.ny : y - L.ny;
+// window position p on one axis (cell coordinate, may be -1 or n) -> storage
+// coordinate; false when no record is stored there (a wall axis without a
+// halo). Halo axes (ET: wall axes carry one mailbox layer, o = 1) keep the
+// position, periodic axes wrap.
+__device__ __forceinline__ bool axis_pos(int p, int n, bool wall, int o, int& st) {
+  if ((p < 0 || p >= n) && !o) {
+    if (wall) return false;
+    p = p < 0 ? p + n : p - n;
   }
-  if (z < 0 || z >= L.nz) {
-    if (L.wall[2]) return false;
-    z = z < 0 ? z + L.nz : z - L.nz;
-  }
-  rb = (uint32_t)L.nx * ((uint32_t)y + (uint32_t)L.ny * (uint32_t)z);
+  st = p + o;
   return true;
 }
-// wrapped x of window column rx; false if beyond a wall
-__device__ __forceinline__ bool col_x(const Lat& L, int x0, int rx, int& x) {
-  x = x0 - 1 + rx;
-  if (x < 0 || x >= L.nx) {
-    if (L.wall[0]) return false;
-    x = x < 0 ? x + L.nx : x - L.nx;
+// storage index of the record at storage x = 0 of window row (y, z)
+__device__ __forceinline__ bool row_base(const Lat& L, int y, int z, uint32_t& rb) {
+  int ys, zs;
+  if (!axis_pos(y, L.ny, L.wall[1], L.oy, ys) || !axis_pos(z, L.nz, L.wall[2], L.oz, zs))
+    return false;
+  rb = (uint32_t)L.sx * ((uint32_t)ys + (uint32_t)L.sy * (uint32_t)zs);
+  return true;
+}
+// storage x of window column rx
+__device__ __forceinline__ bool col_xs(const Lat& L, int x0, int rx, int& xs) {
+  return axis_pos(x0 - 1 + rx, L.nx, L.wall[0], L.ox, xs);
+}
+// cell coordinate (wrapped) of a window position, false outside the domain
+__device__ __forceinline__ bool axis_cell(int p, int n, bool wall, int o, int& c) {
+  if (p < 0 || p >= n) {
+    if (o || wall) return false;
+    p = p < 0 ? p + n : p - n;
   }
+  c = p;
   return true;
 }
 // links of an in-range cell (resolve_link, p/src/geometry.cpp:49-60)
@@ -149,6 +160,20 @@ struct Tile {
   int x0, y0, txv, tyv, zb, ze;
 };
 
+// the record at window (rx, r, z) is an in-domain fluid cell; its links
+__device__ __forceinline__ bool win_cell(const Lat& L, const Tile& t, int rx, int r, int z,
+                                         uint32_t& bounce) {
+  int x, y, zc;
+  if (!axis_cell(t.x0 - 1 + rx, L.nx, L.wall[0], L.ox, x) ||
+      !axis_cell(t.y0 - 1 + r, L.ny, L.wall[1], L.oy, y) ||
+      !axis_cell(z, L.nz, L.wall[2], L.oz, zc))
+    return false;
+  return cell_links(L, x, y, zc, bounce);
+}
+__device__ __forceinline__ bool in_block(const Tile& t, int rx, int r, int z) {
+  return rx >= 1 && rx <= t.txv && r >= 1 && r <= t.tyv && z >= t.zb && z < t.ze;
+}
+
 // issue the cp.async copies of window plane z (cell z, may be -1 / nz)
 template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
@@ -158,13 +183,13 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
     uint32_t rb;
     int phase = 0;
     if (row_base(L, t.y0 - 1 + r, z, rb)) {
-      const long long v0 = (long long)rb + t.x0 - 1;  // record under window column 0
+      const long long v0 = (long long)rb + L.ox + t.x0 - 1;  // record under window column 0
       phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
       T* srow = buf + r * WinSz<T>::ROW + phase;
-      const int xa = max(t.x0 - 1, 0), xb = min(t.x0 + t.txv, L.nx - 1);
-      copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)xa) * 19, (xb - xa + 1) * 19,
-              lane);
-      if (!L.wall[0]) {
+      const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
+      copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
+              (xb - xa + 1) * 19, lane);
+      if (!L.wall[0] && !L.ox) {
         if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
         if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
       }
@@ -177,19 +202,11 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
 template <class T>
 __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T* buf,
                                               const int* ph, const Tile& t, int z) {
-  if ((z < 0 || z >= L.nz) && L.wall[2]) return;
-  const int zw = z < 0 ? z + L.nz : (z >= L.nz ? z - L.nz : z);
   const int w = t.txv + 2, n = w * (t.tyv + 2);
   for (int q = threadIdx.x; q < n; q += kWinThreads) {
     const int r = q / w, rx = q - r * w;
-    int x, y = t.y0 - 1 + r;
-    if (y < 0 || y >= L.ny) {
-      if (L.wall[1]) continue;
-      y = y < 0 ? y + L.ny : y - L.ny;
-    }
-    if (!col_x(L, t.x0, rx, x)) continue;
     uint32_t bounce;
-    if (!cell_links(L, x, y, zw, bounce)) continue;
+    if (!win_cell(L, t, rx, r, z, bounce)) continue;
     T* rec = buf + r * WinSz<T>::ROW + ph[r] + rx * 19;
     T f[19];
 #pragma unroll
@@ -206,13 +223,28 @@ __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T*
 // records are owned whole (one 16-byte vector run plus the 4 rim columns
 // 0, 1, txv, txv+1 slot by slot). Lanes first compute the 19-bit ownership
 // mask of each of the item's columns (into msk), then store element-parallel
-// (coalesced, with holes).
+// (coalesced, with holes). A slot is written back when the node that writes
+// it in this sweep belongs to the block: slot (k, R) is written by R if link
+// opp k of R bounces, else by R - c_k. (The same machinery for ET, whose
+// every sweep is in place, measured slower than the per-thread ET kernel:
+// 0.23 vs 0.28 of the roofline on C1 AoS fp64, so ET keeps that kernel.)
+__device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int rx, int r, int z) {
+  uint32_t bR = 0;
+  if (!win_cell(L, t, rx, r, z, bR)) return 0;  // solids and halo records are never written
+  const bool selfin = in_block(t, rx, r, z);
+  uint32_t m = selfin ? 1u : 0u;
+#pragma unroll
+  for (int k = 1; k < 19; ++k) {
+    const bool own = ((bR >> opp(k)) & 1u) ? selfin : in_block(t, rx - cx(k), r - cy(k), z - cz(k));
+    m |= own ? (1u << k) : 0u;
+  }
+  return m;
+}
+
 template <class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
                                                 const int* ph, uint32_t* msk, const Tile& t,
                                                 int z) {
-  if ((z < 0 || z >= L.nz) && L.wall[2]) return;
-  const int zw = z < 0 ? z + L.nz : (z >= L.nz ? z - L.nz : z);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
   const int w = t.txv + 2, rows = t.tyv + 2;
@@ -239,46 +271,26 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
     }
     uint32_t rb;
     if (!row_base(L, t.y0 - 1 + r, z, rb)) continue;
-    int y = t.y0 - 1 + r;
-    y = y < 0 ? y + L.ny : (y >= L.ny ? y - L.ny : y);
     const T* srow = buf + r * WinSz<T>::ROW + ph[r];
     // column q of the item: [c0, c1) directly, or the rim list of a run row
     auto col_of = [&](int q) { return run ? (q < 2 ? q : t.txv + q - 2) : q; };
     uint32_t* mk = msk + warp * kWC;
     for (int q = c0 + lane; q < c1; q += 32) {
-      const int rx = col_of(q);
-      uint32_t m = 0;
-      int x;
-      uint32_t bounce;
-      if (col_x(L, t.x0, rx, x) && cell_links(L, x, y, zw, bounce)) {
-        const bool self_in =
-            rx >= 1 && rx <= t.txv && r >= 1 && r <= t.tyv && z >= t.zb && z < t.ze;
-        m = self_in ? 1u : 0u;
-#pragma unroll
-        for (int k = 1; k < 19; ++k) {
-          bool own;
-          if ((bounce >> opp(k)) & 1u) {
-            own = self_in;
-          } else {
-            const int ox = rx - cx(k), oy = r - cy(k), oz = z - cz(k);
-            own = ox >= 1 && ox <= t.txv && oy >= 1 && oy <= t.tyv && oz >= t.zb && oz < t.ze;
-          }
-          m |= own ? (1u << k) : 0u;
-        }
-      }  // beyond a wall or solid: never written
-      mk[q - c0] = m;
+      int xs;
+      mk[q - c0] = col_xs(L, t.x0, col_of(q), xs) ? owned_slots(L, t, col_of(q), r, z) : 0u;
     }
     __syncwarp();
     if (run)
-      copy_out(g + ((size_t)rb + (size_t)(t.x0 + 1)) * 19, srow + 2 * 19, (t.txv - 2) * 19, lane);
+      copy_out(g + ((size_t)rb + (size_t)(L.ox + t.x0 + 1)) * 19, srow + 2 * 19, (t.txv - 2) * 19,
+               lane);
     const int n = (c1 - c0) * 19;
     for (int e = lane; e < n; e += 32) {
       const int qq = e / 19, k = e - qq * 19;
       if (!((mk[qq] >> k) & 1u)) continue;
       const int rx = col_of(c0 + qq);
-      int x = t.x0 - 1 + rx;
-      x = x < 0 ? x + L.nx : (x >= L.nx ? x - L.nx : x);
-      g[((size_t)rb + (size_t)x) * 19 + k] = srow[rx * 19 + k];
+      int xs;
+      col_xs(L, t.x0, rx, xs);
+      g[((size_t)rb + (size_t)xs) * 19 + k] = srow[rx * 19 + k];
     }
     __syncwarp();
   }
@@ -395,7 +407,7 @@ __global__ void __launch_bounds__(kWinThreads, sizeof(T) == 8 ? 1 : 2)
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
       row_base(L, t.y0 + ty, z, rb);
-      const long long v0 = (long long)rb + t.x0;
+      const long long v0 = (long long)rb + L.ox + t.x0;
       const int phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
       T* srow = sm + slot(z - 1) * BUF + ty * ROW + phase;
       if (tx < t.txv) {
@@ -520,13 +532,17 @@ static int window_chunk(const Lat& L, bool fp64, bool inplace) {
   return (int)std::max(1LL, std::min<long long>(zc, L.nz));
 }
 
-// Applicability: AoS, plain x-fastest storage (no halo/padding/ghost planes),
-// the whole lattice in one launch. In place additionally needs every window
-// position to be a distinct record (periodic nx >= 34, ny >= 10, nz >= 3).
+// Applicability: AoS, x-fastest storage (a one-layer halo is allowed on wall
+// axes), the whole lattice in one launch. In place additionally needs every
+// window position to be a distinct record (periodic nx >= 34, ny >= 10,
+// nz >= 3).
 bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField& b,
                        const Lat& L, const TrtHost& op) {
   if (!a.aos || !window_enabled()) return false;
-  if (L.sx != L.nx || L.sy != L.ny || L.ox || L.oy || L.oz || L.zghost || L.znowrap) return false;
+  const int o[3] = {L.ox, L.oy, L.oz};
+  for (int k = 0; k < 3; ++k)
+    if (o[k] < 0 || o[k] > 1 || (o[k] && !L.wall[k])) return false;
+  if (L.sx != L.nx + 2 * L.ox || L.sy != L.ny + 2 * L.oy || L.zghost || L.znowrap) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
     return false;
   const bool inplace = mode == kWinAaOdd;
@@ -535,21 +551,19 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     return false;
   const bool f64 = a.prec == Prec::f64;
   const int zc = window_chunk(L, f64, inplace);
-  if (f64) {
-    switch (mode) {
-      case kWinPull: launch_win<double, kWinPull>(st, a, b, L, op, zc); break;
-      case kWinStream: launch_win<double, kWinStream>(st, a, b, L, op, zc); break;
-      case kWinPush: launch_win<double, kWinPush>(st, a, b, L, op, zc); break;
-      default: launch_win<double, kWinAaOdd>(st, a, b, L, op, zc); break;
-    }
-  } else {
-    switch (mode) {
-      case kWinPull: launch_win<float, kWinPull>(st, a, b, L, op, zc); break;
-      case kWinStream: launch_win<float, kWinStream>(st, a, b, L, op, zc); break;
-      case kWinPush: launch_win<float, kWinPush>(st, a, b, L, op, zc); break;
-      default: launch_win<float, kWinAaOdd>(st, a, b, L, op, zc); break;
-    }
+#define LBM_WIN_CASES(T)                                                \
+  switch (mode) {                                                       \
+    case kWinPull: launch_win<T, kWinPull>(st, a, b, L, op, zc); break;     \
+    case kWinStream: launch_win<T, kWinStream>(st, a, b, L, op, zc); break; \
+    case kWinPush: launch_win<T, kWinPush>(st, a, b, L, op, zc); break;     \
+    default: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc); break;          \
   }
+  if (f64) {
+    LBM_WIN_CASES(double)
+  } else {
+    LBM_WIN_CASES(float)
+  }
+#undef LBM_WIN_CASES
   return true;
 }
 

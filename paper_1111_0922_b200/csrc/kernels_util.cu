@@ -15,6 +15,8 @@
 #include "dispatch.h"
 #include "launch.h"
 
+#include <stdexcept>
+
 namespace lbmgpu {
 using namespace dev;
 
@@ -26,12 +28,17 @@ __device__ __forceinline__ double weight(int i) {
   return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0);
 }
 
-// counter-based uniform in [-1, 1): splitmix64 of (seed, stream)
-__device__ __forceinline__ double urand(unsigned long long seed, unsigned long long stream) {
+// splitmix64 of (seed, stream)
+__device__ __forceinline__ unsigned long long urand_bits(unsigned long long seed,
+                                                         unsigned long long stream) {
   unsigned long long z = seed + 0x9e3779b97f4a7c15ull * (stream + 1);
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  z ^= z >> 31;
+  return z ^ (z >> 31);
+}
+// counter-based uniform in [-1, 1)
+__device__ __forceinline__ double urand(unsigned long long seed, unsigned long long stream) {
+  const unsigned long long z = urand_bits(seed, stream);
   return __dsub_rn(__dmul_rn((double)(z >> 11), 0x1.0p-52), 1.0);
 }
 
@@ -529,6 +536,50 @@ void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::
     k_load_idx<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), I, Lcells, cell_of_node,
                                                          n0, count, mode, buf, init);
   });
+}
+
+// ---- division self-test -----------------------------------------------------
+namespace {
+__device__ double test_value(uint64_t h, int kind) {
+  const uint64_t r = h >> 11;
+  const double u = (double)r * 0x1.0p-53;  // [0, 1)
+  switch (kind) {
+    case 0: return __longlong_as_double((long long)h);                       // any bit pattern
+    case 1: return 1.0 + (u - 0.5) * 1e-2;                                   // rho-like
+    case 2: return (u - 0.5) * ldexp(1.0, (int)(h & 127) - 100);             // momenta, wide range
+    case 3: return (h & 1) ? -0.0 : 0.0;                                     // signed zeros
+    case 4: return ldexp(u, -1030);                                          // denormals
+    case 5: return (h & 1) ? -INFINITY : INFINITY;
+    case 6: return __longlong_as_double(0x7ff8000000000000LL | (long long)(h & 0xfffff));
+    default: return ldexp(1.0 + u, (int)(h % 2046) - 1022);                  // any normal
+  }
+}
+__global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long* bad) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h1 = urand_bits(seed, 2 * k), h2 = urand_bits(seed, 2 * k + 1);
+    // numerator kinds weighted towards the collision's (2, 3), denominator rho-like
+    const int ka = (int)((h1 >> 3) % 10), kb = (int)((h2 >> 3) % 10);
+    const int kinds_a[10] = {0, 2, 2, 2, 3, 4, 5, 6, 7, 1};
+    const int kinds_b[10] = {1, 1, 1, 1, 1, 7, 0, 4, 5, 2};
+    const double a = test_value(h1, kinds_a[ka]), b = test_value(h2 * 0x9e3779b97f4a7c15ull, kinds_b[kb]);
+    const double want = __ddiv_rn(a, b);
+    const double got = dev::div_by(a, dev::rcp_prep(b));
+    if (__double_as_longlong(got) != __double_as_longlong(want)) atomicAdd(bad, 1ull);
+  }
+}
+}  // namespace
+
+uint64_t selftest_division(uint64_t n, uint64_t seed) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+  cudaMemset(d, 0, sizeof(*d));
+  k_selftest_div<<<1184, 256>>>(n, seed, d);
+  unsigned long long h = 0;
+  const cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  return h;
 }
 
 void launch_fill(cudaStream_t st, const DField& f, long long count, double v) {

@@ -128,6 +128,8 @@ void launch_extract_idx(cudaStream_t st, const DField& f, const Idx& I, uint32_t
 void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::Lat& Lcells,
                      const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
                      const double* buf, const InitSpec& init);
+// mismatches of the shared-reciprocal division against __ddiv_rn (synchronous)
+uint64_t selftest_division(uint64_t n, uint64_t seed);
 void launch_fill(cudaStream_t st, const DField& f, long long count, double v);
 
 // ---- geometry / IDX construction -------------------------------------------

@@ -1936,6 +1936,14 @@ int lbmgpu_run_bench(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgp
 // (optionally also AoS and fp32) against the GPU two-step reference on the
 // seeded geometry, compared after every step; fp64 must be bitwise (1e-13
 // relative is the reference's recorded fallback), fp32 within 1e-5.
+int lbmgpu_selftest_division(uint64_t n, uint64_t seed, int32_t device, uint64_t* mismatches) {
+  return guard([&] {
+    CK(cudaSetDevice(device));
+    const uint64_t m = selftest_division(n, seed);
+    if (mismatches) *mismatches = m;
+  });
+}
+
 int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t all_variants,
                         lbmgpu_verify_entry* entries, int32_t capacity, int32_t* count,
                         int32_t* all_pass) {

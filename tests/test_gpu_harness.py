@@ -73,3 +73,10 @@ def test_poiseuille_acceptance_criterion_5(gpu, scheme, addr):
     yc = np.arange(32) + 0.5 - h / 2
     ana = p.body_force[0] / (2 * nu) * (h * h / 4 - yc * yc)
     assert np.max(np.abs(prev - ana)) / np.max(np.abs(ana)) <= 1e-6
+
+
+def test_shared_reciprocal_division_is_ddiv_rn(gpu):
+    """the collision's three divisions by rho share one reciprocal
+    (dev::rcp_prep / div_by); bit patterns must equal __ddiv_rn's on 2^26
+    seeded inputs incl. signed zeros, denormals, infinities and NaNs"""
+    assert gpu.selftest_division(1 << 26, seed=20251019) == 0
