@@ -40,6 +40,11 @@ CONFIGS = {
     # BASELINE.json configs[4]
     "c4": dict(dims=(200, 200, 200), policy=("periodic",) * 3, omega=1.0, force=(0.0, 0.0, 0.0),
                init="taylor_green", desc="C4: 200^3 periodic, BGK omega=1.0, Taylor-Green"),
+    # BASELINE.json configs[2] (porous, indirect); over z-slabs with --slabs / N>1
+    "c2": dict(dims=(256, 256, 256), policy=("periodic",) * 3, omega=1.7,
+               force=(1e-6, 0.0, 0.0), init="rest", porous=True,
+               desc="C2: 256^3 periodic, random r=8 spheres to porosity 0.40 (seed 2011), "
+                    "indirect, BGK omega=1.7, g=1e-6 x, rest start"),
     # BASELINE.json configs[3] (multi-GPU z-slabs)
     "c3": dict(dims=(512, 512, 1024), policy=("periodic",) * 3, omega=1.0,
                force=(0.0, 0.0, 0.0), init="taylor_green",
@@ -133,6 +138,15 @@ def reduce_max(dist, v):
     return float(t.item())
 
 
+def reduce_sum(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -186,6 +200,8 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
+    if cfg.get("porous"):
+        raise SystemExit("--impl reference: the porous C2 sample is not wired (use c0/c1/c3/c4)")
     budget = float(os.environ.get("LBM_REF_BUDGET_S", "90"))
     base = cpu_reference_sample(cfg, args.scheme, budget_s=budget, max_steps=args.steps)
     line = {
@@ -193,7 +209,7 @@ def run_reference_arm(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (rest start, BASELINE.json config)",
-        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": "direct",
+        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
                    "layout": "soa", "dims": list(cfg["dims"])},
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
@@ -216,7 +232,12 @@ def run_ours(args):
 
     cfg = CONFIGS[args.config]
     dims = cfg["dims"]
-    geo = L.GridGeometry(*dims, cfg["policy"])
+    if cfg.get("porous"):
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        geo = gen_random_spheres(*dims)
+        args.addressing = "indirect"
+    else:
+        geo = L.GridGeometry(*dims, cfg["policy"])
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
     opts = L.StepperOptions(layout=args.layout, precision=args.precision, device=local,
                             extensions=args.scheme in ("ts", "swap-push", "swap-pull")
@@ -311,9 +332,14 @@ def run_slabs(args, ws, rank, local, dist, L):
     if nz % ws:
         raise SystemExit(f"nz={nz} not divisible by {ws} ranks")
     z0, z1 = rank * nz // ws, (rank + 1) * nz // ws
-    geo = L.GridGeometry(nx, ny, nz, cfg["policy"])
+    if cfg.get("porous"):
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        geo = gen_random_spheres(nx, ny, nz)
+        args.addressing = "indirect"
+    else:
+        geo = L.GridGeometry(nx, ny, nz, cfg["policy"])
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
-    st = L.create_stepper(args.scheme, "direct", geo, flow,
+    st = L.create_stepper(args.scheme, args.addressing, geo, flow,
                           L.StepperOptions(device=local, z_begin=z0, z_end=z1))
     uid = [L.nccl_unique_id() if rank == 0 else None]
     if dist is not None:
@@ -321,7 +347,7 @@ def run_slabs(args, ws, rank, local, dist, L):
     st.slab_connect_nccl(uid[0], ws, rank)
     st.init_field(cfg["init"], seed=2011)
     nodes_local = st.node_count()
-    nodes = nx * ny * nz
+    nodes = int(reduce_sum(dist, nodes_local))
     st.step_n(args.warmup)
     st.synchronize()
     barrier(dist)
@@ -330,16 +356,16 @@ def run_slabs(args, ws, rank, local, dist, L):
     ms = reduce_max(dist, ms_local)
     value = nodes * args.steps / (ms * 1e-3) / 1e6
     peak, peak_src = load_peaks()
-    bpl = L.gpu_bytes_per_lup(args.scheme, "direct", 8)
+    bpl = L.gpu_bytes_per_lup(args.scheme, args.addressing, 8)
     achieved = bpl * nodes_local / (ms / args.steps * 1e-3) / 1e9
     launches = st.launches_per_step()
-    halo = 2 * 2 * 5 * nx * ny * 8  # bytes per rank per odd step, each direction
+    halo = 2 * 2 * 5 * nx * ny * 8  # bytes per rank per exchange (all-fluid planes)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MFLUP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json configs[3]; seeded device-side Taylor-Green init)",
-        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": "direct",
+        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
                    "layout": "soa", "dims": [nx, ny, nz], "fluid_nodes": nodes,
                    "parallelism": f"z-slabs x{ws} (NCCL halo, 5 slot planes/face)",
                    "l2": "inputs larger than L2, no flush needed"},

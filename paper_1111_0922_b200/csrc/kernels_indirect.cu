@@ -19,8 +19,8 @@ __device__ __forceinline__ uint32_t ldidx(const uint32_t* p) { return __ldg(p); 
 // local collision over nodes (TS collide, precollide, AA even, SWAP collide)
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
-                                                      uint32_t n, Trt<T> op) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
+                                                      uint32_t first, uint32_t n, Trt<T> op) {
+  const uint32_t node = first + blockIdx.x * kBlock + threadIdx.x;
   if (node >= n) return;
   T f[19];
 #pragma unroll
@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local_idx(Fld<T
 // direct-only, stepper.cpp:140-153): A[i][n] = src == n ? B[opp i][n] : B[i][src]
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
   T v[19];
   v[0] = ld(b.at(0, node));
 #pragma unroll
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream_idx(F
 template <class T, bool AOS, bool NT, bool TWO_S>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
                                                         Trt<T> op) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
   T f[19];
   f[0] = ld(a.at(0, node));
 #pragma unroll
@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull_idx(Fld
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
                                                         Trt<T> op) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
   T f[19];
 #pragma unroll
   for (int i = 0; i < 19; ++i) f[i] = ld(a.at(i, node));
@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push_idx(Fld
 // same 18 entries, loaded once.
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
   uint32_t e[19];
 #pragma unroll
   for (int i = 1; i < 19; ++i) e[i] = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd_idx(Fld<
 // along c_i or a mailbox slot >= N (i-link bounces), bit 31 = j-link bounces.
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op, EtBase B) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
   uint32_t rs[9];
   T f[19];
   f[0] = ld(F.at(0, node));
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, A
 // non-bounce back-half link swaps (i, n) <-> (opp i, adj[i][n]).
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap_idx(Fld<T, AOS> F, Idx I) {
-  const uint32_t node = blockIdx.x * kBlock + threadIdx.x;
-  if (node >= I.n) return;
+  const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
+  if (node >= I.end()) return;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     const int i = back_dir(k);
@@ -172,9 +172,9 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap_idx(Fld<T,
 // ---------------------------------------------------------------------------
 template <class T, bool RD_OPP, bool WR_OPP>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
-    k_local_idx_aos(Fld<T, true> src, Fld<T, true> dst, uint32_t n, Trt<T> op) {
+    k_local_idx_aos(Fld<T, true> src, Fld<T, true> dst, uint32_t first, uint32_t n, Trt<T> op) {
   __shared__ __align__(16) T sm[kBlock * 19];
-  const uint32_t n0 = blockIdx.x * kBlock;
+  const uint32_t n0 = first + blockIdx.x * kBlock;
   const uint32_t nrec = min((uint32_t)kBlock, n - n0);
   aos_stage_in(sm, src.p + (size_t)n0 * 19, nrec);
   __syncthreads();
@@ -195,8 +195,8 @@ template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_os_pull_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I, Trt<T> op) {
   __shared__ __align__(16) T sm[kBlock * 19];
-  const uint32_t n0 = blockIdx.x * kBlock;
-  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  const uint32_t n0 = I.first + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.end() - n0);
   const uint32_t k = threadIdx.x;
   if (k < nrec) {
     const uint32_t node = n0 + k;
@@ -220,8 +220,8 @@ template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_os_push_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I, Trt<T> op) {
   __shared__ __align__(16) T sm[kBlock * 19];
-  const uint32_t n0 = blockIdx.x * kBlock;
-  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  const uint32_t n0 = I.first + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.end() - n0);
   aos_stage_in(sm, a.p + (size_t)n0 * 19, nrec);
   __syncthreads();
   const uint32_t k = threadIdx.x;
@@ -243,8 +243,8 @@ template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
   __shared__ __align__(16) T sm[kBlock * 19];
-  const uint32_t n0 = blockIdx.x * kBlock;
-  const uint32_t nrec = min((uint32_t)kBlock, I.n - n0);
+  const uint32_t n0 = I.first + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.end() - n0);
   const uint32_t k = threadIdx.x;
   if (k < nrec) {
     const uint32_t node = n0 + k;
@@ -264,18 +264,29 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
 
 void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uint32_t n,
                       const TrtHost& op, bool rd_opp, bool wr_opp) {
-  if (n == 0) return;
+  launch_local_idx_range(st, src, dst, 0, n, op, rd_opp, wr_opp);
+}
+
+void launch_local_idx_range(cudaStream_t st, const DField& src, const DField& dst, uint32_t first,
+                            uint32_t n, const TrtHost& op, bool rd_opp, bool wr_opp) {
+  if (n <= first) return;
+  const unsigned g = grid_for(n - first);
   if (src.aos) {
-    const unsigned g = grid_for(n);
+    // node records are contiguous: the streamed AoS local sweep applies
+    dev::Lat L{};
+    L.cell_begin = first;
+    L.ncells = n;
+    L.linkmask = nullptr;
+    if (launch_aos_local_stream(st, src, dst, L, op, rd_opp, wr_opp, 0)) return;
     LBM_DISPATCH(src, {
       if constexpr (A) {
         auto a = fld<T, true>(src);
         auto b = fld<T, true>(dst);
         const auto o = cast_op<T>(op);
-        if (!rd_opp && !wr_opp) k_local_idx_aos<T, false, false><<<g, kBlock, 0, st>>>(a, b, n, o);
-        if (!rd_opp && wr_opp) k_local_idx_aos<T, false, true><<<g, kBlock, 0, st>>>(a, b, n, o);
-        if (rd_opp && !wr_opp) k_local_idx_aos<T, true, false><<<g, kBlock, 0, st>>>(a, b, n, o);
-        if (rd_opp && wr_opp) k_local_idx_aos<T, true, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+        if (!rd_opp && !wr_opp) k_local_idx_aos<T, false, false><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+        if (!rd_opp && wr_opp) k_local_idx_aos<T, false, true><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+        if (rd_opp && !wr_opp) k_local_idx_aos<T, true, false><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+        if (rd_opp && wr_opp) k_local_idx_aos<T, true, true><<<g, kBlock, 0, st>>>(a, b, first, n, o);
       }
     });
     return;
@@ -284,35 +295,34 @@ void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uin
     auto a = fld<T, A>(src);
     auto b = fld<T, A>(dst);
     const auto o = cast_op<T>(op);
-    const unsigned g = grid_for(n);
-    if (!rd_opp && !wr_opp) k_local_idx<T, A, false, false><<<g, kBlock, 0, st>>>(a, b, n, o);
-    if (!rd_opp && wr_opp) k_local_idx<T, A, false, true><<<g, kBlock, 0, st>>>(a, b, n, o);
-    if (rd_opp && !wr_opp) k_local_idx<T, A, true, false><<<g, kBlock, 0, st>>>(a, b, n, o);
-    if (rd_opp && wr_opp) k_local_idx<T, A, true, true><<<g, kBlock, 0, st>>>(a, b, n, o);
+    if (!rd_opp && !wr_opp) k_local_idx<T, A, false, false><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+    if (!rd_opp && wr_opp) k_local_idx<T, A, false, true><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+    if (rd_opp && !wr_opp) k_local_idx<T, A, true, false><<<g, kBlock, 0, st>>>(a, b, first, n, o);
+    if (rd_opp && wr_opp) k_local_idx<T, A, true, true><<<g, kBlock, 0, st>>>(a, b, first, n, o);
   });
 }
 
 void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I) {
-  if (I.n == 0) return;
+  if (I.count() == 0) return;
   if (a.aos) {
     LBM_DISPATCH(a, {
       if constexpr (A)
-        k_ts_stream_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I);
+        k_ts_stream_idx_aos<T><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I);
     });
     return;
   }
   LBM_DISPATCH(a, {
-    k_ts_stream_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I);
+    k_ts_stream_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I);
   });
 }
 
 void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
                         const TrtHost& op, bool streaming, bool two_s) {
-  if (I.n == 0) return;
+  if (I.count() == 0) return;
   if (a.aos) {
     LBM_DISPATCH(a, {
       if constexpr (A)
-        k_os_pull_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
+        k_os_pull_idx_aos<T><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
                                                                cast_op<T>(op));
     });
     return;
@@ -321,7 +331,7 @@ void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const
     auto fa = fld<T, A>(a);
     auto fb = fld<T, A>(b);
     const auto o = cast_op<T>(op);
-    const unsigned g = grid_for(I.n);
+    const unsigned g = grid_for(I.count());
     if (!streaming && !two_s) k_os_pull_idx<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, I, o);
     if (!streaming && two_s) k_os_pull_idx<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, I, o);
     if (streaming && !two_s) k_os_pull_idx<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, I, o);
@@ -331,39 +341,39 @@ void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const
 
 void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
                         const TrtHost& op) {
-  if (I.n == 0) return;
+  if (I.count() == 0) return;
   if (a.aos) {
     LBM_DISPATCH(a, {
       if constexpr (A)
-        k_os_push_idx_aos<T><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
+        k_os_push_idx_aos<T><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, true>(a), fld<T, true>(b), I,
                                                                cast_op<T>(op));
     });
     return;
   }
   LBM_DISPATCH(a, {
-    k_os_push_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I,
+    k_os_push_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), I,
                                                           cast_op<T>(op));
   });
 }
 
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
-  if (I.n == 0) return;
+  if (I.count() == 0) return;
   LBM_DISPATCH(f, {
-    k_aa_odd_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
+    k_aa_odd_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
   });
 }
 
 void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
                    const EtBase& base) {
-  if (I.n == 0) return;
+  if (I.count() == 0) return;
   LBM_DISPATCH(f, {
-    k_et_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op), base);
+    k_et_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op), base);
   });
 }
 
 void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I) {
-  if (I.n == 0) return;
-  LBM_DISPATCH(f, { k_swap_idx<T, A><<<grid_for(I.n), kBlock, 0, st>>>(fld<T, A>(f), I); });
+  if (I.count() == 0) return;
+  LBM_DISPATCH(f, { k_swap_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I); });
 }
 
 }  // namespace lbmgpu

@@ -538,6 +538,41 @@ void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::
   });
 }
 
+// ---- z-slab phase-1 merge ---------------------------------------------------
+namespace {
+template <class T>
+__global__ void k_slab_merge(T* dst, const T* src, uint32_t count, int dir, uint32_t first,
+                             const uint32_t* adj, uint32_t n, int nx, uint8_t wx, uint8_t wy,
+                             int ny) {
+  const uint32_t q = blockIdx.x * kBlock + threadIdx.x;
+  if (q >= count) return;
+  bool bounce;
+  if (adj) {
+    const uint32_t node = first + q;
+    bounce = adj[(size_t)(dir - 1) * n + node] == node;
+  } else {
+    const int x = (int)(q % (uint32_t)nx), y = (int)(q / (uint32_t)nx);
+    bounce = (wx && ((x == 0 && dev::cx(dir) < 0) || (x == nx - 1 && dev::cx(dir) > 0))) ||
+             (wy && ((y == 0 && dev::cy(dir) < 0) || (y == ny - 1 && dev::cy(dir) > 0)));
+  }
+  if (!bounce) dst[q] = src[q];
+}
+}  // namespace
+
+void launch_slab_merge(cudaStream_t st, Prec prec, void* dst, const void* src, uint32_t count,
+                       int dir, uint32_t first, const uint32_t* adj, uint32_t n, int nx, int ny,
+                       bool wx, bool wy) {
+  if (count == 0) return;
+  if (prec == Prec::f64)
+    k_slab_merge<double><<<grid_for(count), kBlock, 0, st>>>(
+        static_cast<double*>(dst), static_cast<const double*>(src), count, dir, first, adj, n, nx,
+        wx, wy, ny);
+  else
+    k_slab_merge<float><<<grid_for(count), kBlock, 0, st>>>(
+        static_cast<float*>(dst), static_cast<const float*>(src), count, dir, first, adj, n, nx,
+        wx, wy, ny);
+}
+
 // ---- division self-test -----------------------------------------------------
 namespace {
 __device__ double test_value(uint64_t h, int kind) {

@@ -85,10 +85,17 @@ bool launch_aos_local_stream(cudaStream_t st, const DField& src, const DField& d
 struct Idx {
   const uint32_t* adj;  // transposed [18][n]: adj[(i-1)*n + node]
   const uint32_t* rem;  // ET: transposed [9][n] (bit 31 = j-link bounces)
-  uint32_t n;
+  uint32_t n;           // nodes in storage (the stride of adj / rem)
+  uint32_t first = 0;   // sweeps update nodes [first, min(last, n)) (z-slabs:
+  uint32_t last = ~0u;  // the slab's own nodes, not its ghost planes)
+  __host__ __device__ uint32_t end() const { return last < n ? last : n; }
+  __host__ __device__ uint32_t count() const { return end() > first ? end() - first : 0; }
 };
 void launch_local_idx(cudaStream_t st, const DField& src, const DField& dst, uint32_t n,
                       const TrtHost& op, bool rd_opp, bool wr_opp);
+// the same over nodes [first, last)
+void launch_local_idx_range(cudaStream_t st, const DField& src, const DField& dst, uint32_t first,
+                            uint32_t last, const TrtHost& op, bool rd_opp, bool wr_opp);
 void launch_ts_stream_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I);
 void launch_os_pull_idx(cudaStream_t st, const DField& a, const DField& b, const Idx& I,
                         const TrtHost& op, bool streaming, bool two_s);
@@ -128,6 +135,13 @@ void launch_extract_idx(cudaStream_t st, const DField& f, const Idx& I, uint32_t
 void launch_load_idx(cudaStream_t st, const DField& f, const Idx& I, const dev::Lat& Lcells,
                      const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
                      const double* buf, const InitSpec& init);
+// z-slab phase 1 into an owner plane: dst[q] = src[q] unless the owner node's
+// link `dir` bounces (then the owner wrote that slot itself). Indirect: node
+// first + q, bounce = adj[dir-1][node] == node; direct: cell q of an nx*ny
+// plane against the x/y walls.
+void launch_slab_merge(cudaStream_t st, Prec prec, void* dst, const void* src, uint32_t count,
+                       int dir, uint32_t first, const uint32_t* adj, uint32_t n, int nx, int ny,
+                       bool wx, bool wy);
 // mismatches of the shared-reciprocal division against __ddiv_rn (synchronous)
 uint64_t selftest_division(uint64_t n, uint64_t seed);
 void launch_fill(cudaStream_t st, const DField& f, long long count, double v);

@@ -232,6 +232,9 @@ class Stepper {
   virtual bool exchange_opposite_handles() { return false; }
   virtual uint64_t pdf_bytes() const = 0;
   virtual uint64_t idx_bytes() const { return 0; }
+  // nodes of the canonical snapshot (a z-slab on indirect addressing stores
+  // ghost-plane nodes besides its own)
+  virtual uint64_t snapshot_nodes() const { return nodes_; }
 
   void step(long long n) {
     CK(cudaSetDevice(opt_.device));
@@ -249,8 +252,9 @@ class Stepper {
   // [first, first + count) selects a node range (out holds count*19 values)
   void extract(double* out, bool out_on_device, uint64_t first = 0, uint64_t count = ~0ull) {
     CK(cudaSetDevice(opt_.device));
-    if (count == ~0ull) count = nodes_ - std::min(first, nodes_);
-    if (first > nodes_ || count > nodes_ - first)
+    const uint64_t nsnap = snapshot_nodes();
+    if (count == ~0ull) count = nsnap - std::min(first, nsnap);
+    if (first > nsnap || count > nsnap - first)
       throw std::invalid_argument("node range outside the snapshot");
     before_extract();
     const uint64_t ch = chunk_nodes();
@@ -340,13 +344,14 @@ class Stepper {
     return stage_.get<double>();
   }
   uint32_t chunk_nodes() const {
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(nodes_, uint64_t{1} << 20));
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(snapshot_nodes(), uint64_t{1} << 20));
   }
   template <class F>
   void for_chunks(F&& f) {
     const uint32_t ch = chunk_nodes();
-    for (uint64_t n0 = 0; n0 < nodes_; n0 += ch)
-      f((uint32_t)n0, (uint32_t)std::min<uint64_t>(ch, nodes_ - n0));
+    const uint64_t nsnap = snapshot_nodes();
+    for (uint64_t n0 = 0; n0 < nsnap; n0 += ch)
+      f((uint32_t)n0, (uint32_t)std::min<uint64_t>(ch, nsnap - n0));
   }
 
   // fluid enumeration x-fastest (build_sparse, p/src/geometry.cpp:187-194)
@@ -787,6 +792,7 @@ class IndirectStepper : public Stepper {
     launch_load_idx(stream_, f, I_, Lcells_, cell_of_node(), n0, cnt, mode, d, in);
   }
   uint64_t idx_bytes() const override { return adj_.bytes(); }
+  size_t elem_bytes() const { return esize(); }
   DevMem adj_;
   Idx I_;
   dev::Lat Lcells_;
@@ -1133,13 +1139,48 @@ class SlabStepper final : public Stepper {
     two_s_ = o.scheme == LBMGPU_OSNT_PULL_2S;
     nzl_ = z1_ - z0_;
     plane_ = (uint64_t)g.nx * g.ny;
-    L_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
-    L_.zghost = 1;
-    L_.oz = 1;
-    L_.wall[2] = 0;
-    storage_ = plane_ * (nzl_ + 2);
+    idx_ = o.addressing == LBMGPU_INDIRECT;
+    if (idx_) {
+      // geo_ is the slab plus one ghost plane per face (slab_geo); its fluid
+      // nodes in x-fastest order are [lower ghost | own planes | upper ghost]
+      poff_.assign((size_t)nzl_ + 3, 0);
+      for (int k = 0; k < nzl_ + 2; ++k) {
+        uint64_t c = plane_;
+        if (geo_.solids) {
+          c = 0;
+          for (uint64_t q = 0; q < plane_; ++q) c += geo_.mask[(uint64_t)k * plane_ + q] ? 1 : 0;
+        }
+        poff_[k + 1] = poff_[k] + c;
+      }
+      if (nodes_ >= (uint64_t{1} << 31))
+        throw std::runtime_error("fluid count exceeds 32-bit index range");
+      storage_ = nodes_;
+      adj_.alloc((size_t)nodes_ * 18 * sizeof(uint32_t));
+      Lcells_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
+      launch_adjacency(stream_, geo_.solids ? mask_d_.get<uint8_t>() : nullptr, Lcells_,
+                       geo_.solids ? node_of_.get<uint32_t>() : nullptr, cell_of_node(),
+                       (uint32_t)nodes_, adj_.get<uint32_t>());
+      ck_launch();
+      I_.adj = adj_.get<uint32_t>();
+      I_.rem = nullptr;
+      I_.n = (uint32_t)nodes_;
+    } else {
+      L_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
+      L_.zghost = 1;
+      L_.oz = 1;
+      L_.wall[2] = 0;
+      storage_ = plane_ * (nzl_ + 2);
+    }
     ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt) ? 1 : 2;
     for (int k = 0; k < ngrids_; ++k) alloc_field(g_[k], storage_);
+    // an owner node whose link towards the neighbour slab bounces (x/y wall,
+    // solid) writes that face slot itself: phase 1 then merges, not copies
+    merge_ = geo_.policy[0] == 1 || geo_.policy[1] == 1 || (idx_ && geo_.solids);
+    if (merge_) {
+      maxcount_ = 0;
+      for (int pl : {0, nzl_ - 1}) maxcount_ = std::max(maxcount_, plane_count(pl));
+      rbuf_.alloc(std::max<uint64_t>(1, maxcount_) * 10 * esize());
+    }
     CK(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
     for (auto* e : {&ev_c_, &ev_halo_, &ev_odd_, &ev_back_})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -1161,15 +1202,37 @@ class SlabStepper final : public Stepper {
     const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_OS_PUSH ||
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
-    if (!ok_scheme || o.addressing != LBMGPU_DIRECT || o.layout != LBMGPU_SOA)
+    const bool idx = o.addressing == LBMGPU_INDIRECT;
+    if (!ok_scheme || o.layout != LBMGPU_SOA || (idx && o.scheme == LBMGPU_ET))
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern, ET and OS/OSNT, direct, SoA");
-    if (g.solids) throw std::invalid_argument("z-slab decomposition needs an all-fluid box");
+          "z-slab decomposition supports the AA pattern, ET and OS/OSNT (direct), "
+          "AA and OS/OSNT (indirect), SoA");
+    if (g.solids && !idx)
+      throw std::invalid_argument("z-slab decomposition needs an all-fluid box (direct)");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
+    if (o.scheme == LBMGPU_ET && (g.policy[0] != 0 || g.policy[1] != 0))
+      throw std::invalid_argument("ET z-slabs need periodic x and y (no mailbox halo)");
     if (o.z_begin < 0 || o.z_end > g.nz || o.z_end <= o.z_begin)
       throw std::invalid_argument("z-slab range must satisfy 0 <= z_begin < z_end <= nz");
     HostGeo s = g;
-    s.nz = o.z_end - o.z_begin;
+    const int nzl = o.z_end - o.z_begin;
+    if (!idx) {
+      s.nz = nzl;
+      return s;
+    }
+    // indirect: planes z_begin-1 .. z_end (wrapped) with a wall policy in z,
+    // so build_sparse links own nodes to the ghost planes and never wraps
+    s.nz = nzl + 2;
+    s.policy[2] = 1;
+    if (g.solids) {
+      const uint64_t pl = (uint64_t)g.nx * g.ny;
+      s.mask.assign(pl * (uint64_t)(nzl + 2), 0);
+      for (int k = 0; k < nzl + 2; ++k) {
+        const int gz = ((o.z_begin - 1 + k) % g.nz + g.nz) % g.nz;
+        std::copy(g.mask.begin() + (size_t)(gz * pl), g.mask.begin() + (size_t)((gz + 1) * pl),
+                  s.mask.begin() + (size_t)(k * pl));
+      }
+    }
     return s;
   }
 
@@ -1198,33 +1261,61 @@ class SlabStepper final : public Stepper {
     if (kind_ == kSlabOsPull) return active_;
     return phase == 1 ? active_ ^ 1 : active_;
   }
-  void* slot_ptr(int grid, int slot, int plane) const {
-    // storage plane = local plane + 1 (ghost below is storage plane 0)
-    return static_cast<char*>(g_[grid].get()) +
-           ((size_t)slot * soa_stride(storage_) + (size_t)(plane + 1) * plane_) * esize();
+  // local plane -1 .. nzl (ghost planes -1 and nzl): direct, storage plane
+  // + 1; indirect, the plane's node range of the extended numbering
+  uint64_t plane_first(int plane) const { return idx_ ? poff_[plane + 1] : (uint64_t)(plane + 1) * plane_; }
+  uint64_t plane_count(int plane) const {
+    return idx_ ? poff_[plane + 2] - poff_[plane + 1] : plane_;
   }
-  size_t plane_bytes() const { return plane_ * esize(); }
+  void* slot_ptr(int grid, int slot, int plane) const {
+    return static_cast<char*>(g_[grid].get()) +
+           ((size_t)slot * soa_stride(storage_) + plane_first(plane)) * esize();
+  }
+  uint64_t snapshot_nodes() const override {
+    return idx_ ? poff_[nzl_ + 1] - poff_[1] : nodes_;
+  }
+  uint64_t idx_bytes() const override { return adj_.bytes(); }
+  size_t elem_bytes() const { return esize(); }
   // storage plane of a logical slot (ET: through the handle table)
   int phys_slot(int slot) const { return kind_ == kSlabEt ? base_.b[slot] : slot; }
   void swap_base() {
     for (int q = 0; q < 9; ++q) std::swap(base_.b[kPi[q]], base_.b[kPj[q]]);
   }
 
+  // phase-1 receive into an owner plane that must be merged (see merge_)
+  bool merged(const HaloOp& op) const { return merge_ && op.phase == 1 && !op.send; }
+  void* rbuf_slot(int q) const { return static_cast<char*>(rbuf_.get()) + (size_t)q * maxcount_ * esize(); }
+  // the link of the owner node pointing at the slot's writer in the other
+  // slab: AA / OS push slot k is written by R - c_k; ET slot j by R + c_j
+  int merge_dir(const HaloOp& op) const { return kind_ == kSlabEt ? op.slot : dev::opp(op.slot); }
+  void merge_into(cudaStream_t st, int grid, const HaloOp& op, const void* src) {
+    launch_slab_merge(st, prec_, slot_ptr(grid, phys_slot(op.slot), op.plane), src,
+                      (uint32_t)plane_count(op.plane), merge_dir(op), (uint32_t)plane_first(op.plane),
+                      idx_ ? I_.adj : nullptr, idx_ ? I_.n : 0u, geo_.nx, geo_.ny,
+                      geo_.policy[0] == 1, geo_.policy[1] == 1);
+  }
+
   // NCCL phase: the plan's sends and receives in plan order, one group
   void nccl_phase(int phase, int grid) {
     Nccl& N = Nccl::get();
     const ncclDataType_t ty = prec_ == Prec::f64 ? ncclDouble : ncclFloat;
+    const std::vector<HaloOp> plan = halo_plan(kind_, nzl_);
     N.check(N.groupStart(), "ncclGroupStart");
-    for (const HaloOp& op : halo_plan(kind_, nzl_)) {
+    int q = 0;
+    for (const HaloOp& op : plan) {
       if (op.phase != phase) continue;
       const int peer = (rank_ + op.peer + nranks_) % nranks_;
-      void* p = slot_ptr(grid, phys_slot(op.slot), op.plane);
+      void* p = merged(op) ? rbuf_slot(q++) : slot_ptr(grid, phys_slot(op.slot), op.plane);
+      const size_t cnt = plane_count(op.plane);
       if (op.send)
-        N.check(N.send(p, plane_, ty, peer, nccl_, comm_), "ncclSend");
+        N.check(N.send(p, cnt, ty, peer, nccl_, comm_), "ncclSend");
       else
-        N.check(N.recv(p, plane_, ty, peer, nccl_, comm_), "ncclRecv");
+        N.check(N.recv(p, cnt, ty, peer, nccl_, comm_), "ncclRecv");
     }
     N.check(N.groupEnd(), "ncclGroupEnd");
+    q = 0;
+    for (const HaloOp& op : plan)
+      if (op.phase == phase && merged(op)) merge_into(comm_, grid, op, rbuf_slot(q++));
   }
   // comm stream runs `phase` after everything enqueued on stream_ so far
   void enqueue_phase(int phase, int grid, cudaEvent_t done) {
@@ -1245,6 +1336,25 @@ class SlabStepper final : public Stepper {
   void sweep(int za, int zb) {
     if (zb <= za) return;
     const long long st = soa_stride(storage_);
+    if (idx_) {
+      Idx I = I_;
+      I.first = (uint32_t)poff_[za + 1];
+      I.last = (uint32_t)poff_[zb + 1];
+      if (kind_ == kSlabAA) {
+        const DField f = field(g_[0], st);
+        if ((t_ & 1) == 0)
+          launch_local_idx_range(stream_, f, f, I.first, I.last, op_, false, true);
+        else
+          launch_aa_odd_idx(stream_, f, I, op_);
+      } else {
+        const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
+        if (kind_ == kSlabOsPull)
+          launch_os_pull_idx(stream_, a, b, I, op_, nt_, two_s_);
+        else
+          launch_os_push_idx(stream_, a, b, I, op_);
+      }
+      return;
+    }
     const dev::Lat L = planes(za, zb);
     if (kind_ == kSlabAA) {
       const DField f = field(g_[0], st);
@@ -1274,7 +1384,11 @@ class SlabStepper final : public Stepper {
   void precollide_if_fresh() {
     if (kind_ == kSlabOsPull && fresh_) {
       const DField a = field(g_[active_], soa_stride(storage_));
-      launch_local(stream_, a, a, planes(0, nzl_), op_, false, false);
+      if (idx_)
+        launch_local_idx_range(stream_, a, a, (uint32_t)poff_[1], (uint32_t)poff_[nzl_ + 1], op_,
+                               false, false);
+      else
+        launch_local(stream_, a, a, planes(0, nzl_), op_, false, false);
       fresh_ = false;
     }
   }
@@ -1354,6 +1468,17 @@ class SlabStepper final : public Stepper {
   }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
     const long long st = soa_stride(storage_);
+    if (idx_) {
+      const uint32_t n = (uint32_t)poff_[1] + n0;
+      if (kind_ == kSlabAA)
+        launch_extract_idx(stream_, field(g_[0], st), I_, n, c, (t_ & 1) ? kExAaOdd : kExNatural,
+                           EtBase{}, d);
+      else if (kind_ == kSlabOsPull && !fresh_)
+        launch_extract_idx(stream_, field(g_[active_ ^ 1], st), I_, n, c, kExGather, EtBase{}, d);
+      else
+        launch_extract_idx(stream_, field(g_[active_], st), I_, n, c, kExNatural, EtBase{}, d);
+      return;
+    }
     if (kind_ == kSlabAA)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
                      (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
@@ -1369,6 +1494,12 @@ class SlabStepper final : public Stepper {
   void load_range(uint32_t n0, uint32_t c, const double* d, const InitSpec& in) override {
     InitSpec s = in;
     if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
+    if (idx_) {
+      s.z0 = z0_ - 1;  // extended plane 0 is global plane z_begin - 1
+      launch_load_idx(stream_, field(g_[active_], soa_stride(storage_)), I_, Lcells_,
+                      cell_of_node(), (uint32_t)poff_[1] + n0, c, kExNatural, d, s);
+      return;
+    }
     if (kind_ == kSlabEt) {
       for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
       launch_load(stream_, field(g_[0], soa_stride(storage_)), L_, nullptr, n0, c, kExEt, d, s);
@@ -1408,6 +1539,14 @@ class SlabStepper final : public Stepper {
   bool nt_ = false, two_s_ = false, fresh_ = false;
   bool ghosts_fresh_ = false, owners_stale_ = false;
   EtBase base_;
+  bool idx_ = false;
+  bool merge_ = false;
+  uint64_t maxcount_ = 0;
+  DevMem rbuf_;
+  std::vector<uint64_t> poff_;  // indirect: node offset of extended plane k
+  DevMem adj_;
+  Idx I_{};
+  dev::Lat Lcells_{};
   uint64_t plane_ = 0, storage_ = 0;
   dev::Lat L_;
   DevMem g_[2];
@@ -1425,6 +1564,14 @@ static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_
   for (auto* s : S) s->sync();
   std::vector<std::vector<HaloOp>> plans(n);
   for (int k = 0; k < n; ++k) plans[k] = halo_plan(S[k]->kind_, S[k]->nzl_);
+  // receives that merge: (peer, op, scratch slot) applied after all copies
+  struct Pending {
+    int peer;
+    HaloOp op;
+    int q;
+  };
+  std::vector<Pending> pend;
+  std::vector<int> nq(n, 0);
   for (int k = 0; k < n; ++k) {
     std::vector<size_t> cursor(n, 0);
     const int gk = use_ghost_grid ? S[k]->ghost_grid() : S[k]->phase_grid(phase);
@@ -1441,11 +1588,25 @@ static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_
       if (c == pp.size()) throw std::runtime_error("halo plan: unmatched send");
       const HaloOp& r = pp[c++];
       const int gp = use_ghost_grid ? S[peer]->ghost_grid() : S[peer]->phase_grid(phase);
-      CK(cudaMemcpyPeerAsync(S[peer]->slot_ptr(gp, S[peer]->phys_slot(r.slot), r.plane),
-                             S[peer]->opt_.device,
+      const uint64_t cnt = S[k]->plane_count(op.plane);
+      if (cnt != S[peer]->plane_count(r.plane))
+        throw std::runtime_error("halo plan: message sizes differ between neighbours");
+      void* dst = S[peer]->slot_ptr(gp, S[peer]->phys_slot(r.slot), r.plane);
+      if (S[peer]->merged(r)) {
+        dst = S[peer]->rbuf_slot(nq[peer]);
+        pend.push_back({peer, r, nq[peer]++});
+      }
+      CK(cudaMemcpyPeerAsync(dst, S[peer]->opt_.device,
                              S[k]->slot_ptr(gk, S[k]->phys_slot(op.slot), op.plane),
-                             S[k]->opt_.device, S[k]->plane_bytes(), S[k]->stream_));
+                             S[k]->opt_.device, cnt * S[k]->elem_bytes(), S[k]->stream_));
     }
+  }
+  for (auto* s : S) s->sync();
+  for (const Pending& m : pend) {
+    SlabStepper* R = S[m.peer];
+    CK(cudaSetDevice(R->opt_.device));
+    const int g = use_ghost_grid ? R->ghost_grid() : R->phase_grid(phase);
+    R->merge_into(R->stream_, g, m.op, R->rbuf_slot(m.q));
   }
   for (auto* s : S) s->sync();
 }
@@ -1790,7 +1951,7 @@ int lbmgpu_time_step(lbmgpu_stepper* h, int64_t* t) {
   return guard([&] { *t = S(h).t_; });
 }
 int lbmgpu_node_count(lbmgpu_stepper* h, uint64_t* n) {
-  return guard([&] { *n = S(h).nodes_; });
+  return guard([&] { *n = S(h).snapshot_nodes(); });
 }
 int lbmgpu_storage_bytes(lbmgpu_stepper* h, uint64_t* pdf, uint64_t* idx) {
   return guard([&] {
@@ -1915,10 +2076,10 @@ int lbmgpu_run_bench(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgp
     std::memset(r, 0, sizeof(*r));
     r->scheme = o->scheme, r->addressing = o->addressing, r->layout = o->layout;
     r->precision = o->precision;
-    r->fluid_count = st->nodes_;
+    r->fluid_count = st->snapshot_nodes();
     r->steps = steps;
     r->seconds = sec;
-    r->mlups = (double)st->nodes_ * steps / sec / 1.0e6;  // p/src/bench.cpp:184
+    r->mlups = (double)st->snapshot_nodes() * steps / sec / 1.0e6;  // p/src/bench.cpp:184
     static const int fam[10] = {0, 1, 1, 2, 2, 3, 4, 4, 5, 6};
     int32_t cnt[6];
     double bpl = 0, gbpl = 0;

@@ -79,6 +79,11 @@ def test_slab_errors(gpu):
     with pytest.raises(ValueError, match="periodic z"):
         L.create_stepper("aap", "direct", L.gen_channel(8, 8, 8),
                          options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="ET z-slabs need periodic x and y"):
+        L.create_stepper("et", "direct", L.GridGeometry(8, 8, 8, ("wall", "periodic", "periodic")),
+                         options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="AA and OS/OSNT \\(indirect\\)"):
+        L.create_stepper("et", "indirect", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     s = L.create_stepper("aap", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(RuntimeError, match="no transport"):
         s.step()
@@ -106,3 +111,108 @@ def test_nccl_transport_single_rank_ring(gpu, scheme):
         if _needs_ghosts(scheme, s.time_step()):
             s.slab_sync_ghosts()
         assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
+
+
+def _porous(L, dims, solid=0.25, seed=5):
+    rng = np.random.default_rng(seed)
+    mask = (rng.random(dims[0] * dims[1] * dims[2]) >= solid).astype(np.uint8)
+    return L.GridGeometry(*dims, ("periodic", "periodic", "periodic"), mask)
+
+
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s"])
+@pytest.mark.parametrize("bounds", [[(0, 12)], [(0, 5), (5, 12)], [(0, 1), (1, 7), (7, 12)]])
+def test_indirect_slabs_match_single_domain(gpu, scheme, bounds):
+    """indirect z-slabs: each slab numbers its fluid nodes over its planes plus
+    one ghost plane per face, the exchanges move node ranges; porous box,
+    bitwise = the single-domain indirect stepper"""
+    L = gpu
+    dims = (20, 16, 12)
+    geo = _porous(L, dims)
+    flow = L.bgk(1.3, (1e-5, 2e-6, 0.0))
+    ref = L.create_stepper(scheme, "indirect", geo, flow)
+    ref.init_field("random", seed=4)
+    slabs = [L.create_stepper(scheme, "indirect", geo, flow,
+                              L.StepperOptions(z_begin=a, z_end=b)) for a, b in bounds]
+    for s in slabs:
+        s.init_field("random", seed=4)
+    assert sum(s.node_count() for s in slabs) == ref.node_count()
+    assert bitwise_equal(np.concatenate([s.extract_natural() for s in slabs]),
+                         ref.extract_natural())
+    for steps in (1, 4, 3):
+        ref.step_n(steps)
+        ref.synchronize()
+        L.slab_group_step(slabs, steps)
+        if _needs_ghosts(scheme, ref.time_step()):
+            L.slab_group_sync_ghosts(slabs)
+        got = np.concatenate([s.extract_natural() for s in slabs])
+        assert bitwise_equal(got, ref.extract_natural()), (bounds, ref.time_step())
+
+
+def test_indirect_slab_host_load(gpu):
+    L = gpu
+    dims = (16, 12, 10)
+    geo = _porous(L, dims, 0.3, seed=9)
+    flow = L.bgk(1.7, (1e-6, 0, 0))
+    ref = L.create_stepper("aap", "indirect", geo, flow)
+    ref.init_field("random", seed=3)
+    f0 = ref.extract_natural()
+    bounds = [(0, 3), (3, 10)]
+    slabs = [L.create_stepper("aap", "indirect", geo, flow, L.StepperOptions(z_begin=a, z_end=b))
+             for a, b in bounds]
+    k = 0
+    for s in slabs:
+        n = s.node_count()
+        s.load_natural(f0[k * 19:(k + n) * 19])
+        k += n
+    ref.step_n(5)
+    ref.synchronize()
+    L.slab_group_step(slabs, 5)
+    L.slab_group_sync_ghosts(slabs)
+    assert bitwise_equal(np.concatenate([s.extract_natural() for s in slabs]),
+                         ref.extract_natural())
+
+
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push"])
+def test_indirect_nccl_single_rank_ring(gpu, scheme):
+    L = gpu
+    dims = (24, 20, 14)
+    geo = _porous(L, dims, 0.2, seed=2)
+    flow = L.bgk(1.0)
+    ref = L.create_stepper(scheme, "indirect", geo, flow)
+    ref.init_field("taylor_green", seed=9, u0=0.05)
+    s = L.create_stepper(scheme, "indirect", geo, flow, L.StepperOptions(z_begin=0, z_end=dims[2]))
+    s.slab_connect_nccl(L.nccl_unique_id(), 1, 0)
+    s.init_field("taylor_green", seed=9, u0=0.05)
+    for steps in (6, 3):
+        ref.step_n(steps)
+        ref.synchronize()
+        s.step_n(steps)
+        s.synchronize()
+        if _needs_ghosts(scheme, s.time_step()):
+            s.slab_sync_ghosts()
+        assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
+
+
+@pytest.mark.parametrize("scheme", ["aap", "os-push", "os-pull"])
+def test_direct_slabs_with_xy_walls(gpu, scheme):
+    """x/y walls: an owner node whose link towards the neighbour slab bounces
+    writes that face slot itself, so phase 1 merges instead of copying"""
+    L = gpu
+    dims = (20, 14, 12)
+    geo = L.GridGeometry(*dims, ("wall", "wall", "periodic"))
+    flow = L.bgk(1.7, (1e-5, 0, 2e-6))
+    ref = L.create_stepper(scheme, "direct", geo, flow)
+    ref.init_field("random", seed=8)
+    bounds = [(0, 4), (4, 9), (9, 12)]
+    slabs = [L.create_stepper(scheme, "direct", geo, flow, L.StepperOptions(z_begin=a, z_end=b))
+             for a, b in bounds]
+    for s in slabs:
+        s.init_field("random", seed=8)
+    for steps in (1, 4, 3):
+        ref.step_n(steps)
+        ref.synchronize()
+        L.slab_group_step(slabs, steps)
+        if _needs_ghosts(scheme, ref.time_step()):
+            L.slab_group_sync_ghosts(slabs)
+        assert bitwise_equal(np.concatenate([s.extract_natural() for s in slabs]),
+                             ref.extract_natural()), ref.time_step()
