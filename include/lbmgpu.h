@@ -186,9 +186,9 @@ int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t al
                         int32_t* all_pass);
 
 /* Device self-test of the collision's shared-reciprocal division against
- * __ddiv_rn: n seeded inputs (random bit patterns, collision-like ranges,
- * signed zeros, denormals, infinities, NaNs); *mismatches = results whose
- * bit patterns differ. */
+ * __ddiv_rn (fp64) and __fdiv_rn (fp32): n seeded inputs (random bit
+ * patterns, collision-like ranges, signed zeros, denormals, infinities,
+ * NaNs); *mismatches = results whose bit patterns differ. */
 int lbmgpu_selftest_division(uint64_t n, uint64_t seed, int32_t device, uint64_t* mismatches);
 
 /* kernel_available (p/src/stepper.cpp:140-153): 10 direct + 6 indirect */

@@ -601,6 +601,12 @@ __global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long* ba
     const double want = __ddiv_rn(a, b);
     const double got = dev::div_by(a, dev::rcp_prep(b));
     if (__double_as_longlong(got) != __double_as_longlong(want)) atomicAdd(bad, 1ull);
+    // fp32: the same inputs rounded to float, plus float-range momenta
+    const float af = (k & 1) ? (float)a : (float)test_value(h1 ^ 0x5bd1e995ull, 2) * 1e-3f;
+    const float bf = (float)b;
+    const float wantf = __fdiv_rn(af, bf);
+    const float gotf = dev::div_by(af, dev::rcp_prep(bf));
+    if (__float_as_int(gotf) != __float_as_int(wantf)) atomicAdd(bad, 1ull);
   }
 }
 }  // namespace

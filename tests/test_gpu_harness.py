@@ -77,6 +77,7 @@ def test_poiseuille_acceptance_criterion_5(gpu, scheme, addr):
 
 def test_shared_reciprocal_division_is_ddiv_rn(gpu):
     """the collision's three divisions by rho share one reciprocal
-    (dev::rcp_prep / div_by); bit patterns must equal __ddiv_rn's on 2^26
-    seeded inputs incl. signed zeros, denormals, infinities and NaNs"""
+    (dev::rcp_prep / div_by, fp64 and fp32); bit patterns must equal
+    __ddiv_rn's / __fdiv_rn's on 2^26 seeded inputs incl. signed zeros,
+    denormals, infinities and NaNs"""
     assert gpu.selftest_division(1 << 26, seed=20251019) == 0
