@@ -8,6 +8,8 @@
 #include "dispatch.h"
 #include "launch.h"
 
+#include <stdexcept>
+
 namespace lbmgpu {
 using namespace dev;
 
@@ -163,37 +165,36 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, A
 // tmp_i = F[b_i][X], tmp_j = F[b_(db?i:j)][X + c_i]; collide;
 // F[b_(ub?j:i)][X] = tmp_j, F[b_j][X + c_i] = tmp_i. Wall axes carry a halo
 // plane, solid cells act as mailboxes, so X + c_i is always a storage slot.
-template <bool BB, class T, bool AOS>
-__device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, const Trt<T>& op,
-                                        const EtBase& B) {
+template <bool BB, bool SW, class T, bool AOS>
+__device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, const Trt<T>& op) {
   constexpr bool NC = sizeof(T) == 4 && !AOS;
   T f[19];
   f[0] = ldsel<NC>(F.at(0, c.s));
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    f[i] = ldsel<NC>(F.at(B.b[i], c.s));
-    f[j] = ldsel<NC>(F.at((BB && c.bb(i)) ? B.b[i] : B.b[j], c.nb(i)));
+    f[i] = ldsel<NC>(F.at(hb<SW>(i), c.s));
+    f[j] = ldsel<NC>(F.at((BB && c.bb(i)) ? hb<SW>(i) : hb<SW>(j), c.nb(i)));
   }
   collide(op, f);
   st<false>(F.at(0, c.s), f[0]);
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    st<false>(F.at((BB && c.bb(j)) ? B.b[j] : B.b[i], c.s), f[j]);
-    st<false>(F.at_off(B.b[j], c.s, c.off(i)), f[i]);
+    st<false>(F.at((BB && c.bb(j)) ? hb<SW>(j) : hb<SW>(i), c.s), f[j]);
+    st<false>(F.at_off(hb<SW>(j), c.s, c.off(i)), f[i]);
   }
 }
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op, EtBase B) {
+template <class T, bool AOS, bool SW>
+__global__ void __launch_bounds__(kBlock, EtMinBlocks<T>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
   if (warp_interior(c))
-    et_body<false>(F, c, op, B);
+    et_body<false, SW>(F, c, op);
   else
-    et_body<true>(F, c, op, B);
+    et_body<true, SW>(F, c, op);
 }
 
 // SWAP link exchange (p/src/scheme_swap.cpp:172-235, fix-ups :127-131).
@@ -530,7 +531,11 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
                const EtBase& base) {
   if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(f, {
-    k_et<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), base);
+    const unsigned g = grid_for(L.ncells - L.cell_begin);
+    if (base.swapped())
+      k_et<T, A, true><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+    else
+      k_et<T, A, false><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
   });
 }
 
@@ -564,6 +569,10 @@ void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, cons
   LBM_DISPATCH(f, {
     k_swap_list<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), a, b, dir, count);
   });
+}
+
+void EtBase::throw_bad_handles() {
+  throw std::logic_error("ET handle table is neither the identity nor fully swapped");
 }
 
 }  // namespace lbmgpu

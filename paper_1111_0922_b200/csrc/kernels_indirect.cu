@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd_idx(Fld<
 
 // ET sweep, indirect (p/src/scheme_et.cpp:241-272): rem[p][n] = neighbour
 // along c_i or a mailbox slot >= N (i-link bounces), bit 31 = j-link bounces.
-template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op, EtBase B) {
+template <class T, bool AOS, bool SW>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
   const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.end()) return;
   uint32_t rs[9];
@@ -132,8 +132,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, A
     rs[p] = ldidx(I.rem + (size_t)p * I.n + node);
     const uint32_t r = rs[p] & 0x7fffffffu;
     const bool db = r >= I.n;
-    f[i] = ld(F.at(B.b[i], node));
-    f[j] = ld(F.at(db ? B.b[i] : B.b[j], r));
+    f[i] = ld(F.at(hb<SW>(i), node));
+    f[j] = ld(F.at(db ? hb<SW>(i) : hb<SW>(j), r));
   }
   collide(op, f);
   st<false>(F.at(0, node), f[0]);
@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, A
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
     const bool ub = (rs[p] & 0x80000000u) != 0;
-    st<false>(F.at(ub ? B.b[j] : B.b[i], node), f[j]);
-    st<false>(F.at(B.b[j], rs[p] & 0x7fffffffu), f[i]);
+    st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
+    st<false>(F.at(hb<SW>(j), rs[p] & 0x7fffffffu), f[i]);
   }
 }
 
@@ -367,7 +367,10 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
                    const EtBase& base) {
   if (I.count() == 0) return;
   LBM_DISPATCH(f, {
-    k_et_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op), base);
+    if (base.swapped())
+      k_et_idx<T, A, true><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
+    else
+      k_et_idx<T, A, false><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
   });
 }
 

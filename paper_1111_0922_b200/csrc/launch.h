@@ -27,6 +27,14 @@ struct TrtHost {
 
 struct EtBase {
   int8_t b[20];
+  // the table is the identity or all pairs swapped (see dev::hb)
+  bool swapped() const {
+    const bool sw = b[1] == 2;
+    for (int i = 1; i < 19; ++i)
+      if (b[i] != (sw ? dev::opp(i) : i)) throw_bad_handles();
+    return sw;
+  }
+  [[noreturn]] static void throw_bad_handles();
 };
 
 constexpr int kBlock = 256;
@@ -43,6 +51,14 @@ constexpr int kBlock = 256;
 template <class T>
 struct MinBlocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_MIN_BLOCKS_F32;
+};
+// the ET sweep (two handle lookups per pair) under its own register budget
+#ifndef LBM_ET_MIN_BLOCKS_F32
+#define LBM_ET_MIN_BLOCKS_F32 LBM_MIN_BLOCKS_F32
+#endif
+template <class T>
+struct EtMinBlocks {
+  static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_ET_MIN_BLOCKS_F32;
 };
 
 // ---- direct (full-grid) addressing -----------------------------------------

@@ -592,14 +592,21 @@ static std::vector<SeamLink> seam_links(const HostGeo& g, const int* dirs, int n
 // CG (p/src/scheme_cg.cpp): one grid, two origins S planes apart, sweeps
 // alternate the read origin (even: read S, write 0, ascending plane groups;
 // odd: read 0, write S, descending), each plane group of P < S planes one
-// push launch; z-periodic seam values land in padding planes and are copied
-// to their wrapped planes after the sweep. Storage: nz + S + 2 planes
+// push launch (P = nz/4 clamped to [16, 64]); z-periodic seam values land in
+// padding planes and are copied to their wrapped planes after the sweep.
+// Storage: nz + S + 2 planes
 // (planes 0 and nz+S+1 pad; origin o's plane z at storage z + 1 + o).
 class CgDirect final : public DirectStepper {
  public:
   CgDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
       : DirectStepper(g, p, o) {
-    P_ = std::min(16, g.nz);
+    // planes per launch: more planes, fewer launch tails, but S = P + 1
+    // extra storage planes (C1 256^3: P 16 / 32 / 64 / 128 -> 0.83 / 0.92 /
+    // 0.95 / 0.96 of the roofline fp64, 0.74 / 0.82 / 0.85 / 0.87 fp32).
+    // Default nz/4 in [16, 64]: +25% storage on 256^3; LBMGPU_CG_PLANES overrides.
+    int planes = std::max(16, std::min(64, g.nz / 4));
+    if (const char* e = std::getenv("LBMGPU_CG_PLANES")) planes = std::max(1, std::atoi(e));
+    P_ = std::min(planes, g.nz);
     S_ = P_ + 1;
     plane_ = (uint64_t)g.nx * g.ny;
     storage_ = plane_ * (uint64_t)(g.nz + S_ + 2);
