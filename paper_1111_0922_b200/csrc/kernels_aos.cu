@@ -43,7 +43,16 @@ namespace {
 constexpr int kTX = 32, kTY = 8;             // tile: one warp per x-row
 constexpr int kWC = kTX + 2, kWR = kTY + 2;  // window columns / rows (1-cell halo)
 constexpr int kNB = 4;                       // plane buffers in the ring
-constexpr int kWinThreads = kTX * kTY;
+// threads per block: one warp per tile row computes; fp64 runs one block per
+// SM (the ring takes 207 KB) and adds 3 warps that only load and store
+// (11 x 32 = 352 threads <= 184 registers; C1 OS pull 0.62 -> 0.67) ...
+// for the gather modes (OS push's ring collisions need more than 184
+// registers; AA odd measured no better)
+template <class T, int MODE>
+struct WinThreads {
+  static constexpr int value = sizeof(T) == 8 && MODE <= 1 ? 352 : kTX * kTY;
+  static constexpr int warps = value / 32;
+};
 
 enum WinMode : int { kWinPull = 0, kWinStream = 1, kWinPush = 2, kWinAaOdd = 3 };
 
@@ -179,7 +188,7 @@ template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
                                            int* ph, const Tile& t, int z) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < t.tyv + 2; r += kTY) {
+  for (int r = warp; r < t.tyv + 2; r += (int)(blockDim.x >> 5)) {
     uint32_t rb;
     int phase = 0;
     if (row_base(L, t.y0 - 1 + r, z, rb)) {
@@ -203,7 +212,7 @@ template <class T>
 __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T* buf,
                                               const int* ph, const Tile& t, int z) {
   const int w = t.txv + 2, n = w * (t.tyv + 2);
-  for (int q = threadIdx.x; q < n; q += kWinThreads) {
+  for (int q = threadIdx.x; q < n; q += (int)blockDim.x) {
     const int r = q / w, rx = q - r * w;
     uint32_t bounce;
     if (!win_cell(L, t, rx, r, z, bounce)) continue;
@@ -253,7 +262,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
   const int nrun = can_run ? max(0, t.tyv - 2) : 0;
   const int nfull = rows - nrun;
   const int nitems = 2 * nfull + nrun;
-  for (int it = warp; it < nitems; it += kTY) {
+  for (int it = warp; it < nitems; it += (int)(blockDim.x >> 5)) {
     int r, c0, c1;  // row, column range [c0, c1) for the slot-by-slot pass
     bool run;
     if (it < 2 * nfull) {
@@ -328,12 +337,12 @@ __device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&
 }
 
 template <class T, int MODE>
-__global__ void __launch_bounds__(kWinThreads, sizeof(T) == 8 ? 1 : 2)
+__global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1 : 2)
     k_win(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
   extern __shared__ __align__(16) unsigned char win_smem[];
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
-  __shared__ uint32_t msk[MODE == kWinAaOdd ? kTY * kWC : 1];
+  __shared__ uint32_t msk[MODE == kWinAaOdd ? WinThreads<T, MODE>::warps * kWC : 1];
   constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
 
   const int ntile = tiles_x * tiles_y;
@@ -377,28 +386,30 @@ __global__ void __launch_bounds__(kWinThreads, sizeof(T) == 8 ? 1 : 2)
       collide_plane(L, op, sm + slot(z + 1) * BUF, ph[slot(z + 1)], t, z + 1);
       __syncthreads();
     }
-    // element offsets of the 3 x 3 (z, y) neighbourhood at this thread's column
-    int rp[3][3];
-#pragma unroll
-    for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 3; ++dy) {
-        const int s = slot(z - 1 + dz), r = ty + dy;
-        rp[dz][dy] = s * BUF + r * ROW + ph[s][r] + (tx + 1) * 19;
-      }
-    auto at = [&](int i, int k) -> T& {  // slot k of the record at X + c_i
-      return sm[rp[1 + cz(i)][1 + cy(i)] + cx(i) * 19 + k];
-    };
     T f[19];
     bool live = false;
-    uint32_t bounce = 0;
-    if (valid) live = cell_links(L, t.x0 + tx, t.y0 + ty, z, bounce);
-    const bool interior = __all_sync(0xffffffffu, bounce == 0u);
-    if (live) {
-      if (interior)
-        win_node<MODE, false>(op, bounce, f, at);
-      else
-        win_node<MODE, true>(op, bounce, f, at);
+    if (ty < kTY) {  // warps beyond the tile rows only move data
+      // element offsets of the 3 x 3 (z, y) neighbourhood at this thread's column
+      int rp[3][3];
+#pragma unroll
+      for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+          const int s = slot(z - 1 + dz), r = ty + dy;
+          rp[dz][dy] = s * BUF + r * ROW + ph[s][r] + (tx + 1) * 19;
+        }
+      auto at = [&](int i, int k) -> T& {  // slot k of the record at X + c_i
+        return sm[rp[1 + cz(i)][1 + cy(i)] + cx(i) * 19 + k];
+      };
+      uint32_t bounce = 0;
+      if (valid) live = cell_links(L, t.x0 + tx, t.y0 + ty, z, bounce);
+      const bool interior = __all_sync(0xffffffffu, bounce == 0u);
+      if (live) {
+        if (interior)
+          win_node<MODE, false>(op, bounce, f, at);
+        else
+          win_node<MODE, true>(op, bounce, f, at);
+      }
     }
     __syncthreads();  // every read of plane z - 1 is done
     if constexpr (MODE == kWinAaOdd) {
@@ -510,7 +521,7 @@ void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
   const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTY - 1) / kTY;
   const int nzc = (L.nz + zc - 1) / zc;
   const unsigned grid = (unsigned)(tiles_x * tiles_y * nzc);
-  k_win<T, MODE><<<grid, kWinThreads, WinSz<T>::kBytes, st>>>(fld<T, true>(a), fld<T, true>(b), L,
+  k_win<T, MODE><<<grid, WinThreads<T, MODE>::value, WinSz<T>::kBytes, st>>>(fld<T, true>(a), fld<T, true>(b), L,
                                                              cast_op<T>(op), tiles_x, tiles_y, zc);
 }
 
