@@ -180,16 +180,22 @@ def cpu_reference_sample(cfg, scheme, budget_s=20.0, max_steps=None):
     pol = [1 if p == "wall" else 0 for p in cfg["policy"]]
     om = cfg["omega"]
     magic = (1.0 / om - 0.5) ** 2
+    addr, mask = 0, None
+    if cfg.get("porous"):  # C2: the same seeded spheres, the reference's indirect path
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        mask = gen_random_spheres(*dims).mask
+        addr = 1
     # one probe step sizes the sample to the budget
-    s1, _, _ = R.run_bench(scheme, 0, dims, pol, None, om, magic, cfg["force"], 1, workers=0,
+    s1, _, _ = R.run_bench(scheme, addr, dims, pol, mask, om, magic, cfg["force"], 1, workers=0,
                            warmup=0, timed_runs=1)
     steps = max(2, int(budget_s / 3.0 / max(s1, 1e-6)))
     if max_steps:
         steps = min(steps, max_steps)
-    sec, mlups, workers = R.run_bench(scheme, 0, dims, pol, None, om, magic, cfg["force"],
+    sec, mlups, workers = R.run_bench(scheme, addr, dims, pol, mask, om, magic, cfg["force"],
                                       steps, workers=0, warmup=1, timed_runs=3)
     return dict(value=mlups, unit="MFLUP/s", cores=workers, kind="reference",
-                sample=f"{cfg['desc']}{sub}; reference {scheme}/direct run_bench, {steps} steps x 3 "
+                sample=f"{cfg['desc']}{sub}; reference {scheme}/{'indirect' if addr else 'direct'} "
+                       f"run_bench, {steps} steps x 3 "
                        f"runs (median) after 1 warm-up step, workers=0 -> {workers} threads, "
                        f"nproc={os.cpu_count()}, OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND', 'unset')}")
 
@@ -201,7 +207,7 @@ def run_reference_arm(args):
         return 0
     cfg = CONFIGS[args.config]
     if cfg.get("porous"):
-        raise SystemExit("--impl reference: the porous C2 sample is not wired (use c0/c1/c3/c4)")
+        args.addressing = "indirect"
     budget = float(os.environ.get("LBM_REF_BUDGET_S", "90"))
     base = cpu_reference_sample(cfg, args.scheme, budget_s=budget, max_steps=args.steps)
     line = {
@@ -216,6 +222,9 @@ def run_reference_arm(args):
                 "d2h_bytes_per_step": 0},
     }
     nodes = cfg["dims"][0] * cfg["dims"][1] * cfg["dims"][2]
+    if cfg.get("porous"):
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        nodes = gen_random_spheres(*cfg["dims"]).fluid_count()
     line["ms_per_step"] = nodes / (base["value"] * 1e6) * 1e3
     print(json.dumps(line), flush=True)
     return 0
