@@ -33,6 +33,7 @@
 #include "launch.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 namespace lbmgpu {
@@ -502,6 +503,24 @@ __global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
   }
 }
 
+// opt Kernel into more than 48 KB of dynamic shared memory on the current
+// device, once per (kernel, device): the attribute is per device and a
+// process may drive several GPUs. Returns the resident blocks per SM.
+template <auto Kernel>
+int ensure_smem(int threads, size_t bytes) {
+  static std::atomic<int> per_sm[64];  // 0 = not yet set on that device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int n = per_sm[dev].load(std::memory_order_acquire);
+  if (n > 0) return n;
+  cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kernel, threads, bytes) != cudaSuccess ||
+      n < 1)
+    n = 1;
+  per_sm[dev].store(n, std::memory_order_release);
+  return n;
+}
+
 bool window_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("LBMGPU_AOS_WINDOW");
@@ -513,11 +532,7 @@ bool window_enabled() {
 template <class T, int MODE>
 void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
                 const TrtHost& op, int zc) {
-  static bool attr = [] {
-    return cudaFuncSetAttribute(k_win<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)WinSz<T>::kBytes) == cudaSuccess;
-  }();
-  (void)attr;
+  ensure_smem<k_win<T, MODE>>(WinThreads<T, MODE>::value, WinSz<T>::kBytes);
   const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTY - 1) / kTY;
   const int nzc = (L.nz + zc - 1) / zc;
   const unsigned grid = (unsigned)(tiles_x * tiles_y * nzc);
@@ -581,15 +596,8 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
 template <class T, bool RD, bool WR>
 static void launch_stream_t(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
                             const TrtHost& op, uint32_t soff) {
-  static int per_sm = [] {
-    cudaFuncSetAttribute(k_local_stream<T, RD, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)RunSz<T>::kBytes);
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_local_stream<T, RD, WR>, kRun,
-                                                      RunSz<T>::kBytes) != cudaSuccess || n < 1)
-      n = 1;
-    return n;
-  }();
+  // resident blocks per SM (registers and the two-slot ring)
+  const int per_sm = ensure_smem<k_local_stream<T, RD, WR>>(kRun, RunSz<T>::kBytes);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
