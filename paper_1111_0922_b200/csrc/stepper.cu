@@ -1033,7 +1033,7 @@ struct HaloOp {
   int slot;   // direction slot (a whole nx*ny slot plane)
 };
 
-enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3 };
+enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3, kSlabTs = 4 };
 // ET remote slots crossing a face (logical directions, mapped through the
 // handle table base[] when executed): a top cell reads and rewrites the second
 // members j of the pairs whose first member points up (5,9,12 -> 6,16,13) one
@@ -1048,6 +1048,8 @@ static constexpr int kEtDown[2] = {17, 14};
 //     the face (bottom cells read cz=+1 slots below, top cells cz=-1 above)
 //  OS push (every step, destination grid): 1 = the slots pushed into the
 //     ghosts (top cells push cz=+1 up, bottom cells cz=-1 down) -> owners
+//  TS (every step, post-collision grid B between collide and stream): the
+//     OS pull plan (the stream pass is a pull gather from B)
 static std::vector<HaloOp> halo_plan(int kind, int nzl) {
   std::vector<HaloOp> v;
   auto add = [&](int ph, int send, int peer, int plane, const int* slots) {
@@ -1060,7 +1062,7 @@ static std::vector<HaloOp> halo_plan(int kind, int nzl) {
     add(0, 0, -1, -1, kZm);
     add(0, 0, +1, nzl, kZp);
   }
-  if (kind == kSlabOsPull) {
+  if (kind == kSlabOsPull || kind == kSlabTs) {
     // phase 0: sends [up: top cz+] [down: bottom cz-]; recvs [down: lower ghost cz+] [up: upper ghost cz-]
     add(0, 1, +1, nzl - 1, kZp);
     add(0, 1, -1, 0, kZm);
@@ -1139,6 +1141,7 @@ class SlabStepper final : public Stepper {
       : Stepper(slab_geo(g, o), p, o), gnz_(g.nz), z0_(o.z_begin), z1_(o.z_end) {
     kind_ = o.scheme == LBMGPU_AAP    ? kSlabAA
             : o.scheme == LBMGPU_ET   ? kSlabEt
+            : o.scheme == LBMGPU_TS   ? kSlabTs
             : o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush
                                          : kSlabOsPull;
     for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
@@ -1206,14 +1209,15 @@ class SlabStepper final : public Stepper {
   }
 
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
-    const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_OS_PUSH ||
+    const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_TS ||
+                           o.scheme == LBMGPU_OS_PUSH ||
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
     const bool idx = o.addressing == LBMGPU_INDIRECT;
     if (!ok_scheme || o.layout != LBMGPU_SOA || (idx && o.scheme == LBMGPU_ET))
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern, ET and OS/OSNT (direct), "
-          "AA and OS/OSNT (indirect), SoA");
+          "z-slab decomposition supports the AA pattern, ET, TS and OS/OSNT (direct), "
+          "AA, TS and OS/OSNT (indirect), SoA");
     if (g.solids && !idx)
       throw std::invalid_argument("z-slab decomposition needs an all-fluid box (direct)");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
@@ -1265,6 +1269,7 @@ class SlabStepper final : public Stepper {
   // active grid (read by the coming pull); OS push the grid just written
   int phase_grid(int phase) const {
     if (kind_ == kSlabAA || kind_ == kSlabEt) return 0;
+    if (kind_ == kSlabTs) return 1;  // B, the post-collision grid the stream reads
     if (kind_ == kSlabOsPull) return active_;
     return phase == 1 ? active_ ^ 1 : active_;
   }
@@ -1353,6 +1358,8 @@ class SlabStepper final : public Stepper {
           launch_local_idx_range(stream_, f, f, I.first, I.last, op_, false, true);
         else
           launch_aa_odd_idx(stream_, f, I, op_);
+      } else if (kind_ == kSlabTs) {
+        launch_ts_stream_idx(stream_, field(g_[0], st), field(g_[1], st), I);
       } else {
         const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
         if (kind_ == kSlabOsPull)
@@ -1371,6 +1378,8 @@ class SlabStepper final : public Stepper {
         launch_aa_odd(stream_, f, L, op_);
     } else if (kind_ == kSlabEt) {
       launch_et(stream_, field(g_[0], st), L, op_, base_);
+    } else if (kind_ == kSlabTs) {
+      launch_ts_stream(stream_, field(g_[0], st), field(g_[1], st), L);
     } else {
       const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
       if (kind_ == kSlabOsPull)
@@ -1386,6 +1395,17 @@ class SlabStepper final : public Stepper {
     CK(cudaStreamWaitEvent(stream_, wait_before_boundary, 0));
     sweep(0, 1);
     if (nzl_ > 1) sweep(nzl_ - 1, nzl_);
+  }
+
+  // TS collide sweep A -> B over the own planes (p/src/scheme_ts.cpp:59-80)
+  void ts_collide() {
+    const long long st = soa_stride(storage_);
+    const DField a = field(g_[0], st), b = field(g_[1], st);
+    if (idx_)
+      launch_local_idx_range(stream_, a, b, (uint32_t)poff_[1], (uint32_t)poff_[nzl_ + 1], op_,
+                             false, false);
+    else
+      launch_local(stream_, a, b, planes(0, nzl_), op_, false, false);
   }
 
   void precollide_if_fresh() {
@@ -1424,6 +1444,10 @@ class SlabStepper final : public Stepper {
         enqueue_phase(0, active_, ev_halo_);
         sweep_split(ev_halo_);
         active_ ^= 1;
+      } else if (kind_ == kSlabTs) {
+        ts_collide();
+        enqueue_phase(0, 1, ev_halo_);
+        sweep_split(ev_halo_);
       } else {  // push: interior and boundary, then ghosts -> owners of the new grid
         sweep_split(ev_back_);
         enqueue_phase(1, active_ ^ 1, ev_back_);
@@ -1438,12 +1462,13 @@ class SlabStepper final : public Stepper {
     sweep(0, nzl_);
     if (kind_ == kSlabEt)
       swap_base();
-    else if (kind_ != kSlabAA)
+    else if (kind_ == kSlabOsPull || kind_ == kSlabOsPush)
       active_ ^= 1;
   }
   int launches_per_step() const override {
-    if (transport_ != kNccl) return 1;
-    return nzl_ > 2 ? 3 : nzl_;
+    const int collide = kind_ == kSlabTs ? 1 : 0;
+    if (transport_ != kNccl) return 1 + collide;
+    return (nzl_ > 2 ? 3 : nzl_) + collide;
   }
 
   void finish() override {
@@ -1632,11 +1657,15 @@ static void group_step(std::vector<SlabStepper*>& S, long long steps) {
     if (kind == kSlabOsPull) {
       for (auto* s : S) s->precollide_if_fresh();
     }
+    if (kind == kSlabTs) {
+      for (auto* s : S) s->ts_collide();
+    }
     if (kind == kSlabEt && S[0]->owners_stale_) {
       local_phase(S, 1);
       for (auto* s : S) s->owners_stale_ = false;
     }
-    const bool pre = (kind == kSlabAA && odd) || kind == kSlabOsPull || kind == kSlabEt;
+    const bool pre = (kind == kSlabAA && odd) || kind == kSlabOsPull || kind == kSlabEt ||
+                     kind == kSlabTs;
     const bool post = (kind == kSlabAA && odd) || kind == kSlabOsPush || kind == kSlabEt;
     if (pre) local_phase(S, 0);
     for (auto* s : S) s->step(1);
@@ -1984,6 +2013,7 @@ int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* 
       case LBMGPU_OSNT_PULL_1S:
       case LBMGPU_OSNT_PULL_2S: kind = kSlabOsPull; break;
       case LBMGPU_ET: kind = kSlabEt; break;
+      case LBMGPU_TS: kind = kSlabTs; break;
       default: throw std::invalid_argument("no z-slab decomposition for this scheme");
     }
     const auto plan = halo_plan(kind, nzl);

@@ -133,6 +133,7 @@ def test_halo_plan_shape():
     push = L.halo_plan(5, "os-push")
     assert push.shape == (20, 5) and (push[:, 0] == 1).all()
     assert np.array_equal(L.halo_plan(5, "osnt-pull-2s"), pull)
+    assert np.array_equal(L.halo_plan(5, "ts"), pull)  # TS streams by pulling from B
     et = L.halo_plan(5, "et")
     assert et.shape == (20, 5)
     assert set(et[et[:, 3] == 5][:, 4]) == {6, 16, 13}  # upper ghost
