@@ -799,7 +799,6 @@ class IndirectStepper : public Stepper {
     launch_load_idx(stream_, f, I_, Lcells_, cell_of_node(), n0, cnt, mode, d, in);
   }
   uint64_t idx_bytes() const override { return adj_.bytes(); }
-  size_t elem_bytes() const { return esize(); }
   DevMem adj_;
   Idx I_;
   dev::Lat Lcells_;
@@ -1174,6 +1173,16 @@ class SlabStepper final : public Stepper {
       I_.adj = adj_.get<uint32_t>();
       I_.rem = nullptr;
       I_.n = (uint32_t)nodes_;
+      if (kind_ == kSlabEt) {
+        // ET remote table over the extended numbering; bounced links get
+        // mailbox slots after all nodes, touched only by their own node
+        rem_.alloc((size_t)nodes_ * 9 * sizeof(uint32_t));
+        DevMem scratch(scan_scratch_elems(nodes_) * sizeof(uint32_t));
+        const uint32_t nmail = build_et_rem(stream_, adj_.get<uint32_t>(), (uint32_t)nodes_,
+                                            rem_.get<uint32_t>(), scratch.get<uint32_t>(), 0);
+        I_.rem = rem_.get<uint32_t>();
+        storage_ = nodes_ + nmail;
+      }
     } else {
       L_ = make_lat(geo_, nullptr, 0, 0, 0, 0);
       L_.zghost = 1;
@@ -1214,10 +1223,10 @@ class SlabStepper final : public Stepper {
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
     const bool idx = o.addressing == LBMGPU_INDIRECT;
-    if (!ok_scheme || o.layout != LBMGPU_SOA || (idx && o.scheme == LBMGPU_ET))
+    if (!ok_scheme || o.layout != LBMGPU_SOA)
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern, ET, TS and OS/OSNT (direct), "
-          "AA, TS and OS/OSNT (indirect), SoA");
+          "z-slab decomposition supports the AA pattern, ET, TS and OS/OSNT "
+          "(direct and indirect), SoA");
     if (g.solids && !idx)
       throw std::invalid_argument("z-slab decomposition needs an all-fluid box (direct)");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
@@ -1286,7 +1295,7 @@ class SlabStepper final : public Stepper {
   uint64_t snapshot_nodes() const override {
     return idx_ ? poff_[nzl_ + 1] - poff_[1] : nodes_;
   }
-  uint64_t idx_bytes() const override { return adj_.bytes(); }
+  uint64_t idx_bytes() const override { return adj_.bytes() + rem_.bytes(); }
   size_t elem_bytes() const { return esize(); }
   // storage plane of a logical slot (ET: through the handle table)
   int phys_slot(int slot) const { return kind_ == kSlabEt ? base_.b[slot] : slot; }
@@ -1360,6 +1369,8 @@ class SlabStepper final : public Stepper {
           launch_aa_odd_idx(stream_, f, I, op_);
       } else if (kind_ == kSlabTs) {
         launch_ts_stream_idx(stream_, field(g_[0], st), field(g_[1], st), I);
+      } else if (kind_ == kSlabEt) {
+        launch_et_idx(stream_, field(g_[0], st), I, op_, base_);
       } else {
         const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
         if (kind_ == kSlabOsPull)
@@ -1505,6 +1516,8 @@ class SlabStepper final : public Stepper {
       if (kind_ == kSlabAA)
         launch_extract_idx(stream_, field(g_[0], st), I_, n, c, (t_ & 1) ? kExAaOdd : kExNatural,
                            EtBase{}, d);
+      else if (kind_ == kSlabEt)
+        launch_extract_idx(stream_, field(g_[0], st), I_, n, c, kExEt, base_, d);
       else if (kind_ == kSlabOsPull && !fresh_)
         launch_extract_idx(stream_, field(g_[active_ ^ 1], st), I_, n, c, kExGather, EtBase{}, d);
       else
@@ -1528,8 +1541,13 @@ class SlabStepper final : public Stepper {
     if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
     if (idx_) {
       s.z0 = z0_ - 1;  // extended plane 0 is global plane z_begin - 1
+      int mode = kExNatural;
+      if (kind_ == kSlabEt) {
+        for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
+        mode = kExEt;
+      }
       launch_load_idx(stream_, field(g_[active_], soa_stride(storage_)), I_, Lcells_,
-                      cell_of_node(), (uint32_t)poff_[1] + n0, c, kExNatural, d, s);
+                      cell_of_node(), (uint32_t)poff_[1] + n0, c, mode, d, s);
       return;
     }
     if (kind_ == kSlabEt) {
@@ -1576,7 +1594,7 @@ class SlabStepper final : public Stepper {
   uint64_t maxcount_ = 0;
   DevMem rbuf_;
   std::vector<uint64_t> poff_;  // indirect: node offset of extended plane k
-  DevMem adj_;
+  DevMem adj_, rem_;
   Idx I_{};
   dev::Lat Lcells_{};
   uint64_t plane_ = 0, storage_ = 0;

@@ -82,8 +82,9 @@ def test_slab_errors(gpu):
     with pytest.raises(ValueError, match="ET z-slabs need periodic x and y"):
         L.create_stepper("et", "direct", L.GridGeometry(8, 8, 8, ("wall", "periodic", "periodic")),
                          options=L.StepperOptions(z_begin=0, z_end=4))
-    with pytest.raises(ValueError, match="AA, TS and OS/OSNT \\(indirect\\)"):
-        L.create_stepper("et", "indirect", geo, options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="supports the AA pattern, ET, TS and OS/OSNT"):
+        L.create_stepper("swap-push", "indirect", geo,
+                         options=L.StepperOptions(z_begin=0, z_end=4, extensions=True))
     s = L.create_stepper("aap", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(RuntimeError, match="no transport"):
         s.step()
@@ -119,7 +120,7 @@ def _porous(L, dims, solid=0.25, seed=5):
     return L.GridGeometry(*dims, ("periodic", "periodic", "periodic"), mask)
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "ts"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "ts", "et"])
 @pytest.mark.parametrize("bounds", [[(0, 12)], [(0, 5), (5, 12)], [(0, 1), (1, 7), (7, 12)]])
 def test_indirect_slabs_match_single_domain(gpu, scheme, bounds):
     """indirect z-slabs: each slab numbers its fluid nodes over its planes plus
@@ -174,7 +175,7 @@ def test_indirect_slab_host_load(gpu):
                          ref.extract_natural())
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et"])
 def test_indirect_nccl_single_rank_ring(gpu, scheme):
     L = gpu
     dims = (24, 20, 14)
