@@ -1032,7 +1032,7 @@ struct HaloOp {
   int slot;   // direction slot (a whole nx*ny slot plane)
 };
 
-enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3, kSlabTs = 4 };
+enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3, kSlabTs = 4, kSlabSwap = 5 };
 // ET remote slots crossing a face (logical directions, mapped through the
 // handle table base[] when executed): a top cell reads and rewrites the second
 // members j of the pairs whose first member points up (5,9,12 -> 6,16,13) one
@@ -1049,6 +1049,9 @@ static constexpr int kEtDown[2] = {17, 14};
 //     ghosts (top cells push cz=+1 up, bottom cells cz=-1 down) -> owners
 //  TS (every step, post-collision grid B between collide and stream): the
 //     OS pull plan (the stream pass is a pull gather from B)
+//  SWAP (every swap pass): the pairs crossing a face are the bottom cells'
+//     back links with cz=-1 against the lower neighbour's top-plane cz=+1
+//     slots: 0 = those slots -> the lower ghost, 1 = swapped values -> owner
 static std::vector<HaloOp> halo_plan(int kind, int nzl) {
   std::vector<HaloOp> v;
   auto add = [&](int ph, int send, int peer, int plane, const int* slots) {
@@ -1067,6 +1070,12 @@ static std::vector<HaloOp> halo_plan(int kind, int nzl) {
     add(0, 1, -1, 0, kZm);
     add(0, 0, -1, -1, kZp);
     add(0, 0, +1, nzl, kZm);
+  }
+  if (kind == kSlabSwap) {
+    add(0, 1, +1, nzl - 1, kZp);
+    add(0, 0, -1, -1, kZp);
+    add(1, 1, -1, -1, kZp);
+    add(1, 0, +1, nzl - 1, kZp);
   }
   if (kind == kSlabEt) {
     // every sweep. phase 0: sends [up: top {17,14}] [down: bottom {6,16,13}];
@@ -1141,10 +1150,12 @@ class SlabStepper final : public Stepper {
     kind_ = o.scheme == LBMGPU_AAP    ? kSlabAA
             : o.scheme == LBMGPU_ET   ? kSlabEt
             : o.scheme == LBMGPU_TS   ? kSlabTs
+            : (o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL) ? kSlabSwap
             : o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush
                                          : kSlabOsPull;
     for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
     nt_ = (o.scheme == LBMGPU_OSNT_PULL_1S || o.scheme == LBMGPU_OSNT_PULL_2S) && o.streaming_stores;
+    swap_pull_ = o.scheme == LBMGPU_SWAP_PULL;
     two_s_ = o.scheme == LBMGPU_OSNT_PULL_2S;
     nzl_ = z1_ - z0_;
     plane_ = (uint64_t)g.nx * g.ny;
@@ -1190,11 +1201,14 @@ class SlabStepper final : public Stepper {
       L_.wall[2] = 0;
       storage_ = plane_ * (nzl_ + 2);
     }
-    ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt) ? 1 : 2;
+    ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap) ? 1 : 2;
     for (int k = 0; k < ngrids_; ++k) alloc_field(g_[k], storage_);
     // an owner node whose link towards the neighbour slab bounces (x/y wall,
     // solid) writes that face slot itself: phase 1 then merges, not copies
-    merge_ = geo_.policy[0] == 1 || geo_.policy[1] == 1 || (idx_ && geo_.solids);
+    // (SWAP: a face pair exists only between two fluid nodes, so the returned
+    // values are always the swapped ones: plain copies)
+    merge_ = kind_ != kSlabSwap &&
+             (geo_.policy[0] == 1 || geo_.policy[1] == 1 || (idx_ && geo_.solids));
     if (merge_) {
       maxcount_ = 0;
       for (int pl : {0, nzl_ - 1}) maxcount_ = std::max(maxcount_, plane_count(pl));
@@ -1219,14 +1233,17 @@ class SlabStepper final : public Stepper {
 
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
     const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_TS ||
+                           o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL ||
                            o.scheme == LBMGPU_OS_PUSH ||
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
     const bool idx = o.addressing == LBMGPU_INDIRECT;
     if (!ok_scheme || o.layout != LBMGPU_SOA)
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern, ET, TS and OS/OSNT "
+          "z-slab decomposition supports the AA pattern, ET, TS, SWAP and OS/OSNT "
           "(direct and indirect), SoA");
+    if ((o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL) && o.swap_deferred_fixup)
+      throw std::invalid_argument("SWAP z-slabs swap every link each sweep (swap_deferred_fixup = 0)");
     if (g.solids && !idx)
       throw std::invalid_argument("z-slab decomposition needs an all-fluid box (direct)");
     if (g.policy[2] != 0) throw std::invalid_argument("z-slab decomposition needs periodic z");
@@ -1277,7 +1294,7 @@ class SlabStepper final : public Stepper {
   // the grid an exchange phase applies to: AA its one grid; OS pull the
   // active grid (read by the coming pull); OS push the grid just written
   int phase_grid(int phase) const {
-    if (kind_ == kSlabAA || kind_ == kSlabEt) return 0;
+    if (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap) return 0;
     if (kind_ == kSlabTs) return 1;  // B, the post-collision grid the stream reads
     if (kind_ == kSlabOsPull) return active_;
     return phase == 1 ? active_ ^ 1 : active_;
@@ -1317,10 +1334,13 @@ class SlabStepper final : public Stepper {
   }
 
   // NCCL phase: the plan's sends and receives in plan order, one group
-  void nccl_phase(int phase, int grid) {
+  // the plan that refreshes the ghosts an extraction gathers from (SWAP pull
+  // gathers like OS pull)
+  int sync_kind() const { return kind_ == kSlabSwap ? kSlabOsPull : kind_; }
+  void nccl_phase(int phase, int grid, int plan_kind = -1) {
     Nccl& N = Nccl::get();
     const ncclDataType_t ty = prec_ == Prec::f64 ? ncclDouble : ncclFloat;
-    const std::vector<HaloOp> plan = halo_plan(kind_, nzl_);
+    const std::vector<HaloOp> plan = halo_plan(plan_kind < 0 ? kind_ : plan_kind, nzl_);
     N.check(N.groupStart(), "ncclGroupStart");
     int q = 0;
     for (const HaloOp& op : plan) {
@@ -1339,10 +1359,10 @@ class SlabStepper final : public Stepper {
       if (op.phase == phase && merged(op)) merge_into(comm_, grid, op, rbuf_slot(q++));
   }
   // comm stream runs `phase` after everything enqueued on stream_ so far
-  void enqueue_phase(int phase, int grid, cudaEvent_t done) {
+  void enqueue_phase(int phase, int grid, cudaEvent_t done, int plan_kind = -1) {
     CK(cudaEventRecord(ev_c_, stream_));
     CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
-    nccl_phase(phase, grid);
+    nccl_phase(phase, grid, plan_kind);
     CK(cudaEventRecord(done, comm_));
   }
 
@@ -1371,6 +1391,8 @@ class SlabStepper final : public Stepper {
         launch_ts_stream_idx(stream_, field(g_[0], st), field(g_[1], st), I);
       } else if (kind_ == kSlabEt) {
         launch_et_idx(stream_, field(g_[0], st), I, op_, base_);
+      } else if (kind_ == kSlabSwap) {
+        launch_swap_idx(stream_, field(g_[0], st), I);
       } else {
         const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
         if (kind_ == kSlabOsPull)
@@ -1391,6 +1413,8 @@ class SlabStepper final : public Stepper {
       launch_et(stream_, field(g_[0], st), L, op_, base_);
     } else if (kind_ == kSlabTs) {
       launch_ts_stream(stream_, field(g_[0], st), field(g_[1], st), L);
+    } else if (kind_ == kSlabSwap) {
+      launch_swap(stream_, field(g_[0], st), L, 0);  // z never wraps inside a slab
     } else {
       const DField a = field(g_[active_], st), b = field(g_[active_ ^ 1], st);
       if (kind_ == kSlabOsPull)
@@ -1417,6 +1441,18 @@ class SlabStepper final : public Stepper {
                              false, false);
     else
       launch_local(stream_, a, b, planes(0, nzl_), op_, false, false);
+  }
+
+  // SWAP collide pass: opposed slots in, natural out (push: before the swaps;
+  // pull: after them); the first pull step only precollides (natural in place)
+  void swap_collide(bool first_pull = false) {
+    const long long st = soa_stride(storage_);
+    const DField f = field(g_[0], st);
+    if (idx_)
+      launch_local_idx_range(stream_, f, f, (uint32_t)poff_[1], (uint32_t)poff_[nzl_ + 1], op_,
+                             !first_pull, false);
+    else
+      launch_local(stream_, f, f, planes(0, nzl_), op_, !first_pull, false);
   }
 
   void precollide_if_fresh() {
@@ -1459,6 +1495,21 @@ class SlabStepper final : public Stepper {
         ts_collide();
         enqueue_phase(0, 1, ev_halo_);
         sweep_split(ev_halo_);
+      } else if (kind_ == kSlabSwap) {
+        CK(cudaStreamWaitEvent(stream_, ev_back_, 0));  // last phase 1 reached my top plane
+        if (swap_pull_ && fresh_) {
+          swap_collide(true);
+          fresh_ = false;
+        } else {
+          if (!swap_pull_) swap_collide();
+          enqueue_phase(0, 0, ev_halo_);
+          sweep_split(ev_halo_);
+          enqueue_phase(1, 0, ev_back_);
+          if (swap_pull_) {
+            CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
+            swap_collide();
+          }
+        }
       } else {  // push: interior and boundary, then ghosts -> owners of the new grid
         sweep_split(ev_back_);
         enqueue_phase(1, active_ ^ 1, ev_back_);
@@ -1470,6 +1521,11 @@ class SlabStepper final : public Stepper {
     if (transport_ != kLocalGroup)
       throw std::runtime_error("slab stepper has no transport: connect NCCL or step as a group");
     // in-process group: group_step runs the exchange phases around the sweep
+    if (kind_ == kSlabSwap && swap_pull_ && fresh_) {
+      swap_collide(true);
+      fresh_ = false;
+      return;
+    }
     sweep(0, nzl_);
     if (kind_ == kSlabEt)
       swap_base();
@@ -1477,7 +1533,7 @@ class SlabStepper final : public Stepper {
       active_ ^= 1;
   }
   int launches_per_step() const override {
-    const int collide = kind_ == kSlabTs ? 1 : 0;
+    const int collide = (kind_ == kSlabTs || kind_ == kSlabSwap) ? 1 : 0;
     if (transport_ != kNccl) return 1 + collide;
     return (nzl_ > 2 ? 3 : nzl_) + collide;
   }
@@ -1490,6 +1546,7 @@ class SlabStepper final : public Stepper {
   // streams the idle grid (phase-0 slot set applied to that grid)
   bool extract_needs_ghosts() const {
     if (kind_ == kSlabAA) return (t_ & 1) != 0;
+    if (kind_ == kSlabSwap) return swap_pull_ && !fresh_;
     if (kind_ == kSlabEt) return true;
     if (kind_ == kSlabOsPull) return !fresh_;
     return false;
@@ -1498,7 +1555,7 @@ class SlabStepper final : public Stepper {
 
   void sync_ghosts_nccl() {
     if (transport_ != kNccl) throw std::runtime_error("slab stepper is not connected to NCCL");
-    enqueue_phase(0, ghost_grid(), ev_halo_);
+    enqueue_phase(0, ghost_grid(), ev_halo_, sync_kind());
     CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
     ghosts_fresh_ = true;
   }
@@ -1516,6 +1573,10 @@ class SlabStepper final : public Stepper {
       if (kind_ == kSlabAA)
         launch_extract_idx(stream_, field(g_[0], st), I_, n, c, (t_ & 1) ? kExAaOdd : kExNatural,
                            EtBase{}, d);
+      else if (kind_ == kSlabSwap)
+        launch_extract_idx(stream_, field(g_[0], st), I_, n, c,
+                           !swap_pull_ ? kExOpposed : (fresh_ ? kExNatural : kExGather), EtBase{},
+                           d);
       else if (kind_ == kSlabEt)
         launch_extract_idx(stream_, field(g_[0], st), I_, n, c, kExEt, base_, d);
       else if (kind_ == kSlabOsPull && !fresh_)
@@ -1527,6 +1588,9 @@ class SlabStepper final : public Stepper {
     if (kind_ == kSlabAA)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
                      (t_ & 1) ? kExAaOdd : kExNatural, EtBase{}, d);
+    else if (kind_ == kSlabSwap)
+      launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
+                     !swap_pull_ ? kExOpposed : (fresh_ ? kExNatural : kExGather), EtBase{}, d);
     else if (kind_ == kSlabEt)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c, kExEt, base_, d);
     else if (kind_ == kSlabOsPull && !fresh_)
@@ -1541,7 +1605,7 @@ class SlabStepper final : public Stepper {
     if (s.source != kSrcBuffer) s.gnz = gnz_, s.z0 = z0_;
     if (idx_) {
       s.z0 = z0_ - 1;  // extended plane 0 is global plane z_begin - 1
-      int mode = kExNatural;
+      int mode = (kind_ == kSlabSwap && !swap_pull_) ? kExOpposed : kExNatural;
       if (kind_ == kSlabEt) {
         for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
         mode = kExEt;
@@ -1556,11 +1620,11 @@ class SlabStepper final : public Stepper {
       return;
     }
     launch_load(stream_, field(g_[active_], soa_stride(storage_)), L_, nullptr, n0, c,
-                kExNatural, d, s);
+                (kind_ == kSlabSwap && !swap_pull_) ? kExOpposed : kExNatural, d, s);
   }
   void after_load() override {
     t_ = 0;
-    fresh_ = kind_ == kSlabOsPull;
+    fresh_ = kind_ == kSlabOsPull || (kind_ == kSlabSwap && swap_pull_);
     // ET's load writes the remote slots of the boundary cells into the ghost
     // planes: they are fresh, and their owners get them before the first sweep
     ghosts_fresh_ = kind_ == kSlabEt;
@@ -1577,6 +1641,7 @@ class SlabStepper final : public Stepper {
         if (base_.b[i] != i) return LBMGPU_TWISTED;
       return LBMGPU_NATURAL;
     }
+    if (kind_ == kSlabSwap) return swap_pull_ ? LBMGPU_NATURAL : LBMGPU_OPPOSED;
     return (kind_ == kSlabAA && (t_ & 1)) ? LBMGPU_OPPOSED : LBMGPU_NATURAL;
   }
   uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
@@ -1586,7 +1651,7 @@ class SlabStepper final : public Stepper {
   int transport_ = kNone;
   int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
   int ngrids_ = 1, active_ = 0;
-  bool nt_ = false, two_s_ = false, fresh_ = false;
+  bool nt_ = false, two_s_ = false, fresh_ = false, swap_pull_ = false;
   bool ghosts_fresh_ = false, owners_stale_ = false;
   EtBase base_;
   bool idx_ = false;
@@ -1613,7 +1678,8 @@ static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_
   const int n = (int)S.size();
   for (auto* s : S) s->sync();
   std::vector<std::vector<HaloOp>> plans(n);
-  for (int k = 0; k < n; ++k) plans[k] = halo_plan(S[k]->kind_, S[k]->nzl_);
+  for (int k = 0; k < n; ++k)
+    plans[k] = halo_plan(use_ghost_grid ? S[k]->sync_kind() : S[k]->kind_, S[k]->nzl_);
   // receives that merge: (peer, op, scratch slot) applied after all copies
   struct Pending {
     int peer;
@@ -1672,6 +1738,20 @@ static void group_step(std::vector<SlabStepper*>& S, long long steps) {
     const bool odd = (S[0]->t_ & 1) != 0;
     for (auto* s : S)
       if (((s->t_ & 1) != 0) != odd) throw std::invalid_argument("slabs out of step");
+    if (kind == kSlabSwap) {
+      const bool fresh = S[0]->swap_pull_ && S[0]->fresh_;
+      if (!fresh && !S[0]->swap_pull_)
+        for (auto* s : S) s->swap_collide();
+      if (!fresh) local_phase(S, 0);
+      for (auto* s : S) s->step(1);  // the swap pass (first pull step: precollide)
+      if (!fresh) {
+        local_phase(S, 1);
+        if (S[0]->swap_pull_)
+          for (auto* s : S) s->swap_collide();
+      }
+      for (auto* s : S) s->ghosts_fresh_ = false;
+      continue;
+    }
     if (kind == kSlabOsPull) {
       for (auto* s : S) s->precollide_if_fresh();
     }
@@ -2032,6 +2112,8 @@ int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* 
       case LBMGPU_OSNT_PULL_2S: kind = kSlabOsPull; break;
       case LBMGPU_ET: kind = kSlabEt; break;
       case LBMGPU_TS: kind = kSlabTs; break;
+      case LBMGPU_SWAP_PUSH:
+      case LBMGPU_SWAP_PULL: kind = kSlabSwap; break;
       default: throw std::invalid_argument("no z-slab decomposition for this scheme");
     }
     const auto plan = halo_plan(kind, nzl);

@@ -22,7 +22,12 @@ def _needs_ghosts(scheme, t):
     return (scheme == "aap" and t % 2 == 1) or "pull" in scheme or scheme == "et"
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "et", "ts"])
+def _ext(scheme):  # TS / SWAP indirect are GPU extensions (the reference's are direct-only)
+    return scheme in ("ts", "swap-push", "swap-pull")
+
+
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "et", "ts",
+                                    "swap-push", "swap-pull"])
 @pytest.mark.parametrize("nslab", [1, 2, 3, 4])
 def test_slabs_match_single_domain(gpu, nslab, scheme):
     L = gpu
@@ -74,23 +79,24 @@ def test_slab_load_and_uneven_split(gpu, scheme):
 def test_slab_errors(gpu):
     L = gpu
     geo = L.GridGeometry(8, 8, 8)
-    with pytest.raises(ValueError, match="supports the AA pattern, ET, TS and OS/OSNT"):
-        L.create_stepper("swap-pull", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="supports the AA pattern, ET, TS, SWAP and OS/OSNT"):
+        L.create_stepper("cg", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="swap_deferred_fixup"):
+        L.create_stepper("swap-push", "direct", geo,
+                         options=L.StepperOptions(z_begin=0, z_end=4, swap_deferred_fixup=True))
     with pytest.raises(ValueError, match="periodic z"):
         L.create_stepper("aap", "direct", L.gen_channel(8, 8, 8),
                          options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(ValueError, match="ET z-slabs need periodic x and y"):
         L.create_stepper("et", "direct", L.GridGeometry(8, 8, 8, ("wall", "periodic", "periodic")),
                          options=L.StepperOptions(z_begin=0, z_end=4))
-    with pytest.raises(ValueError, match="supports the AA pattern, ET, TS and OS/OSNT"):
-        L.create_stepper("swap-push", "indirect", geo,
-                         options=L.StepperOptions(z_begin=0, z_end=4, extensions=True))
     s = L.create_stepper("aap", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
     with pytest.raises(RuntimeError, match="no transport"):
         s.step()
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et", "ts"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et", "ts", "swap-push",
+                                    "swap-pull"])
 def test_nccl_transport_single_rank_ring(gpu, scheme):
     """The NCCL transport itself (liblbmgpu.so dlopens libnccl): one rank whose
     ring neighbours are itself, the overlapped interior/boundary schedule, the
@@ -120,7 +126,8 @@ def _porous(L, dims, solid=0.25, seed=5):
     return L.GridGeometry(*dims, ("periodic", "periodic", "periodic"), mask)
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "ts", "et"])
+@pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "ts", "et",
+                                    "swap-push", "swap-pull"])
 @pytest.mark.parametrize("bounds", [[(0, 12)], [(0, 5), (5, 12)], [(0, 1), (1, 7), (7, 12)]])
 def test_indirect_slabs_match_single_domain(gpu, scheme, bounds):
     """indirect z-slabs: each slab numbers its fluid nodes over its planes plus
@@ -130,7 +137,7 @@ def test_indirect_slabs_match_single_domain(gpu, scheme, bounds):
     dims = (20, 16, 12)
     geo = _porous(L, dims)
     flow = L.bgk(1.3, (1e-5, 2e-6, 0.0))
-    ext = scheme == "ts"  # TS indirect is a GPU extension (the reference's TS is direct-only)
+    ext = _ext(scheme)
     ref = L.create_stepper(scheme, "indirect", geo, flow, L.StepperOptions(extensions=ext))
     ref.init_field("random", seed=4)
     slabs = [L.create_stepper(scheme, "indirect", geo, flow,
@@ -196,7 +203,7 @@ def test_indirect_nccl_single_rank_ring(gpu, scheme):
         assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-push", "os-pull", "ts"])
+@pytest.mark.parametrize("scheme", ["aap", "os-push", "os-pull", "ts", "swap-push", "swap-pull"])
 def test_direct_slabs_with_xy_walls(gpu, scheme):
     """x/y walls: an owner node whose link towards the neighbour slab bounces
     writes that face slot itself, so phase 1 merges instead of copying"""

@@ -134,12 +134,15 @@ def test_halo_plan_shape():
     assert push.shape == (20, 5) and (push[:, 0] == 1).all()
     assert np.array_equal(L.halo_plan(5, "osnt-pull-2s"), pull)
     assert np.array_equal(L.halo_plan(5, "ts"), pull)  # TS streams by pulling from B
+    sw = L.halo_plan(5, "swap-pull")  # one-way per face: lower ghost <-> lower neighbour's top
+    assert sw.shape == (20, 5) and np.array_equal(sw, L.halo_plan(5, "swap-push"))
+    assert set(sw[:, 3]) == {-1, 4} and set(sw[:, 4]) == {5, 9, 12, 14, 17}
     et = L.halo_plan(5, "et")
     assert et.shape == (20, 5)
     assert set(et[et[:, 3] == 5][:, 4]) == {6, 16, 13}  # upper ghost
     assert set(et[et[:, 3] == -1][:, 4]) == {17, 14}  # lower ghost
     with pytest.raises(ValueError):
-        L.halo_plan(5, "swap-pull")
+        L.halo_plan(5, "cg")
 
 
 @pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et"])
