@@ -1032,7 +1032,15 @@ struct HaloOp {
   int slot;   // direction slot (a whole nx*ny slot plane)
 };
 
-enum SlabKind { kSlabAA = 0, kSlabOsPull = 1, kSlabOsPush = 2, kSlabEt = 3, kSlabTs = 4, kSlabSwap = 5 };
+enum SlabKind {
+  kSlabAA = 0,
+  kSlabOsPull = 1,
+  kSlabOsPush = 2,
+  kSlabEt = 3,
+  kSlabTs = 4,
+  kSlabSwap = 5,
+  kSlabCg = 6
+};
 // ET remote slots crossing a face (logical directions, mapped through the
 // handle table base[] when executed): a top cell reads and rewrites the second
 // members j of the pairs whose first member points up (5,9,12 -> 6,16,13) one
@@ -1049,6 +1057,9 @@ static constexpr int kEtDown[2] = {17, 14};
 //     ghosts (top cells push cz=+1 up, bottom cells cz=-1 down) -> owners
 //  TS (every step, post-collision grid B between collide and stream): the
 //     OS pull plan (the stream pass is a pull gather from B)
+//  CG (every sweep, write frame): the OS push plan — a sweep's cross-face
+//     pushes land in the write frame's padding planes (the single-domain
+//     z-seam fix-up becomes this exchange)
 //  SWAP (every swap pass): the pairs crossing a face are the bottom cells'
 //     back links with cz=-1 against the lower neighbour's top-plane cz=+1
 //     slots: 0 = those slots -> the lower ghost, 1 = swapped values -> owner
@@ -1092,7 +1103,7 @@ static std::vector<HaloOp> halo_plan(int kind, int nzl) {
     addn(1, 0, +1, nzl - 1, kEtDown, 2);
     addn(1, 0, -1, 0, kEtUp, 3);
   }
-  if (kind == kSlabAA || kind == kSlabOsPush) {
+  if (kind == kSlabAA || kind == kSlabOsPush || kind == kSlabCg) {
     // phase 1: sends [down: lower ghost cz-] [up: upper ghost cz+]; recvs [up: top cz-] [down: bottom cz+]
     add(1, 1, -1, -1, kZm);
     add(1, 1, +1, nzl, kZp);
@@ -1151,6 +1162,7 @@ class SlabStepper final : public Stepper {
             : o.scheme == LBMGPU_ET   ? kSlabEt
             : o.scheme == LBMGPU_TS   ? kSlabTs
             : (o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL) ? kSlabSwap
+            : o.scheme == LBMGPU_CG   ? kSlabCg
             : o.scheme == LBMGPU_OS_PUSH ? kSlabOsPush
                                          : kSlabOsPull;
     for (int i = 0; i < 20; ++i) base_.b[i] = (int8_t)(i < 19 ? i : 0);
@@ -1200,8 +1212,16 @@ class SlabStepper final : public Stepper {
       L_.oz = 1;
       L_.wall[2] = 0;
       storage_ = plane_ * (nzl_ + 2);
+      if (kind_ == kSlabCg) {  // CgDirect's layout over the slab: nzl + S + 2 planes
+        cg_p_ = std::min(std::max(16, std::min(64, nzl_ / 4)), nzl_);
+        cg_s_ = cg_p_ + 1;
+        storage_ = plane_ * (uint64_t)(nzl_ + cg_s_ + 2);
+        if (storage_ >= (uint64_t{1} << 32))
+          throw std::runtime_error("grid exceeds 32-bit cell index range");
+      }
     }
-    ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap) ? 1 : 2;
+    ngrids_ = (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap || kind_ == kSlabCg) ? 1
+                                                                                            : 2;
     for (int k = 0; k < ngrids_; ++k) alloc_field(g_[k], storage_);
     // an owner node whose link towards the neighbour slab bounces (x/y wall,
     // solid) writes that face slot itself: phase 1 then merges, not copies
@@ -1234,14 +1254,13 @@ class SlabStepper final : public Stepper {
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
     const bool ok_scheme = o.scheme == LBMGPU_AAP || o.scheme == LBMGPU_ET || o.scheme == LBMGPU_TS ||
                            o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL ||
-                           o.scheme == LBMGPU_OS_PUSH ||
+                           o.scheme == LBMGPU_CG || o.scheme == LBMGPU_OS_PUSH ||
                            o.scheme == LBMGPU_OS_PULL || o.scheme == LBMGPU_OSNT_PULL_1S ||
                            o.scheme == LBMGPU_OSNT_PULL_2S;
     const bool idx = o.addressing == LBMGPU_INDIRECT;
     if (!ok_scheme || o.layout != LBMGPU_SOA)
       throw std::invalid_argument(
-          "z-slab decomposition supports the AA pattern, ET, TS, SWAP and OS/OSNT "
-          "(direct and indirect), SoA");
+          "z-slab decomposition supports every scheme (CG direct only), SoA");
     if ((o.scheme == LBMGPU_SWAP_PUSH || o.scheme == LBMGPU_SWAP_PULL) && o.swap_deferred_fixup)
       throw std::invalid_argument("SWAP z-slabs swap every link each sweep (swap_deferred_fixup = 0)");
     if (g.solids && !idx)
@@ -1294,14 +1313,17 @@ class SlabStepper final : public Stepper {
   // the grid an exchange phase applies to: AA its one grid; OS pull the
   // active grid (read by the coming pull); OS push the grid just written
   int phase_grid(int phase) const {
-    if (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap) return 0;
+    if (kind_ == kSlabAA || kind_ == kSlabEt || kind_ == kSlabSwap || kind_ == kSlabCg) return 0;
     if (kind_ == kSlabTs) return 1;  // B, the post-collision grid the stream reads
     if (kind_ == kSlabOsPull) return active_;
     return phase == 1 ? active_ ^ 1 : active_;
   }
   // local plane -1 .. nzl (ghost planes -1 and nzl): direct, storage plane
   // + 1; indirect, the plane's node range of the extended numbering
-  uint64_t plane_first(int plane) const { return idx_ ? poff_[plane + 1] : (uint64_t)(plane + 1) * plane_; }
+  // (CG: planes of the current exchange frame, zoff_ = its origin)
+  uint64_t plane_first(int plane) const {
+    return idx_ ? poff_[plane + 1] : (uint64_t)(plane + 1 + zoff_) * plane_;
+  }
   uint64_t plane_count(int plane) const {
     return idx_ ? poff_[plane + 2] - poff_[plane + 1] : plane_;
   }
@@ -1432,6 +1454,32 @@ class SlabStepper final : public Stepper {
     if (nzl_ > 1) sweep(nzl_ - 1, nzl_);
   }
 
+  // CG (CgDirect over the slab): frame(origin) addresses plane z at storage
+  // z + 1 + origin; a sweep is a sequence of plane-group push launches from
+  // the read origin to the write origin; the pushes across the slab faces land
+  // in the write frame's padding planes, which phase 1 delivers
+  dev::Lat cg_frame(int origin) const {
+    dev::Lat L = L_;
+    L.zghost = 0;
+    L.oz = 1 + origin;
+    L.znowrap = 1;
+    return L;
+  }
+  void cg_sweep() {
+    const DField f = field(g_[0], soa_stride(storage_));
+    const bool even = (t_ & 1) == 0;
+    const int R = even ? cg_s_ : 0, W = even ? 0 : cg_s_;
+    const int ngroups = (nzl_ + cg_p_ - 1) / cg_p_;
+    for (int k = 0; k < ngroups; ++k) {
+      const int gi = even ? k : ngroups - 1 - k;
+      dev::Lat L = cg_frame(R);
+      L.cell_begin = (uint32_t)(gi * cg_p_ * plane_);
+      L.ncells = (uint32_t)(std::min(nzl_, (gi + 1) * cg_p_) * plane_);
+      launch_cg_push(stream_, f, L, op_, (W - R) * (int)plane_);
+    }
+    cg_w_ = W;
+  }
+
   // TS collide sweep A -> B over the own planes (p/src/scheme_ts.cpp:59-80)
   void ts_collide() {
     const long long st = soa_stride(storage_);
@@ -1495,6 +1543,12 @@ class SlabStepper final : public Stepper {
         ts_collide();
         enqueue_phase(0, 1, ev_halo_);
         sweep_split(ev_halo_);
+      } else if (kind_ == kSlabCg) {
+        CK(cudaStreamWaitEvent(stream_, ev_back_, 0));  // my read frame got its face values
+        cg_sweep();
+        zoff_ = cg_w_;
+        enqueue_phase(1, 0, ev_back_);
+        zoff_ = 0;
       } else if (kind_ == kSlabSwap) {
         CK(cudaStreamWaitEvent(stream_, ev_back_, 0));  // last phase 1 reached my top plane
         if (swap_pull_ && fresh_) {
@@ -1526,6 +1580,10 @@ class SlabStepper final : public Stepper {
       fresh_ = false;
       return;
     }
+    if (kind_ == kSlabCg) {
+      cg_sweep();
+      return;
+    }
     sweep(0, nzl_);
     if (kind_ == kSlabEt)
       swap_base();
@@ -1533,6 +1591,7 @@ class SlabStepper final : public Stepper {
       active_ ^= 1;
   }
   int launches_per_step() const override {
+    if (kind_ == kSlabCg) return (nzl_ + cg_p_ - 1) / cg_p_;
     const int collide = (kind_ == kSlabTs || kind_ == kSlabSwap) ? 1 : 0;
     if (transport_ != kNccl) return 1 + collide;
     return (nzl_ > 2 ? 3 : nzl_) + collide;
@@ -1591,6 +1650,9 @@ class SlabStepper final : public Stepper {
     else if (kind_ == kSlabSwap)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c,
                      !swap_pull_ ? kExOpposed : (fresh_ ? kExNatural : kExGather), EtBase{}, d);
+    else if (kind_ == kSlabCg)
+      launch_extract(stream_, field(g_[0], st), cg_frame((t_ & 1) ? 0 : cg_s_), nullptr, n0, c,
+                     kExNatural, EtBase{}, d);
     else if (kind_ == kSlabEt)
       launch_extract(stream_, field(g_[0], st), L_, nullptr, n0, c, kExEt, base_, d);
     else if (kind_ == kSlabOsPull && !fresh_)
@@ -1619,7 +1681,8 @@ class SlabStepper final : public Stepper {
       launch_load(stream_, field(g_[0], soa_stride(storage_)), L_, nullptr, n0, c, kExEt, d, s);
       return;
     }
-    launch_load(stream_, field(g_[active_], soa_stride(storage_)), L_, nullptr, n0, c,
+    launch_load(stream_, field(g_[active_], soa_stride(storage_)),
+                kind_ == kSlabCg ? cg_frame(cg_s_) : L_, nullptr, n0, c,
                 (kind_ == kSlabSwap && !swap_pull_) ? kExOpposed : kExNatural, d, s);
   }
   void after_load() override {
@@ -1642,6 +1705,7 @@ class SlabStepper final : public Stepper {
       return LBMGPU_NATURAL;
     }
     if (kind_ == kSlabSwap) return swap_pull_ ? LBMGPU_NATURAL : LBMGPU_OPPOSED;
+    if (kind_ == kSlabCg) return (t_ & 1) ? LBMGPU_SHIFTED_EVEN : LBMGPU_SHIFTED_ODD;
     return (kind_ == kSlabAA && (t_ & 1)) ? LBMGPU_OPPOSED : LBMGPU_NATURAL;
   }
   uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
@@ -1652,6 +1716,7 @@ class SlabStepper final : public Stepper {
   int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
   int ngrids_ = 1, active_ = 0;
   bool nt_ = false, two_s_ = false, fresh_ = false, swap_pull_ = false;
+  int cg_p_ = 1, cg_s_ = 2, cg_w_ = 0, zoff_ = 0;
   bool ghosts_fresh_ = false, owners_stale_ = false;
   EtBase base_;
   bool idx_ = false;
@@ -1738,6 +1803,13 @@ static void group_step(std::vector<SlabStepper*>& S, long long steps) {
     const bool odd = (S[0]->t_ & 1) != 0;
     for (auto* s : S)
       if (((s->t_ & 1) != 0) != odd) throw std::invalid_argument("slabs out of step");
+    if (kind == kSlabCg) {
+      for (auto* s : S) s->step(1);  // the plane-group sweep
+      for (auto* s : S) s->zoff_ = s->cg_w_;
+      local_phase(S, 1);
+      for (auto* s : S) s->zoff_ = 0;
+      continue;
+    }
     if (kind == kSlabSwap) {
       const bool fresh = S[0]->swap_pull_ && S[0]->fresh_;
       if (!fresh && !S[0]->swap_pull_)
@@ -2114,6 +2186,7 @@ int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* 
       case LBMGPU_TS: kind = kSlabTs; break;
       case LBMGPU_SWAP_PUSH:
       case LBMGPU_SWAP_PULL: kind = kSlabSwap; break;
+      case LBMGPU_CG: kind = kSlabCg; break;
       default: throw std::invalid_argument("no z-slab decomposition for this scheme");
     }
     const auto plan = halo_plan(kind, nzl);

@@ -27,7 +27,7 @@ def _ext(scheme):  # TS / SWAP indirect are GPU extensions (the reference's are 
 
 
 @pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "osnt-pull-2s", "et", "ts",
-                                    "swap-push", "swap-pull"])
+                                    "swap-push", "swap-pull", "cg"])
 @pytest.mark.parametrize("nslab", [1, 2, 3, 4])
 def test_slabs_match_single_domain(gpu, nslab, scheme):
     L = gpu
@@ -79,8 +79,9 @@ def test_slab_load_and_uneven_split(gpu, scheme):
 def test_slab_errors(gpu):
     L = gpu
     geo = L.GridGeometry(8, 8, 8)
-    with pytest.raises(ValueError, match="supports the AA pattern, ET, TS, SWAP and OS/OSNT"):
-        L.create_stepper("cg", "direct", geo, options=L.StepperOptions(z_begin=0, z_end=4))
+    with pytest.raises(ValueError, match="supports every scheme"):
+        L.create_stepper("aap", "direct", geo,
+                         options=L.StepperOptions(z_begin=0, z_end=4, layout="aos"))
     with pytest.raises(ValueError, match="swap_deferred_fixup"):
         L.create_stepper("swap-push", "direct", geo,
                          options=L.StepperOptions(z_begin=0, z_end=4, swap_deferred_fixup=True))
@@ -96,7 +97,7 @@ def test_slab_errors(gpu):
 
 
 @pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et", "ts", "swap-push",
-                                    "swap-pull"])
+                                    "swap-pull", "cg"])
 def test_nccl_transport_single_rank_ring(gpu, scheme):
     """The NCCL transport itself (liblbmgpu.so dlopens libnccl): one rank whose
     ring neighbours are itself, the overlapped interior/boundary schedule, the
@@ -203,7 +204,8 @@ def test_indirect_nccl_single_rank_ring(gpu, scheme):
         assert bitwise_equal(s.extract_natural(), ref.extract_natural()), s.time_step()
 
 
-@pytest.mark.parametrize("scheme", ["aap", "os-push", "os-pull", "ts", "swap-push", "swap-pull"])
+@pytest.mark.parametrize("scheme", ["aap", "os-push", "os-pull", "ts", "swap-push", "swap-pull",
+                                    "cg"])
 def test_direct_slabs_with_xy_walls(gpu, scheme):
     """x/y walls: an owner node whose link towards the neighbour slab bounces
     writes that face slot itself, so phase 1 merges instead of copying"""

@@ -141,8 +141,9 @@ def test_halo_plan_shape():
     assert et.shape == (20, 5)
     assert set(et[et[:, 3] == 5][:, 4]) == {6, 16, 13}  # upper ghost
     assert set(et[et[:, 3] == -1][:, 4]) == {17, 14}  # lower ghost
+    assert np.array_equal(L.halo_plan(5, "cg"), push)  # CG's face pushes land in padding planes
     with pytest.raises(ValueError):
-        L.halo_plan(5, "cg")
+        L.halo_plan(5, "d3q27")
 
 
 @pytest.mark.parametrize("scheme", ["aap", "os-pull", "os-push", "et"])
