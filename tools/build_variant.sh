@@ -10,8 +10,8 @@ rm -rf $OUT; mkdir -p $OUT/src
 cp $SRC/*.cu $SRC/*.h $SRC/*.cuh $OUT/src/
 if [ -n "$LBM_DEVICE_HDR" ]; then cp "$LBM_DEVICE_HDR" $OUT/src/lbm_device.cuh; fi
 mkdir -p $OUT/include; cp $ROOT/include/lbmgpu.h $OUT/include/
-sed -i 's|../../include/lbmgpu.h|../include/lbmgpu.h|' $OUT/src/stepper.cu
-for f in kernels_direct kernels_aos kernels_indirect kernels_util stepper; do
+sed -i "s|../../include/lbmgpu.h|../include/lbmgpu.h|" $OUT/src/runtime.h
+for f in kernels_direct kernels_aos kernels_indirect kernels_util steppers slabs capi; do
   /usr/local/cuda/bin/nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false \
     -Xcompiler -fPIC --expt-relaxed-constexpr -ccbin /usr/bin/g++ "$@" -c $OUT/src/$f.cu -o $OUT/$f.o &
 done
