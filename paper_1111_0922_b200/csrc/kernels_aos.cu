@@ -66,23 +66,6 @@ struct WinSz {
 };
 static_assert(WinSz<double>::kBytes <= 227 * 1024 - 256, "fp64 ring exceeds shared memory");
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-template <int N>
-__device__ __forceinline__ void cp_async(void* s, const void* g) {
-  if constexpr (N == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(s)), "l"(g),
-                 "n"(N)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
 // one warp copies n elements global -> shared; s and g congruent mod 16 bytes
 template <class T>
 __device__ __forceinline__ void copy_in(T* s, const T* g, int n, int lane) {

@@ -114,7 +114,6 @@ static std::vector<HaloOp> halo_plan(int kind, int nzl) {
   }
   return v;
 }
-static std::vector<HaloOp> halo_plan(int nzl) { return halo_plan(kSlabAA, nzl); }
 
 // NCCL, loaded on first use (dlopen) so processes that never decompose do not
 // map it; inside a torch process this resolves to torch's libnccl.so.2.
