@@ -128,30 +128,30 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd_idx(Fld<
   for (int j = 1; j < 19; ++j) st<false>(e[j] == node ? F.at(opp(j), node) : F.at(j, e[j]), f[j]);
 }
 
-// The same AA odd sweep with the adjacency of the next 256-node batch staged
-// in shared memory by cp.async while the current batch computes (persistent
-// blocks): the PDF gathers no longer wait behind their index loads (fp64; C4
-// 0.94 -> 0.97 of the roofline; fp32 spills at its register budget).
-template <class T, bool VEC>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
-    k_aa_odd_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
-  __shared__ __align__(16) uint32_t sadj[2][18][kBlock];
+// Persistent-block pipeline over 256-node batches: ROWS rows of a transposed
+// per-node table (adjacency or ET rem) for the NEXT batch are staged in shared
+// memory by cp.async while the current batch computes, so the PDF accesses do
+// not wait behind their index loads. body(node, row) with row(r) = table[r][node].
+template <int ROWS, bool VEC, class Body>
+__device__ __forceinline__ void staged_batches(const uint32_t* __restrict__ table, const Idx& I,
+                                               uint32_t nbatch, uint32_t (*sm)[ROWS][kBlock],
+                                               Body body) {
   const uint32_t tid = threadIdx.x;
   auto issue = [&](uint32_t k) {
     const uint32_t bt = blockIdx.x + k * gridDim.x;
     if (bt >= nbatch) return;
     const uint32_t n0 = I.first + bt * kBlock;
     const uint32_t cnt = min((uint32_t)kBlock, I.end() - n0);
-    uint32_t* dst = &sadj[k & 1][0][0];
+    uint32_t* dst = &sm[k & 1][0][0];
     if (VEC && cnt == kBlock) {
-      for (uint32_t q = tid; q < 18 * (kBlock / 4); q += kBlock) {
+      for (uint32_t q = tid; q < ROWS * (kBlock / 4); q += kBlock) {
         const uint32_t row = q / (kBlock / 4), c = q - row * (kBlock / 4);
-        cp_async<16>(dst + row * kBlock + c * 4, I.adj + (size_t)row * I.n + n0 + c * 4);
+        cp_async<16>(dst + row * kBlock + c * 4, table + (size_t)row * I.n + n0 + c * 4);
       }
     } else {
-      for (uint32_t q = tid; q < 18 * cnt; q += kBlock) {
+      for (uint32_t q = tid; q < ROWS * cnt; q += kBlock) {
         const uint32_t row = q / cnt, c = q - row * cnt;
-        cp_async<4>(dst + row * kBlock + c, I.adj + (size_t)row * I.n + n0 + c);
+        cp_async<4>(dst + row * kBlock + c, table + (size_t)row * I.n + n0 + c);
       }
     }
   };
@@ -163,24 +163,62 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     cp_wait1();
     __syncthreads();
     const uint32_t node = I.first + (blockIdx.x + k * gridDim.x) * kBlock + tid;
-    if (node < I.end()) {
-      uint32_t e[19];
-#pragma unroll
-      for (int i = 1; i < 19; ++i) e[i] = sadj[k & 1][i - 1][tid];
-      T f[19];
-      f[0] = ld(F.at(0, node));
-#pragma unroll
-      for (int i = 1; i < 19; ++i) {
-        const int j = opp(i);
-        f[i] = ld(e[j] == node ? F.at(i, node) : F.at(j, e[j]));
-      }
-      collide(op, f);
-      st<false>(F.at(0, node), f[0]);
-#pragma unroll
-      for (int j = 1; j < 19; ++j) st<false>(e[j] == node ? F.at(opp(j), node) : F.at(j, e[j]), f[j]);
-    }
+    if (node < I.end()) body(node, [&](int r) { return sm[k & 1][r][tid]; });
     __syncthreads();  // the slot is refilled two batches later
   }
+}
+
+// AA odd sweep with the adjacency staged (fp64; C4 0.94 -> 0.97 of the
+// roofline; fp32 spills at its register budget and keeps k_aa_odd_idx)
+template <class T, bool VEC>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_aa_odd_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  __shared__ __align__(16) uint32_t sadj[2][18][kBlock];
+  staged_batches<18, VEC>(I.adj, I, nbatch, sadj, [&](uint32_t node, auto row) {
+    uint32_t e[19];
+#pragma unroll
+    for (int i = 1; i < 19; ++i) e[i] = row(i - 1);
+    T f[19];
+    f[0] = ld(F.at(0, node));
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      f[i] = ld(e[j] == node ? F.at(i, node) : F.at(j, e[j]));
+    }
+    collide(op, f);
+    st<false>(F.at(0, node), f[0]);
+#pragma unroll
+    for (int j = 1; j < 19; ++j) st<false>(e[j] == node ? F.at(opp(j), node) : F.at(j, e[j]), f[j]);
+  });
+}
+
+// ET sweep with the rem rows staged (fp64)
+template <class T, bool SW, bool VEC>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_et_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  __shared__ __align__(16) uint32_t srem[2][9][kBlock];
+  staged_batches<9, VEC>(I.rem, I, nbatch, srem, [&](uint32_t node, auto row) {
+    uint32_t rs[9];
+    T f[19];
+    f[0] = ld(F.at(0, node));
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      rs[p] = row(p);
+      const uint32_t r = rs[p] & 0x7fffffffu;
+      f[i] = ld(F.at(hb<SW>(i), node));
+      f[j] = ld(F.at(r >= I.n ? hb<SW>(i) : hb<SW>(j), r));
+    }
+    collide(op, f);
+    st<false>(F.at(0, node), f[0]);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      const bool ub = (rs[p] & 0x80000000u) != 0;
+      st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
+      st<false>(F.at(hb<SW>(j), rs[p] & 0x7fffffffu), f[i]);
+    }
+  });
 }
 
 // ET sweep, indirect (p/src/scheme_et.cpp:241-272): rem[p][n] = neighbour
@@ -422,26 +460,24 @@ void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const
   });
 }
 
+// persistent grid of the staged-batch kernels: resident fp64 blocks
+static unsigned staged_grid(uint32_t nbatch) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::min<uint32_t>(nbatch, (uint32_t)(sms * MinBlocks<double>::value));
+}
+
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
   if (I.count() == 0) return;
-  if (!f.aos && f.prec == Prec::f64) {
-    static int sms = [] {
-      int dev = 0, n = 148;
-      if (cudaGetDevice(&dev) == cudaSuccess)
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-      return n;
-    }();
+  if (!f.aos && f.prec == Prec::f64) {  // fp32 spills at its register budget
     const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
-    const bool vec = I.n % 4 == 0 && I.first % 4 == 0;
-    LBM_DISPATCH(f, {
-      if constexpr (!A && sizeof(T) == 8) {  // fp32 spills at its register budget
-        const unsigned g = std::min<uint32_t>(nbatch, (uint32_t)(sms * MinBlocks<T>::value));
-        if (vec)
-          k_aa_odd_idx_pf<T, true><<<g, kBlock, 0, st>>>(fld<T, false>(f), I, cast_op<T>(op), nbatch);
-        else
-          k_aa_odd_idx_pf<T, false><<<g, kBlock, 0, st>>>(fld<T, false>(f), I, cast_op<T>(op), nbatch);
-      }
-    });
+    const unsigned g = staged_grid(nbatch);
+    const auto F = fld<double, false>(f);
+    const auto o = cast_op<double>(op);
+    if (I.n % 4 == 0 && I.first % 4 == 0)
+      k_aa_odd_idx_pf<double, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    else
+      k_aa_odd_idx_pf<double, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     return;
   }
   if (I.count() == 0) return;
@@ -453,6 +489,18 @@ void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const Trt
 void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
                    const EtBase& base) {
   if (I.count() == 0) return;
+  if (!f.aos && f.prec == Prec::f64) {
+    const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
+    const unsigned g = staged_grid(nbatch);
+    const auto F = fld<double, false>(f);
+    const auto o = cast_op<double>(op);
+    const bool vec = I.n % 4 == 0 && I.first % 4 == 0, sw = base.swapped();
+    if (vec && sw) k_et_idx_pf<double, true, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    if (vec && !sw) k_et_idx_pf<double, false, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    if (!vec && sw) k_et_idx_pf<double, true, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    if (!vec && !sw) k_et_idx_pf<double, false, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    return;
+  }
   LBM_DISPATCH(f, {
     if (base.swapped())
       k_et_idx<T, A, true><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I, cast_op<T>(op));
