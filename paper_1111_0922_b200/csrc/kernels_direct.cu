@@ -373,6 +373,11 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
 #pragma unroll
   for (int i = 0; i < 19; ++i) f[i] = ld(F.at(i, c.s));
   collide(op, f);
+  // programmatic dependent launch: this group's reads never depend on the
+  // previous group's writes (only write-after-read hazards in CG), so the
+  // loads and the collision overlap the previous launch's tail and only the
+  // stores wait for it (no-op when launched without the attribute)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t w = c.s + (uint32_t)delta;
   st<false>(F.at(0, w), f[0]);
 #pragma unroll
@@ -382,6 +387,7 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -545,11 +551,19 @@ void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) 
 }
 
 void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-                    int delta) {
+                    int delta, bool early) {
   if (L.ncells <= L.cell_begin) return;
   LBM_DISPATCH(f, {
-    k_cg_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L,
-                                                                          cast_op<T>(op), delta);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(L.ncells - L.cell_begin));
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = early ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_cg_push<T, A>, fld<T, A>(f), L, cast_op<T>(op), delta);
   });
 }
 

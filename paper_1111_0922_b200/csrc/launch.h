@@ -84,8 +84,10 @@ void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, cons
                       const int8_t* dir, long long count);
 // CG as a plane-group push launch: read at the cell's storage index, write at
 // + delta (the other origin); copy of 5 slot planes src -> dst (seam fix-up)
+// early: programmatic dependent launch after the previous group of the same
+// sweep (loads and collision overlap its tail; stores wait for it)
 void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
-                    int delta);
+                    int delta, bool early = false);
 void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, const int* dirs,
                        uint32_t src, uint32_t dst, int writer_z);
 // AoS window kernels (kernels_aos.cu): tile + halo planes staged in shared

@@ -474,7 +474,7 @@ class SlabStepper final : public Stepper {
       dev::Lat L = cg_frame(R);
       L.cell_begin = (uint32_t)(gi * cg_p_ * plane_);
       L.ncells = (uint32_t)(std::min(nzl_, (gi + 1) * cg_p_) * plane_);
-      launch_cg_push(stream_, f, L, op_, (W - R) * (int)plane_);
+      launch_cg_push(stream_, f, L, op_, (W - R) * (int)plane_, k > 0);
     }
     cg_w_ = W;
   }

@@ -250,7 +250,7 @@ class CgDirect final : public DirectStepper {
       dev::Lat L = Lr;
       L.cell_begin = (uint32_t)(gi * P_ * plane_);
       L.ncells = (uint32_t)(std::min(geo_.nz, (gi + 1) * P_) * plane_);
-      launch_cg_push(stream_, f, L, op_, delta);
+      launch_cg_push(stream_, f, L, op_, delta, k > 0);
     }
     if (geo_.policy[2] == 0) {  // z-periodic seam fix-up
       static const int zm[5] = {6, 8, 11, 13, 16}, zp[5] = {5, 9, 12, 14, 17};
