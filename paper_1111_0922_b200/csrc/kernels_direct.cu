@@ -384,10 +384,13 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
   for (int i = 1; i < 19; ++i)
     st<false>((BB && c.bb(i)) ? F.at(opp(i), w) : F.at_off(i, w, c.off(i)), f[i]);
 }
-template <class T, bool AOS>
+template <class T, bool AOS, bool RAW>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  // the first group of a sweep reads what the previous sweep and its seam
+  // copies wrote: wait before the loads
+  if (RAW) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -404,6 +407,10 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
 template <class T, bool AOS>
 __global__ void k_plane_copy(Fld<T, AOS> F, Lat L, int8_t d0, int8_t d1, int8_t d2, int8_t d3,
                              int8_t d4, uint32_t src, uint32_t dst, int writer_z) {
+  // launched early (programmatic dependent launch): copy only once the
+  // sweep's last group is complete
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t plane = (uint32_t)L.nx * L.ny;
   const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
   if (k >= plane) return;
@@ -562,8 +569,11 @@ void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const T
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = early ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k_cg_push<T, A>, fld<T, A>(f), L, cast_op<T>(op), delta);
+    cfg.numAttrs = 1;
+    if (early)
+      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, false>, fld<T, A>(f), L, cast_op<T>(op), delta);
+    else
+      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, true>, fld<T, A>(f), L, cast_op<T>(op), delta);
   });
 }
 
@@ -571,9 +581,17 @@ void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, cons
                        uint32_t src, uint32_t dst, int writer_z) {
   const uint32_t plane = (uint32_t)L.nx * L.ny;
   LBM_DISPATCH(f, {
-    k_plane_copy<T, A><<<grid_for(plane), kBlock, 0, st>>>(
-        fld<T, A>(f), L, (int8_t)dirs[0], (int8_t)dirs[1], (int8_t)dirs[2], (int8_t)dirs[3],
-        (int8_t)dirs[4], src, dst, writer_z);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(plane));
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_plane_copy<T, A>, fld<T, A>(f), L, (int8_t)dirs[0], (int8_t)dirs[1],
+                       (int8_t)dirs[2], (int8_t)dirs[3], (int8_t)dirs[4], src, dst, writer_z);
   });
 }
 

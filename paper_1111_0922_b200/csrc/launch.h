@@ -84,8 +84,9 @@ void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, cons
                       const int8_t* dir, long long count);
 // CG as a plane-group push launch: read at the cell's storage index, write at
 // + delta (the other origin); copy of 5 slot planes src -> dst (seam fix-up)
-// early: programmatic dependent launch after the previous group of the same
-// sweep (loads and collision overlap its tail; stores wait for it)
+// launched with programmatic dependent launch: early = a later group of the
+// same sweep (loads and collision overlap the previous group's tail, stores
+// wait for it); otherwise the kernel waits for its predecessors before loading
 void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                     int delta, bool early = false);
 void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, const int* dirs,
