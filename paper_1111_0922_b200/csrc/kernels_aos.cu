@@ -170,14 +170,25 @@ __device__ __forceinline__ bool in_block(const Tile& t, int rx, int r, int z) {
 // issue the cp.async copies of window plane z (cell z, may be -1 / nz)
 template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
-                                           int* ph, const Tile& t, int z) {
+                                           int* ph, const Tile& t, int z, const T* wlo,
+                                           const T* whi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // a periodic z wrap may read a saved copy of the wrapped plane (CG groups:
+  // the plane itself may already be overwritten by an earlier group)
+  if (z < 0 && wlo) {
+    g = wlo - (size_t)L.sxy * (size_t)(L.nz - 1) * 19;
+  } else if (z >= L.nz && whi) {
+    g = whi;
+  }
   for (int r = warp; r < t.tyv + 2; r += (int)(blockDim.x >> 5)) {
     uint32_t rb;
     int phase = 0;
     if (row_base(L, t.y0 - 1 + r, z, rb)) {
-      const long long v0 = (long long)rb + L.ox + t.x0 - 1;  // record under window column 0
-      phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
+      // byte phase of the record under window column 0 (from its address: g
+      // may be a saved plane copy)
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(g) +
+                           (uintptr_t)(((long long)rb + L.ox + t.x0 - 1) * 19 * (long long)sizeof(T));
+      phase = (int)((a0 & 15u) / sizeof(T));
       T* srow = buf + r * WinSz<T>::ROW + phase;
       const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
       copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
@@ -322,7 +333,8 @@ __device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&
 
 template <class T, int MODE>
 __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1 : 2)
-    k_win(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
+    k_win(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc,
+          int z0, int z1, const T* wlo, const T* whi) {
   extern __shared__ __align__(16) unsigned char win_smem[];
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
@@ -336,14 +348,14 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   t.y0 = (tile / tiles_x) * kTY;
   t.txv = min(kTX, L.nx - t.x0);
   t.tyv = min(kTY, L.ny - t.y0);
-  t.zb = chunk * zc;
-  t.ze = min(L.nz, t.zb + zc);
+  t.zb = z0 + chunk * zc;  // planes [z0, z1) in chunks of zc
+  t.ze = min(z1, t.zb + zc);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const bool valid = tx < t.txv && ty < t.tyv;
   const T* gin = src.p;
   // ring slot of window plane z (z in [zb - 1, ze])
   auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
-  auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z); };
+  auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi); };
 
   // Schedule per plane z: wait for plane z + 1, barrier (every warp has also
   // finished plane z - 1, so slot(z + 2) = slot(z - 2) is free), prefetch
@@ -403,7 +415,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       uint32_t rb;
       row_base(L, t.y0 + ty, z, rb);
       const long long v0 = (long long)rb + L.ox + t.x0;
-      const int phase = (int)((((unsigned long long)v0 * 19ull * sizeof(T)) & 15ull) / sizeof(T));
+      const int phase =
+          (int)(((reinterpret_cast<uintptr_t>(dst.p) + (uintptr_t)(v0 * 19 * (long long)sizeof(T))) &
+                 15u) / sizeof(T));
       T* srow = sm + slot(z - 1) * BUF + ty * ROW + phase;
       if (tx < t.txv) {
 #pragma unroll
@@ -514,13 +528,15 @@ bool window_enabled() {
 
 template <class T, int MODE>
 void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
-                const TrtHost& op, int zc) {
+                const TrtHost& op, int zc, int z0, int z1, const void* wlo = nullptr,
+                const void* whi = nullptr) {
   ensure_smem<k_win<T, MODE>>(WinThreads<T, MODE>::value, WinSz<T>::kBytes);
   const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTY - 1) / kTY;
-  const int nzc = (L.nz + zc - 1) / zc;
+  const int nzc = (z1 - z0 + zc - 1) / zc;
   const unsigned grid = (unsigned)(tiles_x * tiles_y * nzc);
-  k_win<T, MODE><<<grid, WinThreads<T, MODE>::value, WinSz<T>::kBytes, st>>>(fld<T, true>(a), fld<T, true>(b), L,
-                                                             cast_op<T>(op), tiles_x, tiles_y, zc);
+  k_win<T, MODE><<<grid, WinThreads<T, MODE>::value, WinSz<T>::kBytes, st>>>(
+      fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), tiles_x, tiles_y, zc, z0, z1,
+      static_cast<const T*>(wlo), static_cast<const T*>(whi));
 }
 
 }  // namespace
@@ -560,12 +576,12 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     return false;
   const bool f64 = a.prec == Prec::f64;
   const int zc = window_chunk(L, f64, inplace);
-#define LBM_WIN_CASES(T)                                                \
-  switch (mode) {                                                       \
-    case kWinPull: launch_win<T, kWinPull>(st, a, b, L, op, zc); break;     \
-    case kWinStream: launch_win<T, kWinStream>(st, a, b, L, op, zc); break; \
-    case kWinPush: launch_win<T, kWinPush>(st, a, b, L, op, zc); break;     \
-    default: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc); break;          \
+#define LBM_WIN_CASES(T)                                                              \
+  switch (mode) {                                                                     \
+    case kWinPull: launch_win<T, kWinPull>(st, a, b, L, op, zc, 0, L.nz); break;     \
+    case kWinStream: launch_win<T, kWinStream>(st, a, b, L, op, zc, 0, L.nz); break; \
+    case kWinPush: launch_win<T, kWinPush>(st, a, b, L, op, zc, 0, L.nz); break;     \
+    default: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc, 0, L.nz); break;          \
   }
   if (f64) {
     LBM_WIN_CASES(double)
@@ -574,6 +590,30 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   }
 #undef LBM_WIN_CASES
   return true;
+}
+
+// OS-push window over planes [z0, z1) only (CG plane groups: src and dst are
+// the read and write frames of one grid; wlo / whi = saved copies of the
+// planes a periodic z wrap reads, or null)
+bool aos_push_planes_ok(const DField& src, const Lat& L) {
+  if (!src.aos || !window_enabled()) return false;
+  if (L.sx != L.nx || L.sy != L.ny || L.ox || L.oy || L.oz || L.zghost || L.znowrap) return false;
+  return L.cell_begin == 0 &&
+         (unsigned long long)L.ncells == (unsigned long long)L.nx * L.ny * L.nz;
+}
+void launch_aos_push_planes(cudaStream_t st, const DField& src, const DField& dst, const Lat& L,
+                            const TrtHost& op, int z0, int z1, const void* wlo, const void* whi) {
+  if (z1 <= z0) return;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // about two waves of resident blocks over the group's planes
+  const long long tiles = (long long)((L.nx + kTX - 1) / kTX) * ((L.ny + kTY - 1) / kTY);
+  const long long resident = (long long)sms * (src.prec == Prec::f64 ? 1 : 2);
+  const int zc = (int)std::max(4LL, std::min<long long>(z1 - z0, ((z1 - z0) * tiles) / (2 * resident) + 1));
+  if (src.prec == Prec::f64)
+    launch_win<double, kWinPush>(st, src, dst, L, op, zc, z0, z1, wlo, whi);
+  else
+    launch_win<float, kWinPush>(st, src, dst, L, op, zc, z0, z1, wlo, whi);
 }
 
 template <class T, bool RD, bool WR>

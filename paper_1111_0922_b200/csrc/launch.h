@@ -96,6 +96,12 @@ void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, cons
 enum WinModeId : int { kWinModePull = 0, kWinModeStream = 1, kWinModePush = 2, kWinModeAaOdd = 3 };
 bool launch_aos_window(cudaStream_t st, int mode, const DField& src, const DField& dst,
                        const dev::Lat& L, const TrtHost& op);
+// AoS OS-push window over planes [z0, z1) from src to dst (CG plane groups);
+// wlo / whi: saved copies of the planes a periodic z wrap reads (or null)
+bool aos_push_planes_ok(const DField& src, const dev::Lat& L);
+void launch_aos_push_planes(cudaStream_t st, const DField& src, const DField& dst,
+                            const dev::Lat& L, const TrtHost& op, int z0, int z1,
+                            const void* wlo, const void* whi);
 // local AoS sweep over contiguous records (storage index = cell + soff)
 bool launch_aos_local_stream(cudaStream_t st, const DField& src, const DField& dst,
                              const dev::Lat& L, const TrtHost& op, bool rd_opp, bool wr_opp,

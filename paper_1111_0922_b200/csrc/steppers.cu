@@ -229,6 +229,8 @@ class CgDirect final : public DirectStepper {
     if (storage_ >= (uint64_t{1} << 32))
       throw std::runtime_error("grid exceeds 32-bit cell index range");
     alloc_field(f_, storage_);
+    win_ = aos_ && aos_push_planes_ok(field(f_, soa_stride(storage_)),
+                                      make_lat(geo_, linkmask(), 0, 0, 0, 0));
     init(base_init(kSrcRest));
     sync();
   }
@@ -238,9 +240,45 @@ class CgDirect final : public DirectStepper {
     L.znowrap = 1;
     return L;
   }
+  // AoS: each plane group runs as the OS-push tile window (pull form of the
+  // push: gather post-collision values from the read frame into whole
+  // write-frame records). Within a group the read and write storage ranges
+  // are disjoint; a periodic z wrap reads copies of the read frame's planes
+  // 0 and nz-1 taken before the sweep, so no seam fix-up is needed.
+  bool aos_window_step(bool even) {
+    const DField base = field(f_, soa_stride(storage_));
+    const dev::Lat Lc = make_lat(geo_, linkmask(), 0, 0, 0, 0);
+    if (!aos_push_planes_ok(base, Lc)) return false;
+    const size_t pl = (size_t)plane_ * 19 * esize();
+    auto framed = [&](int origin) {
+      DField d = base;
+      d.p = static_cast<char*>(base.p) + (size_t)(1 + origin) * pl;
+      return d;
+    };
+    const int R = even ? S_ : 0, W = even ? 0 : S_;
+    const void *wlo = nullptr, *whi = nullptr;
+    if (geo_.policy[2] == 0) {
+      if (!side_.get()) side_.alloc(2 * pl);
+      const char* r = static_cast<const char*>(framed(R).p);
+      CK(cudaMemcpyAsync(side_.get(), r + (size_t)(geo_.nz - 1) * pl, pl, cudaMemcpyDeviceToDevice,
+                         stream_));
+      CK(cudaMemcpyAsync(static_cast<char*>(side_.get()) + pl, r, pl, cudaMemcpyDeviceToDevice,
+                         stream_));
+      wlo = side_.get();
+      whi = static_cast<char*>(side_.get()) + pl;
+    }
+    const int ngroups = (geo_.nz + P_ - 1) / P_;
+    for (int k = 0; k < ngroups; ++k) {
+      const int gi = even ? k : ngroups - 1 - k;
+      launch_aos_push_planes(stream_, framed(R), framed(W), Lc, op_, gi * P_,
+                             std::min(geo_.nz, (gi + 1) * P_), wlo, whi);
+    }
+    return true;
+  }
   void step_one() override {
     const DField f = field(f_, soa_stride(storage_));
     const bool even = (t_ & 1) == 0;
+    if (win_ && aos_window_step(even)) return;
     const int R = even ? S_ : 0, W = even ? 0 : S_;
     const int delta = (W - R) * (int)plane_;
     const dev::Lat Lr = frame(R);
@@ -261,7 +299,7 @@ class CgDirect final : public DirectStepper {
     }
   }
   int launches_per_step() const override {
-    return (geo_.nz + P_ - 1) / P_ + (geo_.policy[2] == 0 ? 2 : 0);
+    return (geo_.nz + P_ - 1) / P_ + (!win_ && geo_.policy[2] == 0 ? 2 : 0);
   }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
     ex(field(f_, soa_stride(storage_)), frame((t_ & 1) ? 0 : S_), kExNatural, n0, c, d);
@@ -276,8 +314,9 @@ class CgDirect final : public DirectStepper {
 
  private:
   int P_, S_;
+  bool win_ = false;  // AoS plane groups through the tile window
   uint64_t plane_, storage_;
-  DevMem f_;
+  DevMem f_, side_;
 };
 
 // SWAP push/pull (p/src/scheme_swap.cpp): collide pass + link-exchange pass
