@@ -29,6 +29,10 @@
 //              whose 19 owners all lie in this block's tile and z chunk is
 //              written back whole; the others (tile rim, halo ring, chunk
 //              faces) slot by slot, only the owned slots.
+//   kWinSwap   SWAP link exchange in place (p/src/scheme_swap.cpp:172-235,
+//              kernels_direct k_swap mode 1: non-wrapped links): node X swaps
+//              (i, X) <-> (opp i, X + c_i) for its back directions, so slot
+//              (k, R) is swapped by R (k back) or by R + c_k (k forward).
 #include "dispatch.h"
 #include "launch.h"
 
@@ -55,7 +59,8 @@ struct WinThreads {
   static constexpr int warps = value / 32;
 };
 
-enum WinMode : int { kWinPull = 0, kWinStream = 1, kWinPush = 2, kWinAaOdd = 3 };
+enum WinMode : int { kWinPull = 0, kWinStream = 1, kWinPush = 2, kWinAaOdd = 3, kWinSwap = 4 };
+constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap; }
 
 template <class T>
 struct WinSz {
@@ -232,6 +237,7 @@ __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T*
 // opp k of R bounces, else by R - c_k. (The same machinery for ET, whose
 // every sweep is in place, measured slower than the per-thread ET kernel:
 // 0.23 vs 0.28 of the roofline on C1 AoS fp64, so ET keeps that kernel.)
+template <int MODE>
 __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int rx, int r, int z) {
   uint32_t bR = 0;
   if (!win_cell(L, t, rx, r, z, bR)) return 0;  // solids and halo records are never written
@@ -239,13 +245,21 @@ __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int
   uint32_t m = selfin ? 1u : 0u;
 #pragma unroll
   for (int k = 1; k < 19; ++k) {
-    const bool own = ((bR >> opp(k)) & 1u) ? selfin : in_block(t, rx - cx(k), r - cy(k), z - cz(k));
+    bool own;
+    if constexpr (MODE == kWinSwap) {
+      // back slot: swapped by R; forward slot: by R + c_k (a slot nobody
+      // swaps is unchanged, so writing it back from either side is a no-op)
+      const bool back = cz(k) < 0 || (cz(k) == 0 && (cy(k) < 0 || (cy(k) == 0 && cx(k) < 0)));
+      own = back ? selfin : in_block(t, rx + cx(k), r + cy(k), z + cz(k));
+    } else {
+      own = ((bR >> opp(k)) & 1u) ? selfin : in_block(t, rx - cx(k), r - cy(k), z - cz(k));
+    }
     m |= own ? (1u << k) : 0u;
   }
   return m;
 }
 
-template <class T>
+template <int MODE, class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
                                                 const int* ph, uint32_t* msk, const Tile& t,
                                                 int z) {
@@ -281,7 +295,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
     uint32_t* mk = msk + warp * kWC;
     for (int q = c0 + lane; q < c1; q += 32) {
       int xs;
-      mk[q - c0] = col_xs(L, t.x0, col_of(q), xs) ? owned_slots(L, t, col_of(q), r, z) : 0u;
+      mk[q - c0] = col_xs(L, t.x0, col_of(q), xs) ? owned_slots<MODE>(L, t, col_of(q), r, z) : 0u;
     }
     __syncwarp();
     if (run)
@@ -303,8 +317,20 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
 // per-node body: gather (pull form) or in-place AA odd, BB = some lane of the
 // warp has a bounce link
 template <int MODE, bool BB, class T, class At>
-__device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&f)[19], At at) {
-  if constexpr (MODE == kWinAaOdd) {
+__device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&f)[19], At at,
+                                         uint32_t wrapped = 0) {
+  if constexpr (MODE == kWinSwap) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int i = back_dir(k);
+      if ((BB && ((bounce >> i) & 1u)) || ((wrapped >> i) & 1u)) continue;
+      T& a = at(0, i);
+      T& b = at(i, opp(i));
+      const T va = a;
+      a = b;
+      b = va;
+    }
+  } else if constexpr (MODE == kWinAaOdd) {
     f[0] = at(0, 0);
 #pragma unroll
     for (int i = 1; i < 19; ++i) {
@@ -338,7 +364,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   extern __shared__ __align__(16) unsigned char win_smem[];
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
-  __shared__ uint32_t msk[MODE == kWinAaOdd ? WinThreads<T, MODE>::warps * kWC : 1];
+  __shared__ uint32_t msk[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
   constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
 
   const int ntile = tiles_x * tiles_y;
@@ -400,16 +426,27 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       uint32_t bounce = 0;
       if (valid) live = cell_links(L, t.x0 + tx, t.y0 + ty, z, bounce);
       const bool interior = __all_sync(0xffffffffu, bounce == 0u);
+      uint32_t wrapped = 0;
+      if constexpr (MODE == kWinSwap) {  // periodic-seam links are the fix-up list's
+        const int x = t.x0 + tx, y = t.y0 + ty;
+        const bool px = !L.wall[0], py = !L.wall[1], pz = !L.wall[2];
+        if (px && x == 0) wrapped |= kMxm;
+        if (px && x == L.nx - 1) wrapped |= kMxp;
+        if (py && y == 0) wrapped |= kMym;
+        if (py && y == L.ny - 1) wrapped |= kMyp;
+        if (pz && z == 0) wrapped |= kMzm;
+        if (pz && z == L.nz - 1) wrapped |= kMzp;
+      }
       if (live) {
         if (interior)
-          win_node<MODE, false>(op, bounce, f, at);
+          win_node<MODE, false>(op, bounce, f, at, wrapped);
         else
-          win_node<MODE, true>(op, bounce, f, at);
+          win_node<MODE, true>(op, bounce, f, at, wrapped);
       }
     }
     __syncthreads();  // every read of plane z - 1 is done
-    if constexpr (MODE == kWinAaOdd) {
-      writeback_plane(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, t, z - 1);
+    if constexpr (in_place(MODE)) {
+      writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, t, z - 1);
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
@@ -427,10 +464,11 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       copy_out(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
     }
   }
-  if constexpr (MODE == kWinAaOdd) {
+  if constexpr (in_place(MODE)) {
     __syncthreads();
-    writeback_plane(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, t, t.ze - 1);
-    writeback_plane(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, t, t.ze);
+    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, t,
+                          t.ze - 1);
+    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, t, t.ze);
   }
 }
 
@@ -570,7 +608,7 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   if (L.sx != L.nx + 2 * L.ox || L.sy != L.ny + 2 * L.oy || L.zghost || L.znowrap) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
     return false;
-  const bool inplace = mode == kWinAaOdd;
+  const bool inplace = in_place(mode);
   if (inplace && ((!L.wall[0] && L.nx < kTX + 2) || (!L.wall[1] && L.ny < kTY + 2) ||
                   (!L.wall[2] && L.nz < 3)))
     return false;
@@ -581,7 +619,8 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     case kWinPull: launch_win<T, kWinPull>(st, a, b, L, op, zc, 0, L.nz); break;     \
     case kWinStream: launch_win<T, kWinStream>(st, a, b, L, op, zc, 0, L.nz); break; \
     case kWinPush: launch_win<T, kWinPush>(st, a, b, L, op, zc, 0, L.nz); break;     \
-    default: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc, 0, L.nz); break;          \
+    case kWinAaOdd: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc, 0, L.nz); break;   \
+    default: launch_win<T, kWinSwap>(st, a, b, L, op, zc, 0, L.nz); break;           \
   }
   if (f64) {
     LBM_WIN_CASES(double)

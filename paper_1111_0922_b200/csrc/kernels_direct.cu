@@ -554,6 +554,7 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
 
 void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode) {
   if (L.ncells <= L.cell_begin) return;
+  if (mode == 1 && launch_aos_window(st, kWinModeSwap, f, f, L, TrtHost{})) return;
   LBM_DISPATCH(f, { k_swap<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, mode); });
 }
 

@@ -93,7 +93,13 @@ void launch_plane_copy(cudaStream_t st, const DField& f, const dev::Lat& L, cons
                        uint32_t src, uint32_t dst, int writer_z);
 // AoS window kernels (kernels_aos.cu): tile + halo planes staged in shared
 // memory. Returns false (nothing launched) where they do not apply.
-enum WinModeId : int { kWinModePull = 0, kWinModeStream = 1, kWinModePush = 2, kWinModeAaOdd = 3 };
+enum WinModeId : int {
+  kWinModePull = 0,
+  kWinModeStream = 1,
+  kWinModePush = 2,
+  kWinModeAaOdd = 3,
+  kWinModeSwap = 4  // SWAP link exchange, non-wrapped links (k_swap mode 1)
+};
 bool launch_aos_window(cudaStream_t st, int mode, const DField& src, const DField& dst,
                        const dev::Lat& L, const TrtHost& op);
 // AoS OS-push window over planes [z0, z1) from src to dst (CG plane groups);

@@ -1,7 +1,8 @@
 """GPU: the AoS window kernels (kernels_aos.cu: 32x8 tiles marching through
 z chunks with a shared-memory plane ring) against the SoA kernels of the same
-scheme and against the oracle's two-step stepper. Sizes are chosen so the
-in-place AA window applies (periodic nx >= 34, ny >= 10) and tiles are
+scheme and against the oracle's two-step stepper (SWAP's link exchange and
+CG's plane groups run through the same windows). Sizes are chosen so the
+in-place AA / SWAP windows apply (periodic nx >= 34, ny >= 10) and tiles are
 partial in x and y, with walls, solids and several z chunks; fp64 and fp32
 must both be bit-identical to SoA (same arithmetic, different data path)."""
 import numpy as np
@@ -11,7 +12,7 @@ from conftest import bitwise_equal
 
 pytestmark = pytest.mark.gpu
 
-WINDOW_SCHEMES = ["ts", "os-push", "os-pull", "osnt-pull-1s", "aap"]
+WINDOW_SCHEMES = ["ts", "os-push", "os-pull", "osnt-pull-1s", "aap", "swap-push", "swap-pull", "cg"]
 GEOMS = {
     "periodic": ((40, 12, 10), ("periodic", "periodic", "periodic"), None),
     "channel_z": ((45, 17, 11), ("periodic", "periodic", "wall"), None),
