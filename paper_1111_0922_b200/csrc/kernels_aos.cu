@@ -237,6 +237,16 @@ __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T*
 // opp k of R bounces, else by R - c_k. (The same machinery for ET, whose
 // every sweep is in place, measured slower than the per-thread ET kernel:
 // 0.23 vs 0.28 of the roofline on C1 AoS fp64, so ET keeps that kernel.)
+// slot k's owner, as a window position offset from R (no bounce at R)
+template <int MODE>
+__device__ __forceinline__ constexpr int owner_sign(int k) {
+  if constexpr (MODE == kWinSwap) {
+    // back slot: swapped by R itself; forward slot: by R + c_k
+    return (cz(k) < 0 || (cz(k) == 0 && (cy(k) < 0 || (cy(k) == 0 && cx(k) < 0)))) ? 0 : 1;
+  } else {
+    return -1;  // AA odd: R - c_k
+  }
+}
 template <int MODE>
 __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int rx, int r, int z) {
   uint32_t bR = 0;
@@ -246,23 +256,33 @@ __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int
 #pragma unroll
   for (int k = 1; k < 19; ++k) {
     bool own;
-    if constexpr (MODE == kWinSwap) {
-      // back slot: swapped by R; forward slot: by R + c_k (a slot nobody
-      // swaps is unchanged, so writing it back from either side is a no-op)
-      const bool back = cz(k) < 0 || (cz(k) == 0 && (cy(k) < 0 || (cy(k) == 0 && cx(k) < 0)));
-      own = back ? selfin : in_block(t, rx + cx(k), r + cy(k), z + cz(k));
-    } else {
-      own = ((bR >> opp(k)) & 1u) ? selfin : in_block(t, rx - cx(k), r - cy(k), z - cz(k));
-    }
+    const int sg = owner_sign<MODE>(k);
+    if (MODE == kWinAaOdd && ((bR >> opp(k)) & 1u))
+      own = selfin;  // AA odd: a bounced link's slot is written by R itself
+    else
+      own = in_block(t, rx + sg * cx(k), r + sg * cy(k), z + sg * cz(k));
     m |= own ? (1u << k) : 0u;
+  }
+  return m;
+}
+// the same for a record with no bounce link on a plane strictly inside the
+// chunk: depends on the window position only (one table per block)
+template <int MODE>
+__device__ __forceinline__ uint32_t owned_slots_xy(const Tile& t, int rx, int r) {
+  auto in_xy = [&](int a, int b) { return a >= 1 && a <= t.txv && b >= 1 && b <= t.tyv; };
+  uint32_t m = in_xy(rx, r) ? 1u : 0u;
+#pragma unroll
+  for (int k = 1; k < 19; ++k) {
+    const int sg = owner_sign<MODE>(k);
+    m |= in_xy(rx + sg * cx(k), r + sg * cy(k)) ? (1u << k) : 0u;
   }
   return m;
 }
 
 template <int MODE, class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
-                                                const int* ph, uint32_t* msk, const Tile& t,
-                                                int z) {
+                                                const int* ph, uint32_t* msk, int* mcol,
+                                                const uint32_t* gmask, const Tile& t, int z) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
   const int w = t.txv + 2, rows = t.tyv + 2;
@@ -290,25 +310,43 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
     uint32_t rb;
     if (!row_base(L, t.y0 - 1 + r, z, rb)) continue;
     const T* srow = buf + r * WinSz<T>::ROW + ph[r];
-    // column q of the item: [c0, c1) directly, or the rim list of a run row
-    auto col_of = [&](int q) { return run ? (q < 2 ? q : t.txv + q - 2) : q; };
+    // per column q of the item (the range [c0, c1), or the rim list of a run
+    // row): ownership mask, window column, storage x
     uint32_t* mk = msk + warp * kWC;
+    int* mc = mcol + warp * 2 * kWC;
     for (int q = c0 + lane; q < c1; q += 32) {
-      int xs;
-      mk[q - c0] = col_xs(L, t.x0, col_of(q), xs) ? owned_slots<MODE>(L, t, col_of(q), r, z) : 0u;
+      const int rx = run ? (q < 2 ? q : t.txv + q - 2) : q;
+      int xs = 0;
+      uint32_t m = 0;
+      if (col_xs(L, t.x0, rx, xs)) {
+        uint32_t bR = 0;
+        if (zin && win_cell(L, t, rx, r, z, bR) && bR == 0)
+          m = gmask[r * kWC + rx];
+        else
+          m = owned_slots<MODE>(L, t, rx, r, z);
+      }
+      mk[q - c0] = m;
+      mc[2 * (q - c0)] = rx;
+      mc[2 * (q - c0) + 1] = xs;
     }
     __syncwarp();
     if (run)
       copy_out(g + ((size_t)rb + (size_t)(L.ox + t.x0 + 1)) * 19, srow + 2 * 19, (t.txv - 2) * 19,
                lane);
     const int n = (c1 - c0) * 19;
+    // element e = lane + 32 j: column qq = e / 19, slot k = e % 19 (stepped)
+    int qq = lane / 19, k = lane - qq * 19;
     for (int e = lane; e < n; e += 32) {
-      const int qq = e / 19, k = e - qq * 19;
-      if (!((mk[qq] >> k) & 1u)) continue;
-      const int rx = col_of(c0 + qq);
-      int xs;
-      col_xs(L, t.x0, rx, xs);
-      g[((size_t)rb + (size_t)xs) * 19 + k] = srow[rx * 19 + k];
+      if ((mk[qq] >> k) & 1u) {
+        const int rx = mc[2 * qq], xs = mc[2 * qq + 1];
+        g[((size_t)rb + (size_t)xs) * 19 + k] = srow[rx * 19 + k];
+      }
+      k += 13;  // 32 = 19 + 13
+      qq += 1;
+      if (k >= 19) {
+        k -= 19;
+        qq += 1;
+      }
     }
     __syncwarp();
   }
@@ -365,6 +403,8 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
   __shared__ uint32_t msk[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
+  __shared__ int mcol[in_place(MODE) ? WinThreads<T, MODE>::warps * 2 * kWC : 1];
+  __shared__ uint32_t gmask[in_place(MODE) ? kWR * kWC : 1];
   constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
 
   const int ntile = tiles_x * tiles_y;
@@ -379,6 +419,10 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const bool valid = tx < t.txv && ty < t.tyv;
   const T* gin = src.p;
+  if constexpr (in_place(MODE)) {  // ownership masks of no-bounce records inside the chunk
+    for (int q = threadIdx.x; q < kWR * kWC; q += blockDim.x)
+      gmask[q] = owned_slots_xy<MODE>(t, q % kWC, q / kWC);
+  }
   // ring slot of window plane z (z in [zb - 1, ze])
   auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
   auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi); };
@@ -446,7 +490,8 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     }
     __syncthreads();  // every read of plane z - 1 is done
     if constexpr (in_place(MODE)) {
-      writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, t, z - 1);
+      writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask, t,
+                            z - 1);
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
@@ -466,9 +511,10 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   }
   if constexpr (in_place(MODE)) {
     __syncthreads();
-    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, t,
-                          t.ze - 1);
-    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, t, t.ze);
+    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, mcol, gmask,
+                          t, t.ze - 1);
+    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, mcol, gmask, t,
+                          t.ze);
   }
 }
 
