@@ -33,6 +33,13 @@
 //              kernels_direct k_swap mode 1: non-wrapped links): node X swaps
 //              (i, X) <-> (opp i, X + c_i) for its back directions, so slot
 //              (k, R) is swapped by R (k back) or by R + c_k (k forward).
+//   kWinEt*    ET sweep in place (p/src/scheme_et.cpp:191-239) with the handle
+//              table's parity as the mode: physical slot s of R holds logical
+//              direction d (s = b_d); it is written by R when d is 0 or a first
+//              pair member, else (second member j of pair (i, j)) by R + c_j =
+//              R - c_i, or by R itself when link j of R bounces. Solid and
+//              wall-halo records are mailboxes: their second-member slots are
+//              written by the fluid neighbour R + c_j.
 #include "dispatch.h"
 #include "launch.h"
 
@@ -59,8 +66,17 @@ struct WinThreads {
   static constexpr int warps = value / 32;
 };
 
-enum WinMode : int { kWinPull = 0, kWinStream = 1, kWinPush = 2, kWinAaOdd = 3, kWinSwap = 4 };
-constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap; }
+enum WinMode : int {
+  kWinPull = 0,
+  kWinStream = 1,
+  kWinPush = 2,
+  kWinAaOdd = 3,
+  kWinSwap = 4,
+  kWinEtI = 5,  // ET, identity handle table
+  kWinEtS = 6   // ET, all pairs swapped
+};
+constexpr bool is_et(int mode) { return mode == kWinEtI || mode == kWinEtS; }
+constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap || is_et(mode); }
 
 template <class T>
 struct WinSz {
@@ -233,10 +249,9 @@ __device__ __forceinline__ void collide_plane(const Lat& L, const Trt<T>& op, T*
 // 0, 1, txv, txv+1 slot by slot). Lanes first compute the 19-bit ownership
 // mask of each of the item's columns (into msk), then store element-parallel
 // (coalesced, with holes). A slot is written back when the node that writes
-// it in this sweep belongs to the block: slot (k, R) is written by R if link
-// opp k of R bounces, else by R - c_k. (The same machinery for ET, whose
-// every sweep is in place, measured slower than the per-thread ET kernel:
-// 0.23 vs 0.28 of the roofline on C1 AoS fp64, so ET keeps that kernel.)
+// it in this sweep belongs to the block (AA odd: slot (k, R) is written by R
+// if link opp k of R bounces, else by R - c_k; SWAP and ET: see the mode list
+// at the top).
 // slot k's owner, as a window position offset from R (no bounce at R)
 template <int MODE>
 __device__ __forceinline__ constexpr int owner_sign(int k) {
@@ -247,12 +262,38 @@ __device__ __forceinline__ constexpr int owner_sign(int k) {
     return -1;  // AA odd: R - c_k
   }
 }
+// ET: logical direction held in physical slot s, and whether it is the
+// second member of its pair
+template <int MODE>
+__device__ __forceinline__ constexpr int et_dir(int s) {
+  return MODE == kWinEtS ? opp(s) : s;
+}
+__device__ __forceinline__ constexpr bool second_member(int d) {
+  return d == 2 || d == 4 || d == 6 || (d >= 13 && d <= 18);
+}
 template <int MODE>
 __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int rx, int r, int z) {
   uint32_t bR = 0;
-  if (!win_cell(L, t, rx, r, z, bR)) return 0;  // solids and halo records are never written
+  const bool fR = win_cell(L, t, rx, r, z, bR);
   const bool selfin = in_block(t, rx, r, z);
-  uint32_t m = selfin ? 1u : 0u;
+  uint32_t m = 0;
+  if constexpr (is_et(MODE)) {
+#pragma unroll
+    for (int s = 0; s < 19; ++s) {
+      const int d = et_dir<MODE>(s);
+      bool own;
+      if (!second_member(d))
+        own = fR && selfin;  // written by R itself (mailboxes: by nobody)
+      else if (fR && ((bR >> d) & 1u))
+        own = selfin;
+      else
+        own = in_block(t, rx + cx(d), r + cy(d), z + cz(d));
+      m |= own ? (1u << s) : 0u;
+    }
+    return m;
+  }
+  if (!fR) return 0;  // AA / SWAP: solids and halo records are never written
+  m = selfin ? 1u : 0u;
 #pragma unroll
   for (int k = 1; k < 19; ++k) {
     bool own;
@@ -265,12 +306,22 @@ __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int
   }
   return m;
 }
-// the same for a record with no bounce link on a plane strictly inside the
-// chunk: depends on the window position only (one table per block)
+// the same for a fluid record with no bounce link on a plane strictly inside
+// the chunk: depends on the window position only (one table per block)
 template <int MODE>
 __device__ __forceinline__ uint32_t owned_slots_xy(const Tile& t, int rx, int r) {
   auto in_xy = [&](int a, int b) { return a >= 1 && a <= t.txv && b >= 1 && b <= t.tyv; };
-  uint32_t m = in_xy(rx, r) ? 1u : 0u;
+  uint32_t m = 0;
+  if constexpr (is_et(MODE)) {
+#pragma unroll
+    for (int s = 0; s < 19; ++s) {
+      const int d = et_dir<MODE>(s);
+      const bool own = second_member(d) ? in_xy(rx + cx(d), r + cy(d)) : in_xy(rx, r);
+      m |= own ? (1u << s) : 0u;
+    }
+    return m;
+  }
+  m = in_xy(rx, r) ? 1u : 0u;
 #pragma unroll
   for (int k = 1; k < 19; ++k) {
     const int sg = owner_sign<MODE>(k);
@@ -357,7 +408,24 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
 template <int MODE, bool BB, class T, class At>
 __device__ __forceinline__ void win_node(const Trt<T>& op, uint32_t bounce, T (&f)[19], At at,
                                          uint32_t wrapped = 0) {
-  if constexpr (MODE == kWinSwap) {
+  if constexpr (is_et(MODE)) {
+    constexpr bool SW = MODE == kWinEtS;
+    f[0] = at(0, 0);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      f[i] = at(0, hb<SW>(i));
+      f[j] = at(i, (BB && ((bounce >> i) & 1u)) ? hb<SW>(i) : hb<SW>(j));
+    }
+    collide(op, f);
+    at(0, 0) = f[0];
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      at(0, (BB && ((bounce >> j) & 1u)) ? hb<SW>(j) : hb<SW>(i)) = f[j];
+      at(i, hb<SW>(j)) = f[i];
+    }
+  } else if constexpr (MODE == kWinSwap) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       const int i = back_dir(k);
@@ -666,7 +734,9 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     case kWinStream: launch_win<T, kWinStream>(st, a, b, L, op, zc, 0, L.nz); break; \
     case kWinPush: launch_win<T, kWinPush>(st, a, b, L, op, zc, 0, L.nz); break;     \
     case kWinAaOdd: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc, 0, L.nz); break;   \
-    default: launch_win<T, kWinSwap>(st, a, b, L, op, zc, 0, L.nz); break;           \
+    case kWinSwap: launch_win<T, kWinSwap>(st, a, b, L, op, zc, 0, L.nz); break;     \
+    case kWinEtI: launch_win<T, kWinEtI>(st, a, b, L, op, zc, 0, L.nz); break;       \
+    default: launch_win<T, kWinEtS>(st, a, b, L, op, zc, 0, L.nz); break;            \
   }
   if (f64) {
     LBM_WIN_CASES(double)

@@ -543,6 +543,7 @@ void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const Tr
 void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                const EtBase& base) {
   if (L.ncells <= L.cell_begin) return;
+  if (launch_aos_window(st, base.swapped() ? kWinModeEtSw : kWinModeEt, f, f, L, op)) return;
   LBM_DISPATCH(f, {
     const unsigned g = grid_for(L.ncells - L.cell_begin);
     if (base.swapped())

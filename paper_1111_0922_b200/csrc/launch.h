@@ -98,7 +98,9 @@ enum WinModeId : int {
   kWinModeStream = 1,
   kWinModePush = 2,
   kWinModeAaOdd = 3,
-  kWinModeSwap = 4  // SWAP link exchange, non-wrapped links (k_swap mode 1)
+  kWinModeSwap = 4,  // SWAP link exchange, non-wrapped links (k_swap mode 1)
+  kWinModeEt = 5,    // ET sweep, identity handle table
+  kWinModeEtSw = 6   // ET sweep, all pairs swapped
 };
 bool launch_aos_window(cudaStream_t st, int mode, const DField& src, const DField& dst,
                        const dev::Lat& L, const TrtHost& op);

@@ -12,7 +12,8 @@ from conftest import bitwise_equal
 
 pytestmark = pytest.mark.gpu
 
-WINDOW_SCHEMES = ["ts", "os-push", "os-pull", "osnt-pull-1s", "aap", "swap-push", "swap-pull", "cg"]
+WINDOW_SCHEMES = ["ts", "os-push", "os-pull", "osnt-pull-1s", "aap", "swap-push", "swap-pull", "cg",
+                  "et"]
 GEOMS = {
     "periodic": ((40, 12, 10), ("periodic", "periodic", "periodic"), None),
     "channel_z": ((45, 17, 11), ("periodic", "periodic", "wall"), None),
@@ -78,7 +79,7 @@ def test_aos_window_large_c4_shape(gpu):
     an even step count."""
     L = gpu
     geo = L.GridGeometry(200, 40, 48)
-    for scheme in ("aap", "os-pull", "os-push"):
+    for scheme in ("aap", "os-pull", "os-push", "et"):
         st = {lay: L.create_stepper(scheme, "direct", geo, L.bgk(1.0),
                                     L.StepperOptions(layout=lay)) for lay in ("soa", "aos")}
         for s in st.values():
