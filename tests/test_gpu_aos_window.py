@@ -89,3 +89,24 @@ def test_aos_window_large_c4_shape(gpu):
                 s.step_n(steps)
                 s.synchronize()
             assert bitwise_equal(st["soa"].extract_natural(), st["aos"].extract_natural()), scheme
+
+
+@pytest.mark.parametrize("geom", ["periodic", "walls_xy"])
+def test_aos_window_swap_deferred_fixup(gpu, geom):
+    """SWAP push with deferred seam fix-ups (p/src/scheme_swap.cpp:86-95): the
+    window exchanges the non-wrapped links, the pending list the seam links;
+    extraction in between (swap_partial phase) equals SoA bit for bit"""
+    L = gpu
+    geo = _geo(L, geom)
+    flow = L.bgk(1.7, (1e-5, 0.0, 2e-6))
+    st = {lay: L.create_stepper("swap-push", "direct", geo, flow,
+                                L.StepperOptions(layout=lay, swap_deferred_fixup=True))
+          for lay in ("soa", "aos")}
+    for s in st.values():
+        s.init_field("random", seed=12)
+    for steps in (1, 2, 3):
+        for s in st.values():
+            s.step_n(steps)
+            s.synchronize()
+        assert st["soa"].layout_phase() == st["aos"].layout_phase()
+        assert bitwise_equal(st["soa"].extract_natural(), st["aos"].extract_natural()), steps
