@@ -40,6 +40,11 @@
 //              R - c_i, or by R itself when link j of R bounces. Solid and
 //              wall-halo records are mailboxes: their second-member slots are
 //              written by the fluid neighbour R + c_j.
+// CG runs each plane group as a kWinPush window between its two frames
+// (launch_aos_push_planes; a periodic z wrap reads copies of the read
+// frame's planes 0 and nz-1 taken before the sweep). The local sweeps (AA
+// even, TS collide, precollide, SWAP collide) have no neighbour accesses and
+// stream 256-record runs through a two-slot cp.async ring (k_local_stream).
 #include "dispatch.h"
 #include "launch.h"
 
@@ -55,16 +60,6 @@ namespace {
 constexpr int kTX = 32, kTY = 8;             // tile: one warp per x-row
 constexpr int kWC = kTX + 2, kWR = kTY + 2;  // window columns / rows (1-cell halo)
 constexpr int kNB = 4;                       // plane buffers in the ring
-// threads per block: one warp per tile row computes; fp64 runs one block per
-// SM (the ring takes 207 KB) and adds 3 warps that only load and store
-// (11 x 32 = 352 threads <= 184 registers; C1 OS pull 0.62 -> 0.67) ...
-// for the gather modes (OS push's ring collisions need more than 184
-// registers; AA odd measured no better)
-template <class T, int MODE>
-struct WinThreads {
-  static constexpr int value = sizeof(T) == 8 && MODE <= 1 ? 352 : kTX * kTY;
-  static constexpr int warps = value / 32;
-};
 
 enum WinMode : int {
   kWinPull = 0,
@@ -77,6 +72,18 @@ enum WinMode : int {
 };
 constexpr bool is_et(int mode) { return mode == kWinEtI || mode == kWinEtS; }
 constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap || is_et(mode); }
+
+// threads per block: one warp per tile row computes; fp64 runs one block per
+// SM (the ring takes 207 KB) and adds 3 warps that only load and store
+// (11 x 32 = 352 threads <= 184 registers; C1 OS pull 0.62 -> 0.67) ...
+// for the gather modes (OS push's ring collisions need more than 184
+// registers; AA odd measured no better)
+template <class T, int MODE>
+struct WinThreads {
+  static constexpr int value =
+      sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream) ? 352 : kTX * kTY;
+  static constexpr int warps = value / 32;
+};
 
 template <class T>
 struct WinSz {
