@@ -369,11 +369,12 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
     if (!row_base(L, t.y0 - 1 + r, z, rb)) continue;
     const T* srow = buf + r * WinSz<T>::ROW + ph[r];
     // per column q of the item (the range [c0, c1), or the rim list of a run
-    // row): ownership mask, window column, storage x
+    // row): ownership mask and storage x
     uint32_t* mk = msk + warp * kWC;
-    int* mc = mcol + warp * 2 * kWC;
+    int* mc = mcol + warp * kWC;
+    auto col_of = [&](int q) { return run ? (q < 2 ? q : t.txv + q - 2) : q; };
     for (int q = c0 + lane; q < c1; q += 32) {
-      const int rx = run ? (q < 2 ? q : t.txv + q - 2) : q;
+      const int rx = col_of(q);
       int xs = 0;
       uint32_t m = 0;
       if (col_xs(L, t.x0, rx, xs)) {
@@ -384,8 +385,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
           m = owned_slots<MODE>(L, t, rx, r, z);
       }
       mk[q - c0] = m;
-      mc[2 * (q - c0)] = rx;
-      mc[2 * (q - c0) + 1] = xs;
+      mc[q - c0] = xs;
     }
     __syncwarp();
     if (run)
@@ -396,7 +396,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
     int qq = lane / 19, k = lane - qq * 19;
     for (int e = lane; e < n; e += 32) {
       if ((mk[qq] >> k) & 1u) {
-        const int rx = mc[2 * qq], xs = mc[2 * qq + 1];
+        const int rx = col_of(c0 + qq), xs = mc[qq];
         g[((size_t)rb + (size_t)xs) * 19 + k] = srow[rx * 19 + k];
       }
       k += 13;  // 32 = 19 + 13
@@ -407,6 +407,104 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
       }
     }
     __syncwarp();
+  }
+}
+
+// Compact write-back (in-place modes, the planes strictly inside the chunk of
+// a block whose tile touches no x/y wall, all-fluid lattice): every record of
+// such a plane has no bounce link, so its owned slots depend on the window
+// position only (gmask). The block lists, once, the owned (row, column, slot)
+// elements outside the whole-record runs; a plane's write-back is then the
+// runs (16-byte vectors, one warp per row) plus one strided pass of all
+// threads over the list. Entry: row << 12 | column class << 10 | column * 19
+// + slot; class 1 / 2 = window column 0 / w - 1 (their storage x may wrap),
+// 0 = the others.
+constexpr int kListMax = 4 * kWC * 19 + (kWR - 4) * 4 * 19;  // tyv >= 3: 4 full rows + rims
+// static shared memory of an in-place window block (k_win below); fp32 must
+// keep two blocks per SM (228 KB per SM, 1 KB reserved per block)
+constexpr size_t kInPlaceStatic = kNB * kWR * 4 + 8 * kWC * 4 * 2 + kWR * kWC * 4 + kListMax * 2 +
+                                  (kWR + 1) * 4 + kWR * 8 + kWR * 4;
+static_assert(2 * (WinSz<float>::kBytes + kInPlaceStatic + 1024) <= 228 * 1024,
+              "fp32 in-place window no longer fits two blocks per SM");
+
+struct WbList {
+  uint16_t* e;      // entries
+  int n;            // entry count
+  long long colb[3];  // element offset of column class c: storage x of column q = (colb + q*19)/19
+};
+
+// fast-path eligibility of the block (uniform)
+__device__ __forceinline__ bool wb_fast_ok(const Lat& L, const Tile& t) {
+  if (L.linkmask || t.txv < 3 || t.tyv < 3) return false;
+  if (L.wall[0] && (t.x0 == 0 || t.x0 + t.txv == L.nx)) return false;
+  if (L.wall[1] && (t.y0 == 0 || t.y0 + t.tyv == L.ny)) return false;
+  return true;
+}
+
+// build the block's list (all threads; cnt = kWR + 1 ints of scratch)
+__device__ __forceinline__ int wb_build(const Lat& L, const Tile& t, const uint32_t* gmask,
+                                        uint16_t* list, int* cnt) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+  const int w = t.txv + 2, rows = t.tyv + 2;
+  auto row_cols = [&](int r, int j) {  // j-th slot-by-slot column of row r
+    const bool run = r >= 2 && r <= t.tyv - 1;
+    return run ? (j < 2 ? j : t.txv + j - 2) : j;
+  };
+  auto row_ncols = [&](int r) { return (r >= 2 && r <= t.tyv - 1) ? 4 : w; };
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int r = warp; r < rows; r += nw) {
+      const int ne = row_ncols(r) * 19;
+      int pos = pass ? cnt[r] : 0;
+      for (int b = 0; b < ne; b += 32) {
+        const int e = b + lane;
+        bool own = false;
+        int q = 0, k = 0;
+        if (e < ne) {
+          const int j = e / 19;
+          k = e - j * 19;
+          q = row_cols(r, j);
+          own = (gmask[r * kWC + q] >> k) & 1u;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, own);
+        if (pass && own) {
+          const int cls = q == 0 ? 1 : (q == w - 1 ? 2 : 0);
+          list[pos + __popc(bal & ((1u << lane) - 1u))] =
+              (uint16_t)((r << 12) | (cls << 10) | (q * 19 + k));
+        }
+        pos += __popc(bal);
+      }
+      if (!pass && lane == 0) cnt[r] = pos;
+    }
+    __syncthreads();
+    if (!pass && threadIdx.x == 0) {  // counts -> offsets
+      int s = 0;
+      for (int r = 0; r < rows; ++r) {
+        const int c = cnt[r];
+        cnt[r] = s;
+        s += c;
+      }
+      cnt[rows] = s;
+    }
+    __syncthreads();
+  }
+  return cnt[rows];
+}
+
+// one plane's write-back from its ring slot (rbp / sbp: the plane's per-row
+// storage base in elements and ring offset, published before the barrier)
+template <class T>
+__device__ __forceinline__ void writeback_fast(const Lat& L, T* __restrict__ g, const T* ring,
+                                               const WbList& wl, const long long* rbp,
+                                               const int* sbp, const Tile& t) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+  // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
+  for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
+    copy_out(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
+  for (int e = threadIdx.x; e < wl.n; e += (int)blockDim.x) {
+    const uint32_t v = wl.e[e];
+    const int r = (int)(v >> 12), cls = (int)((v >> 10) & 3u), off = (int)(v & 1023u);
+    const long long cb = cls == 0 ? wl.colb[0] : (cls == 1 ? wl.colb[1] : wl.colb[2]);
+    g[rbp[r] + cb + off] = ring[sbp[r] + off];
   }
 }
 
@@ -478,8 +576,12 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
   __shared__ uint32_t msk[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
-  __shared__ int mcol[in_place(MODE) ? WinThreads<T, MODE>::warps * 2 * kWC : 1];
+  __shared__ int mcol[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
   __shared__ uint32_t gmask[in_place(MODE) ? kWR * kWC : 1];
+  __shared__ uint16_t wlist[in_place(MODE) ? kListMax : 1];
+  __shared__ int wcnt[kWR + 1];
+  __shared__ long long rbp[kWR];  // write-back plane: row storage bases (elements)
+  __shared__ int sbp[kWR];        // ... and ring offsets
   constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
 
   const int ntile = tiles_x * tiles_y;
@@ -498,6 +600,23 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     for (int q = threadIdx.x; q < kWR * kWC; q += blockDim.x)
       gmask[q] = owned_slots_xy<MODE>(t, q % kWC, q / kWC);
   }
+  WbList wl{wlist, 0, {0, 0, 0}};
+  bool fast = false;
+  if constexpr (in_place(MODE)) {
+    fast = wb_fast_ok(L, t);
+    if (fast) {
+      __syncthreads();  // gmask
+      wl.n = wb_build(L, t, gmask, wlist, wcnt);
+      int xs0 = 0, xs1 = 0;
+      col_xs(L, t.x0, 0, xs0);
+      col_xs(L, t.x0, t.txv + 1, xs1);
+      wl.colb[0] = (long long)(t.x0 - 1 + L.ox) * 19;
+      wl.colb[1] = (long long)xs0 * 19;
+      wl.colb[2] = (long long)(xs1 - (t.txv + 1)) * 19;
+    }
+  }
+  // plane zp is written back by the compact pass
+  auto fast_plane = [&](int zp) { return fast && zp >= t.zb + 1 && zp <= t.ze - 2; };
   // ring slot of window plane z (z in [zb - 1, ze])
   auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
   auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi); };
@@ -563,10 +682,22 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
           win_node<MODE, true>(op, bounce, f, at, wrapped);
       }
     }
+    if constexpr (in_place(MODE)) {
+      if (fast_plane(z - 1) && (int)threadIdx.x < t.tyv + 2) {
+        const int r = threadIdx.x;
+        uint32_t rb = 0;
+        row_base(L, t.y0 - 1 + r, z - 1, rb);
+        rbp[r] = (long long)rb * 19;
+        sbp[r] = slot(z - 1) * BUF + r * ROW + ph[slot(z - 1)][r];
+      }
+    }
     __syncthreads();  // every read of plane z - 1 is done
     if constexpr (in_place(MODE)) {
-      writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask, t,
-                            z - 1);
+      if (fast_plane(z - 1))
+        writeback_fast(L, dst.p, sm, wl, rbp, sbp, t);
+      else
+        writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask,
+                              t, z - 1);
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
