@@ -337,10 +337,33 @@ __device__ __forceinline__ uint32_t owned_slots_xy(const Tile& t, int rx, int r)
   return m;
 }
 
+// the z part of the ownership rule for window plane z of a chunk [zb, ze):
+// slot k's writer sits at z + dz(k), dz = 0 (written by the record itself) or
+// the owner offset's z component; all ones strictly inside the chunk
+template <int MODE>
+__device__ __forceinline__ uint32_t zmask_of(const Tile& t, int z) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 19; ++k) {
+    int dz;
+    if constexpr (is_et(MODE)) {
+      const int d = et_dir<MODE>(k);
+      dz = second_member(d) ? cz(d) : 0;
+    } else {
+      dz = k == 0 ? 0 : owner_sign<MODE>(k) * cz(k);
+    }
+    m |= (z + dz >= t.zb && z + dz < t.ze) ? (1u << k) : 0u;
+  }
+  return m;
+}
+
+// zm != 0: every record of the plane is bounce-free and its owned slots are
+// gmask & zm (a fast block's chunk-face and halo planes, see zmask_of)
 template <int MODE, class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
                                                 const int* ph, uint32_t* msk, int* mcol,
-                                                const uint32_t* gmask, const Tile& t, int z) {
+                                                const uint32_t* gmask, const Tile& t, int z,
+                                                uint32_t zm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
   const int w = t.txv + 2, rows = t.tyv + 2;
@@ -379,7 +402,9 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
       uint32_t m = 0;
       if (col_xs(L, t.x0, rx, xs)) {
         uint32_t bR = 0;
-        if (zin && win_cell(L, t, rx, r, z, bR) && bR == 0)
+        if (zm)
+          m = gmask[r * kWC + rx] & zm;
+        else if (zin && win_cell(L, t, rx, r, z, bR) && bR == 0)
           m = gmask[r * kWC + rx];
         else
           m = owned_slots<MODE>(L, t, rx, r, z);
@@ -493,9 +518,9 @@ __device__ __forceinline__ int wb_build(const Lat& L, const Tile& t, const uint3
 // one plane's write-back from its ring slot (rbp / sbp: the plane's per-row
 // storage base in elements and ring offset, published before the barrier)
 template <class T>
-__device__ __forceinline__ void writeback_fast(const Lat& L, T* __restrict__ g, const T* ring,
-                                               const WbList& wl, const long long* rbp,
-                                               const int* sbp, const Tile& t) {
+__device__ __forceinline__ void writeback_fast(T* __restrict__ g, const T* ring, const WbList& wl,
+                                               const long long* rbp, const int* sbp,
+                                               const Tile& t) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
   // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
   for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
@@ -617,6 +642,17 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   }
   // plane zp is written back by the compact pass
   auto fast_plane = [&](int zp) { return fast && zp >= t.zb + 1 && zp <= t.ze - 2; };
+  // a fast block's other planes: gmask & zmask when the plane is a bounce-free
+  // domain plane (not a z-wall face, not an ET mailbox halo plane)
+  auto face_zm = [&](int zp) -> uint32_t {
+    int zcell;
+#ifdef LBM_NO_FACE_ZM
+    return 0u;
+#endif
+    if (!fast || !axis_cell(zp, L.nz, L.wall[2], L.oz, zcell)) return 0u;
+    if (L.wall[2] && (zcell == 0 || zcell == L.nz - 1)) return 0u;
+    return zmask_of<MODE>(t, zp);
+  };
   // ring slot of window plane z (z in [zb - 1, ze])
   auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
   auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi); };
@@ -694,10 +730,10 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     __syncthreads();  // every read of plane z - 1 is done
     if constexpr (in_place(MODE)) {
       if (fast_plane(z - 1))
-        writeback_fast(L, dst.p, sm, wl, rbp, sbp, t);
+        writeback_fast(dst.p, sm, wl, rbp, sbp, t);
       else
         writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask,
-                              t, z - 1);
+                              t, z - 1, face_zm(z - 1));
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
@@ -718,9 +754,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   if constexpr (in_place(MODE)) {
     __syncthreads();
     writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, mcol, gmask,
-                          t, t.ze - 1);
+                          t, t.ze - 1, face_zm(t.ze - 1));
     writeback_plane<MODE>(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, mcol, gmask, t,
-                          t.ze);
+                          t.ze, face_zm(t.ze));
   }
 }
 

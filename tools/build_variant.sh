@@ -1,6 +1,7 @@
 #!/bin/bash
 # build an experimental liblbmgpu variant: tools/build_variant.sh NAME [nvcc -D flags...]
-# (the device header can be swapped with LBM_DEVICE_HDR=/path/to/lbm_device.cuh)
+# (the device header can be swapped with LBM_DEVICE_HDR=/path/to/lbm_device.cuh, the AoS
+# window source with LBM_AOS_SRC=/path/to/kernels_aos.cu)
 set -e
 NAME=$1; shift
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
@@ -9,6 +10,7 @@ OUT=$ROOT/build/variants/$NAME
 rm -rf $OUT; mkdir -p $OUT/src
 cp $SRC/*.cu $SRC/*.h $SRC/*.cuh $OUT/src/
 if [ -n "$LBM_DEVICE_HDR" ]; then cp "$LBM_DEVICE_HDR" $OUT/src/lbm_device.cuh; fi
+if [ -n "$LBM_AOS_SRC" ]; then cp "$LBM_AOS_SRC" $OUT/src/kernels_aos.cu; fi
 mkdir -p $OUT/include; cp $ROOT/include/lbmgpu.h $OUT/include/
 sed -i "s|../../include/lbmgpu.h|../include/lbmgpu.h|" $OUT/src/runtime.h
 for f in kernels_direct kernels_aos kernels_indirect kernels_util steppers slabs capi; do
