@@ -129,6 +129,53 @@ __device__ __forceinline__ void copy_out(T* g, const T* s, int n, int lane) {
   if (t0 + lane < n) g[t0 + lane] = s[t0 + lane];
 }
 
+// Bulk (TMA engine) forms, selected by LBM_AOS_BULK (default on): the
+// 16-byte-aligned middle of a row moves as one cp.async.bulk issued by lane 0
+// (loads count their bytes on the ring slot's mbarrier, stores join a bulk
+// group), the unaligned head / tail elements as before.
+#ifndef LBM_AOS_BULK
+#define LBM_AOS_BULK 1
+#endif
+constexpr bool kBulk = LBM_AOS_BULK != 0;
+
+// one warp: n elements global -> shared (congruent mod 16 bytes); lane 0
+// arrives on bar once with the bulk bytes
+template <class T>
+__device__ __forceinline__ void copy_in_bulk(T* s, const T* g, int n, int lane, uint64_t* bar) {
+  constexpr int V = 16 / (int)sizeof(T);
+  int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
+  if (head > n) head = n;
+  const int nmid = (n - head) / V * V;
+  if (lane < head) cp_async<sizeof(T)>(s + lane, g + lane);
+  const int t0 = head + nmid;
+  if (t0 + lane < n) cp_async<sizeof(T)>(s + t0 + lane, g + t0 + lane);
+  if (lane == 0) {
+    const uint32_t bytes = (uint32_t)nmid * (uint32_t)sizeof(T);
+    mbar_arrive_tx(bar, bytes);
+    if (bytes) bulk_g2s(s + head, g + head, bytes, bar);
+  }
+}
+// one warp: n elements shared -> global (congruent mod 16 bytes). The lanes'
+// own shared-memory writes must precede it (each lane fences them for the
+// async proxy here); lane 0 later waits for the group's reads (bulk_wait_read)
+// before the staging area is reused.
+template <class T>
+__device__ __forceinline__ void copy_out_bulk(T* g, const T* s, int n, int lane) {
+  constexpr int V = 16 / (int)sizeof(T);
+  int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
+  if (head > n) head = n;
+  const int nmid = (n - head) / V * V;
+  fence_async_smem();
+  __syncwarp();
+  if (lane < head) g[lane] = s[lane];
+  const int t0 = head + nmid;
+  if (t0 + lane < n) g[t0 + lane] = s[t0 + lane];
+  if (lane == 0 && nmid) {
+    bulk_s2g(g + head, s + head, (uint32_t)nmid * (uint32_t)sizeof(T));
+    bulk_commit();
+  }
+}
+
 // window position p on one axis (cell coordinate, may be -1 or n) -> storage
 // coordinate; false when no record is stored there (a wall axis without a
 // halo). Halo axes (ET: wall axes carry one mailbox layer, o = 1) keep the
@@ -199,7 +246,7 @@ __device__ __forceinline__ bool in_block(const Tile& t, int rx, int r, int z) {
 template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
                                            int* ph, const Tile& t, int z, const T* wlo,
-                                           const T* whi) {
+                                           const T* whi, uint64_t* bar) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // a periodic z wrap may read a saved copy of the wrapped plane (CG groups:
   // the plane itself may already be overwritten by an earlier group)
@@ -219,12 +266,18 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
       phase = (int)((a0 & 15u) / sizeof(T));
       T* srow = buf + r * WinSz<T>::ROW + phase;
       const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
-      copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
-              (xb - xa + 1) * 19, lane);
+      if constexpr (kBulk)
+        copy_in_bulk(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
+                     (xb - xa + 1) * 19, lane, bar);
+      else
+        copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
+                (xb - xa + 1) * 19, lane);
       if (!L.wall[0] && !L.ox) {
         if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
         if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
       }
+    } else if (kBulk && lane == 0) {
+      mbar_arrive_tx(bar, 0);  // every window row arrives once per load
     }
     if (lane == 0) ph[r] = phase;
   }
@@ -448,7 +501,7 @@ constexpr int kListMax = 4 * kWC * 19 + (kWR - 4) * 4 * 19;  // tyv >= 3: 4 full
 // static shared memory of an in-place window block (k_win below); fp32 must
 // keep two blocks per SM (228 KB per SM, 1 KB reserved per block)
 constexpr size_t kInPlaceStatic = kNB * kWR * 4 + 8 * kWC * 4 * 2 + kWR * kWC * 4 + kListMax * 2 +
-                                  (kWR + 1) * 4 + kWR * 8 + kWR * 4;
+                                  (kWR + 1) * 4 + kWR * 8 + kWR * 4 + kNB * 8;
 static_assert(2 * (WinSz<float>::kBytes + kInPlaceStatic + 1024) <= 228 * 1024,
               "fp32 in-place window no longer fits two blocks per SM");
 
@@ -524,7 +577,11 @@ __device__ __forceinline__ void writeback_fast(T* __restrict__ g, const T* ring,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
   // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
   for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
-    copy_out(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
+    if constexpr (kBulk)
+      copy_out_bulk(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19,
+                    lane);
+    else
+      copy_out(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
   for (int e = threadIdx.x; e < wl.n; e += (int)blockDim.x) {
     const uint32_t v = wl.e[e];
     const int r = (int)(v >> 12), cls = (int)((v >> 10) & 3u), off = (int)(v & 1023u);
@@ -607,6 +664,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   __shared__ int wcnt[kWR + 1];
   __shared__ long long rbp[kWR];  // write-back plane: row storage bases (elements)
   __shared__ int sbp[kWR];        // ... and ring offsets
+  __shared__ __align__(8) uint64_t lbar[kNB];  // ring slot s: bulk bytes of its current load
   constexpr int BUF = WinSz<T>::BUF, ROW = WinSz<T>::ROW;
 
   const int ntile = tiles_x * tiles_y;
@@ -655,7 +713,18 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   };
   // ring slot of window plane z (z in [zb - 1, ze])
   auto slot = [&](int z) { return (z - t.zb + 1) & (kNB - 1); };
-  auto load = [&](int z) { load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi); };
+  auto load = [&](int z) {
+    load_plane(L, gin, sm + slot(z) * BUF, ph[slot(z)], t, z, wlo, whi, &lbar[slot(z)]);
+  };
+  // parity of the k-th load into a slot: k & 1
+  auto wait_plane = [&](int z) { mbar_wait(&lbar[slot(z)], (uint32_t)((z - t.zb + 1) >> 2) & 1u); };
+  if constexpr (kBulk) {
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < kNB; ++b) mbar_init(&lbar[b], (uint32_t)(t.tyv + 2));
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
 
   // Schedule per plane z: wait for plane z + 1, barrier (every warp has also
   // finished plane z - 1, so slot(z + 2) = slot(z - 2) is free), prefetch
@@ -667,11 +736,23 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   for (int z = t.zb; z < t.ze; ++z) {
     if (z == t.zb) load(z + 1);
     cp_commit();
-    if (z == t.zb) cp_wait1(); else cp_wait0();
-    __syncthreads();
-    if (z == t.zb) {
-      cp_wait0();  // plane z + 1 of the prologue
+    if constexpr (kBulk) {
+      if (z == t.zb) {
+        wait_plane(z - 1);
+        wait_plane(z);
+      }
+      wait_plane(z + 1);
+      bulk_wait_read();    // plane z - 2's bulk stores have left its slot
+      fence_async_smem();  // this thread's ring accesses before the slot's next bulk load
+      cp_wait0();
       __syncthreads();
+    } else {
+      if (z == t.zb) cp_wait1(); else cp_wait0();
+      __syncthreads();
+      if (z == t.zb) {
+        cp_wait0();  // plane z + 1 of the prologue
+        __syncthreads();
+      }
     }
     if (z + 2 <= t.ze) load(z + 2);
     if constexpr (MODE == kWinPush) {
@@ -726,6 +807,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         rbp[r] = (long long)rb * 19;
         sbp[r] = slot(z - 1) * BUF + r * ROW + ph[slot(z - 1)][r];
       }
+      if constexpr (kBulk) fence_async_smem();  // ring writes before the runs' bulk stores
     }
     __syncthreads();  // every read of plane z - 1 is done
     if constexpr (in_place(MODE)) {
@@ -748,9 +830,13 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         for (int i = 0; i < 19; ++i) srow[tx * 19 + i] = live ? f[i] : T(0);
       }
       __syncwarp();
-      copy_out(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
+      if constexpr (kBulk)
+        copy_out_bulk(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
+      else
+        copy_out(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
     }
   }
+  if constexpr (kBulk) bulk_wait_all();
   if constexpr (in_place(MODE)) {
     __syncthreads();
     writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, mcol, gmask,
