@@ -78,10 +78,14 @@ constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap
 // (11 x 32 = 352 threads <= 184 registers; C1 OS pull 0.62 -> 0.67) ...
 // for the gather modes (OS push's ring collisions need more than 184
 // registers; AA odd measured no better)
+#ifndef LBM_WIN_GATHER_THREADS
+#define LBM_WIN_GATHER_THREADS 352
+#endif
 template <class T, int MODE>
 struct WinThreads {
-  static constexpr int value =
-      sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream) ? 352 : kTX * kTY;
+  static constexpr int value = sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream)
+                                   ? LBM_WIN_GATHER_THREADS
+                                   : kTX * kTY;
   static constexpr int warps = value / 32;
 };
 
@@ -138,8 +142,11 @@ __device__ __forceinline__ void copy_out(T* g, const T* s, int n, int lane) {
 #endif
 constexpr bool kBulk = LBM_AOS_BULK != 0;
 
-// one warp: n elements global -> shared (congruent mod 16 bytes); lane 0
-// arrives on bar once with the bulk bytes
+// one warp: n elements global -> shared (congruent mod 16 bytes). Arrivals on
+// bar (kRowArrivals per row): every lane once when its cp.async copies (the
+// unaligned head / tail, and any the caller issued before) have landed, lane 0
+// once more with the bulk bytes.
+constexpr uint32_t kRowArrivals = 33;
 template <class T>
 __device__ __forceinline__ void copy_in_bulk(T* s, const T* g, int n, int lane, uint64_t* bar) {
   constexpr int V = 16 / (int)sizeof(T);
@@ -149,6 +156,7 @@ __device__ __forceinline__ void copy_in_bulk(T* s, const T* g, int n, int lane, 
   if (lane < head) cp_async<sizeof(T)>(s + lane, g + lane);
   const int t0 = head + nmid;
   if (t0 + lane < n) cp_async<sizeof(T)>(s + t0 + lane, g + t0 + lane);
+  cp_async_mbar_arrive(bar);
   if (lane == 0) {
     const uint32_t bytes = (uint32_t)nmid * (uint32_t)sizeof(T);
     mbar_arrive_tx(bar, bytes);
@@ -266,18 +274,18 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
       phase = (int)((a0 & 15u) / sizeof(T));
       T* srow = buf + r * WinSz<T>::ROW + phase;
       const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
+      if (!L.wall[0] && !L.ox) {
+        if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
+        if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
+      }
       if constexpr (kBulk)
         copy_in_bulk(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
                      (xb - xa + 1) * 19, lane, bar);
       else
         copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
                 (xb - xa + 1) * 19, lane);
-      if (!L.wall[0] && !L.ox) {
-        if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
-        if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
-      }
     } else if (kBulk && lane == 0) {
-      mbar_arrive_tx(bar, 0);  // every window row arrives once per load
+      mbar_arrive(bar, kRowArrivals);  // every window row arrives fully once per load
     }
     if (lane == 0) ph[r] = phase;
   }
@@ -720,7 +728,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   auto wait_plane = [&](int z) { mbar_wait(&lbar[slot(z)], (uint32_t)((z - t.zb + 1) >> 2) & 1u); };
   if constexpr (kBulk) {
     if (threadIdx.x == 0) {
-      for (int b = 0; b < kNB; ++b) mbar_init(&lbar[b], (uint32_t)(t.tyv + 2));
+      for (int b = 0; b < kNB; ++b) mbar_init(&lbar[b], (uint32_t)(t.tyv + 2) * kRowArrivals);
       mbar_fence_init();
     }
     __syncthreads();
@@ -735,26 +743,29 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   cp_commit();
   for (int z = t.zb; z < t.ze; ++z) {
     if (z == t.zb) load(z + 1);
-    cp_commit();
     if constexpr (kBulk) {
+      // every warp is done with plane z - 2's slot (compute of z - 1, write-back
+      // of z - 2 and its bulk stores' reads): refill it with plane z + 2, then
+      // wait for plane z + 1 (two planes in flight while waiting)
+      bulk_wait_read();
+      fence_async_smem();
+      __syncthreads();
+      if (z + 2 <= t.ze) load(z + 2);
       if (z == t.zb) {
         wait_plane(z - 1);
         wait_plane(z);
       }
       wait_plane(z + 1);
-      bulk_wait_read();    // plane z - 2's bulk stores have left its slot
-      fence_async_smem();  // this thread's ring accesses before the slot's next bulk load
-      cp_wait0();
-      __syncthreads();
     } else {
+      cp_commit();
       if (z == t.zb) cp_wait1(); else cp_wait0();
       __syncthreads();
       if (z == t.zb) {
         cp_wait0();  // plane z + 1 of the prologue
         __syncthreads();
       }
+      if (z + 2 <= t.ze) load(z + 2);
     }
-    if (z + 2 <= t.ze) load(z + 2);
     if constexpr (MODE == kWinPush) {
       if (z == t.zb) {
         collide_plane(L, op, sm + slot(z - 1) * BUF, ph[slot(z - 1)], t, z - 1);
