@@ -896,13 +896,7 @@ __global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
   uint32_t nmine = 0;
   while (blockIdx.x + nmine * gridDim.x < nruns) ++nmine;
   if (nmine == 0) return;
-  issue(0);
-  cp_commit();
-  for (uint32_t k = 0; k < nmine; ++k) {
-    if (k + 1 < nmine) issue(k + 1);
-    cp_commit();
-    cp_wait1();
-    __syncthreads();
+  auto compute = [&](uint32_t k) {
     const uint32_t c0 = run_c0(k);
     const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
     T* s = sm + (k & 1) * SLOT + phase_of(c0);
@@ -915,7 +909,56 @@ __global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
 #pragma unroll
       for (int i = 0; i < 19; ++i) s[r * 19 + (WR_OPP ? opp(i) : i)] = f[i];
     }
+  };
+  if constexpr (kBulk) {
+    // warp 0 moves each run: one bulk copy in (bytes on the slot's mbarrier,
+    // head / tail by cp.async) and one bulk copy out
+    __shared__ __align__(8) uint64_t rbar[2];
+    if (threadIdx.x == 0) {
+      mbar_init(&rbar[0], kRowArrivals);
+      mbar_init(&rbar[1], kRowArrivals);
+      mbar_fence_init();
+    }
     __syncthreads();
+    auto issue_bulk = [&](uint32_t k) {
+      const uint32_t c0 = run_c0(k);
+      const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
+      copy_in_bulk(sm + (k & 1) * SLOT + phase_of(c0), src.p + (size_t)(c0 + soff) * 19,
+                   (int)(nrec * 19), lane, &rbar[k & 1]);
+    };
+    if (warp == 0) issue_bulk(0);
+    for (uint32_t k = 0; k < nmine; ++k) {
+      // run k - 1's slot: its collisions are done and its bulk store has read it
+      bulk_wait_read();
+      fence_async_smem();
+      __syncthreads();
+      if (warp == 0 && k + 1 < nmine) issue_bulk(k + 1);
+      mbar_wait(&rbar[k & 1], (k >> 1) & 1u);
+      compute(k);
+      fence_async_smem();
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t c0 = run_c0(k);
+        const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
+        copy_out_bulk(dst.p + (size_t)(c0 + soff) * 19, sm + (k & 1) * SLOT + phase_of(c0),
+                      (int)(nrec * 19), lane);
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+  issue(0);
+  cp_commit();
+  for (uint32_t k = 0; k < nmine; ++k) {
+    if (k + 1 < nmine) issue(k + 1);
+    cp_commit();
+    cp_wait1();
+    __syncthreads();
+    compute(k);
+    __syncthreads();
+    const uint32_t c0 = run_c0(k);
+    const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
+    T* s = sm + (k & 1) * SLOT + phase_of(c0);
     const uint32_t nel = nrec * 19, per = (nel + 7) / 8;
     const uint32_t e0 = min(nel, (uint32_t)warp * per), e1 = min(nel, e0 + per);
     if (e1 > e0) copy_out(dst.p + (size_t)(c0 + soff) * 19 + e0, s + e0, (int)(e1 - e0), lane);
