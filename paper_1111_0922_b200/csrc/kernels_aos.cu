@@ -22,6 +22,10 @@
 //              the same values the scatter B[i][Y + c_i] = post(Y)[i] writes
 //              (p/src/scheme_os.cpp:104-139); halo records are collided
 //              redundantly by both tiles (deterministic, identical)
+//   kWinPushS  OS push, scatter form (fp64): each tile node collides its own
+//              record and stores post(X)[i] into slot i of X + c_i in the
+//              ring; the output leaves through the AA-odd ownership
+//              write-back into the other grid
 //   kWinAaOdd  AA odd sweep in place (p/src/scheme_aap.cpp:133-173). Node X
 //              reads and rewrites the slot set {(opp i, X - c_i)} (bounce:
 //              (i, X)); those sets partition the grid, so the owner of slot
@@ -68,10 +72,14 @@ enum WinMode : int {
   kWinAaOdd = 3,
   kWinSwap = 4,
   kWinEtI = 5,  // ET, identity handle table
-  kWinEtS = 6   // ET, all pairs swapped
+  kWinEtS = 6,  // ET, all pairs swapped
+  kWinPushS = 7 // OS push, scatter form
 };
 constexpr bool is_et(int mode) { return mode == kWinEtI || mode == kWinEtS; }
 constexpr bool in_place(int mode) { return mode == kWinAaOdd || mode == kWinSwap || is_et(mode); }
+// modes whose output leaves through the ownership write-back (in place, or
+// the scatter-form push into the other grid)
+constexpr bool owned_wb(int mode) { return in_place(mode) || mode == kWinPushS; }
 
 // threads per block: one warp per tile row computes; fp64 runs one block per
 // SM (the ring takes 207 KB) and adds 3 warps that only load and store
@@ -336,6 +344,8 @@ template <int MODE>
 __device__ __forceinline__ constexpr int et_dir(int s) {
   return MODE == kWinEtS ? opp(s) : s;
 }
+// the directions with c_z = +1
+__device__ constexpr int kUp[5] = {5, 9, 12, 14, 17};
 __device__ __forceinline__ constexpr bool second_member(int d) {
   return d == 2 || d == 4 || d == 6 || (d >= 13 && d <= 18);
 }
@@ -366,7 +376,7 @@ __device__ __forceinline__ uint32_t owned_slots(const Lat& L, const Tile& t, int
   for (int k = 1; k < 19; ++k) {
     bool own;
     const int sg = owner_sign<MODE>(k);
-    if (MODE == kWinAaOdd && ((bR >> opp(k)) & 1u))
+    if ((MODE == kWinAaOdd || MODE == kWinPushS) && ((bR >> opp(k)) & 1u))
       own = selfin;  // AA odd: a bounced link's slot is written by R itself
     else
       own = in_block(t, rx + sg * cx(k), r + sg * cy(k), z + sg * cz(k));
@@ -665,10 +675,10 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   extern __shared__ __align__(16) unsigned char win_smem[];
   T* sm = reinterpret_cast<T*>(win_smem);
   __shared__ int ph[kNB][kWR];
-  __shared__ uint32_t msk[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
-  __shared__ int mcol[in_place(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
-  __shared__ uint32_t gmask[in_place(MODE) ? kWR * kWC : 1];
-  __shared__ uint16_t wlist[in_place(MODE) ? kListMax : 1];
+  __shared__ uint32_t msk[owned_wb(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
+  __shared__ int mcol[owned_wb(MODE) ? WinThreads<T, MODE>::warps * kWC : 1];
+  __shared__ uint32_t gmask[owned_wb(MODE) ? kWR * kWC : 1];
+  __shared__ uint16_t wlist[owned_wb(MODE) ? kListMax : 1];
   __shared__ int wcnt[kWR + 1];
   __shared__ long long rbp[kWR];  // write-back plane: row storage bases (elements)
   __shared__ int sbp[kWR];        // ... and ring offsets
@@ -687,13 +697,13 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const bool valid = tx < t.txv && ty < t.tyv;
   const T* gin = src.p;
-  if constexpr (in_place(MODE)) {  // ownership masks of no-bounce records inside the chunk
+  if constexpr (owned_wb(MODE)) {  // ownership masks of no-bounce records inside the chunk
     for (int q = threadIdx.x; q < kWR * kWC; q += blockDim.x)
       gmask[q] = owned_slots_xy<MODE>(t, q % kWC, q / kWC);
   }
   WbList wl{wlist, 0, {0, 0, 0}};
   bool fast = false;
-  if constexpr (in_place(MODE)) {
+  if constexpr (owned_wb(MODE)) {
     fast = wb_fast_ok(L, t);
     if (fast) {
       __syncthreads();  // gmask
@@ -741,6 +751,11 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   load(t.zb - 1);
   load(t.zb);
   cp_commit();
+  T pc[19];             // kWinPushS: post-collision values of this thread's node, plane z
+  bool pc_live = false;
+  T pd[5];              // ... and the deferred cz = +1 values of plane z - 1
+  bool pd_live = false;
+  uint32_t pd_mask = 0;
   for (int z = t.zb; z < t.ze; ++z) {
     if (z == t.zb) load(z + 1);
     if constexpr (kBulk) {
@@ -776,7 +791,81 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     }
     T f[19];
     bool live = false;
-    if (ty < kTY) {  // warps beyond the tile rows only move data
+    if constexpr (MODE == kWinPushS) {
+      // Scatter form of OS push: this thread's node X at plane z writes
+      // post(X)[i] into slot i of X + c_i (bounce: slot opp i of X) in the
+      // ring; plane z - 1 is then complete and leaves through the ownership
+      // write-back (the owner of slot (k, R) is R - c_k, as for AA odd), so
+      // no halo node is collided. The cz = +1 values land one iteration
+      // later (pd), after every tile record of plane z + 1 has been read
+      // (this iteration, before the barrier); cz <= 0 targets were read in
+      // earlier iterations.
+      const int x = t.x0 + tx, y = t.y0 + ty;
+      auto own = [&](int zp) -> const T* {
+        const int sl = slot(zp);
+        return sm + sl * BUF + (ty + 1) * ROW + ph[sl][ty + 1] + (tx + 1) * 19;
+      };
+      auto nbr = [&](int zp) {  // element offsets of the 3 x 3 (z, y) neighbourhood
+        int rp[3][3];
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            const int sl = slot(zp - 1 + dz), r = ty + dy;
+            rp[dz][dy] = sl * BUF + r * ROW + ph[sl][r] + (tx + 1) * 19;
+          }
+        return [=](int i, int k) -> T& { return sm[rp[1 + cz(i)][1 + cy(i)] + cx(i) * 19 + k]; };
+      };
+      uint32_t bz = 0;
+      if (z == t.zb) {  // plane zb's post values
+        pc_live = valid && cell_links(L, x, y, z, bz);
+        if (pc_live) {
+          const T* rec = own(z);
+#pragma unroll
+          for (int i = 0; i < 19; ++i) pc[i] = rec[i];
+          collide(op, pc);
+        }
+      }
+      T fr[19];  // plane z + 1, pristine: nothing has landed in it yet
+      bool rlive = false;
+      if (z + 1 < t.ze && valid) rlive = cell_links(L, x, y, z + 1, bz);
+      if (rlive) {
+        const T* rec = own(z + 1);
+#pragma unroll
+        for (int i = 0; i < 19; ++i) fr[i] = rec[i];
+      }
+      if (pd_live) {  // plane z - 1's deferred cz = +1 values into plane z
+        auto at = nbr(z - 1);
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          if ((pd_mask >> kUp[q]) & 1u) at(kUp[q], kUp[q]) = pd[q];
+      }
+      if (pc_live) {
+        auto at = nbr(z);
+        uint32_t bounce = 0;
+        cell_links(L, x, y, z, bounce);
+        at(0, 0) = pc[0];
+#pragma unroll
+        for (int i = 1; i < 19; ++i) {
+          if ((bounce >> i) & 1u)
+            at(0, opp(i)) = pc[i];
+          else if (cz(i) <= 0)
+            at(i, i) = pc[i];
+        }
+        // a bounced cz = +1 link was written above; the deferred store of its
+        // slot is skipped
+#pragma unroll
+        for (int q = 0; q < 5; ++q) pd[q] = pc[kUp[q]];
+        pd_mask = ~bounce;
+      }
+      pd_live = pc_live;
+      if (rlive) {
+        collide(op, fr);
+#pragma unroll
+        for (int i = 0; i < 19; ++i) pc[i] = fr[i];
+      }
+      pc_live = rlive;
+    } else if (ty < kTY) {  // warps beyond the tile rows only move data
       // element offsets of the 3 x 3 (z, y) neighbourhood at this thread's column
       int rp[3][3];
 #pragma unroll
@@ -810,7 +899,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
           win_node<MODE, true>(op, bounce, f, at, wrapped);
       }
     }
-    if constexpr (in_place(MODE)) {
+    if constexpr (owned_wb(MODE)) {
       if (fast_plane(z - 1) && (int)threadIdx.x < t.tyv + 2) {
         const int r = threadIdx.x;
         uint32_t rb = 0;
@@ -821,7 +910,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       if constexpr (kBulk) fence_async_smem();  // ring writes before the runs' bulk stores
     }
     __syncthreads();  // every read of plane z - 1 is done
-    if constexpr (in_place(MODE)) {
+    if constexpr (owned_wb(MODE)) {
       if (fast_plane(z - 1))
         writeback_fast(dst.p, sm, wl, rbp, sbp, t);
       else
@@ -848,7 +937,20 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     }
   }
   if constexpr (kBulk) bulk_wait_all();
-  if constexpr (in_place(MODE)) {
+  if constexpr (MODE == kWinPushS) {  // plane ze - 1's deferred values into the halo plane
+    __syncthreads();
+    if (pd_live) {
+      const int zp = t.ze - 1;
+      auto at = [&](int i, int k) -> T& {
+        const int sl = slot(zp + cz(i)), r = ty + 1 + cy(i);
+        return sm[sl * BUF + r * ROW + ph[sl][r] + (tx + 1 + cx(i)) * 19 + k];
+      };
+#pragma unroll
+      for (int q = 0; q < 5; ++q)
+        if ((pd_mask >> kUp[q]) & 1u) at(kUp[q], kUp[q]) = pd[q];
+    }
+  }
+  if constexpr (owned_wb(MODE)) {
     __syncthreads();
     writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, mcol, gmask,
                           t, t.ze - 1, face_zm(t.ze - 1));
@@ -1036,12 +1138,16 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   if (L.sx != L.nx + 2 * L.ox || L.sy != L.ny + 2 * L.oy || L.zghost || L.znowrap) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
     return false;
-  const bool inplace = in_place(mode);
-  if (inplace && ((!L.wall[0] && L.nx < kTX + 2) || (!L.wall[1] && L.ny < kTY + 2) ||
-                  (!L.wall[2] && L.nz < 3)))
-    return false;
+  // every window position a distinct record (the ownership write-back)
+  const bool distinct = (L.wall[0] || L.nx >= kTX + 2) && (L.wall[1] || L.ny >= kTY + 2) &&
+                        (L.wall[2] || L.nz >= 3);
+  if (in_place(mode) && !distinct) return false;
   const bool f64 = a.prec == Prec::f64;
-  const int zc = window_chunk(L, f64, inplace);
+  // OS push: the scatter form (no redundant halo collisions, ownership
+  // write-back) for fp64; fp32 keeps the gather form (C1 fp64 0.44 -> 0.49,
+  // fp32 0.43 -> 0.38; profiles/r01_variants.md)
+  if (mode == kWinPush && distinct && f64) mode = kWinPushS;
+  const int zc = window_chunk(L, f64, owned_wb(mode));
 #define LBM_WIN_CASES(T)                                                              \
   switch (mode) {                                                                     \
     case kWinPull: launch_win<T, kWinPull>(st, a, b, L, op, zc, 0, L.nz); break;     \
@@ -1050,6 +1156,7 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     case kWinAaOdd: launch_win<T, kWinAaOdd>(st, a, b, L, op, zc, 0, L.nz); break;   \
     case kWinSwap: launch_win<T, kWinSwap>(st, a, b, L, op, zc, 0, L.nz); break;     \
     case kWinEtI: launch_win<T, kWinEtI>(st, a, b, L, op, zc, 0, L.nz); break;       \
+    case kWinPushS: launch_win<T, kWinPushS>(st, a, b, L, op, zc, 0, L.nz); break;   \
     default: launch_win<T, kWinEtS>(st, a, b, L, op, zc, 0, L.nz); break;            \
   }
   if (f64) {
