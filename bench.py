@@ -350,10 +350,20 @@ def run_slabs(args, ws, rank, local, dist, L):
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
     st = L.create_stepper(args.scheme, args.addressing, geo, flow,
                           L.StepperOptions(device=local, z_begin=z0, z_end=z1))
-    uid = [L.nccl_unique_id() if rank == 0 else None]
-    if dist is not None:
-        dist.broadcast_object_list(uid, src=0)
-    st.slab_connect_nccl(uid[0], ws, rank)
+    if args.transport == "p2p":
+        # peer-memory AA: face planes read/rewrite the neighbours' slots in
+        # place (CUDA IPC pointers), steps ordered by flag words; no NCCL
+        blobs = [st.slab_p2p_export()]
+        if dist is not None:
+            blobs = [None] * ws
+            dist.all_gather_object(blobs, st.slab_p2p_export())
+        st.slab_p2p_connect(blobs[(rank - 1) % ws], blobs[(rank + 1) % ws], ws, rank)
+        barrier(dist)
+    else:
+        uid = [L.nccl_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
+        st.slab_connect_nccl(uid[0], ws, rank)
     st.init_field(cfg["init"], seed=2011)
     nodes_local = st.node_count()
     nodes = int(reduce_sum(dist, nodes_local))
@@ -376,7 +386,9 @@ def run_slabs(args, ws, rank, local, dist, L):
         "data": "synthetic (BASELINE.json configs[3]; seeded device-side Taylor-Green init)",
         "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
                    "layout": "soa", "dims": [nx, ny, nz], "fluid_nodes": nodes,
-                   "parallelism": f"z-slabs x{ws} (NCCL halo, 5 slot planes/face)",
+                   "parallelism": (f"z-slabs x{ws} (NCCL halo, 5 slot planes/face)"
+                                   if args.transport == "nccl" else
+                                   f"z-slabs x{ws} (p2p: face sweeps on peer memory)"),
                    "l2": "inputs larger than L2, no flush needed"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
@@ -433,6 +445,9 @@ def main():
     ap.add_argument("--precision", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="z-slab exchange: NCCL halo phases, or p2p (AA direct: face planes "
+                         "read and rewrite the neighbours' slots through peer pointers)")
     ap.add_argument("--slabs", action="store_true",
                     help="run the z-slab/NCCL path even at N=1 (one rank, ring to itself)")
     args = ap.parse_args()

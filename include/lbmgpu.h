@@ -243,6 +243,25 @@ int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h);
 int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps);
 int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n);
 
+/* peer-memory transport for AA slabs on direct addressing ("p2p"): no ghost
+ * exchange and no collective. The face planes' odd sweep reads and rewrites
+ * the neighbour slab's face-plane slots in place through peer pointers
+ * (NVLink loads/stores inside the collision kernel); steps are ordered by
+ * stream events (one process) or by flag words the ranks write into each
+ * other's memory (one rank per process). The reference has no multi-node
+ * path; this replaces the ghost exchange of lbmgpu_slab_connect_nccl. */
+#define LBMGPU_P2P_BLOB_BYTES 256
+/* several slabs of one process (ring in the given order, any devices with
+ * peer access); then lbmgpu_slab_group_step as usual */
+int lbmgpu_slab_group_connect_p2p(lbmgpu_stepper** hs, int32_t n);
+/* one rank per process: publish this slab (CUDA IPC handles + layout) ... */
+int lbmgpu_slab_p2p_export(lbmgpu_stepper* h, uint8_t* blob);
+/* ... and connect to the lower / upper neighbours' blobs (nranks 1: pass
+ * this slab's own blob twice). Collective: every rank connects before any
+ * rank steps; lbmgpu_slab_sync_ghosts works as with NCCL. */
+int lbmgpu_slab_p2p_connect(lbmgpu_stepper* h, const uint8_t* lower, const uint8_t* upper,
+                            int32_t nranks, int32_t rank);
+
 /* page-locked host memory (cudaHostAlloc) for the canonical snapshot, so
  * extract/load run at full host-link bandwidth */
 int lbmgpu_host_alloc(uint64_t bytes, void** p);

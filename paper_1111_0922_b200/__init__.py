@@ -38,6 +38,7 @@ FAMILY_OF = {"ts": "ts", "os-push": "os", "os-pull": "os", "osnt-pull-1s": "osnt
 ADDRESSINGS = ("direct", "indirect")
 LAYOUT_PHASES = ("natural", "opposed", "shifted_even", "shifted_odd", "twisted", "swap_partial")
 Q = 19
+P2P_BLOB_BYTES = 256  # LBMGPU_P2P_BLOB_BYTES
 
 
 class _Geometry(C.Structure):
@@ -111,6 +112,9 @@ _sig = {
     "lbmgpu_slab_sync_ghosts": (C.c_int, [_P]),
     "lbmgpu_slab_group_step": (C.c_int, [_P, C.c_int32, C.c_int64]),
     "lbmgpu_slab_group_sync_ghosts": (C.c_int, [_P, C.c_int32]),
+    "lbmgpu_slab_group_connect_p2p": (C.c_int, [_P, C.c_int32]),
+    "lbmgpu_slab_p2p_export": (C.c_int, [_P, _P]),
+    "lbmgpu_slab_p2p_connect": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32]),
     "lbmgpu_host_free": (C.c_int, [_P]),
     "lbmgpu_run_bench": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
@@ -357,6 +361,20 @@ class Stepper:
     def slab_sync_ghosts(self) -> None:
         _check(_L.lbmgpu_slab_sync_ghosts(self._h))
 
+    def slab_p2p_export(self) -> bytes:
+        """This slab's peer-memory blob (CUDA IPC handles of its field and flag
+        words, its layout) for the neighbours' slab_p2p_connect."""
+        buf = (C.c_uint8 * P2P_BLOB_BYTES)()
+        _check(_L.lbmgpu_slab_p2p_export(self._h, buf))
+        return bytes(buf)
+
+    def slab_p2p_connect(self, lower: bytes, upper: bytes, nranks: int, rank: int) -> None:
+        """One rank per process: AA odd face planes read and rewrite the
+        neighbours' face slots in place through peer pointers (collective)."""
+        lo = (C.c_uint8 * P2P_BLOB_BYTES).from_buffer_copy(lower[:P2P_BLOB_BYTES])
+        hi = (C.c_uint8 * P2P_BLOB_BYTES).from_buffer_copy(upper[:P2P_BLOB_BYTES])
+        _check(_L.lbmgpu_slab_p2p_connect(self._h, lo, hi, nranks, rank))
+
     def cuda_stream(self) -> int:
         v = C.c_void_p()
         _check(_L.lbmgpu_stream(self._h, C.byref(v)))
@@ -576,6 +594,13 @@ def slab_group_step(steppers, steps: int) -> None:
     """Step in-process z-slabs in lockstep (exchanges as device copies)."""
     arr = (C.c_void_p * len(steppers))(*[s._h for s in steppers])
     _check(_L.lbmgpu_slab_group_step(arr, len(steppers), int(steps)))
+
+
+def slab_group_connect_p2p(steppers) -> None:
+    """In-process z-slabs (ring in list order): switch them to the peer-memory
+    transport (AA direct); slab_group_step then orders steps by events only."""
+    arr = (_P * len(steppers))(*[s._h for s in steppers])
+    _check(_L.lbmgpu_slab_group_connect_p2p(arr, len(steppers)))
 
 
 def slab_group_sync_ghosts(steppers) -> None:

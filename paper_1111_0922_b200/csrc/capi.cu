@@ -332,6 +332,31 @@ int lbmgpu_slab_group_step(lbmgpu_stepper** hs, int32_t n, int64_t steps) {
   });
 }
 
+int lbmgpu_slab_group_connect_p2p(lbmgpu_stepper** hs, int32_t n) {
+  return guard([&] {
+    if (n < 1 || !hs) throw std::invalid_argument("empty slab group");
+    std::vector<Stepper*> v;
+    for (int k = 0; k < n; ++k) v.push_back(&S(hs[k]));
+    slab_group_connect_p2p(v);
+  });
+}
+
+int lbmgpu_slab_p2p_export(lbmgpu_stepper* h, uint8_t* blob) {
+  return guard([&] {
+    if (!blob) throw std::invalid_argument("null blob");
+    slab_p2p_export(S(h), blob);
+  });
+}
+
+int lbmgpu_slab_p2p_connect(lbmgpu_stepper* h, const uint8_t* lower, const uint8_t* upper,
+                            int32_t nranks, int32_t rank) {
+  return guard([&] {
+    if (!lower || !upper) throw std::invalid_argument("null blob");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank");
+    slab_p2p_connect(S(h), lower, upper, nranks, rank);
+  });
+}
+
 int lbmgpu_slab_group_sync_ghosts(lbmgpu_stepper** hs, int32_t n) {
   return guard([&] {
     if (n < 1 || !hs) throw std::invalid_argument("empty slab group");

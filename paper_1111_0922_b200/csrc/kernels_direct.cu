@@ -161,6 +161,51 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, A
     aa_odd_body<true>(F, c, op);
 }
 
+// AA odd sweep of one slab face plane over peer memory (the p2p slab
+// transport, slabs.cu): the slots a face cell reads and rewrites across the
+// face, (j, X + c_j) with c_z(j) = dz, live in the neighbour slab's face plane
+// and are addressed there directly (R.p[j] = that slot plane's base, indexed
+// like the local ghost plane); every other access is local. The AA partition
+// (each slot read and rewritten by one node per sweep) makes the neighbour's
+// own odd sweep touch disjoint slots, so no ghost copy and no exchange phase.
+template <class T>
+struct FaceRemote {
+  T* p[19];
+  int dz;               // -1: bottom face (ghost plane below), +1: top face
+  uint32_t ghost_base;  // local storage index of the ghost plane's first cell
+};
+template <bool BB, class T>
+__device__ __forceinline__ void aa_odd_face_body(const Fld<T, false>& F, const Ctx& c,
+                                                 const Trt<T>& op, const FaceRemote<T>& R) {
+  auto slot = [&](int j) -> T* {  // (j, X + c_j), remote when it crosses the face
+    if (cz(j) == R.dz) return R.p[j] + (c.nb(j) - R.ghost_base);
+    return F.at_off(j, c.s, c.off(j));
+  };
+  T f[19];
+  f[0] = ld(F.at(0, c.s));
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    f[i] = ld((BB && c.bb(j)) ? F.at(i, c.s) : slot(j));
+  }
+  collide(op, f);
+  st<false>(F.at(0, c.s), f[0]);
+#pragma unroll
+  for (int j = 1; j < 19; ++j) st<false>((BB && c.bb(j)) ? F.at(opp(j), c.s) : slot(j), f[j]);
+}
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_aa_odd_face(Fld<T, false> F, Lat L, Trt<T> op, FaceRemote<T> R) {
+  const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
+  if (cell >= L.ncells) return;
+  const Ctx c = make_ctx(L, cell);
+  if (!c.fluid) return;
+  if (warp_interior(c))
+    aa_odd_face_body<false>(F, c, op, R);
+  else
+    aa_odd_face_body<true>(F, c, op, R);
+}
+
 // Esoteric twist sweep (p/src/scheme_et.cpp:191-239). For pair (i, j):
 // tmp_i = F[b_i][X], tmp_j = F[b_(db?i:j)][X + c_i]; collide;
 // F[b_(ub?j:i)][X] = tmp_j, F[b_j][X + c_i] = tmp_i. Wall axes carry a halo
@@ -538,6 +583,27 @@ void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const Tr
   LBM_DISPATCH(f, {
     k_aa_odd<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
   });
+}
+
+void launch_aa_odd_face(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                        void* const remote[19], int dz, uint32_t ghost_base) {
+  if (L.ncells <= L.cell_begin) return;
+  if (f.aos) throw std::invalid_argument("p2p face sweep: SoA fields only");
+  if (f.prec == Prec::f64) {
+    FaceRemote<double> R;
+    for (int k = 0; k < 19; ++k) R.p[k] = static_cast<double*>(remote[k]);
+    R.dz = dz;
+    R.ghost_base = ghost_base;
+    k_aa_odd_face<double><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+        fld<double, false>(f), L, cast_op<double>(op), R);
+  } else {
+    FaceRemote<float> R;
+    for (int k = 0; k < 19; ++k) R.p[k] = static_cast<float*>(remote[k]);
+    R.dz = dz;
+    R.ghost_base = ghost_base;
+    k_aa_odd_face<float><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+        fld<float, false>(f), L, cast_op<float>(op), R);
+  }
 }
 
 void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,

@@ -75,6 +75,11 @@ void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev
                     const TrtHost& op);
 // AA-pattern odd sweep (the even sweep is launch_local(rd natural, wr opposed))
 void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op);
+// one slab face plane of the AA odd sweep; the slots crossing the face
+// (c_z = dz) are addressed in peer memory: remote[k] = base of the neighbour's
+// face-plane slot k, indexed like the local ghost plane at ghost_base
+void launch_aa_odd_face(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                        void* const remote[19], int dz, uint32_t ghost_base);
 // Esoteric twist sweep with the current handle table
 void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                const EtBase& base);

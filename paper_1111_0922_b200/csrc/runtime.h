@@ -408,5 +408,10 @@ void slab_connect_nccl(Stepper& s, const uint8_t* id, int nranks, int rank);
 void slab_sync_ghosts(Stepper& s);
 void slab_group_step(const std::vector<Stepper*>& slabs, long long steps);
 void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs);
+// p2p transport (AA direct): in one process over a ring of slabs, or one rank
+// per process through exported blobs (CUDA IPC handles of field and flags)
+void slab_group_connect_p2p(const std::vector<Stepper*>& slabs);
+void slab_p2p_export(Stepper& s, uint8_t* blob);
+void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank);
 
 }  // namespace lbmgpu

@@ -4,6 +4,9 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
+
+#include <cstring>
 
 namespace lbmgpu {
 
@@ -153,6 +156,47 @@ struct Nccl {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Peer-memory transport for AA slabs ("p2p"): no ghost exchange. The face
+// planes' odd sweep (launch_aa_odd_face) reads and rewrites the neighbour's
+// face-plane slots in place over NVLink (the AA partition makes the slots of
+// a sweep disjoint between the two sides), so a step only needs ordering:
+// a face-plane sweep of step t starts after both neighbours finished step
+// t - 1. In one process (kP2PGroup) that is a stream wait on the neighbours'
+// step events; across processes (kP2PIpc: field and flag buffers shared with
+// CUDA IPC handles) a one-thread kernel on the side stream publishes "step
+// t - 1 done" into the neighbours' flag words (st.release.sys) and spins on
+// its own (ld.acquire.sys) while the interior planes run on the main stream.
+// ---------------------------------------------------------------------------
+__global__ void k_slab_flag_barrier(unsigned long long* mine, unsigned long long* to_lo,
+                                    unsigned long long* to_hi, unsigned long long epoch) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(to_lo), "l"(epoch) : "memory");
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(to_hi), "l"(epoch) : "memory");
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int k = 0; k < 2; ++k) {
+    unsigned long long v = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine + k) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 60ull * 1000000000ull) __trap();  // a neighbour stopped stepping
+    }
+  }
+}
+
+// what a rank publishes so its neighbours can address its field and flags
+struct P2PBlob {
+  char magic[8];
+  cudaIpcMemHandle_t field, flags;
+  int64_t stride;  // SoA slot stride (elements)
+  int64_t plane;   // cells per plane
+  int32_t nzl, esize, device, pid;
+};
+static_assert(sizeof(P2PBlob) <= LBMGPU_P2P_BLOB_BYTES, "p2p blob size");
+
 class SlabStepper final : public Stepper {
  public:
   SlabStepper(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
@@ -248,6 +292,9 @@ class SlabStepper final : public Stepper {
     for (auto e : {ev_c_, ev_halo_, ev_odd_, ev_back_})
       if (e) cudaEventDestroy(e);
     if (nccl_) Nccl::get().commDestroy(nccl_);
+    for (auto e : ev_step_)
+      if (e) cudaEventDestroy(e);
+    close_ipc();
   }
 
   static HostGeo slab_geo(const HostGeo& g, const lbmgpu_options& o) {
@@ -296,6 +343,174 @@ class SlabStepper final : public Stepper {
     s.gnz = gnz_;
     s.z0 = z0_;
     return s;
+  }
+
+  // ---- p2p transport (AA, direct) ----------------------------------------
+  void p2p_check() const {
+    if (kind_ != kSlabAA || idx_)
+      throw std::invalid_argument("p2p slab transport: AA on direct addressing only");
+    if (nzl_ < 2) throw std::invalid_argument("p2p slab transport: at least 2 planes per slab");
+  }
+  void ensure_step_events() {
+    for (auto& e : ev_step_)
+      if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto e : ev_step_) CK(cudaEventRecord(e, stream_));
+  }
+  // in-process ring: lower / upper are the neighbouring slabs (may be this one)
+  void connect_p2p_group(SlabStepper& lo, SlabStepper& hi) {
+    p2p_check();
+    if (lo.plane_ != plane_ || hi.plane_ != plane_ || lo.prec_ != prec_ || hi.prec_ != prec_)
+      throw std::invalid_argument("p2p slab transport: slabs of different boxes or precisions");
+    CK(cudaSetDevice(opt_.device));
+    for (SlabStepper* n : {&lo, &hi}) {
+      if (n->opt_.device == opt_.device) continue;
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, opt_.device, n->opt_.device));
+      if (!ok) throw std::runtime_error("p2p slab transport: devices without peer access");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(n->opt_.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else
+        CK(e);
+    }
+    for (int k = 0; k < 19; ++k) {
+      rem_lo_[k] = lo.slot_ptr(0, k, lo.nzl_ - 1);
+      rem_hi_[k] = hi.slot_ptr(0, k, 0);
+    }
+    ensure_step_events();
+    nb_ev_lo_ = lo.ev_step_;
+    nb_ev_hi_ = hi.ev_step_;
+    transport_ = kP2PGroup;
+  }
+  void p2p_export(P2PBlob& b) {
+    p2p_check();
+    CK(cudaSetDevice(opt_.device));
+    if (!flags_.get()) {
+      flags_.alloc(2 * sizeof(unsigned long long));
+      CK(cudaMemset(flags_.get(), 0, 2 * sizeof(unsigned long long)));
+    }
+    std::memset(&b, 0, sizeof(b));
+    std::memcpy(b.magic, "LBMP2P1", 8);
+    CK(cudaIpcGetMemHandle(&b.field, g_[0].get()));
+    CK(cudaIpcGetMemHandle(&b.flags, flags_.get()));
+    b.stride = soa_stride(storage_);
+    b.plane = (int64_t)plane_;
+    b.nzl = nzl_;
+    b.esize = (int32_t)esize();
+    b.device = opt_.device;
+    b.pid = (int32_t)getpid();
+  }
+  void close_ipc() {
+    for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
+    ipc_open_.clear();
+  }
+  // one rank per process: lo / hi = the neighbours' blobs (nranks 1: this
+  // slab's own, opened without IPC). Collective; zeroes the flag words, so
+  // every rank connects before any rank steps.
+  void connect_p2p_ipc(const P2PBlob& lo, const P2PBlob& hi, int nranks, int rank) {
+    p2p_check();
+    for (const P2PBlob* b : {&lo, &hi}) {
+      if (std::memcmp(b->magic, "LBMP2P1", 8) != 0)
+        throw std::invalid_argument("p2p slab transport: not a p2p blob");
+      if (b->plane != (int64_t)plane_ || b->esize != (int32_t)esize())
+        throw std::invalid_argument("p2p slab transport: slabs of different boxes or precisions");
+    }
+    CK(cudaSetDevice(opt_.device));
+    if (!flags_.get()) {
+      P2PBlob mine;
+      p2p_export(mine);
+    }
+    close_ipc();
+    auto open = [&](const P2PBlob& b, char*& field, unsigned long long*& flags) {
+      if (nranks == 1) {
+        field = static_cast<char*>(g_[0].get());
+        flags = flags_.get<unsigned long long>();
+        return;
+      }
+      void* f = nullptr;
+      void* g = nullptr;
+      CK(cudaIpcOpenMemHandle(&f, b.field, cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&g, b.flags, cudaIpcMemLazyEnablePeerAccess));
+      ipc_open_.push_back(f);
+      ipc_open_.push_back(g);
+      field = static_cast<char*>(f);
+      flags = static_cast<unsigned long long*>(g);
+    };
+    char *flo = nullptr, *fhi = nullptr;
+    unsigned long long *glo = nullptr, *ghi = nullptr;
+    open(lo, flo, glo);
+    if (nranks == 2) {  // the same rank is both neighbours
+      fhi = flo;
+      ghi = glo;
+    } else {
+      open(hi, fhi, ghi);
+    }
+    const size_t es = esize();
+    for (int k = 0; k < 19; ++k) {
+      rem_lo_[k] = flo + ((size_t)k * lo.stride + (size_t)lo.nzl * lo.plane) * es;  // its plane nzl-1
+      rem_hi_[k] = fhi + ((size_t)k * hi.stride + (size_t)hi.plane) * es;            // its plane 0
+    }
+    flag_to_lo_ = glo + 1;  // I am my lower neighbour's upper neighbour
+    flag_to_hi_ = ghi + 0;
+    CK(cudaMemset(flags_.get(), 0, 2 * sizeof(unsigned long long)));
+    CK(cudaDeviceSynchronize());
+    epoch_ = 0;
+    nranks_ = nranks, rank_ = rank;
+    transport_ = kP2PIpc;
+  }
+  void flag_barrier(cudaStream_t st) {
+    ++epoch_;
+    k_slab_flag_barrier<<<1, 32, 0, st>>>(flags_.get<unsigned long long>(), flag_to_lo_, flag_to_hi_,
+                                         epoch_);
+  }
+  // the two face planes of the current AA step (odd: over peer memory)
+  void face_sweeps(cudaStream_t st) {
+    const DField f = field(g_[0], soa_stride(storage_));
+    if ((t_ & 1) == 0) {
+      launch_local(st, f, f, planes(0, 1), op_, false, true);
+      launch_local(st, f, f, planes(nzl_ - 1, nzl_), op_, false, true);
+    } else {
+      launch_aa_odd_face(st, f, planes(0, 1), op_, rem_lo_, -1, 0u);
+      launch_aa_odd_face(st, f, planes(nzl_ - 1, nzl_), op_, rem_hi_, +1,
+                         (uint32_t)((nzl_ + 1) * plane_));
+    }
+  }
+  void step_p2p() {
+    sweep(1, nzl_ - 1);  // interior planes: nothing crosses a face
+    if (transport_ == kP2PGroup) {
+      const int prev = (int)((t_ + 1) & 1);  // parity of step t - 1
+      CK(cudaStreamWaitEvent(stream_, nb_ev_lo_[prev], 0));
+      CK(cudaStreamWaitEvent(stream_, nb_ev_hi_[prev], 0));
+      face_sweeps(stream_);
+      CK(cudaEventRecord(ev_step_[t_ & 1], stream_));
+      return;
+    }
+    // kP2PIpc: side stream after my step t - 1: barrier, then the face planes
+    CK(cudaStreamWaitEvent(comm_, ev_back_, 0));
+    flag_barrier(comm_);
+    face_sweeps(comm_);
+    CK(cudaEventRecord(ev_halo_, comm_));
+    CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+    CK(cudaEventRecord(ev_back_, stream_));
+  }
+  // extraction at odd t reads the ghost planes: copy the neighbours' face
+  // slots the odd gather reads (the AA phase-0 receives) over peer memory
+  void sync_ghosts_p2p() {
+    CK(cudaSetDevice(opt_.device));
+    CK(cudaEventRecord(ev_c_, stream_));
+    CK(cudaStreamWaitEvent(comm_, ev_c_, 0));
+    flag_barrier(comm_);
+    const size_t bytes = plane_ * esize();
+    for (int k = 1; k < 19; ++k) {
+      if (dev::cz(k) < 0)
+        CK(cudaMemcpyAsync(slot_ptr(0, k, -1), rem_lo_[k], bytes, cudaMemcpyDefault, comm_));
+      if (dev::cz(k) > 0)
+        CK(cudaMemcpyAsync(slot_ptr(0, k, nzl_), rem_hi_[k], bytes, cudaMemcpyDefault, comm_));
+    }
+    CK(cudaEventRecord(ev_halo_, comm_));
+    CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+    CK(cudaEventRecord(ev_back_, stream_));
+    ghosts_fresh_ = true;
   }
 
   // ---- transports ----------------------------------------------------------
@@ -515,6 +730,11 @@ class SlabStepper final : public Stepper {
   }
 
   void step_one() override {
+    if (transport_ == kP2PGroup || transport_ == kP2PIpc) {
+      step_p2p();
+      ghosts_fresh_ = false;
+      return;
+    }
     if (transport_ == kNccl) {
       if (kind_ == kSlabEt) {
         if (owners_stale_) {  // values a load parked in the ghosts -> owners
@@ -592,12 +812,14 @@ class SlabStepper final : public Stepper {
   int launches_per_step() const override {
     if (kind_ == kSlabCg) return (nzl_ + cg_p_ - 1) / cg_p_;
     const int collide = (kind_ == kSlabTs || kind_ == kSlabSwap) ? 1 : 0;
+    if (transport_ == kP2PGroup) return 3;
+    if (transport_ == kP2PIpc) return 4;  // interior, barrier, two face planes
     if (transport_ != kNccl) return 1 + collide;
     return (nzl_ > 2 ? 3 : nzl_) + collide;
   }
 
   void finish() override {
-    if (transport_ == kNccl) CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
+    if (transport_ == kNccl || transport_ == kP2PIpc) CK(cudaStreamWaitEvent(stream_, ev_back_, 0));
   }
 
   // ghost planes the extraction gathers from: AA at odd t, OS pull once it
@@ -612,6 +834,7 @@ class SlabStepper final : public Stepper {
   int ghost_grid() const { return kind_ == kSlabOsPull ? active_ ^ 1 : 0; }
 
   void sync_ghosts_nccl() {
+    if (transport_ == kP2PIpc) return sync_ghosts_p2p();
     if (transport_ != kNccl) throw std::runtime_error("slab stepper is not connected to NCCL");
     enqueue_phase(0, ghost_grid(), ev_halo_, sync_kind());
     CK(cudaStreamWaitEvent(stream_, ev_halo_, 0));
@@ -709,7 +932,7 @@ class SlabStepper final : public Stepper {
   }
   uint64_t pdf_bytes() const override { return g_[0].bytes() + g_[1].bytes(); }
 
-  enum { kNone = 0, kLocalGroup = 1, kNccl = 2 };
+  enum { kNone = 0, kLocalGroup = 1, kNccl = 2, kP2PGroup = 3, kP2PIpc = 4 };
   int kind_ = kSlabAA;
   int transport_ = kNone;
   int nzl_ = 0, gnz_ = 0, z0_ = 0, z1_ = 0;
@@ -733,6 +956,19 @@ class SlabStepper final : public Stepper {
   cudaEvent_t ev_c_ = nullptr, ev_halo_ = nullptr, ev_odd_ = nullptr, ev_back_ = nullptr;
   ncclComm_t nccl_ = nullptr;
   int nranks_ = 1, rank_ = 0;
+  // p2p transport: base of the neighbours' face-plane slot k (lower: its top
+  // owned plane, upper: its bottom one), step-done events (kP2PGroup: the
+  // neighbours' ev_step_), flag words (kP2PIpc)
+  void* rem_lo_[19] = {};
+  void* rem_hi_[19] = {};
+  cudaEvent_t ev_step_[2] = {nullptr, nullptr};
+  const cudaEvent_t* nb_ev_lo_ = nullptr;
+  const cudaEvent_t* nb_ev_hi_ = nullptr;
+  DevMem flags_;
+  unsigned long long* flag_to_lo_ = nullptr;
+  unsigned long long* flag_to_hi_ = nullptr;
+  unsigned long long epoch_ = 0;
+  std::vector<void*> ipc_open_;
 };
 
 // In-process transport: executes one plan phase for a ring of slabs (rank k
@@ -792,8 +1028,21 @@ static void local_phase(std::vector<SlabStepper*>& S, int phase, bool use_ghost_
 }
 
 static void group_step(std::vector<SlabStepper*>& S, long long steps) {
+  if (S[0]->transport_ == SlabStepper::kP2PGroup) {  // ordering by the step events only
+    for (auto* s : S)
+      if (s->transport_ != SlabStepper::kP2PGroup)
+        throw std::invalid_argument("slab group mixes transports");
+    for (long long k = 0; k < steps; ++k) {
+      for (auto* s : S)
+        if (s->t_ != S[0]->t_) throw std::invalid_argument("slabs out of step");
+      for (auto* s : S) s->step(1);
+    }
+    for (auto* s : S) s->sync();
+    return;
+  }
   for (auto* s : S) {
-    if (s->transport_ == SlabStepper::kNccl) throw std::invalid_argument("slab is NCCL-connected");
+    if (s->transport_ == SlabStepper::kNccl || s->transport_ == SlabStepper::kP2PIpc)
+      throw std::invalid_argument("slab is connected to other processes");
     if (s->kind_ != S[0]->kind_) throw std::invalid_argument("slabs of different schemes");
     s->set_local(SlabStepper::kLocalGroup);
   }
@@ -916,6 +1165,28 @@ void slab_group_step(const std::vector<Stepper*>& slabs, long long steps) {
   std::vector<SlabStepper*> S;
   for (Stepper* s : slabs) S.push_back(&as_slab(*s));
   group_step(S, steps);
+}
+
+void slab_group_connect_p2p(const std::vector<Stepper*>& slabs) {
+  std::vector<SlabStepper*> S;
+  for (Stepper* s : slabs) S.push_back(&as_slab(*s));
+  const int n = (int)S.size();
+  for (auto* s : S) s->sync();
+  for (int k = 0; k < n; ++k) S[k]->connect_p2p_group(*S[(k - 1 + n) % n], *S[(k + 1) % n]);
+}
+
+void slab_p2p_export(Stepper& s, uint8_t* blob) {
+  P2PBlob b;
+  as_slab(s).p2p_export(b);
+  std::memset(blob, 0, LBMGPU_P2P_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof(b));
+}
+
+void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank) {
+  P2PBlob a, b;
+  std::memcpy(&a, lo, sizeof(a));
+  std::memcpy(&b, hi, sizeof(b));
+  as_slab(s).connect_p2p_ipc(a, b, nranks, rank);
 }
 
 void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs) {
