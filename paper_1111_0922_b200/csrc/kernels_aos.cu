@@ -1146,7 +1146,9 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // OS push: the scatter form (no redundant halo collisions, ownership
   // write-back) for fp64; fp32 keeps the gather form (C1 fp64 0.44 -> 0.49,
   // fp32 0.43 -> 0.38; profiles/r01_variants.md)
-  if (mode == kWinPush && distinct && f64) mode = kWinPushS;
+  // (its bulk write-back runs use the source rows' 16-byte phase)
+  const bool congruent = ((reinterpret_cast<uintptr_t>(a.p) ^ reinterpret_cast<uintptr_t>(b.p)) & 15u) == 0;
+  if (mode == kWinPush && distinct && f64 && congruent) mode = kWinPushS;
   const int zc = window_chunk(L, f64, owned_wb(mode));
 #define LBM_WIN_CASES(T)                                                              \
   switch (mode) {                                                                     \
