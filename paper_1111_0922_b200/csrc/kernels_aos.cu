@@ -1121,6 +1121,8 @@ static int window_chunk(const Lat& L, bool fp64, bool inplace) {
   const long long resident = (long long)sms * (fp64 ? 1 : 2);
   long long zc = (L.nz * tiles + resident * 7 - 1) / (resident * 7);
   zc = std::max(4LL, std::min(64LL, zc));
+  if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))  // tests: long chunks on small boxes
+    if (std::atoi(e) > 0) zc = std::atoi(e);
   if (inplace && !L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
   return (int)std::max(1LL, std::min<long long>(zc, L.nz));
 }

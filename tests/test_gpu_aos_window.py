@@ -110,3 +110,26 @@ def test_aos_window_swap_deferred_fixup(gpu, geom):
             s.synchronize()
         assert st["soa"].layout_phase() == st["aos"].layout_phase()
         assert bitwise_equal(st["soa"].extract_natural(), st["aos"].extract_natural()), steps
+
+
+@pytest.mark.parametrize("zchunk", [5, 9, 23])
+@pytest.mark.parametrize("precision", [8, 4])
+@pytest.mark.parametrize("scheme", WINDOW_SCHEMES)
+def test_aos_window_long_z_chunks(gpu, monkeypatch, scheme, precision, zchunk):
+    """z chunks longer than the plane ring (the ring slots and their barrier
+    phases wrap several times per block) on a box small enough to compare."""
+    L = gpu
+    monkeypatch.setenv("LBMGPU_AOS_ZCHUNK", str(zchunk))
+    geo = L.GridGeometry(40, 14, 48, ("periodic", "periodic", "periodic"))
+    flow = L.FlowParams(1.0 / 0.8, 3.0 / 16.0, (2e-5, -1e-5, 5e-6), 1.0)
+    st = {lay: L.create_stepper(scheme, "direct", geo, flow,
+                                L.StepperOptions(layout=lay, precision=precision))
+          for lay in ("soa", "aos")}
+    for s in st.values():
+        s.init_field("random", seed=9)
+    for steps in (1, 2):
+        for s in st.values():
+            s.step_n(steps)
+            s.synchronize()
+        assert bitwise_equal(st["soa"].extract_natural(), st["aos"].extract_natural()), \
+            (scheme, precision, zchunk, st["soa"].time_step())
