@@ -524,9 +524,10 @@ static_assert(2 * (WinSz<float>::kBytes + kInPlaceStatic + 1024) <= 228 * 1024,
               "fp32 in-place window no longer fits two blocks per SM");
 
 struct WbList {
-  uint16_t* e;      // entries
+  uint16_t* e;      // entries: row << 11 | column << 5 | slot
   int n;            // entry count
-  long long colb[3];  // element offset of column class c: storage x of column q = (colb + q*19)/19
+  long long colb0;  // element offset of window column 0 (unwrapped): storage x of column q = x0 - 1 + ox + q
+  int d1, d2;       // + element correction of column 0 / column w - 1 when their x wraps
 };
 
 // fast-path eligibility of the block (uniform)
@@ -562,11 +563,8 @@ __device__ __forceinline__ int wb_build(const Lat& L, const Tile& t, const uint3
           own = (gmask[r * kWC + q] >> k) & 1u;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, own);
-        if (pass && own) {
-          const int cls = q == 0 ? 1 : (q == w - 1 ? 2 : 0);
-          list[pos + __popc(bal & ((1u << lane) - 1u))] =
-              (uint16_t)((r << 12) | (cls << 10) | (q * 19 + k));
-        }
+        if (pass && own)
+          list[pos + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((r << 11) | (q << 5) | k);
         pos += __popc(bal);
       }
       if (!pass && lane == 0) cnt[r] = pos;
@@ -587,24 +585,38 @@ __device__ __forceinline__ int wb_build(const Lat& L, const Tile& t, const uint3
 }
 
 // one plane's write-back from its ring slot (rbp / sbp: the plane's per-row
-// storage base in elements and ring offset, published before the barrier)
+// element offset of window column 0 in storage and in the ring, published
+// before the barrier). zm = the plane's z ownership mask: all ones strictly
+// inside the chunk (the run records leave whole), else (a chunk face or halo
+// plane of a bounce-free block) only the slots in zm, runs included.
 template <class T>
 __device__ __forceinline__ void writeback_fast(T* __restrict__ g, const T* ring, const WbList& wl,
                                                const long long* rbp, const int* sbp,
-                                               const Tile& t) {
+                                               const Tile& t, uint32_t zm = ~0u) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
-  // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
-  for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
-    if constexpr (kBulk)
-      copy_out_bulk(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19,
-                    lane);
-    else
-      copy_out(g + rbp[r] + wl.colb[0] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
+  const int w = t.txv + 2;
+  if (zm == ~0u) {  // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
+    for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
+      if constexpr (kBulk)
+        copy_out_bulk(g + rbp[r] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
+      else
+        copy_out(g + rbp[r] + 2 * 19, ring + sbp[r] + 2 * 19, (t.txv - 2) * 19, lane);
+  } else {  // the run records' zm slots
+    const int nk = __popc(zm), ncol = t.txv - 2, nrun = max(0, t.tyv - 2);
+    const int n = nrun * ncol * nk;
+    for (int e = threadIdx.x; e < n; e += (int)blockDim.x) {
+      const int kk = e % nk, rc = e / nk, r = 2 + rc / ncol, q = 2 + rc % ncol;
+      const int off = q * 19 + (int)__fns(zm, 0, kk + 1);
+      g[rbp[r] + off] = ring[sbp[r] + off];
+    }
+  }
   for (int e = threadIdx.x; e < wl.n; e += (int)blockDim.x) {
     const uint32_t v = wl.e[e];
-    const int r = (int)(v >> 12), cls = (int)((v >> 10) & 3u), off = (int)(v & 1023u);
-    const long long cb = cls == 0 ? wl.colb[0] : (cls == 1 ? wl.colb[1] : wl.colb[2]);
-    g[rbp[r] + cb + off] = ring[sbp[r] + off];
+    const int r = (int)(v >> 11), q = (int)((v >> 5) & 63u), k = (int)(v & 31u);
+    if (!((zm >> k) & 1u)) continue;
+    const int off = q * 19 + k;
+    const int dq = q == 0 ? wl.d1 : (q == w - 1 ? wl.d2 : 0);
+    g[rbp[r] + (off + dq)] = ring[sbp[r] + off];
   }
 }
 
@@ -701,7 +713,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     for (int q = threadIdx.x; q < kWR * kWC; q += blockDim.x)
       gmask[q] = owned_slots_xy<MODE>(t, q % kWC, q / kWC);
   }
-  WbList wl{wlist, 0, {0, 0, 0}};
+  WbList wl{wlist, 0, 0, 0, 0};
   bool fast = false;
   if constexpr (owned_wb(MODE)) {
     fast = wb_fast_ok(L, t);
@@ -711,9 +723,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       int xs0 = 0, xs1 = 0;
       col_xs(L, t.x0, 0, xs0);
       col_xs(L, t.x0, t.txv + 1, xs1);
-      wl.colb[0] = (long long)(t.x0 - 1 + L.ox) * 19;
-      wl.colb[1] = (long long)xs0 * 19;
-      wl.colb[2] = (long long)(xs1 - (t.txv + 1)) * 19;
+      wl.colb0 = (long long)(t.x0 - 1 + L.ox) * 19;
+      wl.d1 = (xs0 - (t.x0 - 1 + L.ox)) * 19;
+      wl.d2 = (xs1 - (t.x0 + t.txv + L.ox)) * 19;
     }
   }
   // plane zp is written back by the compact pass
@@ -900,11 +912,11 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       }
     }
     if constexpr (owned_wb(MODE)) {
-      if (fast_plane(z - 1) && (int)threadIdx.x < t.tyv + 2) {
+      if ((fast_plane(z - 1) || face_zm(z - 1)) && (int)threadIdx.x < t.tyv + 2) {
         const int r = threadIdx.x;
         uint32_t rb = 0;
         row_base(L, t.y0 - 1 + r, z - 1, rb);
-        rbp[r] = (long long)rb * 19;
+        rbp[r] = (long long)rb * 19 + wl.colb0;
         sbp[r] = slot(z - 1) * BUF + r * ROW + ph[slot(z - 1)][r];
       }
       if constexpr (kBulk) fence_async_smem();  // ring writes before the runs' bulk stores
@@ -913,9 +925,11 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     if constexpr (owned_wb(MODE)) {
       if (fast_plane(z - 1))
         writeback_fast(dst.p, sm, wl, rbp, sbp, t);
+      else if (const uint32_t zm = face_zm(z - 1))
+        writeback_fast(dst.p, sm, wl, rbp, sbp, t, zm);
       else
         writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask,
-                              t, z - 1, face_zm(z - 1));
+                              t, z - 1, 0u);
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
@@ -950,12 +964,24 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         if ((pd_mask >> kUp[q]) & 1u) at(kUp[q], kUp[q]) = pd[q];
     }
   }
-  if constexpr (owned_wb(MODE)) {
-    __syncthreads();
-    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze - 1) * BUF, ph[slot(t.ze - 1)], msk, mcol, gmask,
-                          t, t.ze - 1, face_zm(t.ze - 1));
-    writeback_plane<MODE>(L, dst.p, sm + slot(t.ze) * BUF, ph[slot(t.ze)], msk, mcol, gmask, t,
-                          t.ze, face_zm(t.ze));
+  if constexpr (owned_wb(MODE)) {  // the chunk's top plane and the halo plane above
+    for (int zp = t.ze - 1; zp <= t.ze; ++zp) {
+      const uint32_t zm = face_zm(zp);
+      __syncthreads();
+      if (zm && (int)threadIdx.x < t.tyv + 2) {
+        const int r = threadIdx.x;
+        uint32_t rb = 0;
+        row_base(L, t.y0 - 1 + r, zp, rb);
+        rbp[r] = (long long)rb * 19 + wl.colb0;
+        sbp[r] = slot(zp) * BUF + r * ROW + ph[slot(zp)][r];
+      }
+      __syncthreads();
+      if (zm)
+        writeback_fast(dst.p, sm, wl, rbp, sbp, t, zm);
+      else
+        writeback_plane<MODE>(L, dst.p, sm + slot(zp) * BUF, ph[slot(zp)], msk, mcol, gmask, t, zp,
+                              0u);
+    }
   }
 }
 
