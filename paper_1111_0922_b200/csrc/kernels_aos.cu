@@ -428,13 +428,10 @@ __device__ __forceinline__ uint32_t zmask_of(const Tile& t, int z) {
   return m;
 }
 
-// zm != 0: every record of the plane is bounce-free and its owned slots are
-// gmask & zm (a fast block's chunk-face and halo planes, see zmask_of)
 template <int MODE, class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
                                                 const int* ph, uint32_t* msk, int* mcol,
-                                                const uint32_t* gmask, const Tile& t, int z,
-                                                uint32_t zm) {
+                                                const uint32_t* gmask, const Tile& t, int z) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
   const int w = t.txv + 2, rows = t.tyv + 2;
@@ -473,9 +470,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
       uint32_t m = 0;
       if (col_xs(L, t.x0, rx, xs)) {
         uint32_t bR = 0;
-        if (zm)
-          m = gmask[r * kWC + rx] & zm;
-        else if (zin && win_cell(L, t, rx, r, z, bR) && bR == 0)
+        if (zin && win_cell(L, t, rx, r, z, bR) && bR == 0)
           m = gmask[r * kWC + rx];
         else
           m = owned_slots<MODE>(L, t, rx, r, z);
@@ -929,7 +924,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         writeback_fast(dst.p, sm, wl, rbp, sbp, t, zm);
       else
         writeback_plane<MODE>(L, dst.p, sm + slot(z - 1) * BUF, ph[slot(z - 1)], msk, mcol, gmask,
-                              t, z - 1, 0u);
+                              t, z - 1);
     } else if (ty < t.tyv) {
       // stage the tile row in plane z - 1's slot with the phase of dst's row
       uint32_t rb;
@@ -979,8 +974,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       if (zm)
         writeback_fast(dst.p, sm, wl, rbp, sbp, t, zm);
       else
-        writeback_plane<MODE>(L, dst.p, sm + slot(zp) * BUF, ph[slot(zp)], msk, mcol, gmask, t, zp,
-                              0u);
+        writeback_plane<MODE>(L, dst.p, sm + slot(zp) * BUF, ph[slot(zp)], msk, mcol, gmask, t, zp);
     }
   }
 }
