@@ -729,9 +729,6 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   // domain plane (not a z-wall face, not an ET mailbox halo plane)
   auto face_zm = [&](int zp) -> uint32_t {
     int zcell;
-#ifdef LBM_NO_FACE_ZM
-    return 0u;
-#endif
     if (!fast || !axis_cell(zp, L.nz, L.wall[2], L.oz, zcell)) return 0u;
     if (L.wall[2] && (zcell == 0 || zcell == L.nz - 1)) return 0u;
     return zmask_of<MODE>(t, zp);
