@@ -238,3 +238,30 @@ def test_unsupported_pairs_and_option_errors(gpu):
         L.create_stepper("aap", "direct", g, options=L.StepperOptions(workers=-1))
     with pytest.raises(ValueError, match="chunk_length must be >= 1"):
         L.create_stepper("osnt-pull-1s", "direct", g, options=L.StepperOptions(chunk_length=0))
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("scheme,addr", PAIRS + EXT_PAIRS)
+def test_degenerate_geometries(gpu, scheme, addr, layout):
+    """No fluid node at all, and one fluid node walled in by solids: stepping
+    works, the snapshot has the fluid count's length, and the lone node (every
+    link bounces back onto itself) evolves like the oracle's 1-node box."""
+    import oracle
+    L = gpu
+    opts = L.StepperOptions(layout=layout, extensions=(scheme, addr) in EXT_PAIRS)
+    empty = L.GridGeometry(3, 3, 3, ("periodic",) * 3, np.zeros(27, np.uint8))
+    st = L.create_stepper(scheme, addr, empty, L.bgk(1.0), opts)
+    st.step_n(3)
+    st.synchronize()
+    assert st.node_count() == 0 and st.extract_natural().size == 0
+    mask = np.zeros(27, np.uint8)
+    mask[13] = 1  # the centre of a 3^3 box
+    lone = L.GridGeometry(3, 3, 3, ("periodic",) * 3, mask)
+    st = L.create_stepper(scheme, addr, lone, L.bgk(1.7, (1e-4, 0.0, 0.0)), opts)
+    O = oracle.Oracle()
+    f0 = O.random_field(5, 1)
+    st.load_natural(f0)
+    st.step_n(4)
+    st.synchronize()
+    want = O.ts_run(1, 1, 1, [1, 1, 1], None, 1.7, 1.7, [1e-4, 0.0, 0.0], f0, 4)
+    assert bitwise_equal(st.extract_natural(), want)
