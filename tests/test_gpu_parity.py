@@ -265,3 +265,14 @@ def test_degenerate_geometries(gpu, scheme, addr, layout):
     st.synchronize()
     want = O.ts_run(1, 1, 1, [1, 1, 1], None, 1.7, 1.7, [1e-4, 0.0, 0.0], f0, 4)
     assert bitwise_equal(st.extract_natural(), want)
+
+
+def test_index_range_guards(gpu):
+    """build_sparse's guard (p/src/geometry.cpp:177-179): 2^31 fluid nodes are
+    refused with the reference's text before any device allocation; a grid of
+    2^32 cells exceeds the 32-bit storage index of the direct kernels."""
+    L = gpu
+    with pytest.raises(RuntimeError, match="fluid count exceeds 32-bit index range"):
+        L.create_stepper("aap", "indirect", L.GridGeometry(2048, 1024, 1024))
+    with pytest.raises(RuntimeError, match="grid exceeds 32-bit cell index range"):
+        L.create_stepper("aap", "direct", L.GridGeometry(4096, 1024, 1024))
