@@ -126,6 +126,9 @@ struct Idx {
   uint32_t n;           // nodes in storage (the stride of adj / rem)
   uint32_t first = 0;   // sweeps update nodes [first, min(last, n)) (z-slabs:
   uint32_t last = ~0u;  // the slab's own nodes, not its ghost planes)
+  // all-fluid box (node = x + nx (y + ny z)): the AoS kernels may walk the
+  // nodes in x-y tiles marching through z (0 = not available)
+  int bx = 0, by = 0, bz = 0;
   __host__ __device__ uint32_t end() const { return last < n ? last : n; }
   __host__ __device__ uint32_t count() const { return end() > first ? end() - first : 0; }
 };

@@ -442,6 +442,7 @@ class IndirectStepper : public Stepper {
     I_.adj = adj_.get<uint32_t>();
     I_.rem = nullptr;
     I_.n = (uint32_t)nodes_;
+    if (!geo_.solids) I_.bx = geo_.nx, I_.by = geo_.ny, I_.bz = geo_.nz;
   }
 
  protected:
