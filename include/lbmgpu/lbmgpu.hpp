@@ -14,7 +14,9 @@
 //   kernel_available / parse_* / to_string     p/include/lbmlab/stepper.hpp:15-113
 //   TrafficSpec / traffic / predict_mlups      p/include/lbmlab/perfmodel.hpp:17-60
 // GPU additions: StepperOptions::{layout, precision, device, extensions,
-// z_begin, z_end}; Stepper::{step_n, synchronize, step_timed, init_field}.
+// z_begin, z_end}; Stepper::{step_n, synchronize, step_timed, init_field,
+// slab_connect_nccl, slab_sync_ghosts, slab_p2p_export, slab_p2p_connect};
+// nccl_unique_id, slab_group_step, slab_group_sync_ghosts, slab_group_connect_p2p.
 // Differences: Stepper::step() is synchronous (as the reference's); the
 // `workers` option is validated but unused (no CPU threads); CG and SWAP run in
 // parallel on the GPU, so "scheme is sequential; workers must be 1" never fires.
@@ -313,6 +315,27 @@ class Stepper {
   std::size_t values() const { return nodes_ * 19; }
   lbmgpu_stepper* handle() const { return h_; }
 
+  // ---- z-slab of a multi-GPU decomposition (options.z_begin / z_end) ----
+  // one rank per GPU over NCCL: every rank passes rank 0's nccl_unique_id()
+  void slab_connect_nccl(const std::array<std::uint8_t, LBMGPU_NCCL_ID_BYTES>& id, int nranks,
+                         int rank) {
+    detail::check(lbmgpu_slab_connect_nccl(h_, id.data(), nranks, rank));
+  }
+  // ghosts <- owners before an extraction that gathers from them (collective)
+  void slab_sync_ghosts() { detail::check(lbmgpu_slab_sync_ghosts(h_)); }
+  // peer-memory AA transport: publish this slab, then connect to the lower
+  // and upper neighbours' blobs (collective; nranks 1: this slab's own twice)
+  std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES> slab_p2p_export() {
+    std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES> b{};
+    detail::check(lbmgpu_slab_p2p_export(h_, b.data()));
+    return b;
+  }
+  void slab_p2p_connect(const std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES>& lower,
+                        const std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES>& upper, int nranks,
+                        int rank) {
+    detail::check(lbmgpu_slab_p2p_connect(h_, lower.data(), upper.data(), nranks, rank));
+  }
+
  private:
   friend std::unique_ptr<Stepper> create_stepper(SchemeId, Addressing, const GridGeometry&,
                                                  const Stencil&, const FlowParams&,
@@ -387,6 +410,33 @@ inline double predict_mlups(double bandwidth_gbps, double bytes_per_lup) {
   if (bandwidth_gbps <= 0 || bytes_per_lup <= 0)
     throw std::invalid_argument("bandwidth and bytes/LUP must be positive");
   return bandwidth_gbps * 1.0e9 / bytes_per_lup / 1.0e6;
+}
+
+// ---- z-slabs: NCCL id and in-process groups --------------------------------
+inline std::array<std::uint8_t, LBMGPU_NCCL_ID_BYTES> nccl_unique_id() {
+  std::array<std::uint8_t, LBMGPU_NCCL_ID_BYTES> id{};
+  detail::check(lbmgpu_nccl_unique_id(id.data()));
+  return id;
+}
+namespace detail {
+inline std::vector<lbmgpu_stepper*> handles(const std::vector<Stepper*>& slabs) {
+  std::vector<lbmgpu_stepper*> h;
+  for (Stepper* s : slabs) h.push_back(s->handle());
+  return h;
+}
+}  // namespace detail
+// several slabs of one process (ring in list order), stepped in lockstep
+inline void slab_group_step(const std::vector<Stepper*>& slabs, long long steps) {
+  auto h = detail::handles(slabs);
+  detail::check(lbmgpu_slab_group_step(h.data(), (std::int32_t)h.size(), steps));
+}
+inline void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs) {
+  auto h = detail::handles(slabs);
+  detail::check(lbmgpu_slab_group_sync_ghosts(h.data(), (std::int32_t)h.size()));
+}
+inline void slab_group_connect_p2p(const std::vector<Stepper*>& slabs) {
+  auto h = detail::handles(slabs);
+  detail::check(lbmgpu_slab_group_connect_p2p(h.data(), (std::int32_t)h.size()));
 }
 
 }  // namespace lbmgpu
