@@ -1,9 +1,10 @@
-"""Summarise ncu --set full captures of the AoS window kernels into markdown:
+"""Summarise ncu --set full captures (AoS window or any kernels) into markdown:
 per report the kernel, time, DRAM bytes, registers, issue/warp activity, the
 main stall reasons and the top source lines (needs -lineinfo, --import-source).
 usage: python tools/ncu_window_summary.py out.md name=report.ncu-rep ..."""
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -28,7 +29,9 @@ def lines(rep, top):
 
 def main():
     dst = sys.argv[1]
-    md = ["# AoS window kernels, ncu --set full (C1 256^3 channel, fp64, one launch each)", ""]
+    title = os.environ.get("NCU_SUMMARY_TITLE",
+                           "AoS window kernels, ncu --set full (C1 256^3 channel, fp64, one launch each)")
+    md = ["# " + title, ""]
     for arg in sys.argv[2:]:
         name, rep = arg.split("=", 1)
         d = raw(rep)
