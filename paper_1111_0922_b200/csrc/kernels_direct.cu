@@ -432,10 +432,13 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
 template <class T, bool AOS, bool RAW>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // the first group of a sweep reads what the previous sweep and its seam
-  // copies wrote: wait before the loads
+  // copies wrote: wait before the loads, and only then let the next group
+  // launch (its loads start early, so they must not precede the previous
+  // sweep's stores: a dependent starts once every block of this grid has
+  // passed launch_dependents)
   if (RAW) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);

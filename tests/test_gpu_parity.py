@@ -276,3 +276,32 @@ def test_index_range_guards(gpu):
         L.create_stepper("aap", "indirect", L.GridGeometry(2048, 1024, 1024))
     with pytest.raises(RuntimeError, match="grid exceeds 32-bit cell index range"):
         L.create_stepper("aap", "direct", L.GridGeometry(4096, 1024, 1024))
+
+
+def test_cg_sweeps_back_to_back_per_thread_aos(gpu):
+    """CG's plane groups are chained with programmatic dependent launch; a
+    sweep's first group must not let the next group start loading before the
+    previous sweep's stores landed. Many sweeps queued back to back on the
+    per-thread kernels (AoS windows off, in a subprocess: the switch is read
+    once per process), bitwise = the oracle."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_1111_0922_b200 as L, oracle\n"
+        "O = oracle.Oracle(); dims = (35, 10, 70)\n"
+        "geo = L.GridGeometry(*dims)\n"
+        "f0 = O.random_field(99, geo.fluid_count())\n"
+        "for lay in ('aos', 'soa'):\n"
+        "    st = L.create_stepper('cg', 'direct', geo, L.bgk(1.7, (2e-5, 0.0, 0.0)),"
+        " L.StepperOptions(layout=lay))\n"
+        "    st.load_natural(f0); st.step_n(12); st.synchronize()\n"
+        "    want = O.ts_run(*dims, [0, 0, 0], None, 1.7, 1.7, [2e-5, 0.0, 0.0], f0, 12)\n"
+        "    assert (st.extract_natural().view(np.uint64) == want.view(np.uint64)).all(), lay\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ, LBMGPU_AOS_WINDOW="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
