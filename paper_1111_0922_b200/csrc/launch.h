@@ -85,6 +85,12 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
                const EtBase& base);
 // SWAP link exchange: mode 0 all links, 1 only non-wrapped, 2 only wrapped
 void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode);
+// SWAP collisions + non-wrapped link exchanges in one launch (SoA, storage =
+// cells; kernels_swap.cu). rows of a tile (0: not applicable). sync = 1 +
+// ntiles zeroed words per stepper; epoch >= 1 increments per launch.
+int swap_fused_rows(const dev::Lat& L);
+bool launch_swap_fused(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
+                       bool push, unsigned long long* sync, unsigned long long epoch);
 void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
                       const int8_t* dir, long long count);
 // CG as a plane-group push launch: read at the cell's storage index, write at

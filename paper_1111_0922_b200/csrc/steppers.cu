@@ -347,6 +347,16 @@ class SwapDirect final : public DirectStepper {
       CK(cudaMemcpyAsync(fd_.get(), d.data(), nfix_, cudaMemcpyHostToDevice, stream_));
     }
     alloc_field(f_, g.cells());
+    // one-launch sweep (kernels_swap.cu), opt-in with LBMGPU_SWAP_FUSED=1: it
+    // moves only the compulsory bytes but runs slower than the two passes
+    const char* e = std::getenv("LBMGPU_SWAP_FUSED");
+    const int rows = swap_fused_rows(L_);
+    if (!aos_ && rows > 0 && e && std::atoi(e) == 1) {
+      const size_t words = 1 + (size_t)((g.ny + rows - 1) / rows);
+      sync_.alloc(words * 8);
+      CK(cudaMemsetAsync(sync_.get(), 0, words * 8, stream_));
+      fused_ = true;
+    }
     init(base_init(kSrcRest));
     sync();
   }
@@ -380,6 +390,9 @@ class SwapDirect final : public DirectStepper {
   // (pull): the swapped slot pairs are disjoint and independent of the
   // sweep's collisions, so this equals the sequential sweep bit for bit.
   void sweep(const DField& f, bool push) {
+    if (fused_ && launch_swap_fused(stream_, f, L_, op_, push,
+                                    sync_.get<unsigned long long>(), ++epoch_))
+      return;
     if (push) {
       launch_local(stream_, f, f, L_, op_, true, false);
       launch_swap(stream_, f, L_, 1);
@@ -388,7 +401,7 @@ class SwapDirect final : public DirectStepper {
       launch_local(stream_, f, f, L_, op_, true, false);
     }
   }
-  int launches_per_step() const override { return 2 + (nfix_ ? 1 : 0); }
+  int launches_per_step() const override { return (fused_ ? 1 : 2) + (nfix_ ? 1 : 0); }
   void before_extract() override {
     if (!pull_ && pending_) fixup(field(f_, soa_stride(geo_.cells())));
   }
@@ -418,9 +431,10 @@ class SwapDirect final : public DirectStepper {
 
  private:
   bool pull_, defer_;
-  bool fresh_ = false, pending_ = false;
+  bool fresh_ = false, pending_ = false, fused_ = false;
   long long nfix_ = 0;
-  DevMem f_, fa_, fb_, fd_;
+  unsigned long long epoch_ = 0;
+  DevMem f_, fa_, fb_, fd_, sync_;
 };
 
 // ---------------------------------------------------------------------------

@@ -305,3 +305,40 @@ def test_cg_sweeps_back_to_back_per_thread_aos(gpu):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("dims,policy", [
+    ((5, 7, 6), ("periodic", "periodic", "periodic")),
+    ((33, 9, 5), ("periodic", "periodic", "wall")),
+    ((300, 3, 4), ("periodic", "wall", "periodic")),
+    ((512, 2, 3), ("wall", "periodic", "periodic")),
+    ((40, 40, 12), ("periodic", "periodic", "wall")),
+    ((24, 19, 9), "porous"),
+])
+@pytest.mark.parametrize("precision", [8, 4])
+@pytest.mark.parametrize("scheme", ["swap-push", "swap-pull"])
+def test_swap_one_sweep_equals_two_passes(gpu, monkeypatch, dims, policy, precision, scheme):
+    """kernels_swap.cu (collisions + exchanges in one launch, tiles of full x
+    rows ordered by flags) against the collide pass + exchange pass: bitwise,
+    over tile shapes (several rows per tile, one row, a ragged last tile,
+    nx = 512), wall axes, a porous mask, and the deferred seam fix-up."""
+    rng = np.random.default_rng(11)
+    mask = None
+    if policy == "porous":
+        mask = (rng.random(dims[::-1]) > 0.3).astype(np.uint8).reshape(-1)
+        policy = ("periodic", "periodic", "periodic")
+    geo = gpu.GridGeometry(*dims, policy, mask)
+    flow = gpu.bgk(1.7, body_force=(1e-6, 2e-7, -1e-7))
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("LBMGPU_SWAP_FUSED", fused)
+        for deferred in (False, True):
+            st = gpu.create_stepper(scheme, "direct", geo, flow,
+                                    gpu.StepperOptions(precision=precision,
+                                                       swap_deferred_fixup=deferred))
+            st.init_field("taylor_green", seed=5)
+            st.step_n(5)
+            st.synchronize()
+            outs.append(st.extract_natural())
+    for o in outs[1:]:
+        assert bitwise_equal(o, outs[0])
