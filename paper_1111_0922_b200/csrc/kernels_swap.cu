@@ -224,6 +224,36 @@ __global__ void __launch_bounds__(512, 1)
     issue(z + NS - 1);
     const uint32_t s = s0 + (uint32_t)z * plane;  // this plane's node
     const uint32_t sp = s - plane;                // plane z-1's node
+    // plane zc's cross-tile exchanges first (tile T-1 published plane zc before
+    // the last barrier): their L2 round trip overlaps the other tile's work
+    // on this SM, and their registers are free again before the collision
+    const int zc = z - kSwapKC;
+    if (zc >= 0 && active && xrow) {
+      const uint32_t sc = s0 + (uint32_t)zc * plane;
+      bool fc;
+      const uint32_t ux = pairs(use_x, sc, zc, fc);
+      T va[5], vv[5];
+      uint32_t pa9 = sc - (uint32_t)nx;  // tile T-1's last-row node on plane zc
+      bool x9 = false;
+      if (zc >= 1) x9 = lm ? ((lm[pa9] & 1u) && !((lm[pa9] >> 13) & 1u)) : true;
+#pragma unroll
+      for (int k = 0, q = 0; k < 9; ++k) {
+        const int i = back_dir(k);
+        if (cy(i) >= 0) continue;
+        if (ux & (1u << k)) va[q] = __ldcg(F.at(i, sc)), vv[q] = __ldcg(F.at(opp(i), sc + (uint32_t)boff(i)));
+        ++q;
+      }
+      T a9 = T(0), b9 = T(0);
+      if (x9) a9 = __ldcg(F.at(13, pa9)), b9 = __ldcg(F.at(12, sc - plane));
+#pragma unroll
+      for (int k = 0, q = 0; k < 9; ++k) {
+        const int i = back_dir(k);
+        if (cy(i) >= 0) continue;
+        if (ux & (1u << k)) F.at(i, sc)[0] = vv[q], F.at(opp(i), sc + (uint32_t)boff(i))[0] = va[q];
+        ++q;
+      }
+      if (x9) F.at(13, pa9)[0] = b9, F.at(12, sc - plane)[0] = a9;
+    }
     // in-tile partner slots of plane z-1 (collided before the last barrier)
     T vb[9];
     if (z >= 1 && z <= nz && active) {
@@ -278,35 +308,6 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
     use_prev = use_z;
-    // plane zc's cross-tile exchanges (tile T-1 published plane zc: see the
-    // barrier below of the previous iteration)
-    const int zc = z - kSwapKC;
-    if (zc >= 0 && active && xrow) {
-      const uint32_t sc = s0 + (uint32_t)zc * plane;
-      bool fc;
-      const uint32_t ux = pairs(use_x, sc, zc, fc);
-      T va[5], vv[5];
-      uint32_t pa9 = sc - (uint32_t)nx;  // tile T-1's last-row node on plane zc
-      bool x9 = false;
-      if (zc >= 1) x9 = lm ? ((lm[pa9] & 1u) && !((lm[pa9] >> 13) & 1u)) : true;
-#pragma unroll
-      for (int k = 0, q = 0; k < 9; ++k) {
-        const int i = back_dir(k);
-        if (cy(i) >= 0) continue;
-        if (ux & (1u << k)) va[q] = __ldcg(F.at(i, sc)), vv[q] = __ldcg(F.at(opp(i), sc + (uint32_t)boff(i)));
-        ++q;
-      }
-      T a9 = T(0), b9 = T(0);
-      if (x9) a9 = __ldcg(F.at(13, pa9)), b9 = __ldcg(F.at(12, sc - plane));
-#pragma unroll
-      for (int k = 0, q = 0; k < 9; ++k) {
-        const int i = back_dir(k);
-        if (cy(i) >= 0) continue;
-        if (ux & (1u << k)) F.at(i, sc)[0] = vv[q], F.at(opp(i), sc + (uint32_t)boff(i))[0] = va[q];
-        ++q;
-      }
-      if (x9) F.at(13, pa9)[0] = b9, F.at(12, sc - plane)[0] = a9;
-    }
     // next iteration's cross-tile plane must be published by tile T-1
     const int zn = z + 1 - kSwapKC;
     if (tid == 0 && T_ > 0 && zn >= 0 && zn < nz) {
