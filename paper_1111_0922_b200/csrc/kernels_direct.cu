@@ -92,7 +92,7 @@ __device__ __forceinline__ void os_pull_body(const Fld<T, AOS>& a, const Fld<T, 
   }
 }
 template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
                                                     Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
@@ -118,7 +118,7 @@ __device__ __forceinline__ void os_push_body(const Fld<T, AOS>& a, const Fld<T, 
     st<false>((BB && c.bb(i)) ? b.at(opp(i), c.s) : b.at_off(i, c.s, c.off(i)), f[i]);
 }
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
+__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
                                                     Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, cons
   }
 }
 template <class T, bool AOS, bool SW>
-__global__ void __launch_bounds__(kBlock, EtMinBlocks<T>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, EtMinBlocks<T, AOS>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);

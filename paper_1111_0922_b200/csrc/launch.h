@@ -52,13 +52,24 @@ template <class T>
 struct MinBlocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_MIN_BLOCKS_F32;
 };
-// the ET sweep (two handle lookups per pair) under its own register budget
-#ifndef LBM_ET_MIN_BLOCKS_F32
-#define LBM_ET_MIN_BLOCKS_F32 LBM_MIN_BLOCKS_F32
+// SoA fp32 OS pull/push and ET sweeps: 5 blocks (<= 51 registers) measured
+// ahead of 4 on C1 (OS pull 0.99 -> 1.02, push 0.92 -> 0.94, ET 0.89 -> 0.91
+// of the roofline); their AoS forms and every other kernel keep MinBlocks.
+#ifndef LBM_OS_MIN_BLOCKS_F32
+#define LBM_OS_MIN_BLOCKS_F32 5
 #endif
-template <class T>
+#ifndef LBM_ET_MIN_BLOCKS_F32
+#define LBM_ET_MIN_BLOCKS_F32 5
+#endif
+template <class T, bool AOS>
+struct OsMinBlocks {
+  static constexpr int value =
+      sizeof(T) == 4 && !AOS ? LBM_OS_MIN_BLOCKS_F32 : MinBlocks<T>::value;
+};
+template <class T, bool AOS = false>
 struct EtMinBlocks {
-  static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_ET_MIN_BLOCKS_F32;
+  static constexpr int value =
+      sizeof(T) == 4 && !AOS ? LBM_ET_MIN_BLOCKS_F32 : MinBlocks<T>::value;
 };
 
 // ---- direct (full-grid) addressing -----------------------------------------
