@@ -25,7 +25,7 @@ inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlo
 //   SWAP collide from opposed slots     (p/src/scheme_swap.cpp:187-190, 228-231)
 // ---------------------------------------------------------------------------
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_local(Fld<T, AOS> src, Fld<T, AOS> dst, Lat L,
                                                   Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
@@ -54,7 +54,7 @@ __device__ __forceinline__ void ts_stream_body(const Fld<T, AOS>& a, const Fld<T
   for (int i = 0; i < 19; ++i) st<false>(a.at(i, c.s), v[i]);
 }
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -150,7 +150,7 @@ __device__ __forceinline__ void aa_odd_body(const Fld<T, AOS>& F, const Ctx& c,
     st<false>((BB && c.bb(j)) ? F.at(opp(j), c.s) : F.at_off(j, c.s, c.off(j)), f[j]);
 }
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -430,7 +430,7 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
     st<false>((BB && c.bb(i)) ? F.at(opp(i), w) : F.at_off(i, w, c.off(i)), f[i]);
 }
 template <class T, bool AOS, bool RAW>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
     k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
   // the first group of a sweep reads what the previous sweep and its seam
   // copies wrote: wait before the loads, and only then let the next group

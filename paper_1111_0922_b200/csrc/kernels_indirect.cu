@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_ts_stream_idx(F
 
 // OS / OSNT pull, indirect (p/src/scheme_os.cpp:203-226, scheme_osnt.cpp:219-260)
 template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_os_pull_idx(Fld<T, AOS> a, Fld<T, AOS> b, Idx I,
                                                         Trt<T> op) {
   const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.end()) return;

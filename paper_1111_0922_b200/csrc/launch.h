@@ -52,9 +52,16 @@ template <class T>
 struct MinBlocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_MIN_BLOCKS_F64 : LBM_MIN_BLOCKS_F32;
 };
-// SoA fp32 OS pull/push and ET sweeps: 5 blocks (<= 51 registers) measured
-// ahead of 4 on C1 (OS pull 0.99 -> 1.02, push 0.92 -> 0.94, ET 0.89 -> 0.91
-// of the roofline); their AoS forms and every other kernel keep MinBlocks.
+// SoA kernels of the direct path (and the indirect OS pull) under their own
+// budgets, measured per kernel (tools/sweep.py, profiles/r01_variants.md):
+// fp64 at 3 blocks (<= 85 registers; C1 AA 1.01 -> 1.04, ET 0.95 -> 1.02, CG
+// 0.98 -> 1.02, OS push 1.00 -> 1.03 of the roofline, a few spilled values
+// land in L1); the indirect OS push / AA / ET lose with it and keep 2. fp32
+// OS pull/push and ET at 5 blocks (<= 51 registers; C1 OS pull 0.99 -> 1.02,
+// ET 0.89 -> 0.91). AoS per-thread kernels keep MinBlocks.
+#ifndef LBM_SOA_MIN_BLOCKS_F64
+#define LBM_SOA_MIN_BLOCKS_F64 3
+#endif
 #ifndef LBM_OS_MIN_BLOCKS_F32
 #define LBM_OS_MIN_BLOCKS_F32 5
 #endif
@@ -62,14 +69,19 @@ struct MinBlocks {
 #define LBM_ET_MIN_BLOCKS_F32 5
 #endif
 template <class T, bool AOS>
+struct SoaMinBlocks {
+  static constexpr int value =
+      sizeof(T) == 8 && !AOS ? LBM_SOA_MIN_BLOCKS_F64 : MinBlocks<T>::value;
+};
+template <class T, bool AOS>
 struct OsMinBlocks {
   static constexpr int value =
-      sizeof(T) == 4 && !AOS ? LBM_OS_MIN_BLOCKS_F32 : MinBlocks<T>::value;
+      sizeof(T) == 4 && !AOS ? LBM_OS_MIN_BLOCKS_F32 : SoaMinBlocks<T, AOS>::value;
 };
 template <class T, bool AOS = false>
 struct EtMinBlocks {
   static constexpr int value =
-      sizeof(T) == 4 && !AOS ? LBM_ET_MIN_BLOCKS_F32 : MinBlocks<T>::value;
+      sizeof(T) == 4 && !AOS ? LBM_ET_MIN_BLOCKS_F32 : SoaMinBlocks<T, AOS>::value;
 };
 
 // ---- direct (full-grid) addressing -----------------------------------------
