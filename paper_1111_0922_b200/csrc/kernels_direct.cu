@@ -17,6 +17,19 @@ namespace {
 
 inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
 
+// shifted plane table of an SoA field (unused for AoS)
+template <class T>
+SoaNb<T> soa_nb(const DField& f, const Lat& L) {
+  SoaNb<T> N;
+  for (int j = 0; j < 19; ++j) {
+    const long long off = (long long)cx(j) + (long long)cy(j) * L.sx + (long long)cz(j) * L.sxy;
+    const uintptr_t b = reinterpret_cast<uintptr_t>(f.p) +
+                        (uintptr_t)((long long)j * f.stride + off) * sizeof(T);
+    N.n[j] = reinterpret_cast<T*>(f.aos ? reinterpret_cast<uintptr_t>(f.p) : b);
+  }
+  return N;
+}
+
 // ---------------------------------------------------------------------------
 // Local collision sweep. Covers
 //   TS collide_sweep A -> B            (p/src/scheme_ts.cpp:59-80)
@@ -149,13 +162,33 @@ __device__ __forceinline__ void aa_odd_body(const Fld<T, AOS>& F, const Ctx& c,
   for (int j = 1; j < 19; ++j)
     st<false>((BB && c.bb(j)) ? F.at(opp(j), c.s) : F.at_off(j, c.s, c.off(j)), f[j]);
 }
+// the same sweep for a warp with no bounce and no y/z wrap, addressed through
+// the shifted plane table (SoaNb)
+template <class T>
+__device__ __forceinline__ void aa_odd_plain(const SoaNb<T>& N, const Ctx& c, const Trt<T>& op) {
+  const uint32_t s = c.s, sm = s + (uint32_t)(c.xm + 1), sp = s + (uint32_t)(c.xp - 1);
+  T f[19];
+  f[0] = ld(N.n[0] + s);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    f[i] = ld(N.n[j] + nb_ix(j, s, sm, sp));
+  }
+  collide(op, f);
+  N.n[0][s] = f[0];
+#pragma unroll
+  for (int j = 1; j < 19; ++j) N.n[j][nb_ix(j, s, sm, sp)] = f[j];
+}
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
+    k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op, SoaNb<T> N) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  if (!AOS && warp_plain(L, c))
+    aa_odd_plain(N, c, op);
+  else if (warp_interior(c))
     aa_odd_body<false>(F, c, op);
   else
     aa_odd_body<true>(F, c, op);
@@ -584,7 +617,8 @@ void launch_aa_odd(cudaStream_t st, const DField& f, const dev::Lat& L, const Tr
   if (L.ncells <= L.cell_begin) return;
   if (launch_aos_window(st, kWinModeAaOdd, f, f, L, op)) return;
   LBM_DISPATCH(f, {
-    k_aa_odd<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+    k_aa_odd<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op),
+                                                                         soa_nb<T>(f, L));
   });
 }
 
