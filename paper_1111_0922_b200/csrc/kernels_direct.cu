@@ -17,18 +17,37 @@ namespace {
 
 inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
 
-// shifted plane table of an SoA field (unused for AoS)
+// shifted plane table of an SoA field (unused for AoS): n[j] = plane j +
+// sign * (c_x + c_y sx + c_z sxy)(j); sign 0 gives the plain plane bases
 template <class T>
-SoaNb<T> soa_nb(const DField& f, const Lat& L) {
+SoaNb<T> soa_nb(const DField& f, const Lat& L, int sign = 1) {
   SoaNb<T> N;
   for (int j = 0; j < 19; ++j) {
     const long long off = (long long)cx(j) + (long long)cy(j) * L.sx + (long long)cz(j) * L.sxy;
     const uintptr_t b = reinterpret_cast<uintptr_t>(f.p) +
-                        (uintptr_t)((long long)j * f.stride + off) * sizeof(T);
+                        (uintptr_t)((long long)j * f.stride + sign * off) * sizeof(T);
     N.n[j] = reinterpret_cast<T*>(f.aos ? reinterpret_cast<uintptr_t>(f.p) : b);
   }
   return N;
 }
+// ET: n[p] = plane hb(pair_j(p)) shifted by c_(pair_i(p)), p = 0..8
+template <class T>
+SoaNb<T> et_nb(const DField& f, const Lat& L, bool sw) {
+  SoaNb<T> N{};
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p), k = sw ? opp(j) : j;
+    const long long off = (long long)cx(i) + (long long)cy(i) * L.sx + (long long)cz(i) * L.sxy;
+    N.n[p] = reinterpret_cast<T*>(
+        f.aos ? reinterpret_cast<uintptr_t>(f.p)
+              : reinterpret_cast<uintptr_t>(f.p) +
+                    (uintptr_t)((long long)k * f.stride + off) * sizeof(T));
+  }
+  return N;
+}
+
+// per-lane indices of a plain warp: s, and s with the x wrap of a -x / +x shift
+#define LBM_PLAIN_IX(c, s, sm, sp)                                             \
+  const uint32_t s = (c).s, sm = s + (uint32_t)((c).xm + 1), sp = s + (uint32_t)((c).xp - 1)
 
 // ---------------------------------------------------------------------------
 // Local collision sweep. Covers
@@ -66,13 +85,26 @@ __device__ __forceinline__ void ts_stream_body(const Fld<T, AOS>& a, const Fld<T
 #pragma unroll
   for (int i = 0; i < 19; ++i) st<false>(a.at(i, c.s), v[i]);
 }
+// plain warp: Bm = b shifted by -c_i, A0 = a's plane bases
+template <class T>
+__device__ __forceinline__ void ts_stream_plain(const SoaNb<T>& A0, const SoaNb<T>& Bm, const Ctx& c) {
+  LBM_PLAIN_IX(c, s, sm, sp);
+  T v[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) v[i] = ld(Bm.n[i] + nb_ix(-cx(i), s, sm, sp));
+#pragma unroll
+  for (int i = 0; i < 19; ++i) A0.n[i][s] = v[i];
+}
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L) {
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
+    k_ts_stream(Fld<T, AOS> a, Fld<T, AOS> b, Lat L, SoaNb<T> A0, SoaNb<T> Bm) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  if (!AOS && warp_plain(L, c))
+    ts_stream_plain(A0, Bm, c);
+  else if (warp_interior(c))
     ts_stream_body<false>(a, b, c);
   else
     ts_stream_body<true>(a, b, c);
@@ -104,14 +136,39 @@ __device__ __forceinline__ void os_pull_body(const Fld<T, AOS>& a, const Fld<T, 
     }
   }
 }
+// plain warp: Am = a shifted by -c_i, B0 = b's plane bases
+template <bool NT, bool TWO_S, class T>
+__device__ __forceinline__ void os_pull_plain(const SoaNb<T>& Am, const SoaNb<T>& B0, const Ctx& c,
+                                              const Trt<T>& op) {
+  LBM_PLAIN_IX(c, s, sm, sp);
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(Am.n[i] + nb_ix(-cx(i), s, sm, sp));
+  collide(op, f);
+  if (!TWO_S) {
+#pragma unroll
+    for (int i = 0; i < 19; ++i) st<NT>(B0.n[i] + s, f[i]);
+  } else {
+    st<NT>(B0.n[0] + s, f[0]);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      st<NT>(B0.n[pair_i(p)] + s, f[pair_i(p)]);
+      st<NT>(B0.n[pair_j(p)] + s, f[pair_j(p)]);
+    }
+  }
+}
 template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value) k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
-                                                    Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
+    k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L, Trt<T> op, SoaNb<T> Am, SoaNb<T> B0) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  // (the streaming-store OSNT forms keep the generic path: measured slower
+  // with the table at their 5-block register budget)
+  if (!AOS && !NT && warp_plain(L, c))
+    os_pull_plain<NT, TWO_S>(Am, B0, c, op);
+  else if (warp_interior(c))
     os_pull_body<false, NT, TWO_S>(a, b, c, op);
   else
     os_pull_body<true, NT, TWO_S>(a, b, c, op);
@@ -130,14 +187,28 @@ __device__ __forceinline__ void os_push_body(const Fld<T, AOS>& a, const Fld<T, 
   for (int i = 1; i < 19; ++i)
     st<false>((BB && c.bb(i)) ? b.at(opp(i), c.s) : b.at_off(i, c.s, c.off(i)), f[i]);
 }
+// plain warp: A0 = a's plane bases, Bp = b shifted by +c_i
+template <class T>
+__device__ __forceinline__ void os_push_plain(const SoaNb<T>& A0, const SoaNb<T>& Bp, const Ctx& c,
+                                              const Trt<T>& op) {
+  LBM_PLAIN_IX(c, s, sm, sp);
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(A0.n[i] + s);
+  collide(op, f);
+#pragma unroll
+  for (int i = 0; i < 19; ++i) Bp.n[i][nb_ix(cx(i), s, sm, sp)] = f[i];
+}
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value) k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L,
-                                                    Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
+    k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L, Trt<T> op, SoaNb<T> A0, SoaNb<T> Bp) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  if (!AOS && warp_plain(L, c))
+    os_push_plain(A0, Bp, c, op);
+  else if (warp_interior(c))
     os_push_body<false>(a, b, c, op);
   else
     os_push_body<true>(a, b, c, op);
@@ -166,18 +237,18 @@ __device__ __forceinline__ void aa_odd_body(const Fld<T, AOS>& F, const Ctx& c,
 // the shifted plane table (SoaNb)
 template <class T>
 __device__ __forceinline__ void aa_odd_plain(const SoaNb<T>& N, const Ctx& c, const Trt<T>& op) {
-  const uint32_t s = c.s, sm = s + (uint32_t)(c.xm + 1), sp = s + (uint32_t)(c.xp - 1);
+  LBM_PLAIN_IX(c, s, sm, sp);
   T f[19];
   f[0] = ld(N.n[0] + s);
 #pragma unroll
   for (int i = 1; i < 19; ++i) {
     const int j = opp(i);
-    f[i] = ld(N.n[j] + nb_ix(j, s, sm, sp));
+    f[i] = ld(N.n[j] + nb_ix(cx(j), s, sm, sp));
   }
   collide(op, f);
   N.n[0][s] = f[0];
 #pragma unroll
-  for (int j = 1; j < 19; ++j) N.n[j][nb_ix(j, s, sm, sp)] = f[j];
+  for (int j = 1; j < 19; ++j) N.n[j][nb_ix(cx(j), s, sm, sp)] = f[j];
 }
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
@@ -263,13 +334,39 @@ __device__ __forceinline__ void et_body(const Fld<T, AOS>& F, const Ctx& c, cons
     st<false>(F.at_off(hb<SW>(j), c.s, c.off(i)), f[i]);
   }
 }
+// plain warp: T0 = plane bases, E[p] = plane hb(j) shifted by c_i for pair p
+template <bool SW, class T>
+__device__ __forceinline__ void et_plain(const SoaNb<T>& T0, const SoaNb<T>& E, const Ctx& c,
+                                         const Trt<T>& op) {
+  constexpr bool NC = sizeof(T) == 4;
+  LBM_PLAIN_IX(c, s, sm, sp);
+  T f[19];
+  f[0] = ldsel<NC>(T0.n[0] + s);
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    f[i] = ldsel<NC>(T0.n[hb<SW>(i)] + s);
+    f[j] = ldsel<NC>(E.n[p] + nb_ix(cx(i), s, sm, sp));
+  }
+  collide(op, f);
+  T0.n[0][s] = f[0];
+#pragma unroll
+  for (int p = 0; p < 9; ++p) {
+    const int i = pair_i(p), j = pair_j(p);
+    T0.n[hb<SW>(i)][s] = f[j];
+    E.n[p][nb_ix(cx(i), s, sm, sp)] = f[i];
+  }
+}
 template <class T, bool AOS, bool SW>
-__global__ void __launch_bounds__(kBlock, EtMinBlocks<T, AOS>::value) k_et(Fld<T, AOS> F, Lat L, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, EtMinBlocks<T, AOS>::value)
+    k_et(Fld<T, AOS> F, Lat L, Trt<T> op, SoaNb<T> T0, SoaNb<T> E) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  if (!AOS && warp_plain(L, c))
+    et_plain<SW>(T0, E, c, op);
+  else if (warp_interior(c))
     et_body<false, SW>(F, c, op);
   else
     et_body<true, SW>(F, c, op);
@@ -462,9 +559,23 @@ __device__ __forceinline__ void cg_push_body(const Fld<T, AOS>& F, const Ctx& c,
   for (int i = 1; i < 19; ++i)
     st<false>((BB && c.bb(i)) ? F.at(opp(i), w) : F.at_off(i, w, c.off(i)), f[i]);
 }
+// plain warp: T0 = plane bases (read frame at s), Tp = planes shifted by +c_i
+// (write frame at w = s + delta)
+template <class T>
+__device__ __forceinline__ void cg_push_plain(const SoaNb<T>& T0, const SoaNb<T>& Tp, const Ctx& c,
+                                              const Trt<T>& op, int delta) {
+  T f[19];
+#pragma unroll
+  for (int i = 0; i < 19; ++i) f[i] = ld(T0.n[i] + c.s);
+  collide(op, f);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const uint32_t w = c.s + (uint32_t)delta, wm = w + (uint32_t)(c.xm + 1), wp = w + (uint32_t)(c.xp - 1);
+#pragma unroll
+  for (int i = 0; i < 19; ++i) Tp.n[i][nb_ix(cx(i), w, wm, wp)] = f[i];
+}
 template <class T, bool AOS, bool RAW>
 __global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
-    k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta) {
+    k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta, SoaNb<T> T0, SoaNb<T> Tp) {
   // the first group of a sweep reads what the previous sweep and its seam
   // copies wrote: wait before the loads, and only then let the next group
   // launch (its loads start early, so they must not precede the previous
@@ -476,7 +587,9 @@ __global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
-  if (warp_interior(c))
+  if (!AOS && warp_plain(L, c))
+    cg_push_plain(T0, Tp, c, op, delta);
+  else if (warp_interior(c))
     cg_push_body<false>(F, c, op, delta);
   else
     cg_push_body<true>(F, c, op, delta);
@@ -563,7 +676,8 @@ void launch_ts_stream(cudaStream_t st, const DField& a, const DField& b, const d
     return;
   }
   LBM_DISPATCH(a, {
-    k_ts_stream<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L);
+    k_ts_stream<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+        fld<T, A>(a), fld<T, A>(b), L, soa_nb<T>(a, L, 0), soa_nb<T>(b, L, -1));
   });
 }
 
@@ -587,10 +701,11 @@ void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev
     auto fb = fld<T, A>(b);
     const auto o = cast_op<T>(op);
     const unsigned g = grid_for(L.ncells - L.cell_begin);
-    if (!streaming && !two_s) k_os_pull<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
-    if (!streaming && two_s) k_os_pull<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, L, o);
-    if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, L, o);
-    if (streaming && two_s) k_os_pull<T, A, true, true><<<g, kBlock, 0, st>>>(fa, fb, L, o);
+    const auto am = soa_nb<T>(a, L, -1), b0 = soa_nb<T>(b, L, 0);
+    if (!streaming && !two_s) k_os_pull<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
+    if (!streaming && two_s) k_os_pull<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
+    if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
+    if (streaming && two_s) k_os_pull<T, A, true, true><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
   });
 }
 
@@ -608,8 +723,8 @@ void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev
     return;
   }
   LBM_DISPATCH(a, {
-    k_os_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(fld<T, A>(a), fld<T, A>(b), L,
-                                                           cast_op<T>(op));
+    k_os_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
+        fld<T, A>(a), fld<T, A>(b), L, cast_op<T>(op), soa_nb<T>(a, L, 0), soa_nb<T>(b, L, 1));
   });
 }
 
@@ -650,9 +765,11 @@ void launch_et(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHos
   LBM_DISPATCH(f, {
     const unsigned g = grid_for(L.ncells - L.cell_begin);
     if (base.swapped())
-      k_et<T, A, true><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+      k_et<T, A, true><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), soa_nb<T>(f, L, 0),
+                                             et_nb<T>(f, L, true));
     else
-      k_et<T, A, false><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op));
+      k_et<T, A, false><<<g, kBlock, 0, st>>>(fld<T, A>(f), L, cast_op<T>(op), soa_nb<T>(f, L, 0),
+                                              et_nb<T>(f, L, false));
   });
 }
 
@@ -676,9 +793,11 @@ void launch_cg_push(cudaStream_t st, const DField& f, const dev::Lat& L, const T
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (early)
-      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, false>, fld<T, A>(f), L, cast_op<T>(op), delta);
+      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, false>, fld<T, A>(f), L, cast_op<T>(op), delta,
+                         soa_nb<T>(f, L, 0), soa_nb<T>(f, L, 1));
     else
-      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, true>, fld<T, A>(f), L, cast_op<T>(op), delta);
+      cudaLaunchKernelEx(&cfg, k_cg_push<T, A, true>, fld<T, A>(f), L, cast_op<T>(op), delta,
+                         soa_nb<T>(f, L, 0), soa_nb<T>(f, L, 1));
   });
 }
 
