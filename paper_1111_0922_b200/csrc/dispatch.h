@@ -10,6 +10,28 @@ inline dev::Fld<T, AOS> fld(const DField& f) {
   return dev::Fld<T, AOS>{static_cast<T*>(f.p), f.stride};
 }
 
+// the field type a kernel was instantiated with (Fld, or FldT with plane bases)
+template <class FT>
+struct MakeFld;
+template <class T, bool AOS>
+struct MakeFld<dev::Fld<T, AOS>> {
+  static dev::Fld<T, AOS> get(const DField& f) { return fld<T, AOS>(f); }
+};
+template <class T>
+struct MakeFld<dev::FldT<T>> {
+  static dev::FldT<T> get(const DField& f) {
+    dev::FldT<T> F;
+    F.p = static_cast<T*>(f.p);
+    F.stride = f.stride;
+    for (int i = 0; i < 19; ++i) F.pl[i] = F.p + (size_t)i * (size_t)f.stride;
+    return F;
+  }
+};
+template <class T, bool AOS, bool TAB>
+inline dev::FldSel<T, AOS, TAB> fld_sel(const DField& f) {
+  return MakeFld<dev::FldSel<T, AOS, TAB>>::get(f);
+}
+
 // TrtOperator coefficients in the kernel's precision (fp32 casts the fp64 ones)
 template <class T>
 inline dev::Trt<T> cast_op(const TrtHost& h) {

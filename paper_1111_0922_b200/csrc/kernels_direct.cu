@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
 // OS pull (p/src/scheme_os.cpp:141-174) and OSNT pull with streaming stores
 // (p/src/scheme_osnt.cpp:131-173, 175-217: 1S = one store loop per direction,
 // 2S = rest then one per opposing pair; st.global.cs replaces _mm_stream_si64).
-template <bool BB, bool NT, bool TWO_S, class T, bool AOS>
-__device__ __forceinline__ void os_pull_body(const Fld<T, AOS>& a, const Fld<T, AOS>& b,
-                                             const Ctx& c, const Trt<T>& op) {
+template <bool BB, bool NT, bool TWO_S, class FA, class T>
+__device__ __forceinline__ void os_pull_body(const FA& a, const FA& b, const Ctx& c,
+                                             const Trt<T>& op) {
   T f[19];
   f[0] = ld(a.at(0, c.s));
 #pragma unroll
@@ -157,9 +157,14 @@ __device__ __forceinline__ void os_pull_plain(const SoaNb<T>& Am, const SoaNb<T>
     }
   }
 }
+// fp32 SoA OSNT (streaming stores) addresses through plane bases (FldT:
+// C1 1S 0.99 -> 1.01, 2S 0.98 -> 1.01, measured)
+template <class T, bool NT>
+constexpr bool kOsPullTab = sizeof(T) == 4 && NT;
 template <class T, bool AOS, bool NT, bool TWO_S>
 __global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
-    k_os_pull(Fld<T, AOS> a, Fld<T, AOS> b, Lat L, Trt<T> op, SoaNb<T> Am, SoaNb<T> B0) {
+    k_os_pull(FldSel<T, AOS, kOsPullTab<T, NT>> a, FldSel<T, AOS, kOsPullTab<T, NT>> b, Lat L,
+              Trt<T> op, SoaNb<T> Am, SoaNb<T> B0) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -175,9 +180,9 @@ __global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
 }
 
 // OS push (p/src/scheme_os.cpp:104-139)
-template <bool BB, class T, bool AOS>
-__device__ __forceinline__ void os_push_body(const Fld<T, AOS>& a, const Fld<T, AOS>& b,
-                                             const Ctx& c, const Trt<T>& op) {
+template <bool BB, class FA, class T>
+__device__ __forceinline__ void os_push_body(const FA& a, const FA& b, const Ctx& c,
+                                             const Trt<T>& op) {
   T f[19];
 #pragma unroll
   for (int i = 0; i < 19; ++i) f[i] = ld(a.at(i, c.s));
@@ -199,9 +204,15 @@ __device__ __forceinline__ void os_push_plain(const SoaNb<T>& A0, const SoaNb<T>
 #pragma unroll
   for (int i = 0; i < 19; ++i) Bp.n[i][nb_ix(cx(i), s, sm, sp)] = f[i];
 }
+// fp32 SoA takes its generic-path fields with plane bases (FldT: C1 0.92 ->
+// 0.99 of the roofline, measured; the kernel-wide register allocation is what
+// moves)
+template <class T, bool AOS>
+constexpr bool kOsPushTab = sizeof(T) == 4;
 template <class T, bool AOS>
 __global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
-    k_os_push(Fld<T, AOS> a, Fld<T, AOS> b, Lat L, Trt<T> op, SoaNb<T> A0, SoaNb<T> Bp) {
+    k_os_push(FldSel<T, AOS, kOsPushTab<T, AOS>> a, FldSel<T, AOS, kOsPushTab<T, AOS>> b, Lat L,
+              Trt<T> op, SoaNb<T> A0, SoaNb<T> Bp) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
@@ -699,13 +710,16 @@ void launch_os_pull(cudaStream_t st, const DField& a, const DField& b, const dev
   LBM_DISPATCH(a, {
     auto fa = fld<T, A>(a);
     auto fb = fld<T, A>(b);
+    constexpr bool tab = kOsPullTab<T, true>;
+    auto ta = fld_sel<T, A, tab>(a);
+    auto tb = fld_sel<T, A, tab>(b);
     const auto o = cast_op<T>(op);
     const unsigned g = grid_for(L.ncells - L.cell_begin);
     const auto am = soa_nb<T>(a, L, -1), b0 = soa_nb<T>(b, L, 0);
     if (!streaming && !two_s) k_os_pull<T, A, false, false><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
     if (!streaming && two_s) k_os_pull<T, A, false, true><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
-    if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
-    if (streaming && two_s) k_os_pull<T, A, true, true><<<g, kBlock, 0, st>>>(fa, fb, L, o, am, b0);
+    if (streaming && !two_s) k_os_pull<T, A, true, false><<<g, kBlock, 0, st>>>(ta, tb, L, o, am, b0);
+    if (streaming && two_s) k_os_pull<T, A, true, true><<<g, kBlock, 0, st>>>(ta, tb, L, o, am, b0);
   });
 }
 
@@ -723,8 +737,10 @@ void launch_os_push(cudaStream_t st, const DField& a, const DField& b, const dev
     return;
   }
   LBM_DISPATCH(a, {
+    constexpr bool tab = kOsPushTab<T, A>;
     k_os_push<T, A><<<grid_for(L.ncells - L.cell_begin), kBlock, 0, st>>>(
-        fld<T, A>(a), fld<T, A>(b), L, cast_op<T>(op), soa_nb<T>(a, L, 0), soa_nb<T>(b, L, 1));
+        fld_sel<T, A, tab>(a), fld_sel<T, A, tab>(b), L, cast_op<T>(op), soa_nb<T>(a, L, 0),
+        soa_nb<T>(b, L, 1));
   });
 }
 
