@@ -395,17 +395,27 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_swap(Fld<T, AOS
   if (cell >= L.ncells) return;
   const Ctx c = make_ctx(L, cell);
   if (!c.fluid) return;
+  // all 18 loads before any store: the compiler cannot prove the nine pairs
+  // disjoint, so load / store / load order would serialise nine round trips
+  uint32_t use = 0;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     const int i = back_dir(k);
     if (c.bb(i)) continue;
     const bool w = c.wrapped(L, i);
     if ((mode == 1 && w) || (mode == 2 && !w)) continue;
-    T* a = F.at(i, c.s);
-    T* b = F.at(opp(i), c.nb(i));
-    const T va = ld(a), vb = ld(b);
-    st<false>(a, vb);
-    st<false>(b, va);
+    use |= 1u << k;
+  }
+  T va[9], vb[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int i = back_dir(k);
+    if (use & (1u << k)) va[k] = ld(F.at(i, c.s)), vb[k] = ld(F.at(opp(i), c.nb(i)));
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int i = back_dir(k);
+    if (use & (1u << k)) st<false>(F.at(i, c.s), vb[k]), st<false>(F.at(opp(i), c.nb(i)), va[k]);
   }
 }
 

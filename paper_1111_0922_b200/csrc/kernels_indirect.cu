@@ -277,16 +277,21 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, A
 // non-bounce back-half link swaps (i, n) <-> (opp i, adj[i][n]).
 template <class T, bool AOS>
 __device__ __forceinline__ void swap_idx_node(const Fld<T, AOS>& F, const Idx& I, uint32_t node) {
+  // all loads before any store (the pairs are disjoint, which the compiler
+  // cannot prove: load / store / load order serialises nine round trips)
+  uint32_t nb[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) nb[k] = ldidx(I.adj + (size_t)(back_dir(k) - 1) * I.n + node);
+  T va[9], vb[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     const int i = back_dir(k);
-    const uint32_t nb = ldidx(I.adj + (size_t)(i - 1) * I.n + node);
-    if (nb == node) continue;
-    T* a = F.at(i, node);
-    T* b = F.at(opp(i), nb);
-    const T va = ld(a), vb = ld(b);
-    st<false>(a, vb);
-    st<false>(b, va);
+    if (nb[k] != node) va[k] = ld(F.at(i, node)), vb[k] = ld(F.at(opp(i), nb[k]));
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int i = back_dir(k);
+    if (nb[k] != node) st<false>(F.at(i, node), vb[k]), st<false>(F.at(opp(i), nb[k]), va[k]);
   }
 }
 template <class T, bool AOS>
