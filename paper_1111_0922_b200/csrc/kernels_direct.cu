@@ -631,6 +631,7 @@ __global__ void k_plane_copy(Fld<T, AOS> F, Lat L, int8_t d0, int8_t d1, int8_t 
   if (k >= plane) return;
   const int x = (int)(k % L.nx), y = (int)(k / L.nx);
   const int8_t d[5] = {d0, d1, d2, d3, d4};
+  uint32_t use = 0;
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
     int xw = x - cx(d[q]), yw = y - cy(d[q]);
@@ -646,8 +647,16 @@ __global__ void k_plane_copy(Fld<T, AOS> F, Lat L, int8_t d0, int8_t d1, int8_t 
       const uint32_t lm = L.linkmask[(uint32_t)xw + (uint32_t)L.nx * ((uint32_t)yw + (uint32_t)L.ny * writer_z)];
       if (!(lm & 1u) || ((lm >> d[q]) & 1u)) continue;
     }
-    *F.at(d[q], dst + k) = *F.at(d[q], src + k);
+    use |= 1u << q;
   }
+  // five loads, then five stores (the planes are distinct; see k_swap)
+  T v[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+    if (use & (1u << q)) v[q] = *F.at(d[q], src + k);
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+    if (use & (1u << q)) *F.at(d[q], dst + k) = v[q];
 }
 
 }  // namespace
