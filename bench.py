@@ -205,6 +205,10 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if ws > 1:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; the lone reference rank
+        # takes every host core (read when the reference's OpenMP starts)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cfg = CONFIGS[args.config]
     if cfg.get("porous"):
         args.addressing = "indirect"
