@@ -595,7 +595,7 @@ __device__ __forceinline__ void cg_push_plain(const SoaNb<T>& T0, const SoaNb<T>
   for (int i = 0; i < 19; ++i) Tp.n[i][nb_ix(cx(i), w, wm, wp)] = f[i];
 }
 template <class T, bool AOS, bool RAW>
-__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
+__global__ void __launch_bounds__(kBlock, CgMinBlocks<T, AOS>::value)
     k_cg_push(Fld<T, AOS> F, Lat L, Trt<T> op, int delta, SoaNb<T> T0, SoaNb<T> Tp) {
   // the first group of a sweep reads what the previous sweep and its seam
   // copies wrote: wait before the loads, and only then let the next group

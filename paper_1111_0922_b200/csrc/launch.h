@@ -66,7 +66,10 @@ struct MinBlocks {
 #define LBM_OS_MIN_BLOCKS_F32 5
 #endif
 #ifndef LBM_ET_MIN_BLOCKS_F32
-#define LBM_ET_MIN_BLOCKS_F32 5
+#define LBM_ET_MIN_BLOCKS_F32 6
+#endif
+#ifndef LBM_CG_MIN_BLOCKS_F32
+#define LBM_CG_MIN_BLOCKS_F32 5
 #endif
 template <class T, bool AOS>
 struct SoaMinBlocks {
@@ -77,6 +80,11 @@ template <class T, bool AOS>
 struct OsMinBlocks {
   static constexpr int value =
       sizeof(T) == 4 && !AOS ? LBM_OS_MIN_BLOCKS_F32 : SoaMinBlocks<T, AOS>::value;
+};
+template <class T, bool AOS>
+struct CgMinBlocks {
+  static constexpr int value =
+      sizeof(T) == 4 && !AOS ? LBM_CG_MIN_BLOCKS_F32 : SoaMinBlocks<T, AOS>::value;
 };
 template <class T, bool AOS = false>
 struct EtMinBlocks {
