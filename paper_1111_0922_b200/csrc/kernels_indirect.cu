@@ -267,7 +267,7 @@ __device__ __forceinline__ void et_idx_node(const Fld<T, AOS>& F, const Idx& I, 
   }
 }
 template <class T, bool AOS, bool SW>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
+__global__ void __launch_bounds__(kBlock, EtMinBlocks<T, AOS>::value) k_et_idx(Fld<T, AOS> F, Idx I, Trt<T> op) {
   const uint32_t node = I.first + blockIdx.x * kBlock + threadIdx.x;
   if (node >= I.end()) return;
   et_idx_node<T, AOS, SW>(F, I, op, node);
