@@ -4,12 +4,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A "step" is one LBM time step (one collide+propagate sweep of the whole
-lattice). At N=1 the workload is BASELINE.json configs[1] ("C1"): a 256^3
-channel, periodic in x/y, half-way bounce-back walls at z=0/255, BGK
-omega=1.7, body force 1e-6 along x, rest start, AA pattern, direct
-addressing, SoA, fp64. value = fluid nodes x K / device time (MFLUP/s).
-Under torchrun (N>1) the box of BASELINE.json configs[3] is split into
-z-slabs, one per rank.
+lattice). The workload at every N is BASELINE.json configs[3] ("C3", the
+config its 1/2/4/8-GPU metric is quoted on): a 512x512x1024 periodic box,
+BGK omega=1.0, seeded Taylor-Green start, AA pattern, direct addressing, SoA,
+fp64 (40.8 GB; it fits one B200). N=1 runs the single-domain stepper; under
+torchrun (N>1) the box is split into z-slabs, one per rank (DESIGN.md
+section 6). Strong scaling: the box is fixed. value = fluid nodes x K / device
+time (MFLUP/s), max over ranks. `--gpus N` outside torchrun relaunches itself
+under torch.distributed.run with N ranks.
 
 Prints ONE JSON line (rank 0). See DESIGN.md section 7 for every key.
 """
@@ -50,6 +52,29 @@ CONFIGS = {
                force=(0.0, 0.0, 0.0), init="taylor_green",
                desc="C3: 512x512x1024 periodic, BGK omega=1.0, Taylor-Green, z-slabs"),
 }
+
+
+def config_dict(name, args, ws, nodes):
+    """The `config` object, identical in both arms for the same invocation."""
+    cfg = CONFIGS[name]
+    pdf = 8 if args.precision == 8 else 4
+    field = nodes * 19 * pdf * (1 if args.scheme in ("aap", "et", "cg", "swap-push", "swap-pull")
+                                else 2)
+    return {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
+            "layout": args.layout, "precision": "f64" if pdf == 8 else "f32",
+            "dims": list(cfg["dims"]), "fluid_nodes": int(nodes),
+            "parallelism": "single domain" if ws == 1 else f"z-slabs x{ws}",
+            "l2": f"inputs larger than L2 ({field / 1e9:.2f} GB of PDFs vs 126 MB L2), "
+                  "no flush needed"}
+
+
+def fluid_nodes(name):
+    cfg = CONFIGS[name]
+    nx, ny, nz = cfg["dims"]
+    if cfg.get("porous"):
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        return gen_random_spheres(nx, ny, nz).fluid_count()
+    return nx * ny * nz
 
 
 def load_peaks():
@@ -210,31 +235,46 @@ def run_reference_arm(args):
         # takes every host core (read when the reference's OpenMP starts)
         os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cfg = CONFIGS[args.config]
-    if cfg.get("porous"):
-        args.addressing = "indirect"
+    n_gpus = max(ws, args.gpus)
     budget = float(os.environ.get("LBM_REF_BUDGET_S", "90"))
     base = cpu_reference_sample(cfg, args.scheme, budget_s=budget, max_steps=args.steps)
+    nodes = fluid_nodes(args.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "MFLUP/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (rest start, BASELINE.json config)",
-        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
-                   "layout": "soa", "dims": list(cfg["dims"])},
+        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": nodes / (base["value"] * 1e6) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json config; seeded start)",
+        "config": config_dict(args.config, args, n_gpus, nodes),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    nodes = cfg["dims"][0] * cfg["dims"][1] * cfg["dims"][2]
-    if cfg.get("porous"):
-        from paper_1111_0922_b200.geometry import gen_random_spheres
-        nodes = gen_random_spheres(*cfg["dims"]).fluid_count()
-    line["ms_per_step"] = nodes / (base["value"] * 1e6) * 1e3
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
+def live_peaks(L, device, field_bytes):
+    """In-place and copy streaming probes on this GPU (lbmgpu_stream_bandwidth),
+    over 4 GiB (or the field size if smaller), best of 10: the second
+    denominator beside MEASURED_PEAKS.json (whose copy is torch's)."""
+    nb = int(min(4 << 30, max(1 << 28, field_bytes)))
+    return {"inplace_gbs": round(L.stream_bandwidth(nb, True, 10, device), 1),
+            "copy_gbs": round(L.stream_bandwidth(nb, False, 10, device), 1),
+            "bytes": nb, "how": "lbmgpu_stream_bandwidth: 16-B vector grid-stride kernel, "
+                                "read+write bytes, best of 10, CUDA events"}
+
+
+def make_geometry(L, name, args):
+    cfg = CONFIGS[name]
+    if cfg.get("porous"):
+        from paper_1111_0922_b200.geometry import gen_random_spheres
+        args.addressing = "indirect"
+        return gen_random_spheres(*cfg["dims"])
+    return L.GridGeometry(*cfg["dims"], cfg["policy"])
+
+
 def run_ours(args):
     ws, rank, local, dist = dist_setup()
     import paper_1111_0922_b200 as L
@@ -245,12 +285,7 @@ def run_ours(args):
 
     cfg = CONFIGS[args.config]
     dims = cfg["dims"]
-    if cfg.get("porous"):
-        from paper_1111_0922_b200.geometry import gen_random_spheres
-        geo = gen_random_spheres(*dims)
-        args.addressing = "indirect"
-    else:
-        geo = L.GridGeometry(*dims, cfg["policy"])
+    geo = make_geometry(L, args.config, args)
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
     opts = L.StepperOptions(layout=args.layout, precision=args.precision, device=local,
                             extensions=args.scheme in ("ts", "swap-push", "swap-pull")
@@ -280,24 +315,25 @@ def run_ours(args):
             "os-push": "k_os_push", "osnt-pull-1s": "k_os_pull", "osnt-pull-2s": "k_os_pull",
             "cg": "k_cg", "ts": "k_local+k_ts_stream", "swap-push": "k_local+k_swap",
             "swap-pull": "k_swap+k_local"}[args.scheme]
-    tr = traffic_from_profiles(f"{args.config}:{args.scheme}:{args.addressing}:{args.layout}:{pdf}")
+    key = f"{args.config}:{args.scheme}:{args.addressing}:{args.layout}:{pdf}"
+    live = live_peaks(L, local, st.storage_bytes()[0]) if not args.no_live_peak else None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": tr,
-                "algorithmic_bytes_per_flup": bpl, "kernel": kern,
+                "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(key),
+                "traffic_key": key, "algorithmic_bytes_per_flup": bpl,
+                "algorithmic_bytes_per_launch": bpl * nodes / launches, "kernel": kern,
                 "per_launch_ms": round(per_launch_ms, 5), "peak_source": peak_src,
                 "model_mflups": round(peak * 1e9 / bpl / 1e6, 1)}
+    if live:
+        roofline["live_peak"] = live
+        roofline["frac_vs_live_inplace"] = round(achieved / live["inplace_gbs"], 4)
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MFLUP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if pdf == 8 else "f32",
-        "data": "synthetic (BASELINE.json config; seeded device-side init)",
-        "config": {"workload": cfg["desc"], "scheme": args.scheme,
-                   "addressing": args.addressing, "layout": args.layout,
-                   "dims": list(dims), "fluid_nodes": nodes,
-                   "l2": f"inputs larger than L2 ({st.storage_bytes()[0] / 1e9:.2f} GB field "
-                         f"vs 126 MB L2), no flush needed"},
+        "data": "synthetic (BASELINE.json config; seeded start)",
+        "config": config_dict(args.config, args, 1, nodes),
         "roofline": roofline,
         "gpu_launches": args.steps * launches,
         "clocks": clk.summary(),
@@ -317,18 +353,19 @@ def run_ours(args):
 
 def e2e_run(L, st, args, nodes):
     """Same metric through the public API with HOST buffers: load the canonical
-    snapshot from pinned host memory, K steps, extract it back to pinned host
-    memory, all inside the timed region (wall clock around synchronous calls)."""
+    snapshot from pinned host memory, K steps, extract it back into the same
+    pinned buffer, all inside the timed region (wall clock around synchronous
+    calls). One pinned buffer (C3: 40.8 GB)."""
     n = nodes * 19
-    src = L.PinnedArray(n)
-    st.extract_natural(src.array)  # a valid state to start from
-    dst = L.PinnedArray(n)
+    buf = L.PinnedArray(n)
+    st.extract_natural(buf.array)  # a valid state to start from
     st.synchronize()
     t0 = time.perf_counter()
-    st.load_natural(src.array)
+    st.load_natural(buf.array)
     st.step_n(args.steps)
-    st.extract_natural(dst.array)
+    st.extract_natural(buf.array)
     t = time.perf_counter() - t0
+    del buf
     return {"value": round(nodes * args.steps / t / 1e6, 2), "unit": "MFLUP/s",
             "h2d_bytes_per_step": n * 8 / args.steps, "d2h_bytes_per_step": n * 8 / args.steps,
             "seconds": round(t, 4),
@@ -336,24 +373,24 @@ def e2e_run(L, st, args, nodes):
 
 
 def run_slabs(args, ws, rank, local, dist, L):
-    """BASELINE.json configs[3]: the box is split into ws z-slabs, one per rank
-    (GPU); AA pattern with the NCCL halo exchange of the 5 crossing slot planes
-    per face before and after every odd sweep, overlapped with the interior
-    planes. Strong scaling: the whole box is fixed."""
+    """BASELINE.json configs[3] over z-slabs: the box is split into ws slabs, one
+    per rank (GPU); AA pattern with the NCCL halo exchange of the 5 crossing slot
+    planes per face before and after every odd sweep, overlapped with the
+    interior planes. Strong scaling: the whole box is fixed."""
     cfg = CONFIGS[args.config]
     nx, ny, nz = cfg["dims"]
     if nz % ws:
         raise SystemExit(f"nz={nz} not divisible by {ws} ranks")
+    if args.layout != "soa":
+        raise SystemExit("z-slabs are SoA only (--layout soa)")
     z0, z1 = rank * nz // ws, (rank + 1) * nz // ws
-    if cfg.get("porous"):
-        from paper_1111_0922_b200.geometry import gen_random_spheres
-        geo = gen_random_spheres(nx, ny, nz)
-        args.addressing = "indirect"
-    else:
-        geo = L.GridGeometry(nx, ny, nz, cfg["policy"])
+    geo = make_geometry(L, args.config, args)
     flow = L.bgk(cfg["omega"], body_force=cfg["force"])
+    pdf = 8 if args.precision == 8 else 4
     st = L.create_stepper(args.scheme, args.addressing, geo, flow,
-                          L.StepperOptions(device=local, z_begin=z0, z_end=z1))
+                          L.StepperOptions(device=local, z_begin=z0, z_end=z1,
+                                           precision=args.precision, layout=args.layout))
+    comm = None
     if args.transport == "p2p":
         # peer-memory AA: face planes read/rewrite the neighbours' slots in
         # place (CUDA IPC pointers), steps ordered by flag words; no NCCL
@@ -363,11 +400,13 @@ def run_slabs(args, ws, rank, local, dist, L):
             dist.all_gather_object(blobs, st.slab_p2p_export())
         st.slab_p2p_connect(blobs[(rank - 1) % ws], blobs[(rank + 1) % ws], ws, rank)
         barrier(dist)
+        comm = {"transport": "p2p (CUDA IPC peer pointers, flag words)"}
     else:
         uid = [L.nccl_unique_id() if rank == 0 else None]
         if dist is not None:
             dist.broadcast_object_list(uid, src=0)
         st.slab_connect_nccl(uid[0], ws, rank)
+        comm = dict(st.slab_comm_info(), transport="nccl (halo send/recv, comm stream)")
     st.init_field(cfg["init"], seed=2011)
     nodes_local = st.node_count()
     nodes = int(reduce_sum(dist, nodes_local))
@@ -379,26 +418,26 @@ def run_slabs(args, ws, rank, local, dist, L):
     ms = reduce_max(dist, ms_local)
     value = nodes * args.steps / (ms * 1e-3) / 1e6
     peak, peak_src = load_peaks()
-    bpl = L.gpu_bytes_per_lup(args.scheme, args.addressing, 8)
+    bpl = L.gpu_bytes_per_lup(args.scheme, args.addressing, pdf)
     achieved = bpl * nodes_local / (ms / args.steps * 1e-3) / 1e9
     launches = st.launches_per_step()
-    halo = 2 * 2 * 5 * nx * ny * 8  # bytes per rank per exchange (all-fluid planes)
+    halo = 2 * 2 * 5 * nx * ny * pdf  # bytes per rank per exchange (all-fluid planes)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MFLUP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE.json configs[3]; seeded device-side Taylor-Green init)",
-        "config": {"workload": cfg["desc"], "scheme": args.scheme, "addressing": args.addressing,
-                   "layout": "soa", "dims": [nx, ny, nz], "fluid_nodes": nodes,
-                   "parallelism": (f"z-slabs x{ws} (NCCL halo, 5 slot planes/face)"
-                                   if args.transport == "nccl" else
-                                   f"z-slabs x{ws} (p2p: face sweeps on peer memory)"),
-                   "l2": "inputs larger than L2, no flush needed"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if pdf == 8 else "f32",
+        "data": "synthetic (BASELINE.json config; seeded start)",
+        "config": config_dict(args.config, args, ws, nodes),
+        "comm": comm,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "algorithmic_bytes_per_flup": bpl, "kernel": f"{args.scheme} sweep (per rank)",
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic_from_profiles(
+                         f"{args.config}:{args.scheme}:{args.addressing}:{args.layout}:{pdf}"),
+                     "algorithmic_bytes_per_flup": bpl,
+                     "kernel": f"{args.scheme} sweep (per rank, slowest rank's step)",
                      "peak_source": peak_src,
-                     "halo_bytes_per_odd_step_per_rank": halo},
+                     "halo_bytes_per_exchange_per_rank": halo},
         "gpu_launches": args.steps * launches,
         "clocks": clk.summary(),
     }
@@ -435,20 +474,38 @@ def e2e_slabs(L, st, args, dist, nodes_local, nodes):
                     "extract_natural(pinned host); bytes are whole-job"}
 
 
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n):
+    """`--gpus N` (N > 1) outside torchrun: re-exec this command with N ranks,
+    exactly as the driver launches it."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, LBM_BENCH_RELAUNCHED="1")
+    os.execvpe(cmd[0], cmd, env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
-                    help="default: c1 at N=1, c3 (z-slabs) at N>1")
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default c3, the metric's config, at every N)")
     ap.add_argument("--scheme", default="aap")
     ap.add_argument("--addressing", default="direct")
     ap.add_argument("--layout", default="soa")
     ap.add_argument("--precision", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-live-peak", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="z-slab exchange: NCCL halo phases, or p2p (AA direct: face planes "
                          "read and rewrite the neighbours' slots through peer pointers)")
@@ -457,10 +514,25 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.config is None:
-        args.config = "c1" if int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.slabs else "c3"
+    if CONFIGS[args.config].get("porous"):
+        args.addressing = "indirect"
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference_arm(args)
+    if ws == 0 and args.gpus > 1:
+        if os.environ.get("LBM_BENCH_RELAUNCHED"):
+            raise SystemExit("relaunch under torch.distributed.run did not set WORLD_SIZE")
+        relaunch_under_torchrun(args.gpus)
+    if ws > 0 and ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: refusing to report a "
+                         "different GPU count than requested")
+    if os.environ.get("LBM_BENCH_DRYRUN"):
+        # launch check only (tests/test_bench_contract.py): report the rank layout
+        print(json.dumps({"dryrun": True, "rank": int(os.environ.get("RANK", "0")),
+                          "world_size": max(ws, 1), "gpus": args.gpus}), flush=True)
+        return 0
     return run_ours(args)
 
 

@@ -190,6 +190,12 @@ int lbmgpu_verify_suite(uint64_t seed, int32_t steps, int32_t device, int32_t al
  * patterns, collision-like ranges, signed zeros, denormals, infinities,
  * NaNs); *mismatches = results whose bit patterns differ. */
 int lbmgpu_selftest_division(uint64_t n, uint64_t seed, int32_t device, uint64_t* mismatches);
+/* HBM streaming probe: best of `reps` launches of a 16-byte-vector copy over
+ * `bytes` (inplace = 0) or an in-place read-modify-write of one buffer
+ * (inplace = 1, the AA/ET/OS sweeps' pattern); GB/s counts read + write bytes.
+ * bench.py reports it beside MEASURED_PEAKS.json as a second denominator. */
+int lbmgpu_stream_bandwidth(int32_t device, uint64_t bytes, int32_t inplace, int32_t reps,
+                            double* gbps);
 
 /* kernel_available (p/src/stepper.cpp:140-153): 10 direct + 6 indirect */
 int lbmgpu_kernel_available(int32_t scheme, int32_t addressing);
@@ -236,6 +242,9 @@ int lbmgpu_scheme_halo_plan(int32_t scheme, int32_t nzl, int32_t* ops, int32_t* 
 int lbmgpu_nccl_unique_id(uint8_t* id);
 /* one rank per GPU: ring over ranks, rank r owns the r-th slab; collective */
 int lbmgpu_slab_connect_nccl(lbmgpu_stepper* h, const uint8_t* id, int32_t nranks, int32_t rank);
+/* the slab's communicator as NCCL reports it: ncclCommCount, ncclCommUserRank,
+ * ncclGetVersion (evidence of the N-rank ring in bench output) */
+int lbmgpu_slab_comm_info(lbmgpu_stepper* h, int32_t* count, int32_t* rank, int32_t* version);
 /* ghosts <- owners (phase 0), needed before extract_natural at odd t; collective */
 int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h);
 /* several slabs in ONE process (any devices): step them in lockstep, the

@@ -88,6 +88,9 @@ class Oracle:
         L.orc_random_field.argtypes = [C.c_uint64, C.c_size_t, C.c_double, _f64p]
         L.orc_stencil.argtypes = [_i32p, _f64p, _i32p]
         L.orc_flops_per_update.restype = C.c_int
+        L.orc_init_field.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, _f64p]
 
     # -- physics -------------------------------------------------------------
     def stencil(self):
@@ -135,6 +138,22 @@ class Oracle:
         rem = np.zeros(n * 9, np.uint32)
         nmail = self.L.orc_et_rem(n, np.ascontiguousarray(adjacency, np.uint32).ravel(), rem)
         return rem.reshape(n, 9), int(nmail)
+
+    def init_field(self, kind, dims, policy=(0, 0, 0), mask=None, seed=0, rho0=1.0,
+                   u0=0.01, drho=1e-3, noise=1e-4, gdims=None, z0=0):
+        """Canonical start snapshot of the BASELINE configs (lbm_oracle.c
+        orc_init_field): kind 'rest' | 'taylor_green' | 'random'; gdims/z0
+        place a z-slab inside a global box."""
+        k = {"rest": 0, "taylor_green": 1, "random": 2}[kind]
+        nx, ny, nz = dims
+        gnx, gny, gnz = gdims or dims
+        g = _geom(nx, ny, nz, policy, mask)
+        n = int(self.L.orc_fluid_count(C.byref(g)))
+        out = np.empty(n * 19)
+        if self.L.orc_init_field(C.byref(g), k, gnx, gny, gnz, z0, seed, rho0, u0, drho, noise,
+                                 out) != 0:
+            raise MemoryError("oracle allocation failed")
+        return out
 
     def make_seeded_geometry(self, seed):
         mask = np.zeros(16 * 8 * 8, np.uint8)

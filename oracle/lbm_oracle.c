@@ -6,6 +6,7 @@
  */
 #include "lbm_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -381,4 +382,81 @@ void orc_random_field(uint64_t seed, size_t nodes, double scale, double* f) {
       const double u = (double)(orc_mt64_next(&r) >> 11) * 0x1.0p-53;
       f[n * 19 + i] = weight(i) * scale * (0.9 + 0.2 * u);
     }
+}
+
+/* Seeded initial fields of the BASELINE configs: the
+ * definition the product's device init (paper_1111_0922_b200/csrc/
+ * kernels_util.cu node_values) implements, restated here so both sides can be
+ * checked bit for bit and so the reference can be started from the same
+ * snapshot.
+ *   U(stream)  = splitmix64(seed + 0x9e3779b97f4a7c15 * (stream + 1)),
+ *                (z >> 11) * 2^-52 - 1  in [-1, 1)
+ *   stream     = 20 * global_cell + k, global_cell = x + gnx (y + gny (z + z0))
+ *   rest       f_i = w_i rho0                           (p/src/scheme_aap.cpp:32-36)
+ *   taylor     rho = rho0 + drho U(.., 19), u = u0 (sin X cos Y cos Z,
+ *              -cos X sin Y cos Z, 0), X = (2 pi) x / gnx (libm sin / cos),
+ *              f_i = equilibrium(rho, u, i) + noise U(.., i)  (p/src/collision.cpp:38-45)
+ *   random     f_i = w_i rho0 (0.9 + 0.2 (U(.., i) + 1) / 2)
+ * Fluid nodes only, x-fastest (the canonical snapshot order, p/include/lbmlab/
+ * stepper.hpp:66-69). */
+static uint64_t splitmix_bits(uint64_t seed, uint64_t stream) {
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+#define ORC_TWO_PI 6.283185307179586476925286766559 /* 2 pi, rounded once */
+static double urand_pm1(uint64_t seed, uint64_t stream) {
+  return (double)(splitmix_bits(seed, stream) >> 11) * 0x1.0p-52 - 1.0;
+}
+
+void orc_trig_table(int n, double* s, double* c) {
+  for (int x = 0; x < n; ++x) {
+    const double a = ORC_TWO_PI * (double)x / (double)n;
+    s[x] = sin(a);
+    c[x] = cos(a);
+  }
+}
+
+int orc_init_field(const orc_geometry* g, int kind, int gnx, int gny, int gnz, int z0,
+                   uint64_t seed, double rho0, double u0, double drho, double noise,
+                   double* out) {
+  double *sx = NULL, *cx = NULL, *sy = NULL, *cy = NULL, *sz = NULL, *cz = NULL;
+  if (kind == 1) {
+    sx = malloc(sizeof(double) * (size_t)(2 * (gnx + gny + gnz)));
+    if (!sx) return -1;
+    cx = sx + gnx;
+    sy = cx + gnx;
+    cy = sy + gny;
+    sz = cy + gny;
+    cz = sz + gnz;
+    orc_trig_table(gnx, sx, cx);
+    orc_trig_table(gny, sy, cy);
+    orc_trig_table(gnz, sz, cz);
+  }
+  size_t n = 0;
+  for (int z = 0; z < g->nz; ++z)
+    for (int y = 0; y < g->ny; ++y)
+      for (int x = 0; x < g->nx; ++x) {
+        if (!is_fluid(g, gidx(g, x, y, z))) continue;
+        const int gz = z + z0;
+        const uint64_t gcell = (uint64_t)x + (uint64_t)gnx * ((uint64_t)y + (uint64_t)gny * gz);
+        double* f = out + n * 19;
+        ++n;
+        if (kind == 0) {
+          for (int i = 0; i < 19; ++i) f[i] = weight(i) * rho0;
+        } else if (kind == 2) {
+          for (int i = 0; i < 19; ++i) {
+            const double u01 = 0.5 * (urand_pm1(seed, gcell * 20 + i) + 1.0);
+            f[i] = weight(i) * rho0 * (0.9 + 0.2 * u01);
+          }
+        } else {
+          const double rho = rho0 + drho * urand_pm1(seed, gcell * 20 + 19);
+          const double u[3] = {u0 * sx[x] * cy[y] * cz[gz], -u0 * cx[x] * sy[y] * cz[gz], 0.0};
+          for (int i = 0; i < 19; ++i)
+            f[i] = orc_equilibrium(rho, u, i) + noise * urand_pm1(seed, gcell * 20 + i);
+        }
+      }
+  free(sx);
+  return 0;
 }

@@ -58,6 +58,12 @@ uint64_t orc_mt64_next(orc_mt64* s);
 void orc_make_seeded_geometry(uint64_t seed, uint8_t* mask /*1024*/, uint8_t* policy /*3*/);
 void orc_random_field(uint64_t seed, size_t nodes, double scale, double* f);
 
+/* seeded initial fields (kind 0 rest, 1 Taylor-Green, 2 random); see lbm_oracle.c */
+void orc_trig_table(int n, double* s, double* c);
+int orc_init_field(const orc_geometry* g, int kind, int gnx, int gny, int gnz, int z0,
+                   uint64_t seed, double rho0, double u0, double drho, double noise,
+                   double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,8 @@ _sig = {
     "lbmgpu_nccl_unique_id": (C.c_int, [_P]),
     "lbmgpu_slab_connect_nccl": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
     "lbmgpu_slab_sync_ghosts": (C.c_int, [_P]),
+    "lbmgpu_slab_comm_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int32)]),
     "lbmgpu_slab_group_step": (C.c_int, [_P, C.c_int32, C.c_int64]),
     "lbmgpu_slab_group_sync_ghosts": (C.c_int, [_P, C.c_int32]),
     "lbmgpu_slab_group_connect_p2p": (C.c_int, [_P, C.c_int32]),
@@ -118,6 +120,8 @@ _sig = {
     "lbmgpu_host_free": (C.c_int, [_P]),
     "lbmgpu_run_bench": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
+    "lbmgpu_stream_bandwidth": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                          C.POINTER(C.c_double)]),
     "lbmgpu_selftest_division": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int32,
                                            C.POINTER(C.c_uint64)]),
     "lbmgpu_verify_suite": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32,
@@ -361,6 +365,12 @@ class Stepper:
     def slab_sync_ghosts(self) -> None:
         _check(_L.lbmgpu_slab_sync_ghosts(self._h))
 
+    def slab_comm_info(self) -> dict:
+        """ncclCommCount / ncclCommUserRank / ncclGetVersion of the slab's communicator"""
+        c, r, v = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(_L.lbmgpu_slab_comm_info(self._h, C.byref(c), C.byref(r), C.byref(v)))
+        return {"ncclCommCount": c.value, "ncclCommUserRank": r.value, "ncclGetVersion": v.value}
+
     def slab_p2p_export(self) -> bytes:
         """This slab's peer-memory blob (CUDA IPC handles of its field and flag
         words, its layout) for the neighbours' slab_p2p_connect."""
@@ -484,6 +494,15 @@ class VerifyEntry:
     bitwise: bool
     passed: bool
     max_rel_linf: float
+
+
+def stream_bandwidth(nbytes: int = 4 << 30, inplace: bool = True, reps: int = 10,
+                     device: int = 0) -> float:
+    """GB/s (read + write) of a streaming copy or in-place update over nbytes
+    (lbmgpu_stream_bandwidth): the live roofline denominator of bench.py."""
+    g = C.c_double()
+    _check(_L.lbmgpu_stream_bandwidth(device, nbytes, int(inplace), reps, C.byref(g)))
+    return g.value
 
 
 def selftest_division(n: int = 1 << 26, seed: int = 1, device: int = 0) -> int:

@@ -319,6 +319,13 @@ int lbmgpu_slab_connect_nccl(lbmgpu_stepper* h, const uint8_t* id, int32_t nrank
   });
 }
 
+int lbmgpu_slab_comm_info(lbmgpu_stepper* h, int32_t* count, int32_t* rank, int32_t* version) {
+  return guard([&] {
+    if (!count || !rank || !version) throw std::invalid_argument("null output");
+    slab_comm_info(S(h), count, rank, version);
+  });
+}
+
 int lbmgpu_slab_sync_ghosts(lbmgpu_stepper* h) {
   return guard([&] { slab_sync_ghosts(S(h)); });
 }
@@ -418,6 +425,15 @@ int lbmgpu_run_bench(const lbmgpu_geometry* g, const lbmgpu_flow* p, const lbmgp
 // (optionally also AoS and fp32) against the GPU two-step reference on the
 // seeded geometry, compared after every step; fp64 must be bitwise (1e-13
 // relative is the reference's recorded fallback), fp32 within 1e-5.
+int lbmgpu_stream_bandwidth(int32_t device, uint64_t bytes, int32_t inplace, int32_t reps,
+                            double* gbps) {
+  return guard([&] {
+    if (!gbps) throw std::invalid_argument("null output");
+    CK(cudaSetDevice(device));
+    *gbps = stream_bandwidth(bytes, inplace, reps);
+  });
+}
+
 int lbmgpu_selftest_division(uint64_t n, uint64_t seed, int32_t device, uint64_t* mismatches) {
   return guard([&] {
     CK(cudaSetDevice(device));

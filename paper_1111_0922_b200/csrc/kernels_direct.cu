@@ -605,9 +605,19 @@ __global__ void __launch_bounds__(kBlock, CgMinBlocks<T, AOS>::value)
   if (RAW) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
-  if (cell >= L.ncells) return;
+  // threads without a node still wait for the previous group before they
+  // exit: a grid's completion must imply its predecessor's, or a group with
+  // no fluid cell could finish before the group ahead of it and let the next
+  // group's stores overtake that group's reads
+  if (cell >= L.ncells) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    return;
+  }
   const Ctx c = make_ctx(L, cell);
-  if (!c.fluid) return;
+  if (!c.fluid) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    return;
+  }
   if (!AOS && warp_plain(L, c))
     cg_push_plain(T0, Tp, c, op, delta);
   else if (warp_interior(c))

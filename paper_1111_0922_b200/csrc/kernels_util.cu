@@ -15,7 +15,9 @@
 #include "dispatch.h"
 #include "launch.h"
 
+#include <cmath>
 #include <stdexcept>
+#include <string>
 
 namespace lbmgpu {
 using namespace dev;
@@ -59,7 +61,8 @@ __device__ __forceinline__ double equilibrium(double rho, double ux, double uy, 
 //  Rest:        w_i rho0 (every reference stepper's start, e.g. scheme_aap.cpp:32-36)
 //  TaylorGreen: equilibrium(rho, u) + noise*U, rho = rho0 + drho*U,
 //               u = u0 (sin X cos Y cos Z, -cos X sin Y cos Z, 0),
-//               X = 2 pi x / gnx (cell index x, likewise Y, Z)
+//               X = (2 pi) x / gnx (cell index x, likewise Y, Z); sin/cos
+//               come from the host's libm table (InitSpec::trig)
 //  Random:      w_i rho0 (0.9 + 0.2 U01)  (shape of test_schemes.cpp:29-39)
 // U draws are keyed by the GLOBAL cell index, so z-slabs reproduce the
 // single-domain field exactly.
@@ -81,22 +84,24 @@ __device__ __forceinline__ void node_values(const InitSpec& in, const double* bu
   if (in.source == kSrcRandom) {
 #pragma unroll
     for (int i = 0; i < 19; ++i) {
-      const double u01 = 0.5 * (urand(in.seed, gcell * 20 + i) + 1.0);
+      const double u01 = __dmul_rn(0.5, __dadd_rn(urand(in.seed, gcell * 20 + i), 1.0));
       v[i] = __dmul_rn(__dmul_rn(weight(i), in.rho0), __dadd_rn(0.9, __dmul_rn(0.2, u01)));
     }
     return;
   }
-  double sx, cxv, sy, cyv, sz, czv;
-  sincospi(2.0 * x / in.gnx, &sx, &cxv);
-  sincospi(2.0 * y / in.gny, &sy, &cyv);
-  sincospi(2.0 * gz / in.gnz, &sz, &czv);
-  const double rho = in.rho0 + in.drho * urand(in.seed, gcell * 20 + 19);
-  const double ux = in.u0 * sx * cyv * czv;
-  const double uy = -in.u0 * cxv * sy * czv;
+  const double* tx = in.trig;
+  const double* ty = tx + 2 * in.gnx;
+  const double* tz = ty + 2 * in.gny;
+  const double sx = tx[x], cxv = tx[in.gnx + x];
+  const double sy = ty[y], cyv = ty[in.gny + y];
+  const double czv = tz[in.gnz + gz];
+  const double rho = __dadd_rn(in.rho0, __dmul_rn(in.drho, urand(in.seed, gcell * 20 + 19)));
+  const double ux = __dmul_rn(__dmul_rn(__dmul_rn(in.u0, sx), cyv), czv);
+  const double uy = __dmul_rn(__dmul_rn(__dmul_rn(-in.u0, cxv), sy), czv);
   const double uz = 0.0;
 #pragma unroll
   for (int i = 0; i < 19; ++i)
-    v[i] = equilibrium(rho, ux, uy, uz, i) + in.noise * urand(in.seed, gcell * 20 + i);
+    v[i] = __dadd_rn(equilibrium(rho, ux, uy, uz, i), __dmul_rn(in.noise, urand(in.seed, gcell * 20 + i)));
 }
 
 template <class T, bool AOS>
@@ -509,6 +514,20 @@ void launch_extract(cudaStream_t st, const DField& f, const dev::Lat& L,
   });
 }
 
+// sin/cos of (2 pi) x / n with the host libm, the oracle's orc_trig_table
+// (oracle/lbm_oracle.c) operation for operation
+void taylor_green_table(int gnx, int gny, int gnz, double* out) {
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int n : {gnx, gny, gnz}) {
+    for (int x = 0; x < n; ++x) {
+      const double a = two_pi * (double)x / (double)n;
+      out[x] = std::sin(a);
+      out[n + x] = std::cos(a);
+    }
+    out += 2 * n;
+  }
+}
+
 void launch_load(cudaStream_t st, const DField& f, const dev::Lat& L,
                  const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
                  const double* buf, const InitSpec& init) {
@@ -621,6 +640,77 @@ uint64_t selftest_division(uint64_t n, uint64_t seed) {
   cudaFree(d);
   if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   return h;
+}
+
+// ---- streaming-bandwidth probe (the roofline denominator, measured live) ----
+// copy b <- a, or the sweeps' own in-place pattern a <- f(a) (every 16-byte
+// line read once and written back, like the AA / ET / OS-pull stores over the
+// slots they read). Four independent 16-byte loads per thread in flight.
+namespace {
+__global__ void __launch_bounds__(256) k_bw(const uint4* __restrict__ a, uint4* __restrict__ b,
+                                            size_t n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    uint4 v0 = a[i], v1 = a[i + stride], v2 = a[i + 2 * stride], v3 = a[i + 3 * stride];
+    v0.x += 1u, v1.x += 1u, v2.x += 1u, v3.x += 1u;
+    b[i] = v0, b[i + stride] = v1, b[i + 2 * stride] = v2, b[i + 3 * stride] = v3;
+  }
+  for (; i < n; i += stride) {
+    uint4 v = a[i];
+    v.x += 1u;
+    b[i] = v;
+  }
+}
+}  // namespace
+
+double stream_bandwidth(uint64_t bytes, int inplace, int reps) {
+  const size_t n = bytes / 16;
+  if (n == 0 || reps < 1) throw std::invalid_argument("bandwidth probe needs bytes >= 16, reps >= 1");
+  uint4 *a = nullptr, *b = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto release = [&] {
+    if (a) cudaFree(a);
+    if (b) cudaFree(b);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (st) cudaStreamDestroy(st);
+  };
+  if (cudaMalloc(&a, n * 16) != cudaSuccess ||
+      (!inplace && cudaMalloc(&b, n * 16) != cudaSuccess)) {
+    release();
+    throw std::bad_alloc();
+  }
+  if (inplace) b = nullptr;
+  uint4* dst = inplace ? a : b;
+  auto CK = [&](cudaError_t e) {
+    if (e != cudaSuccess) {
+      release();
+      throw std::runtime_error(std::string("bandwidth probe: ") + cudaGetErrorString(e));
+    }
+  };
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaMemsetAsync(a, 0, n * 16, st));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)sms * 8;  // 8 resident 256-thread blocks per SM
+  float best = 1e30f;
+  for (int r = 0; r < reps + 1; ++r) {  // the first launch is a warm-up
+    CK(cudaEventRecord(e0, st));
+    k_bw<<<grid, 256, 0, st>>>(a, dst, n);
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (r > 0) best = std::min(best, ms);
+  }
+  CK(cudaGetLastError());
+  release();
+  return 2.0 * (double)n * 16.0 / (best * 1e-3) / 1e9;
 }
 
 void launch_fill(cudaStream_t st, const DField& f, long long count, double v) {

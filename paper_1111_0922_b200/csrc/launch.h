@@ -200,7 +200,13 @@ struct InitSpec {
   double u0 = 0.01, drho = 1e-3, noise = 1e-4;
   int gnx = 0, gny = 0, gnz = 0;  // global box for Taylor-Green phase
   int z0 = 0;                     // global z of local plane 0 (slabs)
+  // Taylor-Green phase table on the device: sin/cos of (2 pi) x / gnx for
+  // x < gnx, then y, then z ([sx | cx | sy | cy | sz | cz]), computed on the
+  // host with libm (Stepper::init) so the field equals the oracle's bit for bit
+  const double* trig = nullptr;
 };
+// host side of the table above (runtime.h)
+void taylor_green_table(int gnx, int gny, int gnz, double* out);
 // nodes [n0, n0+count) of the canonical order; buf[(n-n0)*19 + i] (fp64)
 void launch_extract(cudaStream_t st, const DField& f, const dev::Lat& L,
                     const uint32_t* cell_of_node, uint32_t n0, uint32_t count, int mode,
@@ -222,6 +228,8 @@ void launch_slab_merge(cudaStream_t st, Prec prec, void* dst, const void* src, u
                        bool wx, bool wy);
 // mismatches of the shared-reciprocal division against __ddiv_rn (synchronous)
 uint64_t selftest_division(uint64_t n, uint64_t seed);
+// best-of-reps GB/s (read + write bytes) of a 16-byte streaming copy / in-place update
+double stream_bandwidth(uint64_t bytes, int inplace, int reps);
 void launch_fill(cudaStream_t st, const DField& f, long long count, double v);
 
 // ---- geometry / IDX construction -------------------------------------------

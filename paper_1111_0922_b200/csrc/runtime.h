@@ -247,7 +247,12 @@ class Stepper {
     ck_launch();
   }
 
-  void sync() { CK(cudaStreamSynchronize(stream_)); }
+  void sync() {
+    CK(cudaStreamSynchronize(stream_));
+    check_health();
+  }
+  // errors a transport records on the device instead of trapping (z-slab p2p)
+  virtual void check_health() {}
 
   // canonical snapshot <-> storage, in chunks through a device staging buffer;
   // [first, first + count) selects a node range (out holds count*19 values)
@@ -295,14 +300,24 @@ class Stepper {
     sync();
   }
 
-  void init(const InitSpec& spec) {
+  void init(const InitSpec& spec_in) {
     CK(cudaSetDevice(opt_.device));
+    InitSpec spec = spec_in;
+    double* trig = nullptr;
+    if (spec.source == kSrcTaylorGreen) {
+      std::vector<double> tab(2 * ((size_t)spec.gnx + spec.gny + spec.gnz));
+      taylor_green_table(spec.gnx, spec.gny, spec.gnz, tab.data());
+      CK(cudaMalloc(&trig, tab.size() * sizeof(double)));
+      CK(cudaMemcpy(trig, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+      spec.trig = trig;
+    }
     for_chunks([&](uint32_t n0, uint32_t cnt) {
       load_range(n0, cnt, nullptr, spec);
       ck_launch();
     });
     after_load();
     sync();
+    if (trig) CK(cudaFree(trig));
   }
 
   InitSpec base_init(int source) const {
@@ -406,6 +421,7 @@ std::vector<int32_t> scheme_halo_plan(int scheme, int nzl);
 void nccl_unique_id(uint8_t* id);
 void slab_connect_nccl(Stepper& s, const uint8_t* id, int nranks, int rank);
 void slab_sync_ghosts(Stepper& s);
+void slab_comm_info(const Stepper& s, int32_t* count, int32_t* rank, int32_t* version);
 void slab_group_step(const std::vector<Stepper*>& slabs, long long steps);
 void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs);
 // p2p transport (AA direct): in one process over a ring of slabs, or one rank

@@ -130,6 +130,9 @@ struct Nccl {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommCount) commCount = nullptr;
+  decltype(&ncclCommUserRank) commUserRank = nullptr;
+  decltype(&ncclGetVersion) getVersion = nullptr;
   static Nccl& get() {
     static Nccl n;
     if (!n.h) {
@@ -147,6 +150,9 @@ struct Nccl {
       LBM_SYM(groupStart, "ncclGroupStart")
       LBM_SYM(groupEnd, "ncclGroupEnd")
       LBM_SYM(errStr, "ncclGetErrorString")
+      LBM_SYM(commCount, "ncclCommCount")
+      LBM_SYM(commUserRank, "ncclCommUserRank")
+      LBM_SYM(getVersion, "ncclGetVersion")
 #undef LBM_SYM
     }
     return n;
@@ -168,6 +174,12 @@ struct Nccl {
 // t - 1 done" into the neighbours' flag words (st.release.sys) and spins on
 // its own (ld.acquire.sys) while the interior planes run on the main stream.
 // ---------------------------------------------------------------------------
+// mine[0] / mine[1]: step counts published by the lower / upper neighbour;
+// mine[2]: error word. Epochs carry the connect generation in their high bits
+// (see connect_p2p_ipc), so flag words are never reset while a neighbour may
+// already be storing into them. A neighbour silent for 60 s sets the error
+// word and the barrier returns (no __trap: the context stays usable and
+// Stepper::sync reports the failure).
 __global__ void k_slab_flag_barrier(unsigned long long* mine, unsigned long long* to_lo,
                                     unsigned long long* to_hi, unsigned long long epoch) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -182,7 +194,10 @@ __global__ void k_slab_flag_barrier(unsigned long long* mine, unsigned long long
       if (v >= epoch) break;
       __nanosleep(256);
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 60ull * 1000000000ull) __trap();  // a neighbour stopped stepping
+      if (now - t0 > 60ull * 1000000000ull) {  // a neighbour stopped stepping
+        atomicExch(mine + 2, epoch);
+        return;
+      }
     }
   }
 }
@@ -385,9 +400,10 @@ class SlabStepper final : public Stepper {
   void p2p_export(P2PBlob& b) {
     p2p_check();
     CK(cudaSetDevice(opt_.device));
-    if (!flags_.get()) {
-      flags_.alloc(2 * sizeof(unsigned long long));
-      CK(cudaMemset(flags_.get(), 0, 2 * sizeof(unsigned long long)));
+    if (!flags_.get()) {  // zeroed once, before any neighbour can address it
+      flags_.alloc(3 * sizeof(unsigned long long));
+      CK(cudaMemset(flags_.get(), 0, 3 * sizeof(unsigned long long)));
+      CK(cudaDeviceSynchronize());
     }
     std::memset(&b, 0, sizeof(b));
     std::memcpy(b.magic, "LBMP2P1", 8);
@@ -405,8 +421,13 @@ class SlabStepper final : public Stepper {
     ipc_open_.clear();
   }
   // one rank per process: lo / hi = the neighbours' blobs (nranks 1: this
-  // slab's own, opened without IPC). Collective; zeroes the flag words, so
-  // every rank connects before any rank steps.
+  // slab's own, opened without IPC). Collective (every rank connects before
+  // any rank steps), but with no host handshake needed: the flag words are
+  // not reset here. Each connect starts a new generation g (the same on every
+  // rank: connects are collective) and epochs count on from g << 40, so
+  // values a neighbour stored for an earlier generation never satisfy a
+  // barrier of this one, and a neighbour that connected and stepped first
+  // cannot have its stores wiped.
   void connect_p2p_ipc(const P2PBlob& lo, const P2PBlob& hi, int nranks, int rank) {
     p2p_check();
     for (const P2PBlob* b : {&lo, &hi}) {
@@ -452,11 +473,21 @@ class SlabStepper final : public Stepper {
     }
     flag_to_lo_ = glo + 1;  // I am my lower neighbour's upper neighbour
     flag_to_hi_ = ghi + 0;
-    CK(cudaMemset(flags_.get(), 0, 2 * sizeof(unsigned long long)));
     CK(cudaDeviceSynchronize());
-    epoch_ = 0;
+    ++generation_;
+    epoch_ = (unsigned long long)generation_ << 40;
     nranks_ = nranks, rank_ = rank;
     transport_ = kP2PIpc;
+  }
+  void check_health() override {
+    if (transport_ != kP2PIpc || !flags_.get()) return;
+    unsigned long long err = 0;
+    CK(cudaMemcpy(&err, flags_.get<unsigned long long>() + 2, sizeof(err),
+                  cudaMemcpyDeviceToHost));
+    if (err)
+      throw std::runtime_error("p2p slab transport: a neighbour rank stopped stepping "
+                               "(flag barrier timed out after 60 s at epoch " +
+                               std::to_string(err & ((1ull << 40) - 1)) + ")");
   }
   void flag_barrier(cudaStream_t st) {
     ++epoch_;
@@ -523,6 +554,16 @@ class SlabStepper final : public Stepper {
     transport_ = kNccl;
   }
   void set_local(int transport) { transport_ = transport; }
+  // what the communicator itself reports (ncclCommCount / ncclCommUserRank)
+  void comm_info(int32_t* count, int32_t* rank, int32_t* version) const {
+    if (transport_ != kNccl || !nccl_) throw std::invalid_argument("slab has no NCCL communicator");
+    Nccl& N = Nccl::get();
+    int c = 0, r = 0, v = 0;
+    N.check(N.commCount(nccl_, &c), "ncclCommCount");
+    N.check(N.commUserRank(nccl_, &r), "ncclCommUserRank");
+    N.check(N.getVersion(&v), "ncclGetVersion");
+    *count = c, *rank = r, *version = v;
+  }
 
   // the grid an exchange phase applies to: AA its one grid; OS pull the
   // active grid (read by the coming pull); OS push the grid just written
@@ -968,6 +1009,7 @@ class SlabStepper final : public Stepper {
   unsigned long long* flag_to_lo_ = nullptr;
   unsigned long long* flag_to_hi_ = nullptr;
   unsigned long long epoch_ = 0;
+  int generation_ = 0;  // p2p connects so far (collective, so equal on every rank)
   std::vector<void*> ipc_open_;
 };
 
@@ -1160,6 +1202,12 @@ void slab_connect_nccl(Stepper& s, const uint8_t* id, int nranks, int rank) {
 }
 
 void slab_sync_ghosts(Stepper& s) { as_slab(s).sync_ghosts_nccl(); }
+
+void slab_comm_info(const Stepper& s, int32_t* count, int32_t* rank, int32_t* version) {
+  auto* sl = dynamic_cast<const SlabStepper*>(&s);
+  if (!sl) throw std::invalid_argument("not a z-slab stepper");
+  sl->comm_info(count, rank, version);
+}
 
 void slab_group_step(const std::vector<Stepper*>& slabs, long long steps) {
   std::vector<SlabStepper*> S;

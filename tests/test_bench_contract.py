@@ -40,6 +40,7 @@ def test_reference_arm_prints_one_contract_line():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("C0")
+    assert d["scaling"] == "strong"
 
 
 def test_reference_arm_other_ranks_exit_silently():
@@ -47,3 +48,36 @@ def test_reference_arm_other_ranks_exit_silently():
              env_extra={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip() == ""
+
+
+def test_gpus_flag_relaunches_n_ranks():
+    """`bench.py --gpus 2` outside torchrun re-execs itself under
+    torch.distributed.run with two ranks (never a silent one-GPU line)."""
+    r = _run(["--gpus", "2", "--steps", "3"], env_extra={"LBM_BENCH_DRYRUN": "1"}, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world_size"] == 2 and d["gpus"] == 2 for d in lines)
+
+
+def test_gpus_flag_must_match_world_size():
+    r = _run(["--gpus", "4", "--steps", "3"],
+             env_extra={"LBM_BENCH_DRYRUN": "1", "WORLD_SIZE": "2", "RANK": "0"}, timeout=120)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=2" in r.stderr
+
+
+def test_reference_arm_config_matches_ours_shape():
+    """Both arms build `config` with bench.config_dict, so the driver's
+    same-config check compares like with like (C3 default at every N)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+
+    class A:
+        scheme, addressing, layout, precision = "aap", "direct", "soa", 8
+    c = b.config_dict("c3", A, 1, 512 * 512 * 1024)
+    assert c["workload"].startswith("C3") and c["dims"] == [512, 512, 1024]
+    assert c["parallelism"] == "single domain"
+    assert b.config_dict("c3", A, 8, 512 * 512 * 1024)["parallelism"] == "z-slabs x8"

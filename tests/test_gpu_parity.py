@@ -342,3 +342,35 @@ def test_swap_one_sweep_equals_two_passes(gpu, monkeypatch, dims, policy, precis
             outs.append(st.extract_natural())
     for o in outs[1:]:
         assert bitwise_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("aos_window", ["0", "1"])
+def test_cg_all_solid_plane_groups(gpu, aos_window):
+    """CG plane groups with no fluid cell (a solid band thicker than a group,
+    LBMGPU_CG_PLANES=2): every thread of such a group still waits for the group
+    ahead before it exits, so the chain of programmatic dependent launches
+    keeps its order. Many sweeps back to back, bitwise = the oracle (SoA and
+    AoS; per-thread AoS kernels and the tile windows)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_1111_0922_b200 as L, oracle\n"
+        "O = oracle.Oracle(); dims = (24, 16, 40)\n"
+        "mask = np.ones(dims[::-1], np.uint8); mask[10:21] = 0; mask[30:33, 4:9] = 0\n"
+        "mask = mask.reshape(-1)\n"
+        "geo = L.GridGeometry(*dims, ('periodic',) * 3, mask)\n"
+        "f0 = O.random_field(7, geo.fluid_count())\n"
+        "want = O.ts_run(*dims, [0, 0, 0], mask, 1.7, 1.7, [2e-5, 0.0, 0.0], f0, 15)\n"
+        "for lay in ('soa', 'aos'):\n"
+        "    st = L.create_stepper('cg', 'direct', geo, L.bgk(1.7, (2e-5, 0.0, 0.0)),"
+        " L.StepperOptions(layout=lay))\n"
+        "    st.load_natural(f0); st.step_n(15); st.synchronize()\n"
+        "    assert (st.extract_natural().view(np.uint64) == want.view(np.uint64)).all(), lay\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ, LBMGPU_AOS_WINDOW=aos_window, LBMGPU_CG_PLANES="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
