@@ -13,6 +13,8 @@
 //   StepperOptions / Stepper / create_stepper /
 //   kernel_available / parse_* / to_string     p/include/lbmlab/stepper.hpp:15-113
 //   TrafficSpec / traffic / predict_mlups      p/include/lbmlab/perfmodel.hpp:17-60
+//   Moments / moments                          p/include/lbmlab/collision.hpp:25-33
+//   MacroFields / macroscopic_fields           p/include/lbmlab/stepper.hpp:115-120
 // GPU additions: StepperOptions::{layout, precision, device, extensions,
 // z_begin, z_end}; Stepper::{step_n, synchronize, step_timed, init_field,
 // slab_connect_nccl, slab_sync_ghosts, slab_p2p_export, slab_p2p_connect};
@@ -380,6 +382,45 @@ inline std::unique_ptr<Stepper> create_stepper(SchemeId id, Addressing a, const 
   lbmgpu_stepper* h = nullptr;
   detail::check(lbmgpu_create(&cg, &f, &o, &h));
   return std::unique_ptr<Stepper>(new Stepper(h, id, a));
+}
+
+// ---- macroscopic diagnostics (host side, over the extracted snapshot) ----------
+// moments (p/src/collision.cpp:24-36): rho = sum f_i, u = (sum f_i c_i) / rho
+// + g / 2; std::domain_error("vacuum node") when rho <= 0
+struct Moments {
+  double rho = 0.0;
+  std::array<double, 3> u{0.0, 0.0, 0.0};
+};
+inline Moments moments(const Stencil& s, const double* f, const std::array<double, 3>& g) {
+  double rho = 0.0;
+  std::array<double, 3> m{0.0, 0.0, 0.0};
+  for (int i = 0; i < s.q; ++i) {
+    rho += f[i];
+    for (int k = 0; k < s.d; ++k) m[k] += f[i] * s.c[i][k];
+  }
+  if (!(rho > 0.0)) throw std::domain_error("vacuum node");
+  Moments out;
+  out.rho = rho;
+  for (int k = 0; k < 3; ++k) out.u[k] = m[k] / rho + 0.5 * g[k];
+  return out;
+}
+// MacroFields / macroscopic_fields (p/include/lbmlab/stepper.hpp:115-120,
+// p/src/stepper.cpp:182-193): per fluid node, canonical node order
+struct MacroFields {
+  std::vector<double> rho;
+  std::vector<std::array<double, 3>> u;
+};
+inline MacroFields macroscopic_fields(const Stepper& st, const Stencil& s, const FlowParams& p) {
+  const std::vector<double> f = st.extract_natural();
+  MacroFields out;
+  out.rho.resize(st.node_count());
+  out.u.resize(st.node_count());
+  for (std::size_t n = 0; n < st.node_count(); ++n) {
+    const Moments m = moments(s, f.data() + n * s.q, p.body_force);
+    out.rho[n] = m.rho;
+    out.u[n] = m.u;
+  }
+  return out;
 }
 
 // ---- traffic model (p/src/perfmodel.cpp:12-75, 115-119) ------------------------

@@ -135,8 +135,13 @@ for _name, (_res, _args) in _sig.items():
     _fn.restype = _res
     _fn.argtypes = _args
 
+class DomainError(ValueError):
+    """std::domain_error (a std::logic_error, like invalid_argument -> ValueError):
+    the reference's "vacuum node" (p/src/collision.cpp:31)."""
+
+
 # status -> Python exception, mirroring the reference's C++ exception types
-_ERRORS = {1: ValueError, 2: RuntimeError, 3: ArithmeticError, 4: MemoryError, 5: RuntimeError}
+_ERRORS = {1: ValueError, 2: RuntimeError, 3: DomainError, 4: MemoryError, 5: RuntimeError}
 
 
 def _check(rc: int) -> None:
@@ -529,7 +534,8 @@ def verify_suite(seed: int = 42, steps: int = 10, device: int = 0, all_variants:
 def macroscopic_fields(stepper: Stepper, flow: FlowParams):
     """macroscopic_fields (p/src/stepper.cpp:182-193): per fluid node rho and
     u = (sum f c) / rho + g / 2 (moments, p/src/collision.cpp:24-36); host-side
-    diagnostic over the extracted snapshot. Raises ArithmeticError on vacuum."""
+    diagnostic over the extracted snapshot. Raises DomainError("vacuum node")
+    (std::domain_error in the reference) when a node's rho <= 0."""
     from .geometry import C_VECTORS
     f = stepper.extract_natural().reshape(-1, Q)
     rho = np.zeros(f.shape[0])
@@ -539,7 +545,7 @@ def macroscopic_fields(stepper: Stepper, flow: FlowParams):
         for k in range(3):
             m[:, k] = m[:, k] + f[:, i] * C_VECTORS[i][k]
     if not np.all(rho > 0.0):
-        raise ArithmeticError("vacuum node")
+        raise DomainError("vacuum node")
     u = m / rho[:, None] + 0.5 * np.asarray(flow.body_force)[None, :]
     return rho, u
 

@@ -645,22 +645,38 @@ uint64_t selftest_division(uint64_t n, uint64_t seed) {
 // ---- streaming-bandwidth probe (the roofline denominator, measured live) ----
 // copy b <- a, or the sweeps' own in-place pattern a <- f(a) (every 16-byte
 // line read once and written back, like the AA / ET / OS-pull stores over the
-// slots they read). Four independent 16-byte loads per thread in flight.
+// slots they read). Three launch shapes; the probe reports the best:
+//   0  persistent grid (8 x 256 threads per SM), grid-stride, 4 loads in flight
+//   1  one 16-byte element per thread, one block per 256 elements
+//   2  four 16-byte elements per thread (warp-contiguous), one block per 1024
 namespace {
-__global__ void __launch_bounds__(256) k_bw(const uint4* __restrict__ a, uint4* __restrict__ b,
-                                            size_t n) {
+__device__ __forceinline__ uint4 bump(uint4 v) {
+  v.x += 1u;
+  return v;
+}
+__global__ void __launch_bounds__(256) k_bw0(const uint4* a, uint4* b, size_t n) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + 3 * stride < n; i += 4 * stride) {
-    uint4 v0 = a[i], v1 = a[i + stride], v2 = a[i + 2 * stride], v3 = a[i + 3 * stride];
-    v0.x += 1u, v1.x += 1u, v2.x += 1u, v3.x += 1u;
-    b[i] = v0, b[i + stride] = v1, b[i + 2 * stride] = v2, b[i + 3 * stride] = v3;
+    const uint4 v0 = a[i], v1 = a[i + stride], v2 = a[i + 2 * stride], v3 = a[i + 3 * stride];
+    b[i] = bump(v0), b[i + stride] = bump(v1), b[i + 2 * stride] = bump(v2),
+    b[i + 3 * stride] = bump(v3);
   }
-  for (; i < n; i += stride) {
-    uint4 v = a[i];
-    v.x += 1u;
-    b[i] = v;
-  }
+  for (; i < n; i += stride) b[i] = bump(a[i]);
+}
+__global__ void __launch_bounds__(256) k_bw1(const uint4* a, uint4* b, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = bump(a[i]);
+}
+__global__ void __launch_bounds__(256) k_bw2(const uint4* a, uint4* b, size_t n) {
+  const size_t base = (size_t)blockIdx.x * 1024 + (threadIdx.x / 32) * 128 + (threadIdx.x % 32);
+  uint4 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (base + 32 * k < n) v[k] = a[base + 32 * k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (base + 32 * k < n) b[base + 32 * k] = bump(v[k]);
 }
 }  // namespace
 
@@ -682,7 +698,6 @@ double stream_bandwidth(uint64_t bytes, int inplace, int reps) {
     release();
     throw std::bad_alloc();
   }
-  if (inplace) b = nullptr;
   uint4* dst = inplace ? a : b;
   auto CK = [&](cudaError_t e) {
     if (e != cudaSuccess) {
@@ -697,17 +712,22 @@ double stream_bandwidth(uint64_t bytes, int inplace, int reps) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)sms * 8;  // 8 resident 256-thread blocks per SM
   float best = 1e30f;
-  for (int r = 0; r < reps + 1; ++r) {  // the first launch is a warm-up
-    CK(cudaEventRecord(e0, st));
-    k_bw<<<grid, 256, 0, st>>>(a, dst, n);
-    CK(cudaEventRecord(e1, st));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    if (r > 0) best = std::min(best, ms);
-  }
+  for (int shape = 0; shape < 3; ++shape)
+    for (int r = 0; r < reps + 1; ++r) {  // the first launch of a shape is a warm-up
+      CK(cudaEventRecord(e0, st));
+      if (shape == 0)
+        k_bw0<<<(unsigned)sms * 8, 256, 0, st>>>(a, dst, n);
+      else if (shape == 1)
+        k_bw1<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, dst, n);
+      else
+        k_bw2<<<(unsigned)((n + 1023) / 1024), 256, 0, st>>>(a, dst, n);
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r > 0) best = std::min(best, ms);
+    }
   CK(cudaGetLastError());
   release();
   return 2.0 * (double)n * 16.0 / (best * 1e-3) / 1e9;

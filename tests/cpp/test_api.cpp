@@ -165,6 +165,28 @@ int main() {
     CHECK(bitwise_equal(got, one->extract_natural()));
   }
 
+  // macroscopic_fields (p/src/stepper.cpp:182-193) and moments' domain_error
+  // "vacuum node" (p/src/collision.cpp:31)
+  {
+    auto st = create_stepper(SchemeId::aap, Addressing::direct, g, s, p);
+    const MacroFields m0 = macroscopic_fields(*st, s, p);
+    CHECK(m0.rho.size() == st->node_count() && m0.u.size() == st->node_count());
+    for (std::size_t n = 0; n < m0.rho.size(); ++n) {  // rest start: rho0, u = g/2
+      CHECK(std::abs(m0.rho[n] - p.rho0) < 1e-14);
+      CHECK(std::abs(m0.u[n][0] - 0.5 * p.body_force[0]) < 1e-14);
+    }
+    std::vector<double> f = st->extract_natural();
+    for (int i = 0; i < 19; ++i) f[3 * 19 + i] = 0.0;
+    st->load_natural(f.data());
+    bool threw = false;
+    try {
+      (void)macroscopic_fields(*st, s, p);
+    } catch (const std::domain_error& e) {
+      threw = std::string(e.what()) == "vacuum node";
+    }
+    CHECK(threw);
+  }
+
   std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
   return failures ? 1 : 0;
 }

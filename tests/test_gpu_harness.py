@@ -81,3 +81,15 @@ def test_shared_reciprocal_division_is_ddiv_rn(gpu):
     __ddiv_rn's / __fdiv_rn's on 2^26 seeded inputs incl. signed zeros,
     denormals, infinities and NaNs"""
     assert gpu.selftest_division(1 << 26, seed=20251019) == 0
+
+
+def test_macroscopic_fields_vacuum_node(gpu):
+    """moments' std::domain_error("vacuum node") (p/src/collision.cpp:31) as
+    DomainError, through the Python mirror's macroscopic_fields."""
+    L = gpu
+    st = L.create_stepper("aap", "direct", L.GridGeometry(8, 6, 4), L.bgk(1.0))
+    f = st.extract_natural().reshape(-1, 19)
+    f[2] = 0.0
+    st.load_natural(f.ravel())
+    with pytest.raises(L.DomainError, match="vacuum node"):
+        L.macroscopic_fields(st, L.bgk(1.0))
