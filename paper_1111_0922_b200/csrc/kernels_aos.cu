@@ -7,8 +7,9 @@
 // 0.45, OS push 0.23, AA 0.32 of the HBM roofline). Here a block owns a
 // 32 x 8 x-y tile and marches through a chunk of z planes. Each plane of the
 // tile plus a one-cell halo (34 x 10 records) is copied whole into a 4-plane
-// shared-memory ring with cp.async (16-byte chunks, the row phase in shared
-// memory matches the record's global byte phase); all neighbour accesses are
+// shared-memory ring, one bulk copy (TMA engine) per row issued by one lane
+// of the loading warp (the row phase in shared memory matches the record's
+// global byte phase, so the copy is 16-byte congruent); all neighbour accesses are
 // shared-memory accesses, and the tile's output records leave as contiguous
 // 16-byte stores. DRAM sees each record once per sweep (the halo rows/planes
 // are L2 hits of the neighbouring tiles), L2 sees 1.33x the record bytes.
@@ -61,6 +62,23 @@ using namespace dev;
 
 namespace {
 
+// Phase trace (experiments only, -DLBM_WIN_TRACE): thread 0 of every window
+// block accumulates clock64 cycles per phase of the plane loop; read back
+// with lbmgpu_debug_win_trace (tools/win_trace.py).
+#ifdef LBM_WIN_TRACE
+__device__ unsigned long long g_win_trace[16];
+#define WIN_T0() long long _tt = clock64()
+#define WIN_T(k)                                                                 \
+  do {                                                                           \
+    const long long _n = clock64();                                              \
+    if (threadIdx.x == 0) atomicAdd(&g_win_trace[k], (unsigned long long)(_n - _tt)); \
+    _tt = _n;                                                                    \
+  } while (0)
+#else
+#define WIN_T0()
+#define WIN_T(k)
+#endif
+
 constexpr int kTX = 32, kTY = 8;             // tile: one warp per x-row
 constexpr int kWC = kTX + 2, kWR = kTY + 2;  // window columns / rows (1-cell halo)
 constexpr int kNB = 4;                       // plane buffers in the ring
@@ -89,11 +107,18 @@ constexpr bool owned_wb(int mode) { return in_place(mode) || mode == kWinPushS; 
 #ifndef LBM_WIN_GATHER_THREADS
 #define LBM_WIN_GATHER_THREADS 352
 #endif
+// LBM_WIN_LOADER > 0 (experiments): that many extra warps in the modes that
+// have none; the first of them issues the ring's plane loads (load_plane).
+// Measured slower for the in-place modes (the register cap of the larger
+// block), so off by default.
+#ifndef LBM_WIN_LOADER
+#define LBM_WIN_LOADER 0
+#endif
 template <class T, int MODE>
 struct WinThreads {
   static constexpr int value = sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream)
                                    ? LBM_WIN_GATHER_THREADS
-                                   : kTX * kTY;
+                                   : kTX * kTY + 32 * LBM_WIN_LOADER;
   static constexpr int warps = value / 32;
 };
 
@@ -161,16 +186,57 @@ __device__ __forceinline__ void copy_in_bulk(T* s, const T* g, int n, int lane, 
   int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
   if (head > n) head = n;
   const int nmid = (n - head) / V * V;
+#ifdef LBM_WIN_TRACE
+  long long c0 = clock64();
+#define WIN_T2(k)                                                        \
+  do {                                                                   \
+    const long long c1 = clock64();                                      \
+    if (lane == 0) atomicAdd(&g_win_trace[k], (unsigned long long)(c1 - c0)); \
+    c0 = c1;                                                             \
+  } while (0)
+#else
+#define WIN_T2(k)
+#endif
   if (lane < head) cp_async<sizeof(T)>(s + lane, g + lane);
   const int t0 = head + nmid;
   if (t0 + lane < n) cp_async<sizeof(T)>(s + t0 + lane, g + t0 + lane);
+  WIN_T2(8);
   cp_async_mbar_arrive(bar);
+  WIN_T2(9);
   if (lane == 0) {
     const uint32_t bytes = (uint32_t)nmid * (uint32_t)sizeof(T);
     mbar_arrive_tx(bar, bytes);
+    WIN_T2(10);
     if (bytes) bulk_g2s(s + head, g + head, bytes, bar);
+    WIN_T2(11);
+#ifdef LBM_WIN_TRACE
+    atomicAdd(&g_win_trace[12], 1ull);
+#endif
+  }
+#undef WIN_T2
+}
+// The same as one bulk copy of the 16-byte-aligned superset of the range
+// (at most 15 bytes more on either side, landing in the row's phase slack):
+// lane 0 issues everything, no per-lane cp.async and no per-lane arrival.
+// Only where the superset's extra bytes in shared memory are not also written
+// by another copy (a row without separately copied wrap records). Global
+// over-reads stay inside the allocation (DevMem pads every buffer).
+template <class T>
+__device__ __forceinline__ void copy_in_bulk_superset(T* s, const T* g, int n, int lane,
+                                                      uint64_t* bar) {
+  if (lane == 0) {
+    const uintptr_t gb = reinterpret_cast<uintptr_t>(g), lo = gb & ~(uintptr_t)15;
+    const uintptr_t hi = (gb + (uintptr_t)n * sizeof(T) + 15) & ~(uintptr_t)15;
+    char* sa = reinterpret_cast<char*>(s) - (gb - lo);
+    mbar_arrive(bar, kRowArrivals - 1);
+    mbar_arrive_tx(bar, (uint32_t)(hi - lo));
+    bulk_g2s(sa, reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo), bar);
   }
 }
+#ifndef LBM_AOS_SUPERSET
+#define LBM_AOS_SUPERSET 1
+#endif
+
 // one warp: n elements shared -> global (congruent mod 16 bytes). The lanes'
 // own shared-memory writes must precede it (each lane fences them for the
 // async proxy here); lane 0 later waits for the group's reads (bulk_wait_read)
@@ -258,6 +324,50 @@ __device__ __forceinline__ bool in_block(const Tile& t, int rx, int r, int z) {
   return rx >= 1 && rx <= t.txv && r >= 1 && r <= t.tyv && z >= t.zb && z < t.ze;
 }
 
+// One lane copies one window row: n elements at g -> s (congruent mod 16 B)
+// as one bulk copy of the 16-byte-aligned part plus cp.async for the
+// unaligned head / tail elements; where the row's neighbouring shared memory
+// is not written by anyone else (lo_free / hi_free: no wrap record next to
+// it) the bulk copy takes the aligned superset instead and there are no
+// head / tail copies. Plus the wrap records (19 elements each, cp.async).
+// Arrivals on bar: kRowArrivals per row, like the warp form.
+template <class T>
+__device__ __forceinline__ void copy_row_lane(T* s, const T* g, int n, bool lo_free, bool hi_free,
+                                              T* sl, const T* gl, T* sr, const T* gr,
+                                              uint64_t* bar) {
+  const uintptr_t gb = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t ge = gb + (uintptr_t)n * sizeof(T);
+  const uintptr_t lo = lo_free ? (gb & ~(uintptr_t)15) : ((gb + 15) & ~(uintptr_t)15);
+  const uintptr_t hi = hi_free ? ((ge + 15) & ~(uintptr_t)15) : (ge & ~(uintptr_t)15);
+  bool cp = false;
+  if (gl) {
+    for (int i = 0; i < 19; ++i) cp_async<sizeof(T)>(sl + i, gl + i);
+    cp = true;
+  }
+  if (gr) {
+    for (int i = 0; i < 19; ++i) cp_async<sizeof(T)>(sr + i, gr + i);
+    cp = true;
+  }
+  const int nh = (int)((lo > gb ? lo - gb : 0) / sizeof(T));
+  for (int i = 0; i < nh && i < n; ++i) cp_async<sizeof(T)>(s + i, g + i), cp = true;
+  if (hi < lo) {  // a row shorter than one aligned vector: all elements by cp.async
+    for (int i = nh; i < n; ++i) cp_async<sizeof(T)>(s + i, g + i), cp = true;
+    mbar_arrive(bar, kRowArrivals - 1);
+    cp_async_mbar_arrive(bar);
+    return;
+  }
+  const int nt = (int)((ge > hi ? ge - hi : 0) / sizeof(T));
+  for (int i = n - nt; i < n; ++i) cp_async<sizeof(T)>(s + i, g + i), cp = true;
+  mbar_arrive(bar, kRowArrivals - 1 - (cp ? 1u : 0u));
+  if (cp) cp_async_mbar_arrive(bar);
+  char* sa = reinterpret_cast<char*>(s) + (lo - gb);
+  mbar_arrive_tx(bar, (uint32_t)(hi - lo));
+  if (hi > lo) bulk_g2s(sa, reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo), bar);
+}
+#ifndef LBM_AOS_LANELOAD
+#define LBM_AOS_LANELOAD 1
+#endif
+
 // issue the cp.async copies of window plane z (cell z, may be -1 / nz)
 template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
@@ -271,6 +381,38 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
   } else if (z >= L.nz && whi) {
     g = whi;
   }
+  if constexpr (kBulk && LBM_AOS_LANELOAD) {
+    // warp 0, one lane per window row: a plane costs the loading warp a few
+    // dozen instructions instead of every warp a row loop
+    // the loading warp: the first warp beyond the tile rows where there is
+    // one (the fp64 gather modes' extra warps: loads overlap the compute
+    // warps' work, C1 OS pull 0.68 -> 0.76), else warp 0
+    const int lw = (int)(blockDim.x >> 5) > kTY ? kTY : 0;
+    if (warp != lw) return;
+    const int r = lane;
+    if (r >= t.tyv + 2) return;
+    uint32_t rb;
+    int phase = 0;
+    if (row_base(L, t.y0 - 1 + r, z, rb)) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(g) +
+                           (uintptr_t)(((long long)rb + L.ox + t.x0 - 1) * 19 * (long long)sizeof(T));
+      phase = (int)((a0 & 15u) / sizeof(T));
+      T* srow = buf + r * WinSz<T>::ROW + phase;
+      const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
+      const T *gl = nullptr, *gr = nullptr;
+      if (!L.wall[0] && !L.ox) {
+        if (t.x0 == 0) gl = g + ((size_t)rb + (size_t)(L.nx - 1)) * 19;
+        if (t.x0 + t.txv == L.nx) gr = g + (size_t)rb * 19;
+      }
+      copy_row_lane(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
+                    (xb - xa + 1) * 19, gl == nullptr, gr == nullptr, srow, gl,
+                    srow + (t.txv + 1) * 19, gr, bar);
+    } else {
+      mbar_arrive(bar, kRowArrivals);
+    }
+    ph[r] = phase;
+    return;
+  }
   for (int r = warp; r < t.tyv + 2; r += (int)(blockDim.x >> 5)) {
     uint32_t rb;
     int phase = 0;
@@ -282,13 +424,21 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
       phase = (int)((a0 & 15u) / sizeof(T));
       T* srow = buf + r * WinSz<T>::ROW + phase;
       const int xa = max(t.x0 - 1, -L.ox), xb = min(t.x0 + t.txv, L.nx - 1 + L.ox);
+      bool wrapx = false;
       if (!L.wall[0] && !L.ox) {
         if (t.x0 == 0) copy_in_rec(srow, g + ((size_t)rb + (size_t)(L.nx - 1)) * 19, lane);
         if (t.x0 + t.txv == L.nx) copy_in_rec(srow + (t.txv + 1) * 19, g + (size_t)rb * 19, lane);
+        wrapx = t.x0 == 0 || t.x0 + t.txv == L.nx;
       }
-      if constexpr (kBulk)
-        copy_in_bulk(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
-                     (xb - xa + 1) * 19, lane, bar);
+      if constexpr (kBulk) {
+        if (LBM_AOS_SUPERSET && !wrapx)
+          copy_in_bulk_superset(srow + (xa - t.x0 + 1) * 19,
+                                g + ((size_t)rb + (size_t)(xa + L.ox)) * 19, (xb - xa + 1) * 19,
+                                lane, bar);
+        else
+          copy_in_bulk(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
+                       (xb - xa + 1) * 19, lane, bar);
+      }
       else
         copy_in(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
                 (xb - xa + 1) * 19, lane);
@@ -760,8 +910,10 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
   T pd[5];              // ... and the deferred cz = +1 values of plane z - 1
   bool pd_live = false;
   uint32_t pd_mask = 0;
+  WIN_T0();
   for (int z = t.zb; z < t.ze; ++z) {
     if (z == t.zb) load(z + 1);
+    WIN_T(0);
     if constexpr (kBulk) {
       // every warp is done with plane z - 2's slot (compute of z - 1, write-back
       // of z - 2 and its bulk stores' reads): refill it with plane z + 2, then
@@ -769,12 +921,15 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       bulk_wait_read();
       fence_async_smem();
       __syncthreads();
+      WIN_T(1);  // previous plane's stragglers (barrier)
       if (z + 2 <= t.ze) load(z + 2);
+      WIN_T(2);  // issuing the prefetch
       if (z == t.zb) {
         wait_plane(z - 1);
         wait_plane(z);
       }
       wait_plane(z + 1);
+      WIN_T(3);  // waiting for plane z + 1
     } else {
       cp_commit();
       if (z == t.zb) cp_wait1(); else cp_wait0();
@@ -913,7 +1068,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       }
       if constexpr (kBulk) fence_async_smem();  // ring writes before the runs' bulk stores
     }
+    WIN_T(4);  // compute (+ per-node stores into the ring)
     __syncthreads();  // every read of plane z - 1 is done
+    WIN_T(5);  // waiting for the slowest warp's compute
     if constexpr (owned_wb(MODE)) {
       if (fast_plane(z - 1))
         writeback_fast(dst.p, sm, wl, rbp, sbp, t);
@@ -941,6 +1098,7 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
       else
         copy_out(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
     }
+    WIN_T(6);  // write-back / staging of plane z - 1
   }
   if constexpr (kBulk) bulk_wait_all();
   if constexpr (MODE == kWinPushS) {  // plane ze - 1's deferred values into the halo plane
@@ -1042,8 +1200,13 @@ __global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
     auto issue_bulk = [&](uint32_t k) {
       const uint32_t c0 = run_c0(k);
       const uint32_t nrec = min((uint32_t)kRun, L.ncells - c0);
-      copy_in_bulk(sm + (k & 1) * SLOT + phase_of(c0), src.p + (size_t)(c0 + soff) * 19,
-                   (int)(nrec * 19), lane, &rbar[k & 1]);
+      if (LBM_AOS_SUPERSET)
+        copy_in_bulk_superset(sm + (k & 1) * SLOT + phase_of(c0),
+                              src.p + (size_t)(c0 + soff) * 19, (int)(nrec * 19), lane,
+                              &rbar[k & 1]);
+      else
+        copy_in_bulk(sm + (k & 1) * SLOT + phase_of(c0), src.p + (size_t)(c0 + soff) * 19,
+                     (int)(nrec * 19), lane, &rbar[k & 1]);
     };
     if (warp == 0) issue_bulk(0);
     for (uint32_t k = 0; k < nmine; ++k) {
@@ -1246,3 +1409,15 @@ bool launch_aos_local_stream(cudaStream_t st, const DField& a, const DField& b, 
 }
 
 }  // namespace lbmgpu
+
+#ifdef LBM_WIN_TRACE
+extern "C" int lbmgpu_debug_win_trace(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, lbmgpu::g_win_trace, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(lbmgpu::g_win_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -62,7 +62,9 @@ class DevMem {
   void alloc(size_t bytes) {
     release();
     if (bytes == 0) bytes = 256;
-    CK(cudaMalloc(&p_, bytes));
+    // + 64 bytes: kernels may over-read up to 15 bytes past a row for
+    // 16-byte-aligned bulk copies (kernels_aos.cu copy_in_bulk_superset)
+    CK(cudaMalloc(&p_, bytes + 64));
     n_ = bytes;
   }
   void release() {
