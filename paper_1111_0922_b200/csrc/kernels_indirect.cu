@@ -186,44 +186,69 @@ __device__ __forceinline__ void staged_batches(const uint32_t* __restrict__ tabl
   }
 }
 
+template <int ROWS, bool VEC, class Body>
+__device__ __forceinline__ void staged_rows(const uint32_t* __restrict__ table, const Idx& I,
+                                            uint32_t nbatch, Body body) {
+  __shared__ __align__(16) uint32_t sb[2][ROWS][kBlock];
+  staged_batches<ROWS, VEC>(table, I, nbatch, sb, body);
+}
+
+// Staged-table kernels (fp64): resident blocks per SM, and whether the staged
+// rows are read from shared memory at each use instead of being held in
+// registers across the collision (measured: ET C2 0.73 -> 0.76, C4 0.87 ->
+// 0.96 of the roofline, AA unchanged; 3 blocks per SM and warp-private
+// staging without block barriers both measured slower)
+#ifndef LBM_IDX_PF_MIN_BLOCKS
+#define LBM_IDX_PF_MIN_BLOCKS 2
+#endif
+#ifndef LBM_IDX_PF_LAZY
+#define LBM_IDX_PF_LAZY 1
+#endif
+
 // AA odd sweep with the adjacency staged (fp64; C4 0.94 -> 0.97 of the
 // roofline; fp32 spills at its register budget and keeps k_aa_odd_idx)
 template <class T, bool VEC>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     k_aa_odd_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
-  __shared__ __align__(16) uint32_t sadj[2][18][kBlock];
-  staged_batches<18, VEC>(I.adj, I, nbatch, sadj, [&](uint32_t node, auto row) {
+  staged_rows<18, VEC>(I.adj, I, nbatch, [&](uint32_t node, auto row) {
     uint32_t e[19];
+    if (!LBM_IDX_PF_LAZY) {
 #pragma unroll
-    for (int i = 1; i < 19; ++i) e[i] = row(i - 1);
+      for (int i = 1; i < 19; ++i) e[i] = row(i - 1);
+    }
+    auto nb = [&](int k) { return LBM_IDX_PF_LAZY ? row(k - 1) : e[k]; };
     T f[19];
     f[0] = ld(F.at(0, node));
 #pragma unroll
     for (int i = 1; i < 19; ++i) {
       const int j = opp(i);
-      f[i] = ld(e[j] == node ? F.at(i, node) : F.at(j, e[j]));
+      const uint32_t ej = nb(j);
+      f[i] = ld(ej == node ? F.at(i, node) : F.at(j, ej));
     }
     collide(op, f);
     st<false>(F.at(0, node), f[0]);
 #pragma unroll
-    for (int j = 1; j < 19; ++j) st<false>(e[j] == node ? F.at(opp(j), node) : F.at(j, e[j]), f[j]);
+    for (int j = 1; j < 19; ++j) {
+      const uint32_t ej = nb(j);
+      st<false>(ej == node ? F.at(opp(j), node) : F.at(j, ej), f[j]);
+    }
   });
 }
 
 // ET sweep with the rem rows staged (fp64)
 template <class T, bool SW, bool VEC>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     k_et_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
-  __shared__ __align__(16) uint32_t srem[2][9][kBlock];
-  staged_batches<9, VEC>(I.rem, I, nbatch, srem, [&](uint32_t node, auto row) {
+  staged_rows<9, VEC>(I.rem, I, nbatch, [&](uint32_t node, auto row) {
     uint32_t rs[9];
+    auto rm = [&](int p) { return LBM_IDX_PF_LAZY ? row(p) : rs[p]; };
     T f[19];
     f[0] = ld(F.at(0, node));
 #pragma unroll
     for (int p = 0; p < 9; ++p) {
       const int i = pair_i(p), j = pair_j(p);
-      rs[p] = row(p);
-      const uint32_t r = rs[p] & 0x7fffffffu;
+      if (!LBM_IDX_PF_LAZY) rs[p] = row(p);
+      const uint32_t r = rm(p) & 0x7fffffffu;
       f[i] = ld(F.at(hb<SW>(i), node));
       f[j] = ld(F.at(r >= I.n ? hb<SW>(i) : hb<SW>(j), r));
     }
@@ -232,9 +257,10 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
 #pragma unroll
     for (int p = 0; p < 9; ++p) {
       const int i = pair_i(p), j = pair_j(p);
-      const bool ub = (rs[p] & 0x80000000u) != 0;
+      const uint32_t rv = rm(p);
+      const bool ub = (rv & 0x80000000u) != 0;
       st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
-      st<false>(F.at(hb<SW>(j), rs[p] & 0x7fffffffu), f[i]);
+      st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
     }
   });
 }
@@ -614,7 +640,7 @@ void launch_os_push_idx(cudaStream_t st, const DField& a, const DField& b, const
 static unsigned staged_grid(uint32_t nbatch) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::min<uint32_t>(nbatch, (uint32_t)(sms * MinBlocks<double>::value));
+  return std::min<uint32_t>(nbatch, (uint32_t)(sms * LBM_IDX_PF_MIN_BLOCKS));
 }
 
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
