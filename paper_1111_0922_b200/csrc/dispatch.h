@@ -40,6 +40,7 @@ inline dev::Trt<T> cast_op(const TrtHost& h) {
   o.le_half = (T)h.le_half;
   o.lo_half = (T)h.lo_half;
   o.w0 = (T)h.w0;
+  o.rho0 = (T)h.rho0;
   for (int p = 0; p < 9; ++p) {
     o.w2[p] = (T)h.w2[p];
     o.f3w[p] = (T)h.f3w[p];

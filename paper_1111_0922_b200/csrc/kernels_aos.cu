@@ -411,8 +411,7 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
       mbar_arrive(bar, kRowArrivals);
     }
     ph[r] = phase;
-    return;
-  }
+  } else {
   for (int r = warp; r < t.tyv + 2; r += (int)(blockDim.x >> 5)) {
     uint32_t rb;
     int phase = 0;
@@ -446,6 +445,7 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
       mbar_arrive(bar, kRowArrivals);  // every window row arrives fully once per load
     }
     if (lane == 0) ph[r] = phase;
+  }
   }
 }
 

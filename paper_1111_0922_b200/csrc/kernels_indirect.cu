@@ -211,7 +211,7 @@ template <class T, bool VEC>
 __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     k_aa_odd_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
   staged_rows<18, VEC>(I.adj, I, nbatch, [&](uint32_t node, auto row) {
-    uint32_t e[19];
+    uint32_t e[19] = {};
     if (!LBM_IDX_PF_LAZY) {
 #pragma unroll
       for (int i = 1; i < 19; ++i) e[i] = row(i - 1);
@@ -240,7 +240,7 @@ template <class T, bool SW, bool VEC>
 __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     k_et_idx_pf(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
   staged_rows<9, VEC>(I.rem, I, nbatch, [&](uint32_t node, auto row) {
-    uint32_t rs[9];
+    uint32_t rs[9] = {};
     auto rm = [&](int p) { return LBM_IDX_PF_LAZY ? row(p) : rs[p]; };
     T f[19];
     f[0] = ld(F.at(0, node));

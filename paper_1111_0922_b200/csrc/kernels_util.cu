@@ -57,6 +57,23 @@ __device__ __forceinline__ double equilibrium(double rho, double ux, double uy, 
   return __dmul_rn(__dmul_rn(weight(i), rho), __dsub_rn(a, __dmul_rn(1.5, usq)));
 }
 
+// canonical value of direction i <-> stored value (fp32 fields hold
+// f_i - w_i shift, lbm_device.cuh kShifted; fp64 fields hold f_i)
+template <class T>
+__device__ __forceinline__ T to_store(double v, int i, double shift) {
+  if constexpr (kShifted<T>)
+    return (T)__dsub_rn(v, __dmul_rn(weight(i), shift));
+  else
+    return (T)v;
+}
+template <class T>
+__device__ __forceinline__ double from_store(T s, int i, double shift) {
+  if constexpr (kShifted<T>)
+    return __dadd_rn((double)s, __dmul_rn(weight(i), shift));
+  else
+    return (double)s;
+}
+
 // Initial canonical values of one node (host buffer or a generator).
 //  Rest:        w_i rho0 (every reference stepper's start, e.g. scheme_aap.cpp:32-36)
 //  TaylorGreen: equilibrium(rho, u) + noise*U, rho = rho0 + drho*U,
@@ -106,7 +123,7 @@ __device__ __forceinline__ void node_values(const InitSpec& in, const double* bu
 
 template <class T, bool AOS>
 __global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint32_t n0,
-                          uint32_t count, int mode, EtBase B, double* buf) {
+                          uint32_t count, int mode, EtBase B, double* buf, double shift) {
   const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
   if (k >= count) return;
   const uint32_t node = n0 + k;
@@ -116,35 +133,35 @@ __global__ void k_extract(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, ui
   switch (mode) {
     case kExNatural:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(i, c.s);
+      for (int i = 0; i < 19; ++i) o[i] = from_store(*F.at(i, c.s), i, shift);
       break;
     case kExOpposed:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(opp(i), c.s);
+      for (int i = 0; i < 19; ++i) o[i] = from_store(*F.at(opp(i), c.s), i, shift);
       break;
     case kExGather:  // gather_out_direct (p/src/stepper.cpp:228-252)
-      o[0] = (double)*F.at(0, c.s);
+      o[0] = from_store(*F.at(0, c.s), 0, shift);
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
-        o[i] = (double)*(c.bb(j) ? F.at(j, c.s) : F.at(i, c.nb(j)));
+        o[i] = from_store(*(c.bb(j) ? F.at(j, c.s) : F.at(i, c.nb(j))), i, shift);
       }
       break;
     case kExAaOdd:  // AapStepper::extract_natural, odd (p/src/scheme_aap.cpp:57-75)
-      o[0] = (double)*F.at(0, c.s);
+      o[0] = from_store(*F.at(0, c.s), 0, shift);
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
-        o[i] = (double)*(c.bb(j) ? F.at(i, c.s) : F.at(j, c.nb(j)));
+        o[i] = from_store(*(c.bb(j) ? F.at(i, c.s) : F.at(j, c.nb(j))), i, shift);
       }
       break;
     case kExEt:  // EtStepper::extract_natural, direct (p/src/scheme_et.cpp:83-109)
-      o[0] = (double)*F.at(0, c.s);
+      o[0] = from_store(*F.at(0, c.s), 0, shift);
 #pragma unroll
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
-        o[i] = (double)*F.at(B.b[i], c.s);
-        o[j] = (double)*F.at(c.bb(i) ? B.b[i] : B.b[j], c.nb(i));
+        o[i] = from_store(*F.at(B.b[i], c.s), i, shift);
+        o[j] = from_store(*F.at(c.bb(i) ? B.b[i] : B.b[j], c.nb(i)), j, shift);
       }
       break;
   }
@@ -163,19 +180,19 @@ __global__ void k_load(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint3
   switch (mode) {
     case kExNatural:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) *F.at(i, c.s) = (T)v[i];
+      for (int i = 0; i < 19; ++i) *F.at(i, c.s) = to_store<T>(v[i], i, in.rho0);
       break;
     case kExOpposed:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) *F.at(opp(i), c.s) = (T)v[i];
+      for (int i = 0; i < 19; ++i) *F.at(opp(i), c.s) = to_store<T>(v[i], i, in.rho0);
       break;
     case kExEt:  // EtStepper::fill, direct (p/src/scheme_et.cpp:152-169), identity handles
-      *F.at(0, c.s) = (T)v[0];
+      *F.at(0, c.s) = to_store<T>(v[0], 0, in.rho0);
 #pragma unroll
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
-        *F.at(i, c.s) = (T)v[i];
-        *F.at(c.bb(i) ? i : j, c.nb(i)) = (T)v[j];
+        *F.at(i, c.s) = to_store<T>(v[i], i, in.rho0);
+        *F.at(c.bb(i) ? i : j, c.nb(i)) = to_store<T>(v[j], j, in.rho0);
       }
       break;
   }
@@ -183,7 +200,7 @@ __global__ void k_load(Fld<T, AOS> F, Lat L, const uint32_t* cell_of_node, uint3
 
 template <class T, bool AOS>
 __global__ void k_extract_idx(Fld<T, AOS> F, Idx I, uint32_t n0, uint32_t count, int mode,
-                              EtBase B, double* buf) {
+                              EtBase B, double* buf, double shift) {
   const uint32_t k = blockIdx.x * kBlock + threadIdx.x;
   if (k >= count) return;
   const uint32_t node = n0 + k;
@@ -191,38 +208,38 @@ __global__ void k_extract_idx(Fld<T, AOS> F, Idx I, uint32_t n0, uint32_t count,
   switch (mode) {
     case kExNatural:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(i, node);
+      for (int i = 0; i < 19; ++i) o[i] = from_store(*F.at(i, node), i, shift);
       break;
     case kExOpposed:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) o[i] = (double)*F.at(opp(i), node);
+      for (int i = 0; i < 19; ++i) o[i] = from_store(*F.at(opp(i), node), i, shift);
       break;
     case kExGather:  // gather_out_indirect (p/src/stepper.cpp:254-271)
-      o[0] = (double)*F.at(0, node);
+      o[0] = from_store(*F.at(0, node), 0, shift);
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
         const uint32_t src = I.adj[(size_t)(j - 1) * I.n + node];
-        o[i] = (double)*(src == node ? F.at(j, node) : F.at(i, src));
+        o[i] = from_store(*(src == node ? F.at(j, node) : F.at(i, src)), i, shift);
       }
       break;
     case kExAaOdd:  // p/src/scheme_aap.cpp:81-97
-      o[0] = (double)*F.at(0, node);
+      o[0] = from_store(*F.at(0, node), 0, shift);
 #pragma unroll
       for (int i = 1; i < 19; ++i) {
         const int j = opp(i);
         const uint32_t e = I.adj[(size_t)(j - 1) * I.n + node];
-        o[i] = (double)*(e == node ? F.at(i, node) : F.at(j, e));
+        o[i] = from_store(*(e == node ? F.at(i, node) : F.at(j, e)), i, shift);
       }
       break;
     case kExEt:  // p/src/scheme_et.cpp:110-123
-      o[0] = (double)*F.at(0, node);
+      o[0] = from_store(*F.at(0, node), 0, shift);
 #pragma unroll
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
         const uint32_t r = I.rem[(size_t)p * I.n + node] & 0x7fffffffu;
-        o[i] = (double)*F.at(B.b[i], node);
-        o[j] = (double)*F.at(r >= I.n ? B.b[i] : B.b[j], r);
+        o[i] = from_store(*F.at(B.b[i], node), i, shift);
+        o[j] = from_store(*F.at(r >= I.n ? B.b[i] : B.b[j], r), j, shift);
       }
       break;
   }
@@ -248,20 +265,20 @@ __global__ void k_load_idx(Fld<T, AOS> F, Idx I, Lat L, const uint32_t* cell_of_
   switch (mode) {
     case kExNatural:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) *F.at(i, node) = (T)v[i];
+      for (int i = 0; i < 19; ++i) *F.at(i, node) = to_store<T>(v[i], i, in.rho0);
       break;
     case kExOpposed:
 #pragma unroll
-      for (int i = 0; i < 19; ++i) *F.at(opp(i), node) = (T)v[i];
+      for (int i = 0; i < 19; ++i) *F.at(opp(i), node) = to_store<T>(v[i], i, in.rho0);
       break;
     case kExEt:  // EtStepper::fill, indirect (p/src/scheme_et.cpp:170-183)
-      *F.at(0, node) = (T)v[0];
+      *F.at(0, node) = to_store<T>(v[0], 0, in.rho0);
 #pragma unroll
       for (int p = 0; p < 9; ++p) {
         const int i = pair_i(p), j = pair_j(p);
         const uint32_t r = I.rem[(size_t)p * I.n + node] & 0x7fffffffu;
-        *F.at(i, node) = (T)v[i];
-        *F.at(r >= I.n ? i : j, r) = (T)v[j];
+        *F.at(i, node) = to_store<T>(v[i], i, in.rho0);
+        *F.at(r >= I.n ? i : j, r) = to_store<T>(v[j], j, in.rho0);
       }
       break;
   }
@@ -510,7 +527,7 @@ void launch_extract(cudaStream_t st, const DField& f, const dev::Lat& L,
   if (count == 0) return;
   LBM_DISPATCH(f, {
     k_extract<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), L, cell_of_node, n0,
-                                                        count, mode, base, buf);
+                                                        count, mode, base, buf, f.shift);
   });
 }
 
@@ -543,7 +560,7 @@ void launch_extract_idx(cudaStream_t st, const DField& f, const Idx& I, uint32_t
   if (count == 0) return;
   LBM_DISPATCH(f, {
     k_extract_idx<T, A><<<grid_for(count), kBlock, 0, st>>>(fld<T, A>(f), I, n0, count, mode,
-                                                            base, buf);
+                                                            base, buf, f.shift);
   });
 }
 

@@ -17,12 +17,14 @@ struct DField {
   long long stride = 0;
   bool aos = false;
   Prec prec = Prec::f64;
+  double shift = 0.0;  // rho0 of the stepper: fp32 slots hold f_i - w_i shift (kShifted)
 };
 
 // TrtOperator coefficients in double (cast per launch for fp32)
 struct TrtHost {
   double lambda_e, le_half, lo_half, w0;
   double w2[9], f3w[9];
+  double rho0;  // fp32 fields store f_i - w_i rho0 (lbm_device.cuh kShifted)
 };
 
 struct EtBase {

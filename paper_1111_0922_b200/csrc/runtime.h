@@ -107,6 +107,7 @@ inline TrtHost make_trt(const lbmgpu_flow& p, bool zero_collision) {
   t.le_half = 0.5 * le;
   t.lo_half = 0.5 * lo;
   t.w0 = w_of(0);
+  t.rho0 = p.rho0;
   for (int q = 0; q < 9; ++q) {
     const int i = kPi[q];
     double cg = 0.0;
@@ -286,6 +287,7 @@ class Stepper {
     CK(cudaSetDevice(opt_.device));
     InitSpec spec;
     spec.source = kSrcBuffer;
+    spec.rho0 = rho0_;  // the fp32 storage offset
     for_chunks([&](uint32_t n0, uint32_t cnt) {
       const double* d = in + (size_t)n0 * 19;
       if (!in_on_device) {
@@ -343,6 +345,7 @@ class Stepper {
     f.stride = stride;
     f.aos = aos_;
     f.prec = prec_;
+    f.shift = rho0_;
     return f;
   }
   size_t esize() const { return prec_ == Prec::f64 ? 8 : 4; }
