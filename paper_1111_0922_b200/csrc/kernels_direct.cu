@@ -161,8 +161,12 @@ __device__ __forceinline__ void os_pull_plain(const SoaNb<T>& Am, const SoaNb<T>
 // C1 1S 0.99 -> 1.01, 2S 0.98 -> 1.01, measured)
 template <class T, bool NT>
 constexpr bool kOsPullTab = sizeof(T) == 4 && NT;
+// fp32 SoA OSNT at 6 blocks per SM (<= 40 registers; with the deviation
+// collision C1 1S 0.95 -> 1.01), the plain pull keeps 5 (1.03 vs 1.01)
+template <class T, bool AOS, bool NT>
+constexpr int kOsPullBlocks = (NT && sizeof(T) == 4 && !AOS) ? 6 : OsMinBlocks<T, AOS>::value;
 template <class T, bool AOS, bool NT, bool TWO_S>
-__global__ void __launch_bounds__(kBlock, OsMinBlocks<T, AOS>::value)
+__global__ void __launch_bounds__(kBlock, kOsPullBlocks<T, AOS, NT>)
     k_os_pull(FldSel<T, AOS, kOsPullTab<T, NT>> a, FldSel<T, AOS, kOsPullTab<T, NT>> b, Lat L,
               Trt<T> op, SoaNb<T> Am, SoaNb<T> B0) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;

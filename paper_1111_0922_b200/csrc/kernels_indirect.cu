@@ -287,9 +287,12 @@ __device__ __forceinline__ void et_idx_node(const Fld<T, AOS>& F, const Idx& I, 
 #pragma unroll
   for (int p = 0; p < 9; ++p) {
     const int i = pair_i(p), j = pair_j(p);
-    const bool ub = (rs[p] & 0x80000000u) != 0;
+    // fp32 SoA (6 blocks per SM, <= 42 registers): re-read the rem entry (an
+    // L1 hit) instead of keeping nine live across the collision
+    const uint32_t rv = (sizeof(T) == 4 && !AOS) ? ldidx(I.rem + (size_t)p * I.n + node) : rs[p];
+    const bool ub = (rv & 0x80000000u) != 0;
     st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
-    st<false>(F.at(hb<SW>(j), rs[p] & 0x7fffffffu), f[i]);
+    st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
   }
 }
 template <class T, bool AOS, bool SW>
