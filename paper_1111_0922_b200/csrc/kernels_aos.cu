@@ -372,7 +372,7 @@ __device__ __forceinline__ void copy_row_lane(T* s, const T* g, int n, bool lo_f
 template <class T>
 __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g, T* buf,
                                            int* ph, const Tile& t, int z, const T* wlo,
-                                           const T* whi, uint64_t* bar) {
+                                           const T* whi, uint64_t* bar, int loader = -1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // a periodic z wrap may read a saved copy of the wrapped plane (CG groups:
   // the plane itself may already be overwritten by an earlier group)
@@ -387,7 +387,7 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
     // the loading warp: the first warp beyond the tile rows where there is
     // one (the fp64 gather modes' extra warps: loads overlap the compute
     // warps' work, C1 OS pull 0.68 -> 0.76), else warp 0
-    const int lw = (int)(blockDim.x >> 5) > kTY ? kTY : 0;
+    const int lw = loader >= 0 ? loader : ((int)(blockDim.x >> 5) > kTY ? kTY : 0);
     if (warp != lw) return;
     const int r = lane;
     if (r >= t.tyv + 2) return;
@@ -404,13 +404,14 @@ __device__ __forceinline__ void load_plane(const Lat& L, const T* __restrict__ g
         if (t.x0 == 0) gl = g + ((size_t)rb + (size_t)(L.nx - 1)) * 19;
         if (t.x0 + t.txv == L.nx) gr = g + (size_t)rb * 19;
       }
+      ph[r] = phase;  // before the arrivals: readers acquire it through the barrier
       copy_row_lane(srow + (xa - t.x0 + 1) * 19, g + ((size_t)rb + (size_t)(xa + L.ox)) * 19,
                     (xb - xa + 1) * 19, gl == nullptr, gr == nullptr, srow, gl,
                     srow + (t.txv + 1) * 19, gr, bar);
     } else {
+      ph[r] = phase;
       mbar_arrive(bar, kRowArrivals);
     }
-    ph[r] = phase;
   } else {
   for (int r = warp; r < t.tyv + 2; r += (int)(blockDim.x >> 5)) {
     uint32_t rb;
@@ -581,8 +582,11 @@ __device__ __forceinline__ uint32_t zmask_of(const Tile& t, int z) {
 template <int MODE, class T>
 __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g, const T* buf,
                                                 const int* ph, uint32_t* msk, int* mcol,
-                                                const uint32_t* gmask, const Tile& t, int z) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                                const uint32_t* gmask, const Tile& t, int z,
+                                                int warp0 = 0, int nwarps = 0) {
+  // the warps [warp0, warp0 + nwarps) do the work (default: the whole block)
+  if (nwarps == 0) nwarps = (int)(blockDim.x >> 5);
+  const int warp = (int)(threadIdx.x >> 5) - warp0, lane = threadIdx.x & 31;
   const bool zin = z >= t.zb + 1 && z <= t.ze - 2;
   const int w = t.txv + 2, rows = t.tyv + 2;
   const bool can_run = zin && t.txv >= 3;
@@ -590,7 +594,7 @@ __device__ __forceinline__ void writeback_plane(const Lat& L, T* __restrict__ g,
   const int nrun = can_run ? max(0, t.tyv - 2) : 0;
   const int nfull = rows - nrun;
   const int nitems = 2 * nfull + nrun;
-  for (int it = warp; it < nitems; it += (int)(blockDim.x >> 5)) {
+  for (int it = warp; it < nitems; it += nwarps) {
     int r, c0, c1;  // row, column range [c0, c1) for the slot-by-slot pass
     bool run;
     if (it < 2 * nfull) {
@@ -737,8 +741,12 @@ __device__ __forceinline__ int wb_build(const Lat& L, const Tile& t, const uint3
 template <class T>
 __device__ __forceinline__ void writeback_fast(T* __restrict__ g, const T* ring, const WbList& wl,
                                                const long long* rbp, const int* sbp,
-                                               const Tile& t, uint32_t zm = ~0u) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+                                               const Tile& t, uint32_t zm = ~0u, int warp0 = 0,
+                                               int nwarps = 0) {
+  // the warps [warp0, warp0 + nwarps) do the work (default: the whole block)
+  if (nwarps == 0) nwarps = (int)(blockDim.x >> 5);
+  const int warp = (int)(threadIdx.x >> 5) - warp0, lane = threadIdx.x & 31, nw = nwarps;
+  const int tid = (int)threadIdx.x - 32 * warp0, nthr = 32 * nwarps;
   const int w = t.txv + 2;
   if (zm == ~0u) {  // runs: rows 2 .. tyv-1, columns 2 .. txv-1, whole records
     for (int r = 2 + warp; r <= t.tyv - 1; r += nw)
@@ -749,13 +757,13 @@ __device__ __forceinline__ void writeback_fast(T* __restrict__ g, const T* ring,
   } else {  // the run records' zm slots
     const int nk = __popc(zm), ncol = t.txv - 2, nrun = max(0, t.tyv - 2);
     const int n = nrun * ncol * nk;
-    for (int e = threadIdx.x; e < n; e += (int)blockDim.x) {
+    for (int e = tid; e < n; e += nthr) {
       const int kk = e % nk, rc = e / nk, r = 2 + rc / ncol, q = 2 + rc % ncol;
       const int off = q * 19 + (int)__fns(zm, 0, kk + 1);
       g[rbp[r] + off] = ring[sbp[r] + off];
     }
   }
-  for (int e = threadIdx.x; e < wl.n; e += (int)blockDim.x) {
+  for (int e = tid; e < wl.n; e += nthr) {
     const uint32_t v = wl.e[e];
     const int r = (int)(v >> 11), q = (int)((v >> 5) & 63u), k = (int)(v & 31u);
     if (!((zm >> k) & 1u)) continue;
@@ -1051,6 +1059,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         if (pz && z == 0) wrapped |= kMzm;
         if (pz && z == L.nz - 1) wrapped |= kMzp;
       }
+#ifdef LBM_WIN_NO_COMPUTE
+      live = false;  // experiment: load + write-back pipeline only (wrong results)
+#endif
       if (live) {
         if (interior)
           win_node<MODE, false>(op, bounce, f, at, wrapped);
@@ -1071,6 +1082,9 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
     WIN_T(4);  // compute (+ per-node stores into the ring)
     __syncthreads();  // every read of plane z - 1 is done
     WIN_T(5);  // waiting for the slowest warp's compute
+#ifdef LBM_WIN_NO_WB
+    if (false)  // experiment: load + compute only (wrong results)
+#endif
     if constexpr (owned_wb(MODE)) {
       if (fast_plane(z - 1))
         writeback_fast(dst.p, sm, wl, rbp, sbp, t);
@@ -1132,6 +1146,196 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
         writeback_plane<MODE>(L, dst.p, sm + slot(zp) * BUF, ph[slot(zp)], msk, mcol, gmask, t, zp);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised in-place window (AA odd, ET, SWAP exchange; fp64). The
+// plain k_win runs load issue, compute and write-back of a plane in series
+// between block barriers (C1 fp64 AA odd: load pipeline alone 0.60 ms, +
+// compute 0.31, + write-back 0.43 = 1.35 ms; they add up). Here a 32 x 6
+// tile's six row warps compute plane z while the write-back warps (ten)
+// write back plane z - 2
+// (final once every row warp has computed z - 1) and then refill its ring
+// slot with plane z + 3: a 5-plane ring (34 x 8 records per plane, 207 KB
+// fp64), hand-offs through mbarriers only:
+//   full[s]  the plane in slot s has landed (bulk-copy bytes + cp.async)
+//   comp[s]  the six row warps have computed the plane in slot s
+// Every slot (k, R) is read and rewritten by exactly one node of an in-place
+// sweep, so the row warps need no ordering among themselves; a plane is
+// final (write-back) once the row warps computed the plane above it, and a
+// row warp can be at most three planes ahead of the write-back (it waits for
+// loads that follow the write-back), inside the 5-use parity window.
+constexpr int kTYw = 6, kWRw = kTYw + 2, kNBw = 5;
+// write-back warps (measured on C1 fp64: 2 -> AA 0.51, 4 -> 0.66, 6 -> 0.67,
+// 8 -> 0.74, 10 -> 0.77 of the roofline; the row warps' register cap at 512
+// threads costs a few spills); storing the rim slots straight from the row
+// warps instead of a list pass measured 0.70
+#ifndef LBM_WS_WB
+#define LBM_WS_WB 10
+#endif
+constexpr int kWsCompute = kTYw, kWsWb = LBM_WS_WB, kWsThreads = 32 * (kWsCompute + kWsWb);
+template <class T>
+struct WinSzW {
+  static constexpr int ROW = WinSz<T>::ROW;
+  static constexpr int BUF = kWRw * ROW;
+  static constexpr size_t kBytes = (size_t)kNBw * BUF * sizeof(T);
+};
+static_assert(WinSzW<double>::kBytes <= 227 * 1024 - 12 * 1024, "fp64 ws ring too large");
+
+__device__ __forceinline__ void wb_group_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kWsWb) : "memory");
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(kWsThreads, sizeof(T) == 8 ? 1 : 2)
+    k_win_ws(Fld<T, true> fld_, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
+  static_assert(in_place(MODE), "warp-specialised window: in-place modes only");
+  extern __shared__ __align__(16) unsigned char win_smem[];
+  T* sm = reinterpret_cast<T*>(win_smem);
+  T* const g = fld_.p;
+  __shared__ int ph[kNBw][kWRw];
+  __shared__ uint32_t msk[kWsWb * kWC];
+  __shared__ int mcol[kWsWb * kWC];
+  __shared__ uint32_t gmask[kWR * kWC];
+  __shared__ uint16_t wlist[kListMax];
+  __shared__ int wcnt[kWR + 1];
+  __shared__ long long rbp[kWRw];
+  __shared__ int sbp[kWRw];
+  __shared__ __align__(8) uint64_t full[kNBw];
+  __shared__ __align__(8) uint64_t comp[kNBw];
+  constexpr int BUF = WinSzW<T>::BUF, ROW = WinSzW<T>::ROW;
+
+  const int ntile = tiles_x * tiles_y;
+  const int tile = (int)blockIdx.x % ntile, chunk = (int)blockIdx.x / ntile;
+  Tile t;
+  t.x0 = (tile % tiles_x) * kTX;
+  t.y0 = (tile / tiles_x) * kTYw;
+  t.txv = min(kTX, L.nx - t.x0);
+  t.tyv = min(kTYw, L.ny - t.y0);
+  t.zb = chunk * zc;
+  t.ze = min(L.nz, t.zb + zc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = threadIdx.x; q < kWRw * kWC; q += blockDim.x)
+    gmask[q] = owned_slots_xy<MODE>(t, q % kWC, q / kWC);
+  WbList wl{wlist, 0, 0, 0, 0};
+  const bool fast = wb_fast_ok(L, t);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kNBw; ++b) {
+      mbar_init(&full[b], (uint32_t)(t.tyv + 2) * kRowArrivals);
+      mbar_init(&comp[b], (uint32_t)kWsCompute);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (fast) {
+    wl.n = wb_build(L, t, gmask, wlist, wcnt);  // all threads, block barriers inside
+    int xs0 = 0, xs1 = 0;
+    col_xs(L, t.x0, 0, xs0);
+    col_xs(L, t.x0, t.txv + 1, xs1);
+    wl.colb0 = (long long)(t.x0 - 1 + L.ox) * 19;
+    wl.d1 = (xs0 - (t.x0 - 1 + L.ox)) * 19;
+    wl.d2 = (xs1 - (t.x0 + t.txv + L.ox)) * 19;
+  }
+  auto slot = [&](int z) { return (z - t.zb + 1) % kNBw; };
+  // parity of plane z's phase of full[slot(z)] (every plane zb - 1 .. ze is
+  // loaded once) and of comp[slot(z)] (only planes zb .. ze - 1 are computed;
+  // slot 0's first plane, zb - 1, is not)
+  auto use = [&](int z) { return (uint32_t)((z - t.zb + 1) / kNBw) & 1u; };
+  auto cuse = [&](int z) {
+    return (uint32_t)((z - t.zb + 1) / kNBw - (slot(z) == 0 ? 1 : 0)) & 1u;
+  };
+  auto fast_plane = [&](int zp) { return fast && zp >= t.zb + 1 && zp <= t.ze - 2; };
+  auto face_zm = [&](int zp) -> uint32_t {
+    int zcell;
+    if (!fast || !axis_cell(zp, L.nz, L.wall[2], L.oz, zcell)) return 0u;
+    if (L.wall[2] && (zcell == 0 || zcell == L.nz - 1)) return 0u;
+    return zmask_of<MODE>(t, zp);
+  };
+  constexpr int kLoader = kWsCompute + kWsWb - 1;  // the last write-back warp issues loads
+  auto load = [&](int z) {
+    load_plane(L, (const T*)g, sm + slot(z) * BUF, ph[slot(z)], t, z, (const T*)nullptr,
+               (const T*)nullptr, &full[slot(z)], kLoader);
+  };
+
+  if (warp < kWsCompute) {
+    // ---- row warps: compute planes zb .. ze - 1 --------------------------------
+    const int tx = lane, ty = warp;
+    const bool valid = tx < t.txv && ty < t.tyv;
+    for (int z = t.zb; z < t.ze; ++z) {
+      if (z == t.zb) {
+        mbar_wait(&full[slot(z - 1)], use(z - 1));
+        mbar_wait(&full[slot(z)], use(z));
+      }
+      mbar_wait(&full[slot(z + 1)], use(z + 1));
+      int rp[3][3];
+#pragma unroll
+      for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+          const int sl = slot(z - 1 + dz), r = ty + dy;
+          rp[dz][dy] = sl * BUF + r * ROW + ph[sl][r] + (tx + 1) * 19;
+        }
+      auto at = [&](int i, int k) -> T& { return sm[rp[1 + cz(i)][1 + cy(i)] + cx(i) * 19 + k]; };
+      uint32_t bounce = 0;
+      bool live = false;
+      if (valid) live = cell_links(L, t.x0 + tx, t.y0 + ty, z, bounce);
+      const bool interior = __all_sync(0xffffffffu, bounce == 0u);
+      uint32_t wrapped = 0;
+      if constexpr (MODE == kWinSwap) {
+        const int x = t.x0 + tx, y = t.y0 + ty;
+        if (!L.wall[0] && x == 0) wrapped |= kMxm;
+        if (!L.wall[0] && x == L.nx - 1) wrapped |= kMxp;
+        if (!L.wall[1] && y == 0) wrapped |= kMym;
+        if (!L.wall[1] && y == L.ny - 1) wrapped |= kMyp;
+        if (!L.wall[2] && z == 0) wrapped |= kMzm;
+        if (!L.wall[2] && z == L.nz - 1) wrapped |= kMzp;
+      }
+      T f[19];
+      if (live) {
+        if (interior)
+          win_node<MODE, false>(op, bounce, f, at, wrapped);
+        else
+          win_node<MODE, true>(op, bounce, f, at, wrapped);
+      }
+      if constexpr (kBulk) fence_async_smem();  // ring writes before the write-back's bulk stores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&comp[slot(z)], 1);
+    }
+    return;
+  }
+
+  // ---- write-back warps: plane zp once the row warps computed zp + 1, then
+  // refill its slot with plane zp + kNBw ------------------------------------
+  const int w0 = kWsCompute;
+  if (warp == kLoader)
+    for (int z = t.zb - 1; z <= min(t.ze, t.zb - 1 + kNBw - 1); ++z) load(z);
+  auto writeback = [&](int zp) {
+    const uint32_t zm = fast_plane(zp) ? ~0u : face_zm(zp);
+    if (zm) {
+      const int r = (int)threadIdx.x - 32 * w0;
+      if (r < t.tyv + 2) {
+        uint32_t rb = 0;
+        row_base(L, t.y0 - 1 + r, zp, rb);
+        rbp[r] = (long long)rb * 19 + wl.colb0;
+        sbp[r] = slot(zp) * BUF + r * ROW + ph[slot(zp)][r];
+      }
+      wb_group_sync();
+      writeback_fast(g, sm, wl, rbp, sbp, t, zm, w0, kWsWb);
+    } else {
+      writeback_plane<MODE>(L, g, sm + slot(zp) * BUF, ph[slot(zp)], msk, mcol, gmask, t, zp, w0,
+                            kWsWb);
+    }
+    if constexpr (kBulk) bulk_wait_read();  // the slot's bulk stores have read it
+    wb_group_sync();
+  };
+  for (int z = t.zb; z < t.ze; ++z) {
+    mbar_wait(&comp[slot(z)], cuse(z));
+    writeback(z - 1);
+    if (warp == kLoader && z - 1 + kNBw <= t.ze) load(z - 1 + kNBw);
+  }
+  writeback(t.ze - 1);
+  writeback(t.ze);
+  if constexpr (kBulk) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -1274,6 +1478,30 @@ bool window_enabled() {
   return on;
 }
 
+#ifndef LBM_AOS_WS
+#define LBM_AOS_WS 1
+#endif
+template <class T, int MODE>
+void launch_win_ws(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op) {
+  const int per_sm = ensure_smem<k_win_ws<T, MODE>>(kWsThreads, WinSzW<T>::kBytes);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTYw - 1) / kTYw;
+  // z planes per block: about 7 waves of resident blocks, 4 .. 64 planes, and
+  // at least two chunks on a periodic z axis (the halo plane is not one of
+  // the chunk's own planes)
+  const long long tiles = (long long)tiles_x * tiles_y, resident = (long long)sms * per_sm;
+  long long zc = (L.nz * tiles + resident * 7 - 1) / (resident * 7);
+  zc = std::max(4LL, std::min(64LL, zc));
+  if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))
+    if (std::atoi(e) > 0) zc = std::atoi(e);
+  if (!L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
+  zc = std::max(1LL, std::min<long long>(zc, L.nz));
+  const int nzc = (int)((L.nz + zc - 1) / zc);
+  k_win_ws<T, MODE><<<(unsigned)(tiles * nzc), kWsThreads, WinSzW<T>::kBytes, st>>>(
+      fld<T, true>(f), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc);
+}
+
 template <class T, int MODE>
 void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
                 const TrtHost& op, int zc, int z0, int z1, const void* wlo = nullptr,
@@ -1331,6 +1559,22 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // (its bulk write-back runs use the source rows' 16-byte phase)
   const bool congruent = ((reinterpret_cast<uintptr_t>(a.p) ^ reinterpret_cast<uintptr_t>(b.p)) & 15u) == 0;
   if (mode == kWinPush && distinct && f64 && congruent) mode = kWinPushS;
+  // fp64 in-place modes: the warp-specialised window where its 32 x 6 tile
+  // keeps every window position a distinct record (a 34 x 8 window on
+  // periodic y); fp32 measured no better with it (C1 AA 0.61 -> 0.62, C4 0.51
+  // -> 0.52) and keeps k_win at two blocks per SM
+  if (LBM_AOS_WS && f64 && in_place(mode) && (L.wall[1] || L.ny >= kTYw + 2)) {
+#define LBM_WS_CASES(T)                                                   \
+  switch (mode) {                                                         \
+    case kWinAaOdd: launch_win_ws<T, kWinAaOdd>(st, a, L, op); break;     \
+    case kWinSwap: launch_win_ws<T, kWinSwap>(st, a, L, op); break;       \
+    case kWinEtI: launch_win_ws<T, kWinEtI>(st, a, L, op); break;         \
+    default: launch_win_ws<T, kWinEtS>(st, a, L, op); break;              \
+  }
+    LBM_WS_CASES(double)
+#undef LBM_WS_CASES
+    return true;
+  }
   const int zc = window_chunk(L, f64, owned_wb(mode));
 #define LBM_WIN_CASES(T)                                                              \
   switch (mode) {                                                                     \
