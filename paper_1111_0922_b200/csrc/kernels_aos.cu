@@ -1186,8 +1186,14 @@ __device__ __forceinline__ void wb_group_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kWsWb) : "memory");
 }
 
+#ifndef LBM_WS_F32
+#define LBM_WS_F32 0
+#endif
+#ifndef LBM_WS_F32_BLOCKS
+#define LBM_WS_F32_BLOCKS 1
+#endif
 template <class T, int MODE>
-__global__ void __launch_bounds__(kWsThreads, sizeof(T) == 8 ? 1 : 2)
+__global__ void __launch_bounds__(kWsThreads, sizeof(T) == 8 ? 1 : LBM_WS_F32_BLOCKS)
     k_win_ws(Fld<T, true> fld_, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
   static_assert(in_place(MODE), "warp-specialised window: in-place modes only");
   extern __shared__ __align__(16) unsigned char win_smem[];
@@ -1563,7 +1569,7 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // keeps every window position a distinct record (a 34 x 8 window on
   // periodic y); fp32 measured no better with it (C1 AA 0.61 -> 0.62, C4 0.51
   // -> 0.52) and keeps k_win at two blocks per SM
-  if (LBM_AOS_WS && f64 && in_place(mode) && (L.wall[1] || L.ny >= kTYw + 2)) {
+  if (LBM_AOS_WS && (f64 || LBM_WS_F32) && in_place(mode) && (L.wall[1] || L.ny >= kTYw + 2)) {
 #define LBM_WS_CASES(T)                                                   \
   switch (mode) {                                                         \
     case kWinAaOdd: launch_win_ws<T, kWinAaOdd>(st, a, L, op); break;     \
@@ -1571,7 +1577,11 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     case kWinEtI: launch_win_ws<T, kWinEtI>(st, a, L, op); break;         \
     default: launch_win_ws<T, kWinEtS>(st, a, L, op); break;              \
   }
-    LBM_WS_CASES(double)
+    if (f64) {
+      LBM_WS_CASES(double)
+    } else {
+      LBM_WS_CASES(float)
+    }
 #undef LBM_WS_CASES
     return true;
   }
