@@ -1149,6 +1149,190 @@ __global__ void __launch_bounds__(WinThreads<T, MODE>::value, sizeof(T) == 8 ? 1
 }
 
 // ---------------------------------------------------------------------------
+// Register-carried z pipeline for the gather modes (OS / OSNT pull, TS
+// stream). Node X at plane q reads its 19 values from plane q - 1 (the five
+// c_z = +1 directions), plane q (c_z = 0, the rest value and every bounced
+// link: own record) and plane q + 1 (c_z = -1). A thread owns one (x, y)
+// column of the tile and collects while the planes pass: with plane p in
+// the ring it takes the c_z = -1 values of its node p - 1 (then complete:
+// collide, stage, store), the c_z = 0 values of node p and the c_z = +1
+// values of node p + 1 (five registers carried to the next plane). Every
+// plane is read during ONE iteration, so of the NS ring slots one holds the
+// plane being read, one (the previous plane's) stages this iteration's
+// output records and NS - 2 are loads in flight; k_win keeps three planes
+// resident for its gathers and has one in flight. One block barrier per
+// plane (the previous slot's reads and the bulk stores' reads of the slot
+// before it are done before that slot is refilled).
+// ---------------------------------------------------------------------------
+#ifndef LBM_ZP_NS64
+#define LBM_ZP_NS64 4
+#endif
+#ifndef LBM_ZP_NS32
+#define LBM_ZP_NS32 4
+#endif
+#ifndef LBM_ZP_TY64
+#define LBM_ZP_TY64 8
+#endif
+#ifndef LBM_ZP_TY32
+#define LBM_ZP_TY32 8
+#endif
+template <class T>
+struct ZpCfg {
+  static constexpr int TY = sizeof(T) == 8 ? LBM_ZP_TY64 : LBM_ZP_TY32;  // tile rows (row warps)
+  static constexpr int NS = sizeof(T) == 8 ? LBM_ZP_NS64 : LBM_ZP_NS32;  // ring slots
+  static constexpr int ROW = WinSz<T>::ROW;
+  static constexpr int BUF = (TY + 2) * ROW;
+  static constexpr size_t kBytes = (size_t)NS * BUF * sizeof(T);
+  static constexpr int kThreads = 32 * (TY + 1);  // + one loading warp
+  static constexpr int kBlocks = (int)((227 * 1024) / (kBytes + 2048)) > 0 ? (int)((227 * 1024) / (kBytes + 2048)) : 1;
+};
+static_assert(ZpCfg<double>::kBytes <= 227 * 1024 - 1024, "fp64 z-pipeline ring too large");
+static_assert(ZpCfg<float>::kBytes <= 227 * 1024 - 1024, "fp32 z-pipeline ring too large");
+static_assert(ZpCfg<double>::NS >= 3 && ZpCfg<float>::NS >= 3, "z pipeline: at least one plane in flight");
+
+// the gathers of one plane: node p - 1 (c_z = -1), node p (c_z = 0 and the
+// bounced links of every direction), node p + 1 (c_z = +1 into g5)
+template <bool BB, class T, class At>
+__device__ __forceinline__ void zp_take_prev(T (&f)[19], uint32_t b, At at) {
+#pragma unroll
+  for (int i = 1; i < 19; ++i)
+    if (cz(i) == -1 && !(BB && ((b >> opp(i)) & 1u))) f[i] = at(opp(i), i);
+}
+template <bool BB, class T, class At>
+__device__ __forceinline__ void zp_take_cur(T (&f)[19], const T (&g5)[5], uint32_t b, At at) {
+  f[0] = at(0, 0);
+#pragma unroll
+  for (int i = 1; i < 19; ++i) {
+    const int j = opp(i);
+    const bool bj = BB && ((b >> j) & 1u);
+    if (cz(i) == 0) {
+      f[i] = bj ? at(0, j) : at(j, i);
+    } else if (cz(i) == 1) {
+      int q = 0;
+#pragma unroll
+      for (int k = 1; k < i; ++k) q += cz(k) == 1 ? 1 : 0;
+      f[i] = bj ? at(0, j) : g5[q];
+    } else if (bj) {
+      f[i] = at(0, j);
+    }
+  }
+}
+template <class T, class At>
+__device__ __forceinline__ void zp_take_next(T (&g5)[5], At at) {
+  int q = 0;
+#pragma unroll
+  for (int i = 1; i < 19; ++i)
+    if (cz(i) == 1) g5[q++] = at(opp(i), i);
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(ZpCfg<T>::kThreads, ZpCfg<T>::kBlocks)
+    k_win_zp(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y,
+             int zc) {
+  static_assert(MODE == kWinPull || MODE == kWinStream || MODE == kWinPush,
+                "z pipeline: gather modes");
+  constexpr int TY = ZpCfg<T>::TY, NS = ZpCfg<T>::NS, ROW = ZpCfg<T>::ROW, BUF = ZpCfg<T>::BUF;
+  extern __shared__ __align__(16) unsigned char win_smem[];
+  T* sm = reinterpret_cast<T*>(win_smem);
+  __shared__ int ph[NS][TY + 2];
+  __shared__ __align__(8) uint64_t full[NS];
+
+  const int ntile = tiles_x * tiles_y;
+  const int tile = (int)blockIdx.x % ntile, chunk = (int)blockIdx.x / ntile;
+  Tile t;
+  t.x0 = (tile % tiles_x) * kTX;
+  t.y0 = (tile / tiles_x) * TY;
+  t.txv = min(kTX, L.nx - t.x0);
+  t.tyv = min(TY, L.ny - t.y0);
+  t.zb = chunk * zc;
+  t.ze = min(L.nz, t.zb + zc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) mbar_init(&full[b], (uint32_t)(t.tyv + 2) * kRowArrivals);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int pb = t.zb - 1, pe = t.ze;  // window planes pb .. pe
+  auto slot = [&](int p) { return (p - pb) % NS; };
+  auto par = [&](int p) { return (uint32_t)((p - pb) / NS) & 1u; };
+  auto load = [&](int p) {
+    load_plane(L, (const T*)src.p, sm + slot(p) * BUF, ph[slot(p)], t, p, (const T*)nullptr,
+               (const T*)nullptr, &full[slot(p)], TY);
+  };
+  if (warp == TY)
+    for (int p = pb; p <= min(pe, pb + NS - 1); ++p) load(p);
+
+  const int tx = lane, ty = warp;
+  const bool valid = ty < t.tyv && tx < t.txv;
+  const int x = t.x0 + tx, y = t.y0 + ty;
+  T f[19], g5[5];
+  uint32_t bq = 0;   // bounce mask of the node held in f
+  bool lq = false;   // ... and whether it is a fluid cell
+  for (int p = pb; p <= pe; ++p) {
+    // slot(p - 2) staged iteration p - 1's output: its bulk stores must have
+    // read it, and every thread is done with plane p - 1 (slot(p - 1) stages
+    // this iteration's output)
+    bulk_wait_read();
+    fence_async_smem();
+    __syncthreads();
+    if (warp == TY && p - 2 >= pb && p - 2 + NS <= pe) load(p - 2 + NS);
+    if constexpr (MODE == kWinPush) {
+      // OS push as a gather of post-collision values: every window record of
+      // plane p collides in place first (the halo records redundantly in
+      // both neighbouring tiles: deterministic, identical)
+      mbar_wait(&full[slot(p)], par(p));
+      collide_plane(L, op, sm + slot(p) * BUF, ph[slot(p)], t, p);
+      __syncthreads();
+    }
+    if (warp == TY || ty >= t.tyv) continue;
+    mbar_wait(&full[slot(p)], par(p));
+    const int s = slot(p);
+    int rp[3];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) rp[dy] = s * BUF + (ty + dy) * ROW + ph[s][ty + dy] + (tx + 1) * 19;
+    // slot k of the record at (x + cx(i), y + cy(i)) in plane p
+    auto at = [&](int i, int k) -> T { return sm[rp[1 + cy(i)] + cx(i) * 19 + k]; };
+    if (p - 1 >= t.zb) {  // node p - 1: its last five values, then collide and store
+      const bool plain = __all_sync(0xffffffffu, !lq || bq == 0u);
+      if (lq) {
+        if (plain)
+          zp_take_prev<false>(f, bq, at);
+        else
+          zp_take_prev<true>(f, bq, at);
+        if constexpr (MODE == kWinPull) collide(op, f);
+      }
+      uint32_t rb;
+      row_base(L, y, p - 1, rb);
+      const long long v0 = (long long)rb + L.ox + t.x0;
+      const int phase = (int)(((reinterpret_cast<uintptr_t>(dst.p) +
+                                (uintptr_t)(v0 * 19 * (long long)sizeof(T))) & 15u) / sizeof(T));
+      T* srow = sm + slot(p - 1) * BUF + ty * ROW + phase;
+      if (tx < t.txv) {
+#pragma unroll
+        for (int i = 0; i < 19; ++i) srow[tx * 19 + i] = lq ? f[i] : T(0);
+      }
+      __syncwarp();
+      copy_out_bulk(dst.p + (size_t)v0 * 19, srow, t.txv * 19, tx);
+    }
+    if (p >= t.zb && p < t.ze) {  // node p: c_z = 0, bounced links, c_z = +1 from g5
+      uint32_t b = 0;
+      const bool l = valid && cell_links(L, x, y, p, b);
+      const bool plain = __all_sync(0xffffffffu, !l || b == 0u);
+      if (l) {
+        if (plain)
+          zp_take_cur<false>(f, g5, b, at);
+        else
+          zp_take_cur<true>(f, g5, b, at);
+      }
+      bq = b;
+      lq = l;
+    }
+    if (p + 1 >= t.zb && p + 1 < t.ze && valid) zp_take_next(g5, at);  // node p + 1
+  }
+  bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // Warp-specialised in-place window (AA odd, ET, SWAP exchange; fp64). The
 // plain k_win runs load issue, compute and write-back of a plane in series
 // between block barriers (C1 fp64 AA odd: load pipeline alone 0.60 ms, +
@@ -1458,6 +1642,24 @@ __global__ void __launch_bounds__(kRun, MinBlocks<T>::value)
   }
 }
 
+// z planes per block of a z-marching window: blocks of equal length run in
+// waves of `resident`, a block's time ~ its planes + `halo` prologue planes,
+// so pick the chunk (4 .. 64 planes) minimising waves x (chunk + halo)
+// (C4: nz = 200 over 175 tiles: 34-plane chunks = 7.1 waves -> 8; 40-plane
+// chunks = 5.9 -> 6 waves), ties to the longer chunk
+static long long wave_chunk(long long nz, long long tiles, long long resident, int halo,
+                            long long zmax = 64) {
+  zmax = std::max(1LL, std::min({zmax, nz, 64LL}));
+  long long best = zmax, best_cost = -1;
+  for (long long zc = zmax; zc >= std::min(zmax, 4LL); --zc) {
+    const long long nzc = (nz + zc - 1) / zc, blocks = tiles * nzc;
+    const long long waves = (blocks + resident - 1) / resident;
+    const long long cost = waves * (zc + halo);
+    if (best_cost < 0 || cost < best_cost) best = zc, best_cost = cost;
+  }
+  return best;
+}
+
 // opt Kernel into more than 48 KB of dynamic shared memory on the current
 // device, once per (kernel, device): the attribute is per device and a
 // process may drive several GPUs. Returns the resident blocks per SM.
@@ -1497,8 +1699,7 @@ void launch_win_ws(cudaStream_t st, const DField& f, const Lat& L, const TrtHost
   // at least two chunks on a periodic z axis (the halo plane is not one of
   // the chunk's own planes)
   const long long tiles = (long long)tiles_x * tiles_y, resident = (long long)sms * per_sm;
-  long long zc = (L.nz * tiles + resident * 7 - 1) / (resident * 7);
-  zc = std::max(4LL, std::min(64LL, zc));
+  long long zc = wave_chunk(L.nz, tiles, resident, 2, L.wall[2] ? 64 : L.nz - 2);
   if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))
     if (std::atoi(e) > 0) zc = std::atoi(e);
   if (!L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
@@ -1521,6 +1722,46 @@ void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
       static_cast<const T*>(wlo), static_cast<const T*>(whi));
 }
 
+template <class T, int MODE>
+void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
+                   const TrtHost& op) {
+  using C = ZpCfg<T>;
+  const int per_sm = ensure_smem<k_win_zp<T, MODE>>(C::kThreads, C::kBytes);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + C::TY - 1) / C::TY;
+  // z planes per block: about 7 waves of resident blocks, 4 .. 64 planes
+  const long long tiles = (long long)tiles_x * tiles_y, resident = (long long)sms * per_sm;
+  long long zc = wave_chunk(L.nz, tiles, resident, 2);
+  if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))
+    if (std::atoi(e) > 0) zc = std::atoi(e);
+  zc = std::max(1LL, std::min<long long>(zc, L.nz));
+  const int nzc = (int)((L.nz + zc - 1) / zc);
+  k_win_zp<T, MODE><<<(unsigned)(tiles * nzc), C::kThreads, C::kBytes, st>>>(
+      fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc);
+}
+
+// OS push through the z pipeline (every window record of a plane collided in
+// place, then the stream gathers): measured slower than the scatter form
+// (fp64) and equal to the k_win gather (fp32) on C1 (0.42 / 0.47 vs 0.54 /
+// 0.47): the halo ring's redundant collisions and the extra barrier per
+// plane; opt-in LBMGPU_AOS_ZPIPE_PUSH=1
+bool zpipe_push() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_AOS_ZPIPE_PUSH");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+bool zpipe_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_AOS_ZPIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 // z planes per block: enough blocks for ~7 waves of resident blocks (one
@@ -1533,8 +1774,7 @@ static int window_chunk(const Lat& L, bool fp64, bool inplace) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (long long)((L.nx + kTX - 1) / kTX) * ((L.ny + kTY - 1) / kTY);
   const long long resident = (long long)sms * (fp64 ? 1 : 2);
-  long long zc = (L.nz * tiles + resident * 7 - 1) / (resident * 7);
-  zc = std::max(4LL, std::min(64LL, zc));
+  long long zc = wave_chunk(L.nz, tiles, resident, 2, inplace && !L.wall[2] ? L.nz - 2 : 64);
   if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))  // tests: long chunks on small boxes
     if (std::atoi(e) > 0) zc = std::atoi(e);
   if (inplace && !L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
@@ -1564,7 +1804,8 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // fp32 0.43 -> 0.38; profiles/r01_variants.md)
   // (its bulk write-back runs use the source rows' 16-byte phase)
   const bool congruent = ((reinterpret_cast<uintptr_t>(a.p) ^ reinterpret_cast<uintptr_t>(b.p)) & 15u) == 0;
-  if (mode == kWinPush && distinct && f64 && congruent) mode = kWinPushS;
+  if (mode == kWinPush && distinct && f64 && congruent && !(zpipe_enabled() && zpipe_push()))
+    mode = kWinPushS;
   // fp64 in-place modes: the warp-specialised window where its 32 x 6 tile
   // keeps every window position a distinct record (a 34 x 8 window on
   // periodic y); fp32 measured no better with it (C1 AA 0.61 -> 0.62, C4 0.51
@@ -1583,6 +1824,20 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
       LBM_WS_CASES(float)
     }
 #undef LBM_WS_CASES
+    return true;
+  }
+  // gather modes: the register-carried z pipeline
+  if ((mode == kWinPull || mode == kWinStream || (mode == kWinPush && zpipe_push())) &&
+      zpipe_enabled()) {
+    if (f64) {
+      if (mode == kWinPull) launch_win_zp<double, kWinPull>(st, a, b, L, op);
+      else if (mode == kWinPush) launch_win_zp<double, kWinPush>(st, a, b, L, op);
+      else launch_win_zp<double, kWinStream>(st, a, b, L, op);
+    } else {
+      if (mode == kWinPull) launch_win_zp<float, kWinPull>(st, a, b, L, op);
+      else if (mode == kWinPush) launch_win_zp<float, kWinPush>(st, a, b, L, op);
+      else launch_win_zp<float, kWinStream>(st, a, b, L, op);
+    }
     return true;
   }
   const int zc = window_chunk(L, f64, owned_wb(mode));

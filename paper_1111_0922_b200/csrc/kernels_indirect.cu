@@ -265,6 +265,127 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
   });
 }
 
+// ---------------------------------------------------------------------------
+// Asynchronous-gather pipeline (SoA, in-place sweeps over the IDX graph: AA
+// odd, ET). The register-held gathers of the kernels above leave a warp's
+// loads in flight only until its collision starts (C2 porous: 16 warps per
+// SM, long-scoreboard 8-9 stalls per issue, 0.75-0.89 of the roofline).
+// Here every gather is a cp.async into shared memory, one batch ahead: while
+// batch k collides from shared memory and scatters its results, the 19
+// gathers of batch k + 1 and the index rows (adjacency / rem) of batch k + 2
+// are in flight, without holding registers. Each thread gathers, and later
+// reads, only its own node's column, so only the index rows (copied as
+// 16-byte vectors by the whole block) need the block barrier. In-place
+// safety: the slots a node gathers are exactly the slots it rewrites (AA odd
+// and ET partition the slots among nodes), so batch k + 1's gathers and
+// batch k's stores never touch the same slot.
+// ---------------------------------------------------------------------------
+constexpr int kAgB = 128;  // nodes per batch = threads per block
+template <class T>
+struct AgCfg {
+  static constexpr int kBlocks = sizeof(T) == 8 ? 3 : 4;  // resident blocks per SM
+};
+template <int ROWS, class T>
+constexpr size_t ag_smem_bytes() {
+  return (size_t)3 * ROWS * kAgB * 4 + (size_t)2 * 19 * kAgB * sizeof(T);
+}
+
+template <class T, bool ET, bool SW, bool VEC>
+__global__ void __launch_bounds__(kAgB, AgCfg<T>::kBlocks)
+    k_idx_ag(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  constexpr int ROWS = ET ? 9 : 18;
+  extern __shared__ __align__(16) unsigned char ag_smem[];
+  auto tab = reinterpret_cast<uint32_t(*)[ROWS][kAgB]>(ag_smem);  // [3]
+  auto gs = reinterpret_cast<T(*)[19][kAgB]>(ag_smem + (size_t)3 * ROWS * kAgB * 4);  // [2]
+  const uint32_t* table = ET ? I.rem : I.adj;
+  const uint32_t tid = threadIdx.x;
+  auto batch = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
+  auto issue_tab = [&](uint32_t k) {
+    const uint32_t bt = batch(k);
+    if (bt >= nbatch) return;
+    const uint32_t n0 = I.first + bt * kAgB, cnt = min((uint32_t)kAgB, I.end() - n0);
+    uint32_t* dst = &tab[k % 3][0][0];
+    if (VEC && cnt == kAgB) {
+      for (uint32_t q = tid; q < ROWS * (kAgB / 4); q += kAgB) {
+        const uint32_t row = q / (kAgB / 4), c = q - row * (kAgB / 4);
+        cp_async<16>(dst + row * kAgB + c * 4, table + (size_t)row * I.n + n0 + c * 4);
+      }
+    } else {
+      for (uint32_t q = tid; q < ROWS * cnt; q += kAgB) {
+        const uint32_t row = q / cnt, c = q - row * cnt;
+        cp_async<4>(dst + row * kAgB + c, table + (size_t)row * I.n + n0 + c);
+      }
+    }
+  };
+  auto node_of = [&](uint32_t k) { return I.first + batch(k) * kAgB + tid; };
+  auto issue_gather = [&](uint32_t k) {
+    if (batch(k) >= nbatch) return;
+    const uint32_t node = node_of(k);
+    if (node >= I.end()) return;
+    T* g = &gs[k & 1][0][tid];
+    const uint32_t(&row)[ROWS][kAgB] = tab[k % 3];
+    cp_async<sizeof(T)>(g, F.at(0, node));
+    if constexpr (!ET) {  // AA odd: slot j of the neighbour along c_j (bounce: own slot i)
+#pragma unroll
+      for (int i = 1; i < 19; ++i) {
+        const int j = opp(i);
+        const uint32_t ej = row[j - 1][tid];
+        cp_async<sizeof(T)>(g + i * kAgB, ej == node ? F.at(i, node) : F.at(j, ej));
+      }
+    } else {  // ET: own slot b_i, and slot b_j of the neighbour along c_i (or mailbox)
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        const uint32_t r = row[p][tid] & 0x7fffffffu;
+        cp_async<sizeof(T)>(g + i * kAgB, F.at(hb<SW>(i), node));
+        cp_async<sizeof(T)>(g + j * kAgB, F.at(r >= I.n ? hb<SW>(i) : hb<SW>(j), r));
+      }
+    }
+  };
+  issue_tab(0);
+  issue_tab(1);
+  cp_commit();
+  cp_wait0();
+  __syncthreads();
+  issue_gather(0);
+  cp_commit();
+  for (uint32_t k = 0; batch(k) < nbatch; ++k) {
+    // batch k's gathers and batch k + 1's rows have landed; every thread is
+    // done with batch k - 1 (its row slot is refilled with batch k + 2, its
+    // gather slot with batch k + 1)
+    cp_wait0();
+    __syncthreads();
+    issue_tab(k + 2);
+    issue_gather(k + 1);
+    cp_commit();
+    const uint32_t node = node_of(k);
+    if (node >= I.end()) continue;
+    const T* g = &gs[k & 1][0][tid];
+    const uint32_t(&row)[ROWS][kAgB] = tab[k % 3];
+    T f[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = g[i * kAgB];
+    collide(op, f);
+    st<false>(F.at(0, node), f[0]);
+    if constexpr (!ET) {
+#pragma unroll
+      for (int j = 1; j < 19; ++j) {
+        const uint32_t ej = row[j - 1][tid];
+        st<false>(ej == node ? F.at(opp(j), node) : F.at(j, ej), f[j]);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        const uint32_t rv = row[p][tid];
+        const bool ub = (rv & 0x80000000u) != 0;
+        st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
+        st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
+      }
+    }
+  }
+}
+
 // ET sweep, indirect (p/src/scheme_et.cpp:241-272): rem[p][n] = neighbour
 // along c_i or a mailbox slot >= N (i-link bounces), bit 31 = j-link bounces.
 template <class T, bool AOS, bool SW>
@@ -646,8 +767,46 @@ static unsigned staged_grid(uint32_t nbatch) {
   return std::min<uint32_t>(nbatch, (uint32_t)(sms * LBM_IDX_PF_MIN_BLOCKS));
 }
 
+// the asynchronous-gather pipeline (k_idx_ag), SoA: LBMGPU_IDX_AG=0 restores
+// the register-gather kernels
+static bool idx_ag_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_IDX_AG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <class T, bool ET, bool SW, bool VEC>
+static void launch_ag_t(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
+  constexpr size_t bytes = ag_smem_bytes<ET ? 9 : 18, T>();
+  static int set_dev = -1;  // the attribute is per device
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (set_dev != dev) {
+    cudaFuncSetAttribute(k_idx_ag<T, ET, SW, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set_dev = dev;
+  }
+  const uint32_t nbatch = (I.count() + kAgB - 1) / kAgB;
+  const unsigned g = std::min<uint32_t>(nbatch, (uint32_t)(sms * AgCfg<T>::kBlocks));
+  k_idx_ag<T, ET, SW, VEC><<<g, kAgB, bytes, st>>>(fld<T, false>(f), I, cast_op<T>(op), nbatch);
+}
+template <bool ET, bool SW>
+static bool launch_ag(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
+  if (f.aos || !idx_ag_enabled()) return false;
+  const bool vec = I.n % 4 == 0 && I.first % 4 == 0;
+  if (f.prec == Prec::f64) {
+    if (vec) launch_ag_t<double, ET, SW, true>(st, f, I, op);
+    else launch_ag_t<double, ET, SW, false>(st, f, I, op);
+  } else {
+    if (vec) launch_ag_t<float, ET, SW, true>(st, f, I, op);
+    else launch_ag_t<float, ET, SW, false>(st, f, I, op);
+  }
+  return true;
+}
+
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
   if (I.count() == 0) return;
+  if (launch_ag<false, false>(st, f, I, op)) return;
   if (!f.aos && f.prec == Prec::f64) {  // fp32 spills at its register budget
     const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
     const unsigned g = staged_grid(nbatch);
@@ -672,6 +831,8 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
   if (I.count() == 0) return;
   if (base.swapped() ? launch_idx_tiled<kTiledEtSw>(st, f, f, I, op)
                      : launch_idx_tiled<kTiledEt>(st, f, f, I, op))
+    return;
+  if (base.swapped() ? launch_ag<true, true>(st, f, I, op) : launch_ag<true, false>(st, f, I, op))
     return;
   if (!f.aos && f.prec == Prec::f64) {
     const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
