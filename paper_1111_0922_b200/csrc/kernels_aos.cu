@@ -1349,7 +1349,13 @@ __global__ void __launch_bounds__(ZpCfg<T>::kThreads, ZpCfg<T>::kBlocks)
 // final (write-back) once the row warps computed the plane above it, and a
 // row warp can be at most three planes ahead of the write-back (it waits for
 // loads that follow the write-back), inside the 5-use parity window.
-constexpr int kTYw = 6, kWRw = kTYw + 2, kNBw = 5;
+constexpr int kNBw = 5;
+// tile rows (= row warps): fp64 6 (a 34 x 8 window, 5 planes = 207 KB); fp32
+// records are half as long, so LBM_WS_TY32 rows (34 x 16 window: the
+// slot-by-slot rim rows are 4 of 16 instead of 4 of 8)
+#ifndef LBM_WS_TY32
+#define LBM_WS_TY32 14
+#endif
 // write-back warps (measured on C1 fp64: 2 -> AA 0.51, 4 -> 0.66, 6 -> 0.67,
 // 8 -> 0.74, 10 -> 0.77 of the roofline; the row warps' register cap at 512
 // threads costs a few spills); storing the rim slots straight from the row
@@ -1357,14 +1363,20 @@ constexpr int kTYw = 6, kWRw = kTYw + 2, kNBw = 5;
 #ifndef LBM_WS_WB
 #define LBM_WS_WB 10
 #endif
-constexpr int kWsCompute = kTYw, kWsWb = LBM_WS_WB, kWsThreads = 32 * (kWsCompute + kWsWb);
+constexpr int kWsWb = LBM_WS_WB;
 template <class T>
 struct WinSzW {
+  static constexpr int TY = sizeof(T) == 8 ? 6 : LBM_WS_TY32;  // row warps
+  static constexpr int WR = TY + 2;
+  static constexpr int kThreads = 32 * (TY + kWsWb);
+  static constexpr int kList = 4 * kWC * 19 + (WR - 4) * 4 * 19;
   static constexpr int ROW = WinSz<T>::ROW;
-  static constexpr int BUF = kWRw * ROW;
+  static constexpr int BUF = WR * ROW;
   static constexpr size_t kBytes = (size_t)kNBw * BUF * sizeof(T);
 };
 static_assert(WinSzW<double>::kBytes <= 227 * 1024 - 12 * 1024, "fp64 ws ring too large");
+static_assert(WinSzW<float>::kBytes <= 227 * 1024 - 16 * 1024, "fp32 ws ring too large");
+static_assert(WinSzW<float>::WR <= 32, "one loading lane per window row");
 
 __device__ __forceinline__ void wb_group_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"r"(32 * kWsWb) : "memory");
@@ -1377,18 +1389,19 @@ __device__ __forceinline__ void wb_group_sync() {
 #define LBM_WS_F32_BLOCKS 1
 #endif
 template <class T, int MODE>
-__global__ void __launch_bounds__(kWsThreads, sizeof(T) == 8 ? 1 : LBM_WS_F32_BLOCKS)
+__global__ void __launch_bounds__(WinSzW<T>::kThreads, sizeof(T) == 8 ? 1 : LBM_WS_F32_BLOCKS)
     k_win_ws(Fld<T, true> fld_, Lat L, Trt<T> op, int tiles_x, int tiles_y, int zc) {
   static_assert(in_place(MODE), "warp-specialised window: in-place modes only");
   extern __shared__ __align__(16) unsigned char win_smem[];
   T* sm = reinterpret_cast<T*>(win_smem);
   T* const g = fld_.p;
+  constexpr int kTYw = WinSzW<T>::TY, kWRw = WinSzW<T>::WR, kWsCompute = kTYw;
   __shared__ int ph[kNBw][kWRw];
   __shared__ uint32_t msk[kWsWb * kWC];
   __shared__ int mcol[kWsWb * kWC];
-  __shared__ uint32_t gmask[kWR * kWC];
-  __shared__ uint16_t wlist[kListMax];
-  __shared__ int wcnt[kWR + 1];
+  __shared__ uint32_t gmask[kWRw * kWC];
+  __shared__ uint16_t wlist[WinSzW<T>::kList];
+  __shared__ int wcnt[kWRw + 1];
   __shared__ long long rbp[kWRw];
   __shared__ int sbp[kWRw];
   __shared__ __align__(8) uint64_t full[kNBw];
@@ -1691,10 +1704,10 @@ bool window_enabled() {
 #endif
 template <class T, int MODE>
 void launch_win_ws(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op) {
-  const int per_sm = ensure_smem<k_win_ws<T, MODE>>(kWsThreads, WinSzW<T>::kBytes);
+  const int per_sm = ensure_smem<k_win_ws<T, MODE>>(WinSzW<T>::kThreads, WinSzW<T>::kBytes);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + kTYw - 1) / kTYw;
+  const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + WinSzW<T>::TY - 1) / WinSzW<T>::TY;
   // z planes per block: about 7 waves of resident blocks, 4 .. 64 planes, and
   // at least two chunks on a periodic z axis (the halo plane is not one of
   // the chunk's own planes)
@@ -1705,7 +1718,7 @@ void launch_win_ws(cudaStream_t st, const DField& f, const Lat& L, const TrtHost
   if (!L.wall[2]) zc = std::min<long long>(zc, L.nz - 2);
   zc = std::max(1LL, std::min<long long>(zc, L.nz));
   const int nzc = (int)((L.nz + zc - 1) / zc);
-  k_win_ws<T, MODE><<<(unsigned)(tiles * nzc), kWsThreads, WinSzW<T>::kBytes, st>>>(
+  k_win_ws<T, MODE><<<(unsigned)(tiles * nzc), WinSzW<T>::kThreads, WinSzW<T>::kBytes, st>>>(
       fld<T, true>(f), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc);
 }
 
@@ -1746,6 +1759,16 @@ void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat&
 // (fp64) and equal to the k_win gather (fp32) on C1 (0.42 / 0.47 vs 0.54 /
 // 0.47): the halo ring's redundant collisions and the extra barrier per
 // plane; opt-in LBMGPU_AOS_ZPIPE_PUSH=1
+// fp32 in-place modes through the warp-specialised window (LBMGPU_AOS_WS32=1
+// or -DLBM_WS_F32=1)
+bool ws_f32() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_AOS_WS32");
+    return e ? e[0] == '1' : LBM_WS_F32 != 0;
+  }();
+  return on;
+}
+
 bool zpipe_push() {
   static const bool on = [] {
     const char* e = std::getenv("LBMGPU_AOS_ZPIPE_PUSH");
@@ -1810,7 +1833,8 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // keeps every window position a distinct record (a 34 x 8 window on
   // periodic y); fp32 measured no better with it (C1 AA 0.61 -> 0.62, C4 0.51
   // -> 0.52) and keeps k_win at two blocks per SM
-  if (LBM_AOS_WS && (f64 || LBM_WS_F32) && in_place(mode) && (L.wall[1] || L.ny >= kTYw + 2)) {
+  if (LBM_AOS_WS && (f64 || ws_f32()) && in_place(mode) &&
+      (L.wall[1] || L.ny >= (f64 ? WinSzW<double>::TY : WinSzW<float>::TY) + 2)) {
 #define LBM_WS_CASES(T)                                                   \
   switch (mode) {                                                         \
     case kWinAaOdd: launch_win_ws<T, kWinAaOdd>(st, a, L, op); break;     \

@@ -767,12 +767,13 @@ static unsigned staged_grid(uint32_t nbatch) {
   return std::min<uint32_t>(nbatch, (uint32_t)(sms * LBM_IDX_PF_MIN_BLOCKS));
 }
 
-// the asynchronous-gather pipeline (k_idx_ag), SoA: LBMGPU_IDX_AG=0 restores
-// the register-gather kernels
+// the asynchronous-gather pipeline (k_idx_ag), SoA, opt-in LBMGPU_IDX_AG=1:
+// measured slower than the register gathers on C2 (AA odd fp64 0.88 -> 0.80,
+// fp32 0.94 -> 0.87; ET fp64 0.74 -> 0.74, fp32 0.81 -> 0.66)
 static bool idx_ag_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("LBMGPU_IDX_AG");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

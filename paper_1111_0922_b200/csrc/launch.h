@@ -124,6 +124,26 @@ void launch_swap(cudaStream_t st, const DField& f, const dev::Lat& L, int mode);
 int swap_fused_rows(const dev::Lat& L);
 bool launch_swap_fused(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op,
                        bool push, unsigned long long* sync, unsigned long long epoch);
+// single-pass SWAP with face buffers (SoA direct; kernels_swap1.cu): whether
+// the lattice qualifies, the face-buffer length per parity (elements), one
+// sweep (hcur: this sweep's buffer, hprev: the last sweep's), and the
+// field <-> buffer transfers (fill: field -> hprev after a load; flush (push):
+// latest buffer -> field before an extraction)
+bool swap1_ok(const DField& f, const dev::Lat& L);
+size_t swap1_face_elems(const dev::Lat& L);
+void launch_swap1(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op, bool push,
+                  void* hcur, const void* hprev);
+void launch_swap1_faces(cudaStream_t st, const DField& f, const dev::Lat& L, bool push, bool fill,
+                        void* h);
+// AA pattern on AoS records with face buffers (kernels_aos_fb.cu): whether
+// the lattice qualifies, the face-buffer length (elements), one sweep (even
+// or odd), and the buffer <-> record transfers (fill after a load, flush
+// before an extraction)
+bool aa_fb_ok(const DField& f, const dev::Lat& L);
+size_t aa_fb_face_elems(const DField& f, const dev::Lat& L);
+void launch_aa_fb(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op, bool odd,
+                  void* h);
+void launch_aa_fb_faces(cudaStream_t st, const DField& f, const dev::Lat& L, bool fill, void* h);
 void launch_swap_list(cudaStream_t st, const DField& f, const long long* a, const long long* b,
                       const int8_t* dir, long long count);
 // CG as a plane-group push launch: read at the cell's storage index, write at

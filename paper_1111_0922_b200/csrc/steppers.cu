@@ -110,14 +110,36 @@ class AaDirect final : public DirectStepper {
   AaDirect(const HostGeo& g, const lbmgpu_flow& p, const lbmgpu_options& o)
       : DirectStepper(g, p, o) {
     alloc_field(f_, g.cells());
+    // AoS: face-buffer kernels (kernels_aos_fb.cu); the face slots' home
+    const DField f = field(f_, soa_stride(g.cells()));
+    if (aa_fb_ok(f, L_)) {
+      h_.alloc(aa_fb_face_elems(f, L_) * esize());
+      fb_ = true;
+    }
     init(base_init(kSrcRest));
   }
   void step_one() override {
     const DField f = field(f_, soa_stride(geo_.cells()));
+    if (fb_) {
+      if (!h_valid_) {
+        launch_aa_fb_faces(stream_, f, L_, true, h_.get());
+        h_valid_ = true;
+      }
+      launch_aa_fb(stream_, f, L_, op_, (t_ & 1) != 0, h_.get());
+      return;
+    }
     if ((t_ & 1) == 0)
       launch_local(stream_, f, f, L_, op_, false, true);
     else
       launch_aa_odd(stream_, f, L_, op_);
+  }
+  void before_extract() override {  // the face slots back into their records
+    if (fb_ && h_valid_)
+      launch_aa_fb_faces(stream_, field(f_, soa_stride(geo_.cells())), L_, false, h_.get());
+  }
+  void after_load() override {
+    t_ = 0;
+    h_valid_ = false;
   }
   void extract_range(uint32_t n0, uint32_t c, double* d) override {
     ex(field(f_, soa_stride(geo_.cells())), L_, (t_ & 1) ? kExAaOdd : kExNatural, n0, c, d);
@@ -126,10 +148,11 @@ class AaDirect final : public DirectStepper {
     ld(field(f_, soa_stride(geo_.cells())), L_, kExNatural, n0, c, d, in);
   }
   int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
-  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  uint64_t pdf_bytes() const override { return f_.bytes() + h_.bytes(); }
 
  private:
-  DevMem f_;
+  DevMem f_, h_;
+  bool fb_ = false, h_valid_ = false;
 };
 
 // ET (p/src/scheme_et.cpp): extended grid with a halo plane on wall axes
@@ -357,6 +380,13 @@ class SwapDirect final : public DirectStepper {
       CK(cudaMemsetAsync(sync_.get(), 0, words * 8, stream_));
       fused_ = true;
     }
+    // single pass with face buffers (kernels_swap1.cu), SoA: two parities
+    if (!fused_ && swap1_ok(field(f_, soa_stride(g.cells())), L_)) {
+      hn_ = swap1_face_elems(L_);
+      h_[0].alloc(hn_ * esize());
+      h_[1].alloc(hn_ * esize());
+      single_ = true;
+    }
     init(base_init(kSrcRest));
     sync();
   }
@@ -390,6 +420,15 @@ class SwapDirect final : public DirectStepper {
   // (pull): the swapped slot pairs are disjoint and independent of the
   // sweep's collisions, so this equals the sequential sweep bit for bit.
   void sweep(const DField& f, bool push) {
+    if (single_) {
+      if (!h_valid_) {  // the last sweep's face values, gathered from the field
+        launch_swap1_faces(stream_, f, L_, push, true, h_[hpar_ ^ 1].get());
+        h_valid_ = true;
+      }
+      launch_swap1(stream_, f, L_, op_, push, h_[hpar_].get(), h_[hpar_ ^ 1].get());
+      hpar_ ^= 1;
+      return;
+    }
     if (fused_ && launch_swap_fused(stream_, f, L_, op_, push,
                                     sync_.get<unsigned long long>(), ++epoch_))
       return;
@@ -401,9 +440,13 @@ class SwapDirect final : public DirectStepper {
       launch_local(stream_, f, f, L_, op_, true, false);
     }
   }
-  int launches_per_step() const override { return (fused_ ? 1 : 2) + (nfix_ ? 1 : 0); }
+  int launches_per_step() const override { return (fused_ || single_ ? 1 : 2) + (nfix_ ? 1 : 0); }
   void before_extract() override {
     if (!pull_ && pending_) fixup(field(f_, soa_stride(geo_.cells())));
+    // push: the face links of the last sweep live in the face buffer only
+    if (single_ && h_valid_ && !pull_)
+      launch_swap1_faces(stream_, field(f_, soa_stride(geo_.cells())), L_, true, false,
+                         h_[hpar_ ^ 1].get());
   }
   void after_extract() override {
     if (!pull_ && pending_) fixup(field(f_, soa_stride(geo_.cells())));
@@ -422,16 +465,21 @@ class SwapDirect final : public DirectStepper {
     t_ = 0;
     fresh_ = pull_;
     pending_ = false;
+    h_valid_ = false;
   }
   int layout_phase() const override {
     if (pull_) return LBMGPU_NATURAL;
     return pending_ ? LBMGPU_SWAP_PARTIAL : LBMGPU_OPPOSED;
   }
-  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  uint64_t pdf_bytes() const override { return f_.bytes() + h_[0].bytes() + h_[1].bytes(); }
 
  private:
   bool pull_, defer_;
   bool fresh_ = false, pending_ = false, fused_ = false;
+  bool single_ = false, h_valid_ = false;
+  int hpar_ = 0;     // face buffer the next sweep writes
+  size_t hn_ = 0;    // face-buffer elements per parity
+  DevMem h_[2];
   long long nfix_ = 0;
   unsigned long long epoch_ = 0;
   DevMem f_, fa_, fb_, fd_, sync_;
@@ -569,10 +617,11 @@ class AaIndirect final : public IndirectStepper {
     ld(field(f_, soa_stride(nodes_)), kExNatural, n0, c, d, in);
   }
   int layout_phase() const override { return (t_ & 1) ? LBMGPU_OPPOSED : LBMGPU_NATURAL; }
-  uint64_t pdf_bytes() const override { return f_.bytes(); }
+  uint64_t pdf_bytes() const override { return f_.bytes() + h_.bytes(); }
 
  private:
-  DevMem f_;
+  DevMem f_, h_;
+  bool fb_ = false, h_valid_ = false;
 };
 
 class EtIndirect final : public IndirectStepper {

@@ -13,7 +13,7 @@ if [ -n "$LBM_DEVICE_HDR" ]; then cp "$LBM_DEVICE_HDR" $OUT/src/lbm_device.cuh; 
 if [ -n "$LBM_AOS_SRC" ]; then cp "$LBM_AOS_SRC" $OUT/src/kernels_aos.cu; fi
 mkdir -p $OUT/include; cp $ROOT/include/lbmgpu.h $OUT/include/
 sed -i "s|../../include/lbmgpu.h|../include/lbmgpu.h|" $OUT/src/runtime.h
-for f in kernels_direct kernels_aos kernels_indirect kernels_util kernels_swap steppers slabs capi; do
+for f in kernels_direct kernels_aos kernels_indirect kernels_util kernels_swap kernels_swap1 kernels_aos_fb steppers slabs capi; do
   /usr/local/cuda/bin/nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false \
     -Xcompiler -fPIC --expt-relaxed-constexpr -ccbin /usr/bin/g++ "$@" -c $OUT/src/$f.cu -o $OUT/$f.o &
 done
