@@ -270,6 +270,14 @@ int lbmgpu_slab_p2p_export(lbmgpu_stepper* h, uint8_t* blob);
  * rank steps; lbmgpu_slab_sync_ghosts works as with NCCL. */
 int lbmgpu_slab_p2p_connect(lbmgpu_stepper* h, const uint8_t* lower, const uint8_t* upper,
                             int32_t nranks, int32_t rank);
+/* the same with flags. LBMGPU_P2P_HOST_ORDERED: no flag-word barrier kernel;
+ * the CALLER orders the ranks (after every step / sync_ghosts: synchronize,
+ * then a host barrier across the ranks before the next call). For ranks that
+ * share one GPU, where kernels of different processes that spin on each
+ * other's flags are not guaranteed to run concurrently. */
+#define LBMGPU_P2P_HOST_ORDERED 1u
+int lbmgpu_slab_p2p_connect_ex(lbmgpu_stepper* h, const uint8_t* lower, const uint8_t* upper,
+                               int32_t nranks, int32_t rank, uint32_t flags);
 
 /* page-locked host memory (cudaHostAlloc) for the canonical snapshot, so
  * extract/load run at full host-link bandwidth */

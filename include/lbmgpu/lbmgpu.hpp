@@ -334,8 +334,11 @@ class Stepper {
   }
   void slab_p2p_connect(const std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES>& lower,
                         const std::array<std::uint8_t, LBMGPU_P2P_BLOB_BYTES>& upper, int nranks,
-                        int rank) {
-    detail::check(lbmgpu_slab_p2p_connect(h_, lower.data(), upper.data(), nranks, rank));
+                        int rank, bool host_ordered = false) {
+    // host_ordered: no flag-word barrier; the caller synchronizes and barriers
+    // the ranks after every step (ranks sharing one GPU)
+    detail::check(lbmgpu_slab_p2p_connect_ex(h_, lower.data(), upper.data(), nranks, rank,
+                                             host_ordered ? LBMGPU_P2P_HOST_ORDERED : 0u));
   }
 
  private:

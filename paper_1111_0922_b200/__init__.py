@@ -38,6 +38,7 @@ FAMILY_OF = {"ts": "ts", "os-push": "os", "os-pull": "os", "osnt-pull-1s": "osnt
 ADDRESSINGS = ("direct", "indirect")
 LAYOUT_PHASES = ("natural", "opposed", "shifted_even", "shifted_odd", "twisted", "swap_partial")
 Q = 19
+P2P_HOST_ORDERED = 1
 P2P_BLOB_BYTES = 256  # LBMGPU_P2P_BLOB_BYTES
 
 
@@ -117,6 +118,7 @@ _sig = {
     "lbmgpu_slab_group_connect_p2p": (C.c_int, [_P, C.c_int32]),
     "lbmgpu_slab_p2p_export": (C.c_int, [_P, _P]),
     "lbmgpu_slab_p2p_connect": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32]),
+    "lbmgpu_slab_p2p_connect_ex": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_uint32]),
     "lbmgpu_host_free": (C.c_int, [_P]),
     "lbmgpu_run_bench": (C.c_int, [C.POINTER(_Geometry), C.POINTER(_Flow), C.POINTER(_Options),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double, _P]),
@@ -383,12 +385,17 @@ class Stepper:
         _check(_L.lbmgpu_slab_p2p_export(self._h, buf))
         return bytes(buf)
 
-    def slab_p2p_connect(self, lower: bytes, upper: bytes, nranks: int, rank: int) -> None:
+    def slab_p2p_connect(self, lower: bytes, upper: bytes, nranks: int, rank: int,
+                         host_ordered: bool = False) -> None:
         """One rank per process: AA odd face planes read and rewrite the
-        neighbours' face slots in place through peer pointers (collective)."""
+        neighbours' face slots in place through peer pointers (collective).
+        host_ordered: no flag-word barrier kernel; the caller synchronizes and
+        runs a host barrier across the ranks after every step / sync_ghosts
+        (ranks sharing one GPU)."""
         lo = (C.c_uint8 * P2P_BLOB_BYTES).from_buffer_copy(lower[:P2P_BLOB_BYTES])
         hi = (C.c_uint8 * P2P_BLOB_BYTES).from_buffer_copy(upper[:P2P_BLOB_BYTES])
-        _check(_L.lbmgpu_slab_p2p_connect(self._h, lo, hi, nranks, rank))
+        flags = P2P_HOST_ORDERED if host_ordered else 0
+        _check(_L.lbmgpu_slab_p2p_connect_ex(self._h, lo, hi, nranks, rank, flags))
 
     def cuda_stream(self) -> int:
         v = C.c_void_p()

@@ -360,7 +360,17 @@ int lbmgpu_slab_p2p_connect(lbmgpu_stepper* h, const uint8_t* lower, const uint8
   return guard([&] {
     if (!lower || !upper) throw std::invalid_argument("null blob");
     if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank");
-    slab_p2p_connect(S(h), lower, upper, nranks, rank);
+    slab_p2p_connect(S(h), lower, upper, nranks, rank, 0u);
+  });
+}
+
+int lbmgpu_slab_p2p_connect_ex(lbmgpu_stepper* h, const uint8_t* lower, const uint8_t* upper,
+                               int32_t nranks, int32_t rank, uint32_t flags) {
+  return guard([&] {
+    if (!lower || !upper) throw std::invalid_argument("null blob");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank");
+    if (flags & ~LBMGPU_P2P_HOST_ORDERED) throw std::invalid_argument("unknown p2p flags");
+    slab_p2p_connect(S(h), lower, upper, nranks, rank, flags);
   });
 }
 

@@ -433,6 +433,7 @@ void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs);
 // per process through exported blobs (CUDA IPC handles of field and flags)
 void slab_group_connect_p2p(const std::vector<Stepper*>& slabs);
 void slab_p2p_export(Stepper& s, uint8_t* blob);
-void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank);
+void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank,
+                      unsigned flags);
 
 }  // namespace lbmgpu

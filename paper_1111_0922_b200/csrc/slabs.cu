@@ -428,7 +428,8 @@ class SlabStepper final : public Stepper {
   // values a neighbour stored for an earlier generation never satisfy a
   // barrier of this one, and a neighbour that connected and stepped first
   // cannot have its stores wiped.
-  void connect_p2p_ipc(const P2PBlob& lo, const P2PBlob& hi, int nranks, int rank) {
+  void connect_p2p_ipc(const P2PBlob& lo, const P2PBlob& hi, int nranks, int rank,
+                       bool host_ordered = false) {
     p2p_check();
     for (const P2PBlob* b : {&lo, &hi}) {
       if (std::memcmp(b->magic, "LBMP2P1", 8) != 0)
@@ -477,6 +478,7 @@ class SlabStepper final : public Stepper {
     ++generation_;
     epoch_ = (unsigned long long)generation_ << 40;
     nranks_ = nranks, rank_ = rank;
+    host_ordered_ = host_ordered;
     transport_ = kP2PIpc;
   }
   void check_health() override {
@@ -491,6 +493,7 @@ class SlabStepper final : public Stepper {
   }
   void flag_barrier(cudaStream_t st) {
     ++epoch_;
+    if (host_ordered_) return;  // the caller's host barrier orders the ranks
     k_slab_flag_barrier<<<1, 32, 0, st>>>(flags_.get<unsigned long long>(), flag_to_lo_, flag_to_hi_,
                                          epoch_);
   }
@@ -1009,6 +1012,7 @@ class SlabStepper final : public Stepper {
   unsigned long long* flag_to_lo_ = nullptr;
   unsigned long long* flag_to_hi_ = nullptr;
   unsigned long long epoch_ = 0;
+  bool host_ordered_ = false;  // kP2PIpc without the flag-word barrier kernel
   int generation_ = 0;  // p2p connects so far (collective, so equal on every rank)
   std::vector<void*> ipc_open_;
 };
@@ -1230,11 +1234,12 @@ void slab_p2p_export(Stepper& s, uint8_t* blob) {
   std::memcpy(blob, &b, sizeof(b));
 }
 
-void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank) {
+void slab_p2p_connect(Stepper& s, const uint8_t* lo, const uint8_t* hi, int nranks, int rank,
+                      unsigned flags) {
   P2PBlob a, b;
   std::memcpy(&a, lo, sizeof(a));
   std::memcpy(&b, hi, sizeof(b));
-  as_slab(s).connect_p2p_ipc(a, b, nranks, rank);
+  as_slab(s).connect_p2p_ipc(a, b, nranks, rank, (flags & LBMGPU_P2P_HOST_ORDERED) != 0);
 }
 
 void slab_group_sync_ghosts(const std::vector<Stepper*>& slabs) {
