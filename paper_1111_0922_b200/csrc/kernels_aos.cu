@@ -116,7 +116,10 @@ constexpr bool owned_wb(int mode) { return in_place(mode) || mode == kWinPushS; 
 #endif
 template <class T, int MODE>
 struct WinThreads {
-  static constexpr int value = sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream)
+  // kWinPush (CG plane groups) collides the whole (kTY + 2) x 34 window
+  // before its gathers: enough warps for one round
+  static constexpr int value = (sizeof(T) == 8 && (MODE == kWinPull || MODE == kWinStream)) ||
+                                       MODE == kWinPush
                                    ? LBM_WIN_GATHER_THREADS
                                    : kTX * kTY + 32 * LBM_WIN_LOADER;
   static constexpr int warps = value / 32;
@@ -1186,6 +1189,16 @@ struct ZpCfg {
   static constexpr int kThreads = 32 * (TY + 1);  // + one loading warp
   static constexpr int kBlocks = (int)((227 * 1024) / (kBytes + 2048)) > 0 ? (int)((227 * 1024) / (kBytes + 2048)) : 1;
 };
+// OS push collides every window record of a plane ((TY + 2) x 34) before the
+// gathers: extra warps so that is one round of the block, not two
+#ifndef LBM_ZP_PUSH_EXTRA
+#define LBM_ZP_PUSH_EXTRA 2
+#endif
+template <class T, int MODE>
+struct ZpThreads {
+  static constexpr int value =
+      MODE == kWinPush ? 32 * (ZpCfg<T>::TY + 1 + LBM_ZP_PUSH_EXTRA) : ZpCfg<T>::kThreads;
+};
 static_assert(ZpCfg<double>::kBytes <= 227 * 1024 - 1024, "fp64 z-pipeline ring too large");
 static_assert(ZpCfg<float>::kBytes <= 227 * 1024 - 1024, "fp32 z-pipeline ring too large");
 static_assert(ZpCfg<double>::NS >= 3 && ZpCfg<float>::NS >= 3, "z pipeline: at least one plane in flight");
@@ -1226,7 +1239,7 @@ __device__ __forceinline__ void zp_take_next(T (&g5)[5], At at) {
 }
 
 template <class T, int MODE>
-__global__ void __launch_bounds__(ZpCfg<T>::kThreads, ZpCfg<T>::kBlocks)
+__global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
     k_win_zp(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y,
              int zc) {
   static_assert(MODE == kWinPull || MODE == kWinStream || MODE == kWinPush,
@@ -1739,7 +1752,8 @@ template <class T, int MODE>
 void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
                    const TrtHost& op) {
   using C = ZpCfg<T>;
-  const int per_sm = ensure_smem<k_win_zp<T, MODE>>(C::kThreads, C::kBytes);
+  constexpr int kThr = ZpThreads<T, MODE>::value;
+  const int per_sm = ensure_smem<k_win_zp<T, MODE>>(kThr, C::kBytes);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + C::TY - 1) / C::TY;
@@ -1750,15 +1764,15 @@ void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat&
     if (std::atoi(e) > 0) zc = std::atoi(e);
   zc = std::max(1LL, std::min<long long>(zc, L.nz));
   const int nzc = (int)((L.nz + zc - 1) / zc);
-  k_win_zp<T, MODE><<<(unsigned)(tiles * nzc), C::kThreads, C::kBytes, st>>>(
+  k_win_zp<T, MODE><<<(unsigned)(tiles * nzc), kThr, C::kBytes, st>>>(
       fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc);
 }
 
 // OS push through the z pipeline (every window record of a plane collided in
-// place, then the stream gathers): measured slower than the scatter form
-// (fp64) and equal to the k_win gather (fp32) on C1 (0.42 / 0.47 vs 0.54 /
-// 0.47): the halo ring's redundant collisions and the extra barrier per
-// plane; opt-in LBMGPU_AOS_ZPIPE_PUSH=1
+// place by 11 warps, then the stream gathers): C1 fp64 0.46 vs 0.54 for the
+// scatter form (the halo ring's redundant collisions and the extra barrier
+// per plane), fp32 0.51 vs 0.47 for the k_win gather; LBMGPU_AOS_ZPIPE_PUSH
+// = 1 / 0 forces it on / off for both precisions
 // fp32 in-place modes through the warp-specialised window (LBMGPU_AOS_WS32=1
 // or -DLBM_WS_F32=1)
 bool ws_f32() {
@@ -1769,12 +1783,14 @@ bool ws_f32() {
   return on;
 }
 
-bool zpipe_push() {
-  static const bool on = [] {
+// default: fp32 only (C1 fp32 0.47 -> 0.51, C4 0.42 -> 0.46 with the extra
+// collision warps; fp64 keeps the scatter form, 0.54 vs 0.46)
+bool zpipe_push(bool f64) {
+  static const int env = [] {
     const char* e = std::getenv("LBMGPU_AOS_ZPIPE_PUSH");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  return env < 0 ? !f64 : env == 1;
 }
 
 bool zpipe_enabled() {
@@ -1827,7 +1843,7 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
   // fp32 0.43 -> 0.38; profiles/r01_variants.md)
   // (its bulk write-back runs use the source rows' 16-byte phase)
   const bool congruent = ((reinterpret_cast<uintptr_t>(a.p) ^ reinterpret_cast<uintptr_t>(b.p)) & 15u) == 0;
-  if (mode == kWinPush && distinct && f64 && congruent && !(zpipe_enabled() && zpipe_push()))
+  if (mode == kWinPush && distinct && f64 && congruent && !(zpipe_enabled() && zpipe_push(f64)))
     mode = kWinPushS;
   // fp64 in-place modes: the warp-specialised window where its 32 x 6 tile
   // keeps every window position a distinct record (a 34 x 8 window on
@@ -1851,7 +1867,7 @@ bool launch_aos_window(cudaStream_t st, int mode, const DField& a, const DField&
     return true;
   }
   // gather modes: the register-carried z pipeline
-  if ((mode == kWinPull || mode == kWinStream || (mode == kWinPush && zpipe_push())) &&
+  if ((mode == kWinPull || mode == kWinStream || (mode == kWinPush && zpipe_push(f64))) &&
       zpipe_enabled()) {
     if (f64) {
       if (mode == kWinPull) launch_win_zp<double, kWinPull>(st, a, b, L, op);

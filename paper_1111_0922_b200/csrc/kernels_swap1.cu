@@ -40,120 +40,158 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 
 namespace lbmgpu {
 using namespace dev;
 
 namespace {
 
-// Per-face passes with compile-time directions (as kernels_aos_fb.cu): a
-// warp-uniform (y rows, z planes) or lane (x columns) branch per face of the
-// block box visits the five directions crossing it; a link crossing several
-// faces is taken by the first of y, x, z (the order of fb_slot). A link
-// leaving the domain (bounce or periodic wrap: the fix-up list's) never
-// crosses. F: the node's face flags.
-struct S1Face {
-  bool ylo, yhi, xlo, xhi, zlo, zhi;
+// Per-thread frame of the sweep: the node's position in the block box and
+// the strides of the neighbouring blocks' face regions, and per plane two
+// link masks (bit k: the link along c_k from the node):
+//   local  the link bounces or leaves the domain (a periodic wrap: the fix-up
+//          list's) — its value stays in the node's own column;
+//   cross  the other end is inside the domain but outside the block box — its
+//          value goes through a face buffer.
+// Both come from the stencil's per-axis direction masks (kMxm ... kMzp)
+// selected by the x (per lane), y (per row) and z (per plane) flags, so the
+// per-direction work is a bit test; the face-buffer slot is the one fb_slot
+// (faces.cuh) names, with the receiver block and its coordinates derived
+// from the flags instead of recomputed from cell coordinates.
+struct S1Frame {
+  bool fxl, fxh, fyl, fyh, fzl, fzh;  // on the box's low / high face
+  bool dxl, dxh, dyl, dyh, dzl, dzh;  // on the domain's low / high face
+  int tx, ty, pz;                     // position in the box
+  long long base, rx, ry, rz;         // face region of the block, neighbour strides
+  int zc;
 };
-#define S1_5(D0, D1, D2, D3, D4, OP) OP(D0) OP(D1) OP(D2) OP(D3) OP(D4)
-#define S1_APPLY(M, OP) S1_APPLY_(M, OP)
-#define S1_APPLY_(D0, D1, D2, D3, D4, OP) S1_5(D0, D1, D2, D3, D4, OP)
-#define S1_CY_M 4, 7, 11, 12, 15
-#define S1_CY_P 3, 10, 13, 14, 18
-#define S1_CX_M 2, 7, 8, 9, 10
-#define S1_CX_P 1, 15, 16, 17, 18
-#define S1_CZ_M 6, 8, 11, 13, 16
-#define S1_CZ_P 5, 9, 12, 14, 17
-// the link from the node along c (dx, dy, dz) leaves the box through a y / x face
-__device__ __forceinline__ bool s1_ycross(const S1Face& q, int dy) {
-  return (dy < 0 && q.ylo) || (dy > 0 && q.yhi);
+// the link along (CX, CY, CZ) leaves the domain / crosses the block box;
+// only the flags of the direction's nonzero components are tested (y / z
+// flags are uniform over a warp, x flags per lane)
+template <int CX, int CY, int CZ>
+__device__ __forceinline__ bool s1_leaves(const S1Frame& q) {
+  return (CX < 0 && q.dxl) || (CX > 0 && q.dxh) || (CY < 0 && q.dyl) || (CY > 0 && q.dyh) ||
+         (CZ < 0 && q.dzl) || (CZ > 0 && q.dzh);
 }
-__device__ __forceinline__ bool s1_xcross(const S1Face& q, int dx) {
-  return (dx < 0 && q.xlo) || (dx > 0 && q.xhi);
+template <int CX, int CY, int CZ>
+__device__ __forceinline__ bool s1_crosses(const S1Frame& q) {
+  return (CX < 0 && q.fxl) || (CX > 0 && q.fxh) || (CY < 0 && q.fyl) || (CY > 0 && q.fyh) ||
+         (CZ < 0 && q.fzl) || (CZ > 0 && q.fzh);
 }
-__device__ __forceinline__ bool s1_cross(const S1Face& q, int dx, int dy, int dz) {
-  return s1_ycross(q, dy) || s1_xcross(q, dx) || (dz < 0 && q.zlo) || (dz > 0 && q.zhi);
+// plane bases of the field (kernel parameters, so constant-bank operands):
+// pl[i] = plane i; sh[i] = push: the store target of output i, plane opp i
+// shifted by +c_i (pl[opp i] + off_i); pull: the load source of input i,
+// plane i shifted by -c_i. Every plain access is then one IMAD.WIDE.U32 of
+// the 32-bit storage index.
+template <class T>
+struct S1Tab {
+  T* pl[19];
+  T* sh[19];
+};
+// slot of the value this node receives along direction I from S = X - c_I
+// (outside the box): in this block's region, keyed by the face S lies across
+#ifndef LBM_S1_SLOT_INLINE
+#define LBM_S1_SLOT_INLINE __forceinline__
+#endif
+template <int I>
+__device__ LBM_S1_SLOT_INLINE long long s1_in_slot(const FbGeo& G, const S1Frame& q) {
+  constexpr int X = cx(I), Y = cy(I), Z = cz(I);
+  if ((Y > 0 && q.fyl) || (Y < 0 && q.fyh)) {
+    constexpr int side = Y > 0 ? 0 : 1, qq = face_q(1, Y > 0 ? 1 : -1, I);
+    return q.base + G.hy + ((long long)(q.pz * 2 + side) * 5 + qq) * kFbX + q.tx;
+  }
+  if ((X > 0 && q.fxl) || (X < 0 && q.fxh)) {
+    constexpr int side = X > 0 ? 0 : 1, qq = face_q(0, X > 0 ? 1 : -1, I);
+    return q.base + G.hx + ((long long)(q.pz * 2 + side) * 5 + qq) * kFbY + q.ty;
+  }
+  constexpr int side = Z > 0 ? 0 : 1, qq = face_q(2, Z > 0 ? 1 : -1, I);
+  return q.base + G.hz + ((long long)(side * 5 + qq) * kFbY + q.ty) * kFbX + q.tx;
+}
+// slot of the value this node sends along direction K to R = X + c_K (outside
+// the box): in the receiving block's region, keyed by the face X lies across
+template <int K>
+__device__ LBM_S1_SLOT_INLINE long long s1_out_slot(const FbGeo& G, const S1Frame& q) {
+  constexpr int X = cx(K), Y = cy(K), Z = cz(K);
+  const int ex = (X < 0 && q.fxl) ? -1 : ((X > 0 && q.fxh) ? 1 : 0);
+  const int ey = (Y < 0 && q.fyl) ? -1 : ((Y > 0 && q.fyh) ? 1 : 0);
+  const int ez = (Z < 0 && q.fzl) ? -1 : ((Z > 0 && q.fzh) ? 1 : 0);
+  const long long rb = q.base + ex * q.rx + ey * q.ry + ez * q.rz;
+  const int px = ex > 0 ? 0 : (ex < 0 ? kFbX - 1 : q.tx + X);
+  const int py = ey > 0 ? 0 : (ey < 0 ? kFbY - 1 : q.ty + Y);
+  const int pz = ez > 0 ? 0 : (ez < 0 ? q.zc - 1 : q.pz + Z);
+  if (ey != 0) {
+    constexpr int side = Y > 0 ? 0 : 1, qq = face_q(1, Y > 0 ? 1 : -1, K);
+    return rb + G.hy + ((long long)(pz * 2 + side) * 5 + qq) * kFbX + px;
+  }
+  if (ex != 0) {
+    constexpr int side = X > 0 ? 0 : 1, qq = face_q(0, X > 0 ? 1 : -1, K);
+    return rb + G.hx + ((long long)(pz * 2 + side) * 5 + qq) * kFbY + py;
+  }
+  constexpr int side = Z > 0 ? 0 : 1, qq = face_q(2, Z > 0 ? 1 : -1, K);
+  return rb + G.hz + ((long long)(side * 5 + qq) * kFbY + py) * kFbX + px;
 }
 
-// the 19 inputs of node (x, y, z): push (opp i, X); pull (i, X - c_i), or
-// (opp i, X) on a bounce / wrap; a crossing input then comes from the face
-// buffer of the last sweep
-template <bool PUSH, class T>
-__device__ __forceinline__ void s1_read(const Fld<T, false>& F, const T* hprev, const Lat& L,
-                                        const FbGeo& G, const FbBlock& b, int x, int y, int z,
-                                        uint32_t s, uint32_t bounce, const S1Face& q, T (&v)[19]) {
-  v[0] = *F.at(0, s);
-#pragma unroll
-  for (int i = 1; i < 19; ++i) {
-    const int j = opp(i);
-    if (PUSH) {
-      v[i] = *F.at(j, s);
-    } else {
-      const int off = -cx(i) - cy(i) * L.sx - cz(i) * (int)L.sxy;
-      const bool loc = ((bounce >> j) & 1u) || !fb_inside(L, x - cx(i), y - cy(i), z - cz(i));
-      v[i] = *(loc ? F.at(j, s) : F.at(i, s) + off);
-    }
-  }
-  // input I crosses when its source X - c_I is in the domain, outside the box
-#define S1_RD(I)                                                                        \
-  if (!((bounce >> opp(I)) & 1u) && fb_inside(L, x - cx(I), y - cy(I), z - cz(I)))       \
-    v[I] = hprev[fb_slot<I>(G, b, x, y, z, x - cx(I), y - cy(I), z - cz(I))];
-#define S1_RD_X(I) if (!s1_ycross(q, -cy(I))) { S1_RD(I) }
-#define S1_RD_Z(I) if (!s1_ycross(q, -cy(I)) && !s1_xcross(q, -cx(I))) { S1_RD(I) }
-  if (q.ylo) { S1_APPLY(S1_CY_P, S1_RD) }
-  if (q.yhi) { S1_APPLY(S1_CY_M, S1_RD) }
-  if (q.xlo) { S1_APPLY(S1_CX_P, S1_RD_X) }
-  if (q.xhi) { S1_APPLY(S1_CX_M, S1_RD_X) }
-  if (q.zlo) { S1_APPLY(S1_CZ_P, S1_RD_Z) }
-  if (q.zhi) { S1_APPLY(S1_CZ_M, S1_RD_Z) }
-#undef S1_RD
-#undef S1_RD_X
-#undef S1_RD_Z
+// the 19 inputs of the node: push (opp i, X); pull (i, X - c_i), or (opp i, X)
+// when that link (opp i from X) is local; a crossing input comes from the
+// face buffer of the last sweep (the field load is issued regardless, so the
+// loads of a node leave together)
+template <bool PUSH, int I, class T>
+__device__ __forceinline__ void s1_in(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
+                                      const S1Frame& q, uint32_t s, uint32_t bounce, T (&v)[19]) {
+  constexpr int X = cx(I), Y = cy(I), Z = cz(I), J = opp(I);
+  const bool local = ((bounce >> J) & 1u) || s1_leaves<-X, -Y, -Z>(q);
+  if (!local && s1_crosses<-X, -Y, -Z>(q))
+    v[I] = hprev[s1_in_slot<I>(G, q)];
+  else if (PUSH || local)
+    v[I] = F.pl[J][s];
+  else
+    v[I] = F.sh[I][s];
 }
-// the 19 outputs: push (opp k, X + c_k), or (k, X) on a bounce / wrap; pull
-// (k, X); a crossing link's value goes to the receiver's face buffer instead
+// the 19 outputs: push (opp k, X + c_k), or (k, X) when link k is local;
+// pull (k, X); a crossing output goes to the receiver's face buffer instead
 // (push) or as well (pull)
-template <bool PUSH, class T>
-__device__ __forceinline__ void s1_write(const Fld<T, false>& F, T* hcur, const Lat& L,
-                                         const FbGeo& G, const FbBlock& b, int x, int y, int z,
-                                         uint32_t s, uint32_t bounce, const S1Face& q,
-                                         const T (&v)[19]) {
-  *F.at(0, s) = v[0];
-#pragma unroll
-  for (int k = 1; k < 19; ++k) {
-    if (!PUSH) {
-      *F.at(k, s) = v[k];
-    } else {
-      const bool loc = ((bounce >> k) & 1u) || !fb_inside(L, x + cx(k), y + cy(k), z + cz(k));
-      if (loc) {
-        *F.at(k, s) = v[k];
-      } else if (!s1_cross(q, cx(k), cy(k), cz(k))) {
-        const int off = cx(k) + cy(k) * L.sx + cz(k) * (int)L.sxy;
-        *(F.at(opp(k), s) + off) = v[k];
-      }
-    }
-  }
-#define S1_WR(K)                                                                         \
-  if (!((bounce >> K) & 1u) && fb_inside(L, x + cx(K), y + cy(K), z + cz(K))) {          \
-    const int rx = x + cx(K), ry = y + cy(K), rz = z + cz(K);                             \
-    hcur[fb_slot<K>(G, fb_block_of(L, G, b, rx, ry, rz), rx, ry, rz, x, y, z)] = v[K];    \
-  }
-#define S1_WR_X(K) if (!s1_ycross(q, cy(K))) { S1_WR(K) }
-#define S1_WR_Z(K) if (!s1_ycross(q, cy(K)) && !s1_xcross(q, cx(K))) { S1_WR(K) }
-  if (q.ylo) { S1_APPLY(S1_CY_M, S1_WR) }
-  if (q.yhi) { S1_APPLY(S1_CY_P, S1_WR) }
-  if (q.xlo) { S1_APPLY(S1_CX_M, S1_WR_X) }
-  if (q.xhi) { S1_APPLY(S1_CX_P, S1_WR_X) }
-  if (q.zlo) { S1_APPLY(S1_CZ_M, S1_WR_Z) }
-  if (q.zhi) { S1_APPLY(S1_CZ_P, S1_WR_Z) }
-#undef S1_WR
-#undef S1_WR_X
-#undef S1_WR_Z
+template <bool PUSH, int K, class T>
+__device__ __forceinline__ void s1_out(const S1Tab<T>& F, T* hcur, const FbGeo& G,
+                                       const S1Frame& q, uint32_t s, uint32_t bounce,
+                                       const T (&v)[19]) {
+  constexpr int X = cx(K), Y = cy(K), Z = cz(K);
+  const bool local = ((bounce >> K) & 1u) || s1_leaves<X, Y, Z>(q);
+  const bool cross = !local && s1_crosses<X, Y, Z>(q);
+  if (cross) hcur[s1_out_slot<K>(G, q)] = v[K];
+  if (!PUSH || local)
+    F.pl[K][s] = v[K];
+  else if (!cross)
+    F.sh[K][s] = v[K];
+}
+template <bool PUSH, class T, int... Is>
+__device__ __forceinline__ void s1_read(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
+                                        const S1Frame& q, uint32_t s, uint32_t bounce, T (&v)[19],
+                                        std::integer_sequence<int, Is...>) {
+  v[0] = F.pl[0][s];
+  (s1_in<PUSH, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
+}
+template <bool PUSH, class T, int... Ks>
+__device__ __forceinline__ void s1_write(const S1Tab<T>& F, T* hcur, const FbGeo& G,
+                                         const S1Frame& q, uint32_t s, uint32_t bounce,
+                                         const T (&v)[19], std::integer_sequence<int, Ks...>) {
+  F.pl[0][s] = v[0];
+  (s1_out<PUSH, Ks + 1>(F, hcur, G, q, s, bounce, v), ...);
 }
 
+// resident 256-thread blocks per SM (the register budget; the z chunks are
+// sized for these waves): fp64 2 (<= 128 registers), fp32 LBM_S1_BLOCKS32
 #ifndef LBM_S1_BLOCKS
 #define LBM_S1_BLOCKS 2
 #endif
+#ifndef LBM_S1_BLOCKS32
+#define LBM_S1_BLOCKS32 3
+#endif
+template <class T>
+struct S1Blocks {
+  static constexpr int value = sizeof(T) == 8 ? LBM_S1_BLOCKS : LBM_S1_BLOCKS32;
+};
+static int s1_blocks(Prec p) { return p == Prec::f64 ? LBM_S1_BLOCKS : LBM_S1_BLOCKS32; }
 
 // One sweep over a block's planes. Iteration z reads node z + 1's inputs
 // (push: its own slots in plane z + 1; pull: planes z .. z + 2), then, after
@@ -163,8 +201,8 @@ __device__ __forceinline__ void s1_write(const Fld<T, false>& F, T* hcur, const 
 // outputs land, pull plane z is read by nodes z - 1 .. z + 1 in iterations
 // <= z.
 template <class T, bool PUSH>
-__global__ void __launch_bounds__(kFbThreads, LBM_S1_BLOCKS)
-    k_swap1(Fld<T, false> F, Lat L, Trt<T> op, FbGeo G, T* __restrict__ hcur,
+__global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
+    k_swap1(const __grid_constant__ S1Tab<T> F, Lat L, Trt<T> op, FbGeo G, T* __restrict__ hcur,
             const T* __restrict__ hprev) {
   const int ntile = G.tiles_x * G.tiles_y;
   const int tile = (int)blockIdx.x % ntile, ch = (int)blockIdx.x / ntile;
@@ -172,30 +210,42 @@ __global__ void __launch_bounds__(kFbThreads, LBM_S1_BLOCKS)
   const int tx = threadIdx.x % kFbX, ty = threadIdx.x / kFbX;
   const bool act = tx < b.txv && ty < b.tyv;
   const int x = b.x0 + tx, y = b.y0 + ty;
-  const uint32_t s0 = (uint32_t)x + (uint32_t)L.sx * (uint32_t)y;
   const uint32_t sxy = (uint32_t)L.sxy;
-  S1Face qf{ty == 0, ty == b.tyv - 1, tx == 0, tx == b.txv - 1, false, false}, qg = qf;
+  const uint32_t s0 = (uint32_t)x + (uint32_t)L.sx * (uint32_t)y;
+  const auto seq = std::make_integer_sequence<int, 18>{};
+  S1Frame qf;
+  qf.fxl = tx == 0, qf.fxh = tx == b.txv - 1, qf.fyl = ty == 0, qf.fyh = ty == b.tyv - 1;
+  qf.dxl = x == 0, qf.dxh = x == L.nx - 1, qf.dyl = y == 0, qf.dyh = y == L.ny - 1;
+  qf.tx = tx, qf.ty = ty, qf.zc = G.zc;
+  qf.base = b.base;
+  qf.rx = G.region;
+  qf.ry = (long long)G.tiles_x * G.region;
+  qf.rz = (long long)G.tiles_x * G.tiles_y * G.region;
+  auto at_plane = [&](S1Frame& q, int z) {
+    q.pz = z - b.zb;
+    q.fzl = z == b.zb, q.fzh = z == b.ze - 1;
+    q.dzl = z == 0, q.dzh = z == L.nz - 1;
+  };
+  S1Frame qg = qf;
   T f[19], g[19];
   uint32_t bf = 0, bg = 0;
   bool lf = false, lg = false;
   if (act) {
+    at_plane(qf, b.zb);
     lf = fb_cell(L, x, y, b.zb, bf);
-    qf.zlo = true;
-    qf.zhi = b.zb == b.ze - 1;
-    if (lf) s1_read<PUSH>(F, hprev, L, G, b, x, y, b.zb, s0 + (uint32_t)b.zb * sxy, bf, qf, f);
+    if (lf) s1_read<PUSH>(F, hprev, G, qf, s0 + (uint32_t)b.zb * sxy, bf, f, seq);
   }
   for (int z = b.zb; z < b.ze; ++z) {
     lg = false;
     if (act && z + 1 < b.ze) {
+      at_plane(qg, z + 1);
       lg = fb_cell(L, x, y, z + 1, bg);
-      qg.zlo = false;
-      qg.zhi = z + 1 == b.ze - 1;
-      if (lg) s1_read<PUSH>(F, hprev, L, G, b, x, y, z + 1, s0 + (uint32_t)(z + 1) * sxy, bg, qg, g);
+      if (lg) s1_read<PUSH>(F, hprev, G, qg, s0 + (uint32_t)(z + 1) * sxy, bg, g, seq);
     }
     __syncthreads();
     if (lf) {
       collide(op, f);
-      s1_write<PUSH>(F, hcur, L, G, b, x, y, z, s0 + (uint32_t)z * sxy, bf, qf, f);
+      s1_write<PUSH>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
     }
 #pragma unroll
     for (int i = 0; i < 19; ++i) f[i] = g[i];
@@ -251,35 +301,48 @@ bool swap1_ok(const DField& f, const Lat& L) {
   return L.cell_begin == 0 && (unsigned long long)L.ncells == (unsigned long long)L.nx * L.ny * L.nz;
 }
 
-size_t swap1_face_elems(const Lat& L) {
-  const FbGeo G = fb_geo(L, LBM_S1_BLOCKS);
+size_t swap1_face_elems(const DField& f, const Lat& L) {
+  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
   return (size_t)G.tiles_x * G.tiles_y * G.nchunks * (size_t)G.region;
+}
+
+template <class T>
+static S1Tab<T> s1_tab(const DField& f, const Lat& L, bool push) {
+  S1Tab<T> t;
+  T* p = static_cast<T*>(f.p);
+  for (int i = 0; i < 19; ++i) t.pl[i] = p + (long long)i * f.stride;
+  for (int i = 0; i < 19; ++i) {
+    const long long off = cx(i) + (long long)cy(i) * L.sx + (long long)cz(i) * L.sxy;
+    t.sh[i] = push ? t.pl[opp(i)] + off : t.pl[i] - off;
+  }
+  t.sh[0] = t.pl[0];
+  return t;
 }
 
 void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev) {
-  const FbGeo G = fb_geo(L, LBM_S1_BLOCKS);
+  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
   if (f.prec == Prec::f64) {
     if (push)
-      k_swap1<double, true><<<grid, kFbThreads, 0, st>>>(fld<double, false>(f), L, cast_op<double>(op), G,
+      k_swap1<double, true><<<grid, kFbThreads, 0, st>>>(s1_tab<double>(f, L, true), L, cast_op<double>(op), G,
                                                         (double*)hcur, (const double*)hprev);
     else
-      k_swap1<double, false><<<grid, kFbThreads, 0, st>>>(fld<double, false>(f), L, cast_op<double>(op), G,
+      k_swap1<double, false><<<grid, kFbThreads, 0, st>>>(s1_tab<double>(f, L, false), L, cast_op<double>(op), G,
                                                          (double*)hcur, (const double*)hprev);
   } else {
     if (push)
-      k_swap1<float, true><<<grid, kFbThreads, 0, st>>>(fld<float, false>(f), L, cast_op<float>(op), G,
+      k_swap1<float, true><<<grid, kFbThreads, 0, st>>>(s1_tab<float>(f, L, true), L, cast_op<float>(op), G,
                                                        (float*)hcur, (const float*)hprev);
     else
-      k_swap1<float, false><<<grid, kFbThreads, 0, st>>>(fld<float, false>(f), L, cast_op<float>(op), G,
+      k_swap1<float, false><<<grid, kFbThreads, 0, st>>>(s1_tab<float>(f, L, false), L, cast_op<float>(op), G,
                                                         (float*)hcur, (const float*)hprev);
   }
 }
 
 void launch_swap1_faces(cudaStream_t st, const DField& f, const Lat& L, bool push, bool fill,
                         void* h) {
-  const FbGeo G = fb_geo(L, LBM_S1_BLOCKS);
+  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
 #define S1_F(T, P, FL) k_swap1_faces<T, P, FL><<<grid, kFbThreads, 0, st>>>(fld<T, false>(f), L, G, (T*)h)
   if (f.prec == Prec::f64) {

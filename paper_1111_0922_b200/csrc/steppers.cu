@@ -382,7 +382,7 @@ class SwapDirect final : public DirectStepper {
     }
     // single pass with face buffers (kernels_swap1.cu), SoA: two parities
     if (!fused_ && swap1_ok(field(f_, soa_stride(g.cells())), L_)) {
-      hn_ = swap1_face_elems(L_);
+      hn_ = swap1_face_elems(field(f_, soa_stride(g.cells())), L_);
       h_[0].alloc(hn_ * esize());
       h_[1].alloc(hn_ * esize());
       single_ = true;

@@ -374,3 +374,53 @@ def test_cg_all_solid_plane_groups(gpu, aos_window):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("dims,policy", [
+    ((5, 7, 6), ("periodic", "periodic", "periodic")),
+    ((70, 20, 30), ("periodic", "periodic", "periodic")),
+    ((33, 9, 17), ("periodic", "periodic", "wall")),
+    ((45, 19, 11), ("wall", "wall", "periodic")),
+    ((64, 16, 9), ("wall", "periodic", "wall")),
+    ((40, 17, 12), "porous"),
+])
+@pytest.mark.parametrize("zchunk", ["", "3"])
+@pytest.mark.parametrize("precision", [8, 4])
+@pytest.mark.parametrize("scheme", ["swap-push", "swap-pull"])
+def test_swap_single_pass_equals_two_passes(gpu, monkeypatch, dims, policy, zchunk, precision,
+                                            scheme):
+    """kernels_swap1.cu (one sweep; links between blocks through face buffers
+    of alternating parity) against the collide pass + exchange pass: bitwise
+    after odd and even step counts, across extractions (push flushes its face
+    values into the field) and reloads, over ragged tiles, several z chunks
+    (LBMGPU_SWAP1_ZCHUNK), wall axes, a porous mask and the deferred seam
+    fix-up."""
+    rng = np.random.default_rng(13)
+    mask = None
+    if policy == "porous":
+        mask = (rng.random(dims[::-1]) > 0.3).astype(np.uint8).reshape(-1)
+        policy = ("periodic", "periodic", "periodic")
+    geo = gpu.GridGeometry(*dims, policy, mask)
+    flow = gpu.bgk(1.7, body_force=(1e-6, 2e-7, -1e-7))
+    monkeypatch.setenv("LBMGPU_SWAP1_ZCHUNK", zchunk)
+    f0 = None
+    for deferred in (False, True):
+        outs = []
+        for single in ("1", "0"):
+            monkeypatch.setenv("LBMGPU_SWAP_SINGLE", single)
+            st = gpu.create_stepper(scheme, "direct", geo, flow,
+                                    gpu.StepperOptions(precision=precision,
+                                                       swap_deferred_fixup=deferred))
+            st.init_field("taylor_green", seed=5)
+            if f0 is None:
+                f0 = st.extract_natural()
+            got = []
+            for n in (3, 4):
+                st.step_n(n)
+                got.append(st.extract_natural())
+            st.load_natural(f0)
+            st.step_n(5)
+            got.append(st.extract_natural())
+            outs.append(got)
+        for a, b in zip(outs[0], outs[1]):
+            assert bitwise_equal(a, b), (deferred,)
