@@ -265,8 +265,19 @@ __device__ __forceinline__ void aa_odd_plain(const SoaNb<T>& N, const Ctx& c, co
 #pragma unroll
   for (int j = 1; j < 19; ++j) N.n[j][nb_ix(cx(j), s, sm, sp)] = f[j];
 }
+// fp32 SoA AA odd sweep at 6 blocks per SM (<= 42 registers; the spilled
+// values are L1 hits): C1 0.92 -> 0.98, C4 0.89 -> 0.96 of the roofline
+// (4: latency-bound at ~28 resident warps, 7: 0.82)
+#ifndef LBM_AA_MIN_BLOCKS_F32
+#define LBM_AA_MIN_BLOCKS_F32 6
+#endif
 template <class T, bool AOS>
-__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value)
+struct AaOddBlocks {
+  static constexpr int value =
+      sizeof(T) == 4 && !AOS ? LBM_AA_MIN_BLOCKS_F32 : SoaMinBlocks<T, AOS>::value;
+};
+template <class T, bool AOS>
+__global__ void __launch_bounds__(kBlock, AaOddBlocks<T, AOS>::value)
     k_aa_odd(Fld<T, AOS> F, Lat L, Trt<T> op, SoaNb<T> N) {
   const uint32_t cell = L.cell_begin + blockIdx.x * kBlock + threadIdx.x;
   if (cell >= L.ncells) return;
