@@ -63,8 +63,13 @@ struct S1Frame {
   bool fxl, fxh, fyl, fyh, fzl, fzh;  // on the box's low / high face
   bool dxl, dxh, dyl, dyh, dzl, dzh;  // on the domain's low / high face
   int tx, ty, pz;                     // position in the box
-  long long base, rx, ry, rz;         // face region of the block, neighbour strides
   int zc;
+  // face-buffer element offsets (32-bit: a whole buffer is < 2^32 elements):
+  // this block's region and its neighbours' strides; the input slots of this
+  // thread on its y / x faces at the current plane and on its z faces
+  uint32_t base, rx, ry, rz, hy, hx, hz;
+  uint32_t iy, ix, iz;
+  uint32_t box;  // LBM_S1_CROSSMASK: links leaving the block box at this plane
 };
 // the link along (CX, CY, CZ) leaves the domain / crosses the block box;
 // only the flags of the direction's nonzero components are tested (y / z
@@ -78,6 +83,36 @@ template <int CX, int CY, int CZ>
 __device__ __forceinline__ bool s1_crosses(const S1Frame& q) {
   return (CX < 0 && q.fxl) || (CX > 0 && q.fxh) || (CY < 0 && q.fyl) || (CY > 0 && q.fyh) ||
          (CZ < 0 && q.fzl) || (CZ > 0 && q.fzh);
+}
+// link K (along (CX, CY, CZ)) stays local: it bounces or leaves the domain.
+// LBM_S1_LOCALMASK: `bounce` already holds the leaving links (one mask per
+// plane, a bit test per link) instead of testing the edge flags per link
+#ifndef LBM_S1_LOCALMASK
+#define LBM_S1_LOCALMASK 1
+#endif
+template <int K, int CX, int CY, int CZ>
+__device__ __forceinline__ bool s1_local(const S1Frame& q, uint32_t bounce) {
+  if (LBM_S1_LOCALMASK) return (bounce >> K) & 1u;
+  return ((bounce >> K) & 1u) || s1_leaves<CX, CY, CZ>(q);
+}
+// link K crosses the block box: a bit of the plane's box mask (CM) or the
+// face flags of the direction's components
+template <bool CM, int K, int CX, int CY, int CZ>
+__device__ __forceinline__ bool s1_cross(const S1Frame& q) {
+  if (CM) return (q.box >> K) & 1u;
+  return s1_crosses<CX, CY, CZ>(q);
+}
+// Per kernel (measured on C1 / C4, the choices only change registers and
+// schedule): the box as a mask for fp64 push (no spills: C1 0.77 -> 0.81);
+// pull keeps a second frame for the next node across the barrier (C1 fp64
+// 0.53 -> 0.56), push recomputes the plane fields instead (fp64 0.58 -> 0.77)
+template <class T, bool PUSH>
+struct S1Cfg {
+  static constexpr bool kCrossMask = PUSH && sizeof(T) == 8;
+  static constexpr bool kTwoFrames = !PUSH;
+};
+__device__ __forceinline__ uint32_t s1_axis_mask(bool lo, bool hi, uint32_t mlo, uint32_t mhi) {
+  return (lo ? mlo : 0u) | (hi ? mhi : 0u);
 }
 // plane bases of the field (kernel parameters, so constant-bank operands):
 // pl[i] = plane i; sh[i] = push: the store target of output i, plane opp i
@@ -95,54 +130,54 @@ struct S1Tab {
 #define LBM_S1_SLOT_INLINE __forceinline__
 #endif
 template <int I>
-__device__ LBM_S1_SLOT_INLINE long long s1_in_slot(const FbGeo& G, const S1Frame& q) {
+__device__ LBM_S1_SLOT_INLINE uint32_t s1_in_slot(const S1Frame& q) {
   constexpr int X = cx(I), Y = cy(I), Z = cz(I);
   if ((Y > 0 && q.fyl) || (Y < 0 && q.fyh)) {
     constexpr int side = Y > 0 ? 0 : 1, qq = face_q(1, Y > 0 ? 1 : -1, I);
-    return q.base + G.hy + ((long long)(q.pz * 2 + side) * 5 + qq) * kFbX + q.tx;
+    return q.iy + (uint32_t)((side * 5 + qq) * kFbX);
   }
   if ((X > 0 && q.fxl) || (X < 0 && q.fxh)) {
     constexpr int side = X > 0 ? 0 : 1, qq = face_q(0, X > 0 ? 1 : -1, I);
-    return q.base + G.hx + ((long long)(q.pz * 2 + side) * 5 + qq) * kFbY + q.ty;
+    return q.ix + (uint32_t)((side * 5 + qq) * kFbY);
   }
   constexpr int side = Z > 0 ? 0 : 1, qq = face_q(2, Z > 0 ? 1 : -1, I);
-  return q.base + G.hz + ((long long)(side * 5 + qq) * kFbY + q.ty) * kFbX + q.tx;
+  return q.iz + (uint32_t)((side * 5 + qq) * kFbY * kFbX);
 }
 // slot of the value this node sends along direction K to R = X + c_K (outside
 // the box): in the receiving block's region, keyed by the face X lies across
 template <int K>
-__device__ LBM_S1_SLOT_INLINE long long s1_out_slot(const FbGeo& G, const S1Frame& q) {
+__device__ LBM_S1_SLOT_INLINE uint32_t s1_out_slot(const S1Frame& q) {
   constexpr int X = cx(K), Y = cy(K), Z = cz(K);
   const int ex = (X < 0 && q.fxl) ? -1 : ((X > 0 && q.fxh) ? 1 : 0);
   const int ey = (Y < 0 && q.fyl) ? -1 : ((Y > 0 && q.fyh) ? 1 : 0);
   const int ez = (Z < 0 && q.fzl) ? -1 : ((Z > 0 && q.fzh) ? 1 : 0);
-  const long long rb = q.base + ex * q.rx + ey * q.ry + ez * q.rz;
+  const uint32_t rb = q.base + (uint32_t)ex * q.rx + (uint32_t)ey * q.ry + (uint32_t)ez * q.rz;
   const int px = ex > 0 ? 0 : (ex < 0 ? kFbX - 1 : q.tx + X);
   const int py = ey > 0 ? 0 : (ey < 0 ? kFbY - 1 : q.ty + Y);
   const int pz = ez > 0 ? 0 : (ez < 0 ? q.zc - 1 : q.pz + Z);
   if (ey != 0) {
     constexpr int side = Y > 0 ? 0 : 1, qq = face_q(1, Y > 0 ? 1 : -1, K);
-    return rb + G.hy + ((long long)(pz * 2 + side) * 5 + qq) * kFbX + px;
+    return rb + q.hy + (uint32_t)(((pz * 2 + side) * 5 + qq) * kFbX + px);
   }
   if (ex != 0) {
     constexpr int side = X > 0 ? 0 : 1, qq = face_q(0, X > 0 ? 1 : -1, K);
-    return rb + G.hx + ((long long)(pz * 2 + side) * 5 + qq) * kFbY + py;
+    return rb + q.hx + (uint32_t)(((pz * 2 + side) * 5 + qq) * kFbY + py);
   }
   constexpr int side = Z > 0 ? 0 : 1, qq = face_q(2, Z > 0 ? 1 : -1, K);
-  return rb + G.hz + ((long long)(side * 5 + qq) * kFbY + py) * kFbX + px;
+  return rb + q.hz + (uint32_t)(((side * 5 + qq) * kFbY + py) * kFbX + px);
 }
 
 // the 19 inputs of the node: push (opp i, X); pull (i, X - c_i), or (opp i, X)
 // when that link (opp i from X) is local; a crossing input comes from the
 // face buffer of the last sweep (the field load is issued regardless, so the
 // loads of a node leave together)
-template <bool PUSH, int I, class T>
+template <bool PUSH, bool CM, int I, class T>
 __device__ __forceinline__ void s1_in(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
                                       const S1Frame& q, uint32_t s, uint32_t bounce, T (&v)[19]) {
   constexpr int X = cx(I), Y = cy(I), Z = cz(I), J = opp(I);
-  const bool local = ((bounce >> J) & 1u) || s1_leaves<-X, -Y, -Z>(q);
-  if (!local && s1_crosses<-X, -Y, -Z>(q))
-    v[I] = hprev[s1_in_slot<I>(G, q)];
+  const bool local = s1_local<J, -X, -Y, -Z>(q, bounce);
+  if (!local && s1_cross<CM, J, -X, -Y, -Z>(q))
+    v[I] = hprev[s1_in_slot<I>(q)];
   else if (PUSH || local)
     v[I] = F.pl[J][s];
   else
@@ -151,32 +186,32 @@ __device__ __forceinline__ void s1_in(const S1Tab<T>& F, const T* hprev, const F
 // the 19 outputs: push (opp k, X + c_k), or (k, X) when link k is local;
 // pull (k, X); a crossing output goes to the receiver's face buffer instead
 // (push) or as well (pull)
-template <bool PUSH, int K, class T>
+template <bool PUSH, bool CM, int K, class T>
 __device__ __forceinline__ void s1_out(const S1Tab<T>& F, T* hcur, const FbGeo& G,
                                        const S1Frame& q, uint32_t s, uint32_t bounce,
                                        const T (&v)[19]) {
   constexpr int X = cx(K), Y = cy(K), Z = cz(K);
-  const bool local = ((bounce >> K) & 1u) || s1_leaves<X, Y, Z>(q);
-  const bool cross = !local && s1_crosses<X, Y, Z>(q);
-  if (cross) hcur[s1_out_slot<K>(G, q)] = v[K];
+  const bool local = s1_local<K, X, Y, Z>(q, bounce);
+  const bool cross = !local && s1_cross<CM, K, X, Y, Z>(q);
+  if (cross) hcur[s1_out_slot<K>(q)] = v[K];
   if (!PUSH || local)
     F.pl[K][s] = v[K];
   else if (!cross)
     F.sh[K][s] = v[K];
 }
-template <bool PUSH, class T, int... Is>
+template <bool PUSH, bool CM, class T, int... Is>
 __device__ __forceinline__ void s1_read(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
                                         const S1Frame& q, uint32_t s, uint32_t bounce, T (&v)[19],
                                         std::integer_sequence<int, Is...>) {
   v[0] = F.pl[0][s];
-  (s1_in<PUSH, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
+  (s1_in<PUSH, CM, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
 }
-template <bool PUSH, class T, int... Ks>
+template <bool PUSH, bool CM, class T, int... Ks>
 __device__ __forceinline__ void s1_write(const S1Tab<T>& F, T* hcur, const FbGeo& G,
                                          const S1Frame& q, uint32_t s, uint32_t bounce,
                                          const T (&v)[19], std::integer_sequence<int, Ks...>) {
   F.pl[0][s] = v[0];
-  (s1_out<PUSH, Ks + 1>(F, hcur, G, q, s, bounce, v), ...);
+  (s1_out<PUSH, CM, Ks + 1>(F, hcur, G, q, s, bounce, v), ...);
 }
 
 // resident 256-thread blocks per SM (the register budget; the z chunks are
@@ -213,45 +248,59 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
   const uint32_t sxy = (uint32_t)L.sxy;
   const uint32_t s0 = (uint32_t)x + (uint32_t)L.sx * (uint32_t)y;
   const auto seq = std::make_integer_sequence<int, 18>{};
+  constexpr bool CM = S1Cfg<T, PUSH>::kCrossMask, TWO = S1Cfg<T, PUSH>::kTwoFrames;
   S1Frame qf;
   qf.fxl = tx == 0, qf.fxh = tx == b.txv - 1, qf.fyl = ty == 0, qf.fyh = ty == b.tyv - 1;
   qf.dxl = x == 0, qf.dxh = x == L.nx - 1, qf.dyl = y == 0, qf.dyh = y == L.ny - 1;
   qf.tx = tx, qf.ty = ty, qf.zc = G.zc;
-  qf.base = b.base;
-  qf.rx = G.region;
-  qf.ry = (long long)G.tiles_x * G.region;
-  qf.rz = (long long)G.tiles_x * G.tiles_y * G.region;
+  qf.base = (uint32_t)b.base;
+  qf.rx = (uint32_t)G.region;
+  qf.ry = (uint32_t)((long long)G.tiles_x * G.region);
+  qf.rz = (uint32_t)((long long)G.tiles_x * G.tiles_y * G.region);
+  qf.hy = (uint32_t)G.hy, qf.hx = (uint32_t)G.hx, qf.hz = (uint32_t)G.hz;
+  qf.iz = qf.base + qf.hz + (uint32_t)(ty * kFbX + tx);
+  const uint32_t leave_xy = s1_axis_mask(qf.dxl, qf.dxh, kMxm, kMxp) | s1_axis_mask(qf.dyl, qf.dyh, kMym, kMyp);
+  const uint32_t box_xy = s1_axis_mask(qf.fxl, qf.fxh, kMxm, kMxp) | s1_axis_mask(qf.fyl, qf.fyh, kMym, kMyp);
   auto at_plane = [&](S1Frame& q, int z) {
     q.pz = z - b.zb;
     q.fzl = z == b.zb, q.fzh = z == b.ze - 1;
     q.dzl = z == 0, q.dzh = z == L.nz - 1;
+    q.iy = q.base + q.hy + (uint32_t)(q.pz * 10 * kFbX + tx);
+    q.ix = q.base + q.hx + (uint32_t)(q.pz * 10 * kFbY + ty);
+    if (CM) q.box = box_xy | s1_axis_mask(q.fzl, q.fzh, kMzm, kMzp);
   };
+  // qg: the frame of node z + 1 (TWO), else qf's per-plane fields are
+  // recomputed (at_plane) before each node's reads and writes
   S1Frame qg = qf;
   T f[19], g[19];
   uint32_t bf = 0, bg = 0;
   bool lf = false, lg = false;
   if (act) {
-    at_plane(qf, b.zb);
     lf = fb_cell(L, x, y, b.zb, bf);
-    if (lf) s1_read<PUSH>(F, hprev, G, qf, s0 + (uint32_t)b.zb * sxy, bf, f, seq);
+    if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
+    at_plane(qf, b.zb);
+    if (lf) s1_read<PUSH, CM>(F, hprev, G, qf, s0 + (uint32_t)b.zb * sxy, bf, f, seq);
   }
   for (int z = b.zb; z < b.ze; ++z) {
     lg = false;
     if (act && z + 1 < b.ze) {
-      at_plane(qg, z + 1);
       lg = fb_cell(L, x, y, z + 1, bg);
-      if (lg) s1_read<PUSH>(F, hprev, G, qg, s0 + (uint32_t)(z + 1) * sxy, bg, g, seq);
+      if (LBM_S1_LOCALMASK) bg |= leave_xy | s1_axis_mask(z + 1 == 0, z + 1 == L.nz - 1, kMzm, kMzp);
+      S1Frame& qn = TWO ? qg : qf;
+      at_plane(qn, z + 1);
+      if (lg) s1_read<PUSH, CM>(F, hprev, G, qn, s0 + (uint32_t)(z + 1) * sxy, bg, g, seq);
     }
     __syncthreads();
     if (lf) {
       collide(op, f);
-      s1_write<PUSH>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
+      if (!TWO) at_plane(qf, z);
+      s1_write<PUSH, CM>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
     }
 #pragma unroll
     for (int i = 0; i < 19; ++i) f[i] = g[i];
     bf = bg;
     lf = lg;
-    qf = qg;
+    if (TWO) qf = qg;
   }
 }
 
@@ -293,12 +342,21 @@ __global__ void __launch_bounds__(kFbThreads)
 }  // namespace
 
 // SoA, full-grid direct lattice without halo or ghost planes
-bool swap1_ok(const DField& f, const Lat& L) {
+bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (f.aos) return false;
-  const char* e = std::getenv("LBMGPU_SWAP_SINGLE");  // opt-in until it beats two passes
-  if (!(e && e[0] == '1')) return false;
+  // default: SWAP push in one sweep (C1 fp64 0.81 / fp32 0.53, C4 0.68 / 0.47
+  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull keeps the two passes
+  // (one sweep: C1 0.56 / 0.46, C4 0.48 / 0.42). LBMGPU_SWAP_SINGLE=1 / 0
+  // forces it on / off for both.
+  const char* e = std::getenv("LBMGPU_SWAP_SINGLE");
+  const bool on = e ? e[0] == '1' : push;
+  if (!on) return false;
   if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
-  return L.cell_begin == 0 && (unsigned long long)L.ncells == (unsigned long long)L.nx * L.ny * L.nz;
+  if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
+    return false;
+  // face-buffer slots are 32-bit element offsets
+  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
+  return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
 }
 
 size_t swap1_face_elems(const DField& f, const Lat& L) {

@@ -130,7 +130,7 @@ bool launch_swap_fused(cudaStream_t st, const DField& f, const dev::Lat& L, cons
 // sweep (hcur: this sweep's buffer, hprev: the last sweep's), and the
 // field <-> buffer transfers (fill: field -> hprev after a load; flush (push):
 // latest buffer -> field before an extraction)
-bool swap1_ok(const DField& f, const dev::Lat& L);
+bool swap1_ok(const DField& f, const dev::Lat& L, bool push);
 size_t swap1_face_elems(const DField& f, const dev::Lat& L);
 void launch_swap1(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev);

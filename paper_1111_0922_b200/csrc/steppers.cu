@@ -381,7 +381,7 @@ class SwapDirect final : public DirectStepper {
       fused_ = true;
     }
     // single pass with face buffers (kernels_swap1.cu), SoA: two parities
-    if (!fused_ && swap1_ok(field(f_, soa_stride(g.cells())), L_)) {
+    if (!fused_ && swap1_ok(field(f_, soa_stride(g.cells())), L_, !pull_)) {
       hn_ = swap1_face_elems(field(f_, soa_stride(g.cells())), L_);
       h_[0].alloc(hn_ * esize());
       h_[1].alloc(hn_ * esize());
