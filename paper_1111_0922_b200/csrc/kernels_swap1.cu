@@ -106,9 +106,12 @@ __device__ __forceinline__ bool s1_cross(const S1Frame& q) {
 // schedule): the box as a mask for fp64 push (no spills: C1 0.77 -> 0.81);
 // pull keeps a second frame for the next node across the barrier (C1 fp64
 // 0.53 -> 0.56), push recomputes the plane fields instead (fp64 0.58 -> 0.77)
+#ifndef LBM_S1_PULL_CM
+#define LBM_S1_PULL_CM 0
+#endif
 template <class T, bool PUSH>
 struct S1Cfg {
-  static constexpr bool kCrossMask = PUSH && sizeof(T) == 8;
+  static constexpr bool kCrossMask = sizeof(T) == 8 && (PUSH || LBM_S1_PULL_CM);
   static constexpr bool kTwoFrames = !PUSH;
 };
 __device__ __forceinline__ uint32_t s1_axis_mask(bool lo, bool hi, uint32_t mlo, uint32_t mhi) {
@@ -206,6 +209,22 @@ __device__ __forceinline__ void s1_read(const S1Tab<T>& F, const T* hprev, const
   v[0] = F.pl[0][s];
   (s1_in<PUSH, CM, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
 }
+// the inputs of the node whose source plane offset -c_z(i) is in the set:
+// SEL 1 = sources one plane below (c_z = +1), SEL 2 = the others (and the
+// rest value)
+template <bool PUSH, bool CM, int SEL, int I, class T>
+__device__ __forceinline__ void s1_in_sel(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
+                                          const S1Frame& q, uint32_t s, uint32_t bounce,
+                                          T (&v)[19]) {
+  if constexpr ((SEL == 1) == (cz(I) == 1)) s1_in<PUSH, CM, I>(F, hprev, G, q, s, bounce, v);
+}
+template <bool PUSH, bool CM, int SEL, class T, int... Is>
+__device__ __forceinline__ void s1_read_sel(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
+                                            const S1Frame& q, uint32_t s, uint32_t bounce,
+                                            T (&v)[19], std::integer_sequence<int, Is...>) {
+  if (SEL == 2) v[0] = F.pl[0][s];
+  (s1_in_sel<PUSH, CM, SEL, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
+}
 template <bool PUSH, bool CM, class T, int... Ks>
 __device__ __forceinline__ void s1_write(const S1Tab<T>& F, T* hcur, const FbGeo& G,
                                          const S1Frame& q, uint32_t s, uint32_t bounce,
@@ -269,12 +288,52 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
     q.ix = q.base + q.hx + (uint32_t)(q.pz * 10 * kFbY + ty);
     if (CM) q.box = box_xy | s1_axis_mask(q.fzl, q.fzh, kMzm, kMzp);
   };
+  T f[19];
+  uint32_t bf = 0, bg = 0;
+  bool lf = false, lg = false;
+  if constexpr (!PUSH) {
+    // Pull: only the five inputs of node z + 1 from plane z (c_z = +1) must
+    // be read before node z's stores (iteration z); its other inputs (planes
+    // z + 1, z + 2) are rewritten only by nodes z + 1, z + 2, so they are read
+    // in iteration z + 1 itself. Five values cross the barrier instead of 19.
+    if (act) {
+      lf = fb_cell(L, x, y, b.zb, bf);
+      if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
+      at_plane(qf, b.zb);
+      if (lf) s1_read_sel<PUSH, CM, 1>(F, hprev, G, qf, s0 + (uint32_t)b.zb * sxy, bf, f, seq);
+    }
+    for (int z = b.zb; z < b.ze; ++z) {
+      if (lf) {
+        at_plane(qf, z);
+        s1_read_sel<PUSH, CM, 2>(F, hprev, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
+      }
+      T g[19];
+      lg = false;
+      if (act && z + 1 < b.ze) {
+        lg = fb_cell(L, x, y, z + 1, bg);
+        if (LBM_S1_LOCALMASK) bg |= leave_xy | s1_axis_mask(z + 1 == 0, z + 1 == L.nz - 1, kMzm, kMzp);
+        at_plane(qf, z + 1);
+        if (lg) s1_read_sel<PUSH, CM, 1>(F, hprev, G, qf, s0 + (uint32_t)(z + 1) * sxy, bg, g, seq);
+      }
+      __syncthreads();
+      if (lf) {
+        collide(op, f);
+        at_plane(qf, z);
+        s1_write<PUSH, CM>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
+      }
+#pragma unroll
+      for (int i = 1; i < 19; ++i)
+        if (cz(i) == 1) f[i] = g[i];
+      bf = bg;
+      lf = lg;
+    }
+    return;
+  }
+  // push: node z + 1's inputs (its own column) are all read in iteration z;
   // qg: the frame of node z + 1 (TWO), else qf's per-plane fields are
   // recomputed (at_plane) before each node's reads and writes
   S1Frame qg = qf;
-  T f[19], g[19];
-  uint32_t bf = 0, bg = 0;
-  bool lf = false, lg = false;
+  T g[19];
   if (act) {
     lf = fb_cell(L, x, y, b.zb, bf);
     if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
