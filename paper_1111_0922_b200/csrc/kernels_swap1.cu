@@ -209,14 +209,24 @@ __device__ __forceinline__ void s1_read(const S1Tab<T>& F, const T* hprev, const
   v[0] = F.pl[0][s];
   (s1_in<PUSH, CM, Is + 1>(F, hprev, G, q, s, bounce, v), ...);
 }
-// the inputs of the node whose source plane offset -c_z(i) is in the set:
-// SEL 1 = sources one plane below (c_z = +1), SEL 2 = the others (and the
-// rest value)
+// the inputs of the node read one iteration ahead (SEL 1) or in the node's
+// own iteration (SEL 2, with the rest value). Pull: sources one plane below
+// (c_z = +1) must be read ahead (node z - 1 rewrites them); the others are
+// rewritten in the node's own iteration or later and may be read either way.
+// LBM_S1_PULL_AHEAD = 1: only the c_z = +1 inputs ahead; 2: every c_z != 0
+// input ahead (the nine in-plane ones in the node's iteration; C1 fp64 0.58
+// -> 0.51: more registers live across the barrier)
+#ifndef LBM_S1_PULL_AHEAD
+#define LBM_S1_PULL_AHEAD 1
+#endif
+__host__ __device__ constexpr bool s1_early(int i) {
+  return LBM_S1_PULL_AHEAD == 1 ? cz(i) == 1 : cz(i) != 0;
+}
 template <bool PUSH, bool CM, int SEL, int I, class T>
 __device__ __forceinline__ void s1_in_sel(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
                                           const S1Frame& q, uint32_t s, uint32_t bounce,
                                           T (&v)[19]) {
-  if constexpr ((SEL == 1) == (cz(I) == 1)) s1_in<PUSH, CM, I>(F, hprev, G, q, s, bounce, v);
+  if constexpr ((SEL == 1) == s1_early(I)) s1_in<PUSH, CM, I>(F, hprev, G, q, s, bounce, v);
 }
 template <bool PUSH, bool CM, int SEL, class T, int... Is>
 __device__ __forceinline__ void s1_read_sel(const S1Tab<T>& F, const T* hprev, const FbGeo& G,
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
       }
 #pragma unroll
       for (int i = 1; i < 19; ++i)
-        if (cz(i) == 1) f[i] = g[i];
+        if (s1_early(i)) f[i] = g[i];
       bf = bg;
       lf = lg;
     }
