@@ -256,6 +256,10 @@ struct S1Blocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_S1_BLOCKS : LBM_S1_BLOCKS32;
 };
 static int s1_blocks(Prec p) { return p == Prec::f64 ? LBM_S1_BLOCKS : LBM_S1_BLOCKS32; }
+// AoS: the staged ring (one fp64 / two fp32 blocks per SM)
+static int s1_blocks(const DField& f) {
+  return f.aos ? (f.prec == Prec::f64 ? 1 : 2) : s1_blocks(f.prec);
+}
 
 // One sweep over a block's planes. Iteration z reads node z + 1's inputs
 // (push: its own slots in plane z + 1; pull: planes z .. z + 2), then, after
@@ -373,12 +377,241 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
   }
 }
 
+// ---------------------------------------------------------------------------
+// SWAP push in one sweep on AoS records. The same face buffers as the SoA
+// kernel: a block never writes a record outside its box, so its box planes
+// can be staged in shared memory whole and leave whole — each record row of
+// a plane (txv records, contiguous) arrives as one bulk copy (TMA) and, once
+// final, leaves as one (head / tail elements by the lanes: the bytes around
+// a row belong to other blocks). A 5-plane ring, one row per warp:
+//   iteration z: node z + 1 reads its record (plane z + 1) into registers;
+//   block barrier; plane z - 2 (last written in iteration z - 1) leaves and
+//   its slot is refilled with plane z + 3; node z collides and writes its
+//   outputs into the staged records of planes z - 1 .. z + 1 (or a face
+//   buffer, or its own slot on a local link).
+// ---------------------------------------------------------------------------
+template <class T>
+struct S1Aos {
+  static constexpr int NS = 5;
+  static constexpr int ROWF = kFbX * 19 + 32 / (int)sizeof(T);  // a row + 16-byte phase slack
+  static constexpr int BUF = kFbY * ROWF;
+  static constexpr size_t kBytes = (size_t)NS * BUF * sizeof(T);
+  static constexpr int kBlocks = sizeof(T) == 8 ? 1 : 2;
+};
+static_assert(S1Aos<double>::kBytes <= 227 * 1024 - 1024, "fp64 AoS swap ring too large");
+static_assert(2 * (S1Aos<float>::kBytes + 1024) <= 228 * 1024, "fp32 AoS swap ring: two blocks");
+
+// one warp: n elements shared -> global, s and g congruent mod 16 bytes
+template <class T>
+__device__ __forceinline__ void s1_copy_out(T* g, const T* s, int n, int lane) {
+  constexpr int V = 16 / (int)sizeof(T);
+  int head = (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) / sizeof(T));
+  if (head > n) head = n;
+  const int nmid = (n - head) / V * V;
+  if (lane < head) g[lane] = s[lane];
+  const int t0 = head + nmid;
+  if (t0 + lane < n) g[t0 + lane] = s[t0 + lane];
+  if (lane == 0 && nmid) {
+    bulk_s2g(g + head, s + head, (uint32_t)nmid * (uint32_t)sizeof(T));
+    bulk_commit();
+  }
+}
+
+template <bool CM, int I, class T>
+__device__ __forceinline__ void s1a_in(const T* rec, const T* hprev, const S1Frame& q,
+                                       uint32_t bounce, T (&v)[19]) {
+  constexpr int X = cx(I), Y = cy(I), Z = cz(I), J = opp(I);
+  const bool local = s1_local<J, -X, -Y, -Z>(q, bounce);
+  if (!local && s1_cross<CM, J, -X, -Y, -Z>(q))
+    v[I] = hprev[s1_in_slot<I>(q)];
+  else
+    v[I] = rec[J];
+}
+// nb(K): the staged record X + c_K (in the box)
+template <bool CM, int K, class T, class Nb>
+__device__ __forceinline__ void s1a_out(T* rec, Nb nb, T* hcur, const S1Frame& q, uint32_t bounce,
+                                        const T (&v)[19]) {
+  constexpr int X = cx(K), Y = cy(K), Z = cz(K);
+  const bool local = s1_local<K, X, Y, Z>(q, bounce);
+  const bool cross = !local && s1_cross<CM, K, X, Y, Z>(q);
+  if (cross)
+    hcur[s1_out_slot<K>(q)] = v[K];
+  else if (local)
+    rec[K] = v[K];
+  else
+    nb(K)[opp(K)] = v[K];
+}
+template <bool CM, class T, int... Is>
+__device__ __forceinline__ void s1a_read(const T* rec, const T* hprev, const S1Frame& q,
+                                         uint32_t bounce, T (&v)[19],
+                                         std::integer_sequence<int, Is...>) {
+  v[0] = rec[0];
+  (s1a_in<CM, Is + 1>(rec, hprev, q, bounce, v), ...);
+}
+template <bool CM, class T, class Nb, int... Ks>
+__device__ __forceinline__ void s1a_write(T* rec, Nb nb, T* hcur, const S1Frame& q,
+                                          uint32_t bounce, const T (&v)[19],
+                                          std::integer_sequence<int, Ks...>) {
+  rec[0] = v[0];
+  (s1a_out<CM, Ks + 1>(rec, nb, hcur, q, bounce, v), ...);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kFbThreads, S1Aos<T>::kBlocks)
+    k_swap1_aos(T* __restrict__ fp, Lat L, Trt<T> op, FbGeo G, T* __restrict__ hcur,
+                const T* __restrict__ hprev) {
+  using C = S1Aos<T>;
+  constexpr int NS = C::NS, ROWF = C::ROWF, BUF = C::BUF;
+  constexpr bool CM = sizeof(T) == 8;
+  extern __shared__ __align__(16) unsigned char s1a_smem[];
+  T* sm = reinterpret_cast<T*>(s1a_smem);
+  __shared__ __align__(8) uint64_t full[NS];
+  const int ntile = G.tiles_x * G.tiles_y;
+  const int tile = (int)blockIdx.x % ntile, ch = (int)blockIdx.x / ntile;
+  const FbBlock b = fb_block(L, G, tile % G.tiles_x, tile / G.tiles_x, ch);
+  const int tx = threadIdx.x % kFbX, ty = threadIdx.x / kFbX, lane = tx;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NS; ++k) mbar_init(&full[k], (uint32_t)b.tyv);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto slot = [&](int p) { return (p - b.zb) % NS; };
+  auto par = [&](int p) { return (uint32_t)((p - b.zb) / NS) & 1u; };
+  // element offset of record (x0, y, p) and its 16-byte phase in elements
+  auto rowg = [&](int y, int p) {
+    return ((long long)L.sx * ((long long)y + (long long)L.sy * p) + b.x0) * 19;
+  };
+  auto phase = [&](long long g) { return (int)(g & (long long)(16 / sizeof(T) - 1)); };
+  // row r of plane p (lane 0 of warp r): one bulk copy of the row's 16-byte
+  // superset (the over-read lands in the row's slack)
+  auto load = [&](int p, int r) {
+    const long long g = rowg(b.y0 + r, p);
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(fp + g) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(fp + g + (long long)b.txv * 19) + 15) & ~(uintptr_t)15;
+    mbar_arrive_tx(&full[slot(p)], (uint32_t)(hi - lo));
+    bulk_g2s(sm + slot(p) * BUF + r * ROWF, reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo),
+             &full[slot(p)]);
+  };
+  const bool rowv = ty < b.tyv;
+  if (rowv && lane == 0)
+    for (int p = b.zb; p < min(b.ze, b.zb + NS); ++p) load(p, ty);
+  auto store = [&](int p) {
+    if (!rowv) return;
+    const long long g = rowg(b.y0 + ty, p);
+    s1_copy_out(fp + g, sm + slot(p) * BUF + ty * ROWF + phase(g), b.txv * 19, lane);
+  };
+  // staged record (tx + dx, ty + dy) of the plane in ring slot sl (the row's
+  // phase from its 32-bit cell index: records are 19 elements, 16 / sizeof(T)
+  // elements per phase)
+  const uint32_t sxy32 = (uint32_t)L.sxy, sx32 = (uint32_t)L.sx;
+  auto rowoff = [&](int sl, int p, int dy) -> int {
+    const uint32_t c = (uint32_t)(b.y0 + ty + dy) * sx32 + (uint32_t)p * sxy32 + (uint32_t)b.x0;
+    const int ph = (int)((c * 19u) & (uint32_t)(16 / sizeof(T) - 1));
+    return sl * BUF + (ty + dy) * ROWF + ph + tx * 19;
+  };
+  auto srec = [&](int p, int dx, int dy) -> T* {
+    return sm + rowoff(slot(p), p, dy) + dx * 19;
+  };
+
+  const bool act = tx < b.txv && rowv;
+  const int x = b.x0 + tx, y = b.y0 + ty;
+  const auto seq = std::make_integer_sequence<int, 18>{};
+  S1Frame qf;
+  qf.fxl = tx == 0, qf.fxh = tx == b.txv - 1, qf.fyl = ty == 0, qf.fyh = ty == b.tyv - 1;
+  qf.dxl = x == 0, qf.dxh = x == L.nx - 1, qf.dyl = y == 0, qf.dyh = y == L.ny - 1;
+  qf.tx = tx, qf.ty = ty, qf.zc = G.zc;
+  qf.base = (uint32_t)b.base;
+  qf.rx = (uint32_t)G.region;
+  qf.ry = (uint32_t)((long long)G.tiles_x * G.region);
+  qf.rz = (uint32_t)((long long)G.tiles_x * G.tiles_y * G.region);
+  qf.hy = (uint32_t)G.hy, qf.hx = (uint32_t)G.hx, qf.hz = (uint32_t)G.hz;
+  qf.iz = qf.base + qf.hz + (uint32_t)(ty * kFbX + tx);
+  const uint32_t leave_xy = s1_axis_mask(qf.dxl, qf.dxh, kMxm, kMxp) | s1_axis_mask(qf.dyl, qf.dyh, kMym, kMyp);
+  const uint32_t box_xy = s1_axis_mask(qf.fxl, qf.fxh, kMxm, kMxp) | s1_axis_mask(qf.fyl, qf.fyh, kMym, kMyp);
+  auto at_plane = [&](S1Frame& q, int z) {
+    q.pz = z - b.zb;
+    q.fzl = z == b.zb, q.fzh = z == b.ze - 1;
+    q.dzl = z == 0, q.dzh = z == L.nz - 1;
+    q.iy = q.base + q.hy + (uint32_t)(q.pz * 10 * kFbX + tx);
+    q.ix = q.base + q.hx + (uint32_t)(q.pz * 10 * kFbY + ty);
+    if (CM) q.box = box_xy | s1_axis_mask(q.fzl, q.fzh, kMzm, kMzp);
+  };
+  T f[19], g[19];
+  uint32_t bf = 0, bg = 0;
+  bool lf = false, lg = false;
+  if (rowv) mbar_wait(&full[slot(b.zb)], par(b.zb));
+  if (act) {
+    lf = fb_cell(L, x, y, b.zb, bf);
+    if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
+    at_plane(qf, b.zb);
+    if (lf) s1a_read<CM>(srec(b.zb, 0, 0), hprev, qf, bf, f, seq);
+  }
+  int sz = 0;  // ring slot of plane z
+  for (int z = b.zb; z < b.ze; ++z) {
+    lg = false;
+    if (z + 1 < b.ze) {
+      const int s1 = sz == NS - 1 ? 0 : sz + 1;
+      if (rowv) mbar_wait(&full[s1], par(z + 1));
+      if (act) {
+        lg = fb_cell(L, x, y, z + 1, bg);
+        if (LBM_S1_LOCALMASK) bg |= leave_xy | s1_axis_mask(z + 1 == 0, z + 1 == L.nz - 1, kMzm, kMzp);
+        at_plane(qf, z + 1);
+        if (lg) s1a_read<CM>(sm + rowoff(s1, z + 1, 0), hprev, qf, bg, g, seq);
+      }
+    }
+    // one barrier per plane: node z + 1's record is in registers before node
+    // z writes into it, and iteration z - 1's writes (the last into plane
+    // z - 2) are done, so plane z - 2 leaves now
+    fence_async_smem();
+    __syncthreads();
+    if (z - 2 >= b.zb) {
+      store(z - 2);
+      if (lane == 0 && rowv && z - 2 + NS < b.ze) {
+        bulk_wait_read();  // the slot's store has read it
+        load(z - 2 + NS, ty);
+      }
+    }
+    if (lf) {
+      collide(op, f);
+      at_plane(qf, z);
+      if constexpr (sizeof(T) == 4) {
+        // the nine (plane, row) offsets the node's outputs land in, once per
+        // node (fp32: C1 0.45 -> 0.46; fp64 measured better recomputing them)
+        const int s0r = sz == 0 ? NS - 1 : sz - 1, s2r = sz == NS - 1 ? 0 : sz + 1;
+        int ro[3][3];
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            if ((dz == 0 && z == b.zb) || (dz == 2 && z + 1 >= b.ze)) continue;  // never used
+            ro[dz][dy] = rowoff(dz == 0 ? s0r : (dz == 1 ? sz : s2r), z - 1 + dz, dy - 1);
+          }
+        auto nb = [&](int k) -> T* { return sm + ro[1 + cz(k)][1 + cy(k)] + cx(k) * 19; };
+        s1a_write<CM>(sm + ro[1][1], nb, hcur, qf, bf, f, seq);
+      } else {
+        auto nb = [&](int k) -> T* { return srec(z + cz(k), cx(k), cy(k)); };
+        s1a_write<CM>(srec(z, 0, 0), nb, hcur, qf, bf, f, seq);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = g[i];
+    bf = bg;
+    lf = lg;
+    sz = sz == NS - 1 ? 0 : sz + 1;
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (b.ze - 2 >= b.zb) store(b.ze - 2);
+  store(b.ze - 1);
+  bulk_wait_all();
+}
+
 // face buffer <-> field: every crossing input slot of every node.
 // fill: h = the input the sweep would read in place (push (opp i, X); pull
 // (i, X - c_i)); flush (push only): (opp i, X) = h.
-template <class T, bool PUSH, bool FILL>
+template <class T, bool PUSH, bool FILL, bool AOS>
 __global__ void __launch_bounds__(kFbThreads)
-    k_swap1_faces(Fld<T, false> F, Lat L, FbGeo G, T* __restrict__ h) {
+    k_swap1_faces(Fld<T, AOS> F, Lat L, FbGeo G, T* __restrict__ h) {
   const int ntile = G.tiles_x * G.tiles_y;
   const int tile = (int)blockIdx.x % ntile, ch = (int)blockIdx.x / ntile;
   const FbBlock b = fb_block(L, G, tile % G.tiles_x, tile / G.tiles_x, ch);
@@ -397,7 +630,7 @@ __global__ void __launch_bounds__(kFbThreads)
     if (!local && !fb_in_block(b, sx, sy, sz)) {                                         \
       T* hp = h + fb_slot<I>(G, b, x, y, z, sx, sy, sz);                                 \
       T* fp = PUSH ? F.at(J, s)                                                          \
-                   : F.at(I, s) + (-cx(I) - cy(I) * L.sx - cz(I) * (int)L.sxy);          \
+                   : F.at_off(I, s, -cx(I) - cy(I) * L.sx - cz(I) * (int)L.sxy);         \
       if (FILL) *hp = *fp; else *fp = *hp;                                               \
     }                                                                                    \
   }
@@ -412,7 +645,18 @@ __global__ void __launch_bounds__(kFbThreads)
 
 // SoA, full-grid direct lattice without halo or ghost planes
 bool swap1_ok(const DField& f, const Lat& L, bool push) {
-  if (f.aos) return false;
+  if (f.aos) {
+    // AoS push in one sweep (staged box planes): C1 fp64 0.39 -> 0.50, fp32
+    // 0.33 -> 0.46, C4 0.34 -> 0.45 / 0.32 -> 0.40 against the two-pass
+    // windows; LBMGPU_SWAP_SINGLE_AOS=0 restores those
+    const char* a = std::getenv("LBMGPU_SWAP_SINGLE_AOS");
+    if (!push || (a && a[0] == '0')) return false;
+    if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
+    if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
+      return false;
+    const FbGeo G = fb_geo(L, s1_blocks(f));
+    return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
+  }
   // default: SWAP push in one sweep (C1 fp64 0.81 / fp32 0.53, C4 0.68 / 0.47
   // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull keeps the two passes
   // (one sweep: C1 0.56 / 0.46, C4 0.48 / 0.42). LBMGPU_SWAP_SINGLE=1 / 0
@@ -424,12 +668,12 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
     return false;
   // face-buffer slots are 32-bit element offsets
-  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
+  const FbGeo G = fb_geo(L, s1_blocks(f));
   return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
 }
 
 size_t swap1_face_elems(const DField& f, const Lat& L) {
-  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
+  const FbGeo G = fb_geo(L, s1_blocks(f));
   return (size_t)G.tiles_x * G.tiles_y * G.nchunks * (size_t)G.region;
 }
 
@@ -446,10 +690,33 @@ static S1Tab<T> s1_tab(const DField& f, const Lat& L, bool push) {
   return t;
 }
 
+template <class T>
+static void launch_swap1_aos_t(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op,
+                               const FbGeo& G, T* hcur, const T* hprev) {
+  static int set_dev = -1;  // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev) {
+    cudaFuncSetAttribute(k_swap1_aos<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S1Aos<T>::kBytes);
+    set_dev = dev;
+  }
+  const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
+  k_swap1_aos<T><<<grid, kFbThreads, S1Aos<T>::kBytes, st>>>(static_cast<T*>(f.p), L, cast_op<T>(op),
+                                                            G, hcur, hprev);
+}
+
 void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev) {
-  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
+  const FbGeo G = fb_geo(L, s1_blocks(f));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
+  if (f.aos) {
+    if (f.prec == Prec::f64)
+      launch_swap1_aos_t<double>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
+    else
+      launch_swap1_aos_t<float>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+    return;
+  }
   if (f.prec == Prec::f64) {
     if (push)
       k_swap1<double, true><<<grid, kFbThreads, 0, st>>>(s1_tab<double>(f, L, true), L, cast_op<double>(op), G,
@@ -469,9 +736,13 @@ void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost&
 
 void launch_swap1_faces(cudaStream_t st, const DField& f, const Lat& L, bool push, bool fill,
                         void* h) {
-  const FbGeo G = fb_geo(L, s1_blocks(f.prec));
+  const FbGeo G = fb_geo(L, s1_blocks(f));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
-#define S1_F(T, P, FL) k_swap1_faces<T, P, FL><<<grid, kFbThreads, 0, st>>>(fld<T, false>(f), L, G, (T*)h)
+#define S1_F(T, P, FL)                                                                          \
+  do {                                                                                          \
+    if (f.aos) k_swap1_faces<T, P, FL, true><<<grid, kFbThreads, 0, st>>>(fld<T, true>(f), L, G, (T*)h); \
+    else k_swap1_faces<T, P, FL, false><<<grid, kFbThreads, 0, st>>>(fld<T, false>(f), L, G, (T*)h); \
+  } while (0)
   if (f.prec == Prec::f64) {
     if (push && fill) S1_F(double, true, true);
     if (push && !fill) S1_F(double, true, false);

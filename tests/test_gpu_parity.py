@@ -424,3 +424,44 @@ def test_swap_single_pass_equals_two_passes(gpu, monkeypatch, dims, policy, zchu
             outs.append(got)
         for a, b in zip(outs[0], outs[1]):
             assert bitwise_equal(a, b), (deferred,)
+
+
+@pytest.mark.parametrize("dims,policy", [
+    ((5, 7, 6), ("periodic", "periodic", "periodic")),
+    ((70, 20, 30), ("periodic", "periodic", "periodic")),
+    ((33, 9, 17), ("periodic", "periodic", "wall")),
+    ((45, 19, 11), ("wall", "wall", "periodic")),
+    ((40, 17, 12), "porous"),
+])
+@pytest.mark.parametrize("zchunk", ["", "3"])
+@pytest.mark.parametrize("precision", [8, 4])
+def test_swap_push_single_pass_aos(gpu, monkeypatch, dims, policy, zchunk, precision):
+    """kernels_swap1.cu k_swap1_aos (AoS records staged in shared memory,
+    links between blocks through the face buffers) against the AoS two-pass
+    SWAP push: bitwise over odd and even steps, extractions and a reload."""
+    rng = np.random.default_rng(17)
+    mask = None
+    if policy == "porous":
+        mask = (rng.random(dims[::-1]) > 0.3).astype(np.uint8).reshape(-1)
+        policy = ("periodic", "periodic", "periodic")
+    geo = gpu.GridGeometry(*dims, policy, mask)
+    flow = gpu.bgk(1.7, body_force=(1e-6, 2e-7, -1e-7))
+    monkeypatch.setenv("LBMGPU_SWAP1_ZCHUNK", zchunk)
+    outs, f0 = [], None
+    for single in ("1", "0"):
+        monkeypatch.setenv("LBMGPU_SWAP_SINGLE_AOS", single)  # 0: two-pass windows
+        st = gpu.create_stepper("swap-push", "direct", geo, flow,
+                                gpu.StepperOptions(precision=precision, layout="aos"))
+        st.init_field("taylor_green", seed=5)
+        if f0 is None:
+            f0 = st.extract_natural()
+        got = []
+        for n in (3, 4):
+            st.step_n(n)
+            got.append(st.extract_natural())
+        st.load_natural(f0)
+        st.step_n(5)
+        got.append(st.extract_natural())
+        outs.append(got)
+    for a, b in zip(outs[0], outs[1]):
+        assert bitwise_equal(a, b)
