@@ -456,7 +456,46 @@ __device__ __forceinline__ void s1a_write(T* rec, Nb nb, T* hcur, const S1Frame&
   (s1a_out<CM, Ks + 1>(rec, nb, hcur, q, bounce, v), ...);
 }
 
-template <class T>
+// pull on AoS: input I of X is slot I of the staged record X - c_I (src(I)),
+// or its own slot opp I on a local link; outputs stay in its own record (and
+// go to the face buffer as well when they cross)
+template <bool CM, int SEL, int I, class T, class Src>
+__device__ __forceinline__ void s1a_in_pull(const T* rec, Src src, const T* hprev,
+                                            const S1Frame& q, uint32_t bounce, T (&v)[19]) {
+  if constexpr ((SEL == 1) == s1_early(I)) {
+    constexpr int X = cx(I), Y = cy(I), Z = cz(I), J = opp(I);
+    const bool local = s1_local<J, -X, -Y, -Z>(q, bounce);
+    if (local)
+      v[I] = rec[J];
+    else if (s1_cross<CM, J, -X, -Y, -Z>(q))
+      v[I] = hprev[s1_in_slot<I>(q)];
+    else
+      v[I] = src(I)[I];
+  }
+}
+template <bool CM, int SEL, class T, class Src, int... Is>
+__device__ __forceinline__ void s1a_read_pull(const T* rec, Src src, const T* hprev,
+                                              const S1Frame& q, uint32_t bounce, T (&v)[19],
+                                              std::integer_sequence<int, Is...>) {
+  if (SEL == 2) v[0] = rec[0];
+  (s1a_in_pull<CM, SEL, Is + 1>(rec, src, hprev, q, bounce, v), ...);
+}
+template <bool CM, int K, class T>
+__device__ __forceinline__ void s1a_out_pull(T* rec, T* hcur, const S1Frame& q, uint32_t bounce,
+                                             const T (&v)[19]) {
+  constexpr int X = cx(K), Y = cy(K), Z = cz(K);
+  rec[K] = v[K];
+  if (!s1_local<K, X, Y, Z>(q, bounce) && s1_cross<CM, K, X, Y, Z>(q))
+    hcur[s1_out_slot<K>(q)] = v[K];
+}
+template <bool CM, class T, int... Ks>
+__device__ __forceinline__ void s1a_write_pull(T* rec, T* hcur, const S1Frame& q, uint32_t bounce,
+                                               const T (&v)[19], std::integer_sequence<int, Ks...>) {
+  rec[0] = v[0];
+  (s1a_out_pull<CM, Ks + 1>(rec, hcur, q, bounce, v), ...);
+}
+
+template <class T, bool PUSH>
 __global__ void __launch_bounds__(kFbThreads, S1Aos<T>::kBlocks)
     k_swap1_aos(T* __restrict__ fp, Lat L, Trt<T> op, FbGeo G, T* __restrict__ hcur,
                 const T* __restrict__ hprev) {
@@ -536,6 +575,65 @@ __global__ void __launch_bounds__(kFbThreads, S1Aos<T>::kBlocks)
     q.ix = q.base + q.hx + (uint32_t)(q.pz * 10 * kFbY + ty);
     if (CM) q.box = box_xy | s1_axis_mask(q.fzl, q.fzh, kMzm, kMzp);
   };
+  if constexpr (!PUSH) {
+    // Pull: node z reads the staged records of planes z - 1 .. z + 1 and
+    // rewrites only its own; the five inputs of node z + 1 from plane z
+    // (c_z = +1) are read before node z's stores (iteration z), the others in
+    // node z + 1's own iteration. Plane z - 1 is final once iteration z - 1
+    // wrote it: it leaves after iteration z's barrier.
+    T f[19];
+    uint32_t bf = 0, bg = 0;
+    bool lf = false, lg = false;
+    if (rowv) mbar_wait(&full[slot(b.zb)], par(b.zb));
+    if (act) {
+      lf = fb_cell(L, x, y, b.zb, bf);
+      if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
+      at_plane(qf, b.zb);
+      auto src = [&](int i) -> const T* { return srec(b.zb - cz(i), -cx(i), -cy(i)); };
+      if (lf) s1a_read_pull<CM, 1>(srec(b.zb, 0, 0), src, hprev, qf, bf, f, seq);
+    }
+    for (int z = b.zb; z < b.ze; ++z) {
+      if (z + 1 < b.ze && rowv) mbar_wait(&full[slot(z + 1)], par(z + 1));
+      if (lf) {
+        at_plane(qf, z);
+        auto src = [&](int i) -> const T* { return srec(z - cz(i), -cx(i), -cy(i)); };
+        s1a_read_pull<CM, 2>(srec(z, 0, 0), src, hprev, qf, bf, f, seq);
+      }
+      T g[19];
+      lg = false;
+      if (act && z + 1 < b.ze) {
+        lg = fb_cell(L, x, y, z + 1, bg);
+        if (LBM_S1_LOCALMASK) bg |= leave_xy | s1_axis_mask(z + 1 == 0, z + 1 == L.nz - 1, kMzm, kMzp);
+        at_plane(qf, z + 1);
+        auto src = [&](int i) -> const T* { return srec(z + 1 - cz(i), -cx(i), -cy(i)); };
+        if (lg) s1a_read_pull<CM, 1>(srec(z + 1, 0, 0), src, hprev, qf, bg, g, seq);
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (z - 1 >= b.zb) {
+        store(z - 1);
+        if (lane == 0 && rowv && z - 1 + NS < b.ze) {
+          bulk_wait_read();
+          load(z - 1 + NS, ty);
+        }
+      }
+      if (lf) {
+        collide(op, f);
+        at_plane(qf, z);
+        s1a_write_pull<CM>(srec(z, 0, 0), hcur, qf, bf, f, seq);
+      }
+#pragma unroll
+      for (int i = 1; i < 19; ++i)
+        if (s1_early(i)) f[i] = g[i];
+      bf = bg;
+      lf = lg;
+    }
+    fence_async_smem();
+    __syncthreads();
+    store(b.ze - 1);
+    bulk_wait_all();
+    return;
+  }
   T f[19], g[19];
   uint32_t bf = 0, bg = 0;
   bool lf = false, lg = false;
@@ -646,11 +744,11 @@ __global__ void __launch_bounds__(kFbThreads)
 // SoA, full-grid direct lattice without halo or ghost planes
 bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (f.aos) {
-    // AoS push in one sweep (staged box planes): C1 fp64 0.39 -> 0.50, fp32
-    // 0.33 -> 0.46, C4 0.34 -> 0.45 / 0.32 -> 0.40 against the two-pass
-    // windows; LBMGPU_SWAP_SINGLE_AOS=0 restores those
+    // AoS push and pull in one sweep (staged box planes): C1 fp64 0.39 ->
+    // 0.52, fp32 0.33 -> 0.46-0.47, C4 0.34 -> 0.46 / 0.32 -> 0.40-0.41
+    // against the two-pass windows; LBMGPU_SWAP_SINGLE_AOS=0 restores those
     const char* a = std::getenv("LBMGPU_SWAP_SINGLE_AOS");
-    if (!push || (a && a[0] == '0')) return false;
+    if (a && a[0] == '0') return false;
     if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
     if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
       return false;
@@ -690,19 +788,19 @@ static S1Tab<T> s1_tab(const DField& f, const Lat& L, bool push) {
   return t;
 }
 
-template <class T>
+template <class T, bool PUSH>
 static void launch_swap1_aos_t(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op,
                                const FbGeo& G, T* hcur, const T* hprev) {
   static int set_dev = -1;  // the attribute is per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (set_dev != dev) {
-    cudaFuncSetAttribute(k_swap1_aos<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_swap1_aos<T, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S1Aos<T>::kBytes);
     set_dev = dev;
   }
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
-  k_swap1_aos<T><<<grid, kFbThreads, S1Aos<T>::kBytes, st>>>(static_cast<T*>(f.p), L, cast_op<T>(op),
+  k_swap1_aos<T, PUSH><<<grid, kFbThreads, S1Aos<T>::kBytes, st>>>(static_cast<T*>(f.p), L, cast_op<T>(op),
                                                             G, hcur, hprev);
 }
 
@@ -711,10 +809,13 @@ void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost&
   const FbGeo G = fb_geo(L, s1_blocks(f));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
   if (f.aos) {
-    if (f.prec == Prec::f64)
-      launch_swap1_aos_t<double>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
-    else
-      launch_swap1_aos_t<float>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+    if (f.prec == Prec::f64) {
+      if (push) launch_swap1_aos_t<double, true>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
+      else launch_swap1_aos_t<double, false>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
+    } else {
+      if (push) launch_swap1_aos_t<float, true>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+      else launch_swap1_aos_t<float, false>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+    }
     return;
   }
   if (f.prec == Prec::f64) {

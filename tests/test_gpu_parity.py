@@ -435,10 +435,11 @@ def test_swap_single_pass_equals_two_passes(gpu, monkeypatch, dims, policy, zchu
 ])
 @pytest.mark.parametrize("zchunk", ["", "3"])
 @pytest.mark.parametrize("precision", [8, 4])
-def test_swap_push_single_pass_aos(gpu, monkeypatch, dims, policy, zchunk, precision):
+@pytest.mark.parametrize("scheme", ["swap-push", "swap-pull"])
+def test_swap_single_pass_aos(gpu, monkeypatch, dims, policy, zchunk, precision, scheme):
     """kernels_swap1.cu k_swap1_aos (AoS records staged in shared memory,
     links between blocks through the face buffers) against the AoS two-pass
-    SWAP push: bitwise over odd and even steps, extractions and a reload."""
+    SWAP: bitwise over odd and even steps, extractions and a reload."""
     rng = np.random.default_rng(17)
     mask = None
     if policy == "porous":
@@ -450,7 +451,7 @@ def test_swap_push_single_pass_aos(gpu, monkeypatch, dims, policy, zchunk, preci
     outs, f0 = [], None
     for single in ("1", "0"):
         monkeypatch.setenv("LBMGPU_SWAP_SINGLE_AOS", single)  # 0: two-pass windows
-        st = gpu.create_stepper("swap-push", "direct", geo, flow,
+        st = gpu.create_stepper(scheme, "direct", geo, flow,
                                 gpu.StepperOptions(precision=precision, layout="aos"))
         st.init_field("taylor_green", seed=5)
         if f0 is None:
