@@ -594,6 +594,48 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
   }
 }
 
+// SWAP link exchange, AoS: a node's own side of its nine pairs (its back
+// slots) is staged with the block's contiguous records (coalesced 16-byte
+// vectors in) and only the back slots go out again, as element runs; the
+// partner side (opp i, adj[i][n]) stays a scattered access. Nobody but the
+// node itself writes its back slots (a partner exchange writes front slots),
+// so the staged copies of the back slots are current and no front slot is
+// written back.
+constexpr uint32_t kBackMask = (1u << 2) | (1u << 4) | (1u << 6) | (1u << 7) | (1u << 8) |
+                               (1u << 11) | (1u << 13) | (1u << 15) | (1u << 16);
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_swap_idx_aos(Fld<T, true> F, Idx I) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const uint32_t n0 = I.first + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.end() - n0);
+  aos_stage_in(sm, F.p + (size_t)n0 * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    const uint32_t node = n0 + k;
+    uint32_t nb[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) nb[q] = ldidx(I.adj + (size_t)(back_dir(q) - 1) * I.n + node);
+    T vb[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+      if (nb[q] != node) vb[q] = ld(F.at(opp(back_dir(q)), nb[q]));
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int i = back_dir(q);
+      if (nb[q] != node) {
+        st<false>(F.at(opp(i), nb[q]), sm[k * 19 + i]);
+        sm[k * 19 + i] = vb[q];
+      }
+    }
+  }
+  __syncthreads();
+  T* g = F.p + (size_t)n0 * 19;
+  for (uint32_t e = threadIdx.x; e < nrec * 19; e += blockDim.x)
+    if ((kBackMask >> (e % 19)) & 1u) g[e] = sm[e];
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
@@ -857,6 +899,13 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
 
 void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I) {
   if (I.count() == 0) return;
+  if (f.aos) {
+    if (f.prec == Prec::f64)
+      k_swap_idx_aos<double><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I);
+    else
+      k_swap_idx_aos<float><<<grid_for(I.count()), kBlock, 0, st>>>(fld<float, true>(f), I);
+    return;
+  }
   LBM_DISPATCH(f, { k_swap_idx<T, A><<<grid_for(I.count()), kBlock, 0, st>>>(fld<T, A>(f), I); });
 }
 
