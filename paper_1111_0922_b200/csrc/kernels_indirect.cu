@@ -636,6 +636,59 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     if ((kBackMask >> (e % 19)) & 1u) g[e] = sm[e];
 }
 
+// ET sweep, AoS, the nodes' own records staged (coalesced in). A node's own
+// slots that it writes this sweep — hb(i) of every pair, or hb(j) when its
+// j-link bounces — are written by nobody else, so they go out again from the
+// staged copies (element runs, per-node mask); the slots hb(j) its partners
+// rewrite are never written back from here.
+template <class T, bool SW>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_et_idx_aos(Fld<T, true> F, Idx I, Trt<T> op) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  __shared__ uint32_t wmask[kBlock];
+  const uint32_t n0 = I.first + blockIdx.x * kBlock;
+  const uint32_t nrec = min((uint32_t)kBlock, I.end() - n0);
+  aos_stage_in(sm, F.p + (size_t)n0 * 19, nrec);
+  __syncthreads();
+  const uint32_t k = threadIdx.x;
+  if (k < nrec) {
+    const uint32_t node = n0 + k;
+    T* rec = sm + k * 19;
+    uint32_t rs[9];
+    T f[19];
+    f[0] = rec[0];
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      rs[p] = ldidx(I.rem + (size_t)p * I.n + node);
+      const uint32_t r = rs[p] & 0x7fffffffu;
+      const bool db = r >= I.n;
+      f[i] = rec[hb<SW>(i)];
+      f[j] = ld(F.at(db ? hb<SW>(i) : hb<SW>(j), r));
+    }
+    collide(op, f);
+    rec[0] = f[0];
+    uint32_t m = 1u;
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      const uint32_t rv = rs[p];
+      const bool ub = (rv & 0x80000000u) != 0;
+      const int own = ub ? hb<SW>(j) : hb<SW>(i);
+      rec[own] = f[j];
+      m |= 1u << own;
+      st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
+    }
+    wmask[k] = m;
+  }
+  __syncthreads();
+  T* g = F.p + (size_t)n0 * 19;
+  for (uint32_t e = threadIdx.x; e < nrec * 19; e += blockDim.x) {
+    const uint32_t r = e / 19, sl = e - r * 19;
+    if ((wmask[r] >> sl) & 1u) g[e] = sm[e];
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
@@ -869,11 +922,23 @@ void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const Trt
   });
 }
 
+// ET on AoS with the own records staged (k_et_idx_aos), also on all-fluid
+// boxes instead of the tiled walk; LBMGPU_IDX_ET_STAGED=0 restores the
+// per-thread kernels
+static bool et_aos_staged() {
+  static const bool on = [] {
+    const char* e = std::getenv("LBMGPU_IDX_ET_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op,
                    const EtBase& base) {
   if (I.count() == 0) return;
-  if (base.swapped() ? launch_idx_tiled<kTiledEtSw>(st, f, f, I, op)
-                     : launch_idx_tiled<kTiledEt>(st, f, f, I, op))
+  if (!(f.aos && et_aos_staged()) &&
+      (base.swapped() ? launch_idx_tiled<kTiledEtSw>(st, f, f, I, op)
+                      : launch_idx_tiled<kTiledEt>(st, f, f, I, op)))
     return;
   if (base.swapped() ? launch_ag<true, true>(st, f, I, op) : launch_ag<true, false>(st, f, I, op))
     return;
@@ -887,6 +952,17 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
     if (vec && !sw) k_et_idx_pf<double, false, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     if (!vec && sw) k_et_idx_pf<double, true, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     if (!vec && !sw) k_et_idx_pf<double, false, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
+    return;
+  }
+  if (f.aos && et_aos_staged()) {
+    const bool sw = base.swapped();
+    if (f.prec == Prec::f64) {
+      if (sw) k_et_idx_aos<double, true><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op));
+      else k_et_idx_aos<double, false><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op));
+    } else {
+      if (sw) k_et_idx_aos<float, true><<<grid_for(I.count()), kBlock, 0, st>>>(fld<float, true>(f), I, cast_op<float>(op));
+      else k_et_idx_aos<float, false><<<grid_for(I.count()), kBlock, 0, st>>>(fld<float, true>(f), I, cast_op<float>(op));
+    }
     return;
   }
   LBM_DISPATCH(f, {
