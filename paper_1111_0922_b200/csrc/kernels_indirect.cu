@@ -689,6 +689,69 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
   }
 }
 
+// The same staged ET on an all-fluid box in the tiled walk (x-y tiles
+// marching through z, k_idx_aos_tiled): each warp stages its row of 32
+// records per plane (one contiguous run), so the neighbour gathers keep
+// their L1 reuse and the own side is coalesced.
+template <class T, bool SW>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_et_idx_aos_tiled(Fld<T, true> F, Idx I, Trt<T> op, int tiles_x, int tiles_y, int zc) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const int ntile = tiles_x * tiles_y;
+  const int tile = (int)blockIdx.x % ntile, chunk = (int)blockIdx.x / ntile;
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  const int x0 = (tile % tiles_x) * kIdxTX, y = (tile / tiles_x) * kIdxTY + warp;
+  const int x = x0 + lane;
+  const int txv = y < I.by ? min(kIdxTX, I.bx - x0) : 0;
+  const bool live = lane < txv;
+  T* rec = sm + warp * (kIdxTX * 19) + lane * 19;
+  T* srow = sm + warp * (kIdxTX * 19);
+  const int zb = chunk * zc, ze = min(I.bz, zb + zc);
+  for (int z = zb; z < ze; ++z) {
+    const uint32_t n0 = (uint32_t)x0 + (uint32_t)I.bx * ((uint32_t)y + (uint32_t)I.by * (uint32_t)z);
+    T* g = F.p + (size_t)n0 * 19;
+    const int nel = txv * 19;
+    for (int e = lane; e < nel; e += 32) srow[e] = g[e];
+    __syncwarp();
+    uint32_t m = 0;
+    if (live) {
+      const uint32_t node = n0 + (uint32_t)lane;
+      uint32_t rs[9];
+      T f[19];
+      f[0] = rec[0];
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        rs[p] = ldidx(I.rem + (size_t)p * I.n + node);
+        const uint32_t r = rs[p] & 0x7fffffffu;
+        const bool db = r >= I.n;
+        f[i] = rec[hb<SW>(i)];
+        f[j] = ld(F.at(db ? hb<SW>(i) : hb<SW>(j), r));
+      }
+      collide(op, f);
+      rec[0] = f[0];
+      m = 1u;
+#pragma unroll
+      for (int p = 0; p < 9; ++p) {
+        const int i = pair_i(p), j = pair_j(p);
+        const uint32_t rv = rs[p];
+        const bool ub = (rv & 0x80000000u) != 0;
+        const int own = ub ? hb<SW>(j) : hb<SW>(i);
+        rec[own] = f[j];
+        m |= 1u << own;
+        st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
+      }
+    }
+    __syncwarp();
+    for (int e = lane; e < ((nel + 31) & ~31); e += 32) {
+      const int r = e / 19, sl = e - r * 19;
+      const uint32_t mr = __shfl_sync(0xffffffffu, m, r < 32 ? r : 31);
+      if (e < nel && ((mr >> sl) & 1u)) g[e] = srow[e];
+    }
+    __syncwarp();
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
@@ -956,6 +1019,18 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
   }
   if (f.aos && et_aos_staged()) {
     const bool sw = base.swapped();
+    int tx, ty, zc;
+    unsigned gt;
+    if (idx_tiled_grid(I, tx, ty, zc, gt)) {
+      if (f.prec == Prec::f64) {
+        if (sw) k_et_idx_aos_tiled<double, true><<<gt, kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op), tx, ty, zc);
+        else k_et_idx_aos_tiled<double, false><<<gt, kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op), tx, ty, zc);
+      } else {
+        if (sw) k_et_idx_aos_tiled<float, true><<<gt, kBlock, 0, st>>>(fld<float, true>(f), I, cast_op<float>(op), tx, ty, zc);
+        else k_et_idx_aos_tiled<float, false><<<gt, kBlock, 0, st>>>(fld<float, true>(f), I, cast_op<float>(op), tx, ty, zc);
+      }
+      return;
+    }
     if (f.prec == Prec::f64) {
       if (sw) k_et_idx_aos<double, true><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op));
       else k_et_idx_aos<double, false><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I, cast_op<double>(op));
