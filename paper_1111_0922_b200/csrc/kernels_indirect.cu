@@ -752,6 +752,53 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
   }
 }
 
+// The staged SWAP exchange in the tiled walk (all-fluid boxes): each warp
+// stages its row of 32 records per plane; the partners' records stay in L1
+// while the tile marches through z.
+template <class T>
+__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
+    k_swap_idx_aos_tiled(Fld<T, true> F, Idx I, int tiles_x, int tiles_y, int zc) {
+  __shared__ __align__(16) T sm[kBlock * 19];
+  const int ntile = tiles_x * tiles_y;
+  const int tile = (int)blockIdx.x % ntile, chunk = (int)blockIdx.x / ntile;
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  const int x0 = (tile % tiles_x) * kIdxTX, y = (tile / tiles_x) * kIdxTY + warp;
+  const int txv = y < I.by ? min(kIdxTX, I.bx - x0) : 0;
+  const bool live = lane < txv;
+  T* rec = sm + warp * (kIdxTX * 19) + lane * 19;
+  T* srow = sm + warp * (kIdxTX * 19);
+  const int zb = chunk * zc, ze = min(I.bz, zb + zc);
+  for (int z = zb; z < ze; ++z) {
+    const uint32_t n0 = (uint32_t)x0 + (uint32_t)I.bx * ((uint32_t)y + (uint32_t)I.by * (uint32_t)z);
+    T* g = F.p + (size_t)n0 * 19;
+    const int nel = txv * 19;
+    for (int e = lane; e < nel; e += 32) srow[e] = g[e];
+    __syncwarp();
+    if (live) {
+      const uint32_t node = n0 + (uint32_t)lane;
+      uint32_t nb[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) nb[q] = ldidx(I.adj + (size_t)(back_dir(q) - 1) * I.n + node);
+      T vb[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q)
+        if (nb[q] != node) vb[q] = ld(F.at(opp(back_dir(q)), nb[q]));
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const int i = back_dir(q);
+        if (nb[q] != node) {
+          st<false>(F.at(opp(i), nb[q]), rec[i]);
+          rec[i] = vb[q];
+        }
+      }
+    }
+    __syncwarp();
+    for (int e = lane; e < nel; e += 32)
+      if ((kBackMask >> (e % 19)) & 1u) g[e] = srow[e];
+    __syncwarp();
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock, MinBlocks<T>::value)
     k_ts_stream_idx_aos(Fld<T, true> a, Fld<T, true> b, Idx I) {
@@ -1051,6 +1098,15 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
 void launch_swap_idx(cudaStream_t st, const DField& f, const Idx& I) {
   if (I.count() == 0) return;
   if (f.aos) {
+    int tx, ty, zc;
+    unsigned gt;
+    if (idx_tiled_grid(I, tx, ty, zc, gt)) {
+      if (f.prec == Prec::f64)
+        k_swap_idx_aos_tiled<double><<<gt, kBlock, 0, st>>>(fld<double, true>(f), I, tx, ty, zc);
+      else
+        k_swap_idx_aos_tiled<float><<<gt, kBlock, 0, st>>>(fld<float, true>(f), I, tx, ty, zc);
+      return;
+    }
     if (f.prec == Prec::f64)
       k_swap_idx_aos<double><<<grid_for(I.count()), kBlock, 0, st>>>(fld<double, true>(f), I);
     else
