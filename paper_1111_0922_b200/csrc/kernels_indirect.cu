@@ -204,6 +204,10 @@ __device__ __forceinline__ void staged_rows(const uint32_t* __restrict__ table, 
 #ifndef LBM_IDX_PF_LAZY
 #define LBM_IDX_PF_LAZY 1
 #endif
+// AA odd (fp64 SoA): the software-pipelined staged kernel (k_aa_odd_idx_pp)
+#ifndef LBM_IDX_PP
+#define LBM_IDX_PP 1
+#endif
 
 // AA odd sweep with the adjacency staged (fp64; C4 0.94 -> 0.97 of the
 // roofline; fp32 spills at its register budget and keeps k_aa_odd_idx)
@@ -233,6 +237,82 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
       st<false>(ej == node ? F.at(opp(j), node) : F.at(j, ej), f[j]);
     }
   });
+}
+
+// AA odd sweep, software-pipelined over the staged batches: the adjacency
+// rows are staged two batches ahead (three buffers) and the gathers of batch
+// k + 1 are issued before batch k collides and scatters, so a thread keeps
+// one node's loads in flight across its other node's collision. In place but
+// race-free: every slot is read and rewritten by exactly one node per sweep.
+template <class T, bool VEC>
+__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
+    k_aa_odd_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  extern __shared__ __align__(16) unsigned char pp_smem[];  // [3][18][kBlock] rows
+  uint32_t(*sb)[18][kBlock] = reinterpret_cast<uint32_t(*)[18][kBlock]>(pp_smem);
+  const uint32_t tid = threadIdx.x;
+  auto bat = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
+  auto issue = [&](uint32_t k) {
+    const uint32_t bt = bat(k);
+    if (bt >= nbatch) return;
+    const uint32_t n0 = I.first + bt * kBlock;
+    const uint32_t cnt = min((uint32_t)kBlock, I.end() - n0);
+    uint32_t* dst = &sb[k % 3][0][0];
+    if (VEC && cnt == kBlock) {
+      for (uint32_t q = tid; q < 18 * (kBlock / 4); q += kBlock) {
+        const uint32_t row = q / (kBlock / 4), c = q - row * (kBlock / 4);
+        cp_async<16>(dst + row * kBlock + c * 4, I.adj + (size_t)row * I.n + n0 + c * 4);
+      }
+    } else {
+      for (uint32_t q = tid; q < 18 * cnt; q += kBlock) {
+        const uint32_t row = q / cnt, c = q - row * cnt;
+        cp_async<4>(dst + row * kBlock + c, I.adj + (size_t)row * I.n + n0 + c);
+      }
+    }
+  };
+  auto gather = [&](uint32_t k, uint32_t node, T (&f)[19]) {
+    const uint32_t(*rw)[kBlock] = sb[k % 3];
+    f[0] = ld(F.at(0, node));
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      const uint32_t ej = rw[j - 1][tid];
+      f[i] = ld(ej == node ? F.at(i, node) : F.at(j, ej));
+    }
+  };
+  if (bat(0) >= nbatch) return;
+  issue(0);
+  cp_commit();
+  issue(1);
+  cp_commit();
+  cp_wait1();
+  __syncthreads();
+  T fc[19];
+  uint32_t nc = I.first + bat(0) * kBlock + tid;
+  if (nc < I.end()) gather(0, nc, fc);
+  for (uint32_t k = 0; bat(k) < nbatch; ++k) {
+    __syncthreads();  // batch k - 1 is done with its rows: buffer (k + 2) % 3 is free
+    issue(k + 2);
+    cp_commit();
+    cp_wait1();       // rows of batch k + 1
+    __syncthreads();
+    T fn[19];
+    const uint32_t nn = I.first + bat(k + 1) * kBlock + tid;
+    const bool hn = bat(k + 1) < nbatch && nn < I.end();
+    if (hn) gather(k + 1, nn, fn);
+    if (nc < I.end()) {
+      collide(op, fc);
+      const uint32_t(*rw)[kBlock] = sb[k % 3];
+      st<false>(F.at(0, nc), fc[0]);
+#pragma unroll
+      for (int j = 1; j < 19; ++j) {
+        const uint32_t ej = rw[j - 1][tid];
+        st<false>(ej == nc ? F.at(opp(j), nc) : F.at(j, ej), fc[j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 19; ++i) fc[i] = fn[i];
+    nc = hn ? nn : I.end();
+  }
 }
 
 // ET sweep with the rem rows staged (fp64)
@@ -1018,7 +1098,22 @@ void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const Trt
     const unsigned g = staged_grid(nbatch);
     const auto F = fld<double, false>(f);
     const auto o = cast_op<double>(op);
-    if (I.n % 4 == 0 && I.first % 4 == 0)
+    const bool vec = I.n % 4 == 0 && I.first % 4 == 0;
+    if (LBM_IDX_PP) {
+      constexpr int bytes = 3 * 18 * kBlock * 4;
+      static int set_dev = -1;  // the attribute is per device
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (set_dev != dev) {
+        cudaFuncSetAttribute(k_aa_odd_idx_pp<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_aa_odd_idx_pp<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        set_dev = dev;
+      }
+      if (vec) k_aa_odd_idx_pp<double, true><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      else k_aa_odd_idx_pp<double, false><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      return;
+    }
+    if (vec)
       k_aa_odd_idx_pf<double, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     else
       k_aa_odd_idx_pf<double, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
