@@ -239,16 +239,18 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
   });
 }
 
-// AA odd sweep, software-pipelined over the staged batches: the adjacency
-// rows are staged two batches ahead (three buffers) and the gathers of batch
-// k + 1 are issued before batch k collides and scatters, so a thread keeps
-// one node's loads in flight across its other node's collision. In place but
-// race-free: every slot is read and rewritten by exactly one node per sweep.
-template <class T, bool VEC>
-__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
-    k_aa_odd_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
-  extern __shared__ __align__(16) unsigned char pp_smem[];  // [3][18][kBlock] rows
-  uint32_t(*sb)[18][kBlock] = reinterpret_cast<uint32_t(*)[18][kBlock]>(pp_smem);
+// Software pipeline over the staged batches (AA odd, ET; fp64 SoA): the
+// table rows (adjacency / rem) are staged two batches ahead (three buffers)
+// and the gathers of batch k + 1 are issued before batch k collides and
+// scatters, so a thread keeps one node's loads in flight across its other
+// node's collision. In place but race-free: every slot is read and
+// rewritten by exactly one node per sweep. gather(node, row, f) / finish(node,
+// row, f) with row(r) = table[r][node].
+template <class T, int ROWS, bool VEC, class Gather, class Finish>
+__device__ __forceinline__ void pp_batches(const uint32_t* __restrict__ table, const Idx& I,
+                                           uint32_t nbatch, unsigned char* smem, Gather gather,
+                                           Finish finish) {
+  uint32_t(*sb)[ROWS][kBlock] = reinterpret_cast<uint32_t(*)[ROWS][kBlock]>(smem);
   const uint32_t tid = threadIdx.x;
   auto bat = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
   auto issue = [&](uint32_t k) {
@@ -258,25 +260,15 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     const uint32_t cnt = min((uint32_t)kBlock, I.end() - n0);
     uint32_t* dst = &sb[k % 3][0][0];
     if (VEC && cnt == kBlock) {
-      for (uint32_t q = tid; q < 18 * (kBlock / 4); q += kBlock) {
+      for (uint32_t q = tid; q < ROWS * (kBlock / 4); q += kBlock) {
         const uint32_t row = q / (kBlock / 4), c = q - row * (kBlock / 4);
-        cp_async<16>(dst + row * kBlock + c * 4, I.adj + (size_t)row * I.n + n0 + c * 4);
+        cp_async<16>(dst + row * kBlock + c * 4, table + (size_t)row * I.n + n0 + c * 4);
       }
     } else {
-      for (uint32_t q = tid; q < 18 * cnt; q += kBlock) {
+      for (uint32_t q = tid; q < ROWS * cnt; q += kBlock) {
         const uint32_t row = q / cnt, c = q - row * cnt;
-        cp_async<4>(dst + row * kBlock + c, I.adj + (size_t)row * I.n + n0 + c);
+        cp_async<4>(dst + row * kBlock + c, table + (size_t)row * I.n + n0 + c);
       }
-    }
-  };
-  auto gather = [&](uint32_t k, uint32_t node, T (&f)[19]) {
-    const uint32_t(*rw)[kBlock] = sb[k % 3];
-    f[0] = ld(F.at(0, node));
-#pragma unroll
-    for (int i = 1; i < 19; ++i) {
-      const int j = opp(i);
-      const uint32_t ej = rw[j - 1][tid];
-      f[i] = ld(ej == node ? F.at(i, node) : F.at(j, ej));
     }
   };
   if (bat(0) >= nbatch) return;
@@ -288,7 +280,7 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
   __syncthreads();
   T fc[19];
   uint32_t nc = I.first + bat(0) * kBlock + tid;
-  if (nc < I.end()) gather(0, nc, fc);
+  if (nc < I.end()) gather(nc, [&](int r) { return sb[0][r][tid]; }, fc);
   for (uint32_t k = 0; bat(k) < nbatch; ++k) {
     __syncthreads();  // batch k - 1 is done with its rows: buffer (k + 2) % 3 is free
     issue(k + 2);
@@ -298,21 +290,68 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
     T fn[19];
     const uint32_t nn = I.first + bat(k + 1) * kBlock + tid;
     const bool hn = bat(k + 1) < nbatch && nn < I.end();
-    if (hn) gather(k + 1, nn, fn);
-    if (nc < I.end()) {
-      collide(op, fc);
-      const uint32_t(*rw)[kBlock] = sb[k % 3];
-      st<false>(F.at(0, nc), fc[0]);
-#pragma unroll
-      for (int j = 1; j < 19; ++j) {
-        const uint32_t ej = rw[j - 1][tid];
-        st<false>(ej == nc ? F.at(opp(j), nc) : F.at(j, ej), fc[j]);
-      }
-    }
+    if (hn) gather(nn, [&](int r) { return sb[(k + 1) % 3][r][tid]; }, fn);
+    if (nc < I.end()) finish(nc, [&](int r) { return sb[k % 3][r][tid]; }, fc);
 #pragma unroll
     for (int i = 0; i < 19; ++i) fc[i] = fn[i];
     nc = hn ? nn : I.end();
   }
+}
+template <int ROWS>
+constexpr int kPpBytes = 3 * ROWS * kBlock * 4;
+
+template <class T, bool VEC>
+__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
+    k_aa_odd_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  extern __shared__ __align__(16) unsigned char pp_smem[];
+  auto gather = [&](uint32_t node, auto row, T(&f)[19]) {
+    f[0] = ld(F.at(0, node));
+#pragma unroll
+    for (int i = 1; i < 19; ++i) {
+      const int j = opp(i);
+      const uint32_t ej = row(j - 1);
+      f[i] = ld(ej == node ? F.at(i, node) : F.at(j, ej));
+    }
+  };
+  auto finish = [&](uint32_t node, auto row, T(&f)[19]) {
+    collide(op, f);
+    st<false>(F.at(0, node), f[0]);
+#pragma unroll
+    for (int j = 1; j < 19; ++j) {
+      const uint32_t ej = row(j - 1);
+      st<false>(ej == node ? F.at(opp(j), node) : F.at(j, ej), f[j]);
+    }
+  };
+  pp_batches<T, 18, VEC>(I.adj, I, nbatch, pp_smem, gather, finish);
+}
+
+template <class T, bool SW, bool VEC>
+__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
+    k_et_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
+  extern __shared__ __align__(16) unsigned char pp_smem[];
+  auto gather = [&](uint32_t node, auto row, T(&f)[19]) {
+    f[0] = ld(F.at(0, node));
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      const uint32_t r = row(p) & 0x7fffffffu;
+      f[i] = ld(F.at(hb<SW>(i), node));
+      f[j] = ld(F.at(r >= I.n ? hb<SW>(i) : hb<SW>(j), r));
+    }
+  };
+  auto finish = [&](uint32_t node, auto row, T(&f)[19]) {
+    collide(op, f);
+    st<false>(F.at(0, node), f[0]);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      const int i = pair_i(p), j = pair_j(p);
+      const uint32_t rv = row(p);
+      const bool ub = (rv & 0x80000000u) != 0;
+      st<false>(F.at(ub ? hb<SW>(j) : hb<SW>(i), node), f[j]);
+      st<false>(F.at(hb<SW>(j), rv & 0x7fffffffu), f[i]);
+    }
+  };
+  pp_batches<T, 9, VEC>(I.rem, I, nbatch, pp_smem, gather, finish);
 }
 
 // ET sweep with the rem rows staged (fp64)
@@ -1100,7 +1139,7 @@ void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const Trt
     const auto o = cast_op<double>(op);
     const bool vec = I.n % 4 == 0 && I.first % 4 == 0;
     if (LBM_IDX_PP) {
-      constexpr int bytes = 3 * 18 * kBlock * 4;
+      constexpr int bytes = kPpBytes<18>;
       static int set_dev = -1;  // the attribute is per device
       int dev = 0;
       cudaGetDevice(&dev);
@@ -1153,6 +1192,14 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
     const auto F = fld<double, false>(f);
     const auto o = cast_op<double>(op);
     const bool vec = I.n % 4 == 0 && I.first % 4 == 0, sw = base.swapped();
+    if (LBM_IDX_PP) {
+      constexpr int bytes = kPpBytes<9>;
+      if (vec && sw) k_et_idx_pp<double, true, true><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      if (vec && !sw) k_et_idx_pp<double, false, true><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      if (!vec && sw) k_et_idx_pp<double, true, false><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      if (!vec && !sw) k_et_idx_pp<double, false, false><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+      return;
+    }
     if (vec && sw) k_et_idx_pf<double, true, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     if (vec && !sw) k_et_idx_pf<double, false, true><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
     if (!vec && sw) k_et_idx_pf<double, true, false><<<g, kBlock, 0, st>>>(F, I, o, nbatch);
