@@ -299,9 +299,23 @@ __device__ __forceinline__ void pp_batches(const uint32_t* __restrict__ table, c
 }
 template <int ROWS>
 constexpr int kPpBytes = 3 * ROWS * kBlock * 4;
+// resident blocks per SM of the pipelined kernels: fp64 2 (<= 128 registers),
+// fp32 LBM_IDX_PP32_BLOCKS
+#ifndef LBM_IDX_PP32_BLOCKS
+#define LBM_IDX_PP32_BLOCKS 4
+#endif
+// fp32 through the pipeline (-DLBM_IDX_PP32=1): measured slower on C2 (AA
+// 0.93 -> 0.75-0.88, ET 0.80 -> 0.73-0.78) at 3-4 blocks per SM
+#ifndef LBM_IDX_PP32
+#define LBM_IDX_PP32 0
+#endif
+template <class T>
+struct PpBlocks {
+  static constexpr int value = sizeof(T) == 8 ? LBM_IDX_PF_MIN_BLOCKS : LBM_IDX_PP32_BLOCKS;
+};
 
 template <class T, bool VEC>
-__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBlock, PpBlocks<T>::value)
     k_aa_odd_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
   extern __shared__ __align__(16) unsigned char pp_smem[];
   auto gather = [&](uint32_t node, auto row, T(&f)[19]) {
@@ -326,7 +340,7 @@ __global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
 }
 
 template <class T, bool SW, bool VEC>
-__global__ void __launch_bounds__(kBlock, LBM_IDX_PF_MIN_BLOCKS)
+__global__ void __launch_bounds__(kBlock, PpBlocks<T>::value)
     k_et_idx_pp(Fld<T, false> F, Idx I, Trt<T> op, uint32_t nbatch) {
   extern __shared__ __align__(16) unsigned char pp_smem[];
   auto gather = [&](uint32_t node, auto row, T(&f)[19]) {
@@ -1132,6 +1146,20 @@ static bool launch_ag(cudaStream_t st, const DField& f, const Idx& I, const TrtH
 void launch_aa_odd_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost& op) {
   if (I.count() == 0) return;
   if (launch_ag<false, false>(st, f, I, op)) return;
+  if (LBM_IDX_PP32 && !f.aos && f.prec == Prec::f32) {
+    const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = std::min<uint32_t>(nbatch, (uint32_t)(sms * LBM_IDX_PP32_BLOCKS));
+    constexpr int bytes = kPpBytes<18>;
+    cudaFuncSetAttribute(k_aa_odd_idx_pp<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_aa_odd_idx_pp<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (I.n % 4 == 0 && I.first % 4 == 0)
+      k_aa_odd_idx_pp<float, true><<<g, kBlock, bytes, st>>>(fld<float, false>(f), I, cast_op<float>(op), nbatch);
+    else
+      k_aa_odd_idx_pp<float, false><<<g, kBlock, bytes, st>>>(fld<float, false>(f), I, cast_op<float>(op), nbatch);
+    return;
+  }
   if (!f.aos && f.prec == Prec::f64) {  // fp32 spills at its register budget
     const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
     const unsigned g = staged_grid(nbatch);
@@ -1186,6 +1214,21 @@ void launch_et_idx(cudaStream_t st, const DField& f, const Idx& I, const TrtHost
     return;
   if (base.swapped() ? launch_ag<true, true>(st, f, I, op) : launch_ag<true, false>(st, f, I, op))
     return;
+  if (LBM_IDX_PP32 && !f.aos && f.prec == Prec::f32) {
+    const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = std::min<uint32_t>(nbatch, (uint32_t)(sms * LBM_IDX_PP32_BLOCKS));
+    constexpr int bytes = kPpBytes<9>;
+    const auto F = fld<float, false>(f);
+    const auto o = cast_op<float>(op);
+    const bool vec = I.n % 4 == 0 && I.first % 4 == 0, sw = base.swapped();
+    if (vec && sw) k_et_idx_pp<float, true, true><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+    if (vec && !sw) k_et_idx_pp<float, false, true><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+    if (!vec && sw) k_et_idx_pp<float, true, false><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+    if (!vec && !sw) k_et_idx_pp<float, false, false><<<g, kBlock, bytes, st>>>(F, I, o, nbatch);
+    return;
+  }
   if (!f.aos && f.prec == Prec::f64) {
     const uint32_t nbatch = (I.count() + kBlock - 1) / kBlock;
     const unsigned g = staged_grid(nbatch);
