@@ -756,11 +756,12 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
     return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
   }
   // default: SWAP push in one sweep (C1 fp64 0.81 / fp32 0.53, C4 0.68 / 0.47
-  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull keeps the two passes
-  // (one sweep: C1 0.56 / 0.46, C4 0.48 / 0.42). LBMGPU_SWAP_SINGLE=1 / 0
-  // forces it on / off for both.
+  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull in one sweep only in
+  // fp64 with whole 32-wide x tiles (C1 0.58 vs 0.51; with a ragged last tile,
+  // C4: 0.48 vs 0.50, and fp32: 0.49 / 0.45 vs 0.49 / 0.47, the two passes).
+  // LBMGPU_SWAP_SINGLE=1 / 0 forces it on / off for both.
   const char* e = std::getenv("LBMGPU_SWAP_SINGLE");
-  const bool on = e ? e[0] == '1' : push;
+  const bool on = e ? e[0] == '1' : (push || (f.prec == Prec::f64 && L.nx % kFbX == 0));
   if (!on) return false;
   if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
