@@ -109,9 +109,13 @@ __device__ __forceinline__ bool s1_cross(const S1Frame& q) {
 #ifndef LBM_S1_PULL_CM
 #define LBM_S1_PULL_CM 0
 #endif
+#ifndef LBM_S1_F32_CM
+#define LBM_S1_F32_CM 0
+#endif
 template <class T, bool PUSH>
 struct S1Cfg {
-  static constexpr bool kCrossMask = sizeof(T) == 8 && (PUSH || LBM_S1_PULL_CM);
+  static constexpr bool kCrossMask =
+      sizeof(T) == 8 ? (PUSH || LBM_S1_PULL_CM) : (PUSH && LBM_S1_F32_CM);
   static constexpr bool kTwoFrames = !PUSH;
 };
 __device__ __forceinline__ uint32_t s1_axis_mask(bool lo, bool hi, uint32_t mlo, uint32_t mhi) {
