@@ -1281,23 +1281,18 @@ __global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
   T f[19], g5[5];
   uint32_t bq = 0;   // bounce mask of the node held in f
   bool lq = false;   // ... and whether it is a fluid cell
-  for (int p = pb; p <= pe; ++p) {
-    // slot(p - 2) staged iteration p - 1's output: its bulk stores must have
-    // read it, and every thread is done with plane p - 1 (slot(p - 1) stages
-    // this iteration's output)
-    bulk_wait_read();
-    fence_async_smem();
-    __syncthreads();
-    if (warp == TY && p - 2 >= pb && p - 2 + NS <= pe) load(p - 2 + NS);
-    if constexpr (MODE == kWinPush) {
-      // OS push as a gather of post-collision values: every window record of
-      // plane p collides in place first (the halo records redundantly in
-      // both neighbouring tiles: deterministic, identical)
-      mbar_wait(&full[slot(p)], par(p));
-      collide_plane(L, op, sm + slot(p) * BUF, ph[slot(p)], t, p);
-      __syncthreads();
-    }
-    if (warp == TY || ty >= t.tyv) continue;
+  // OS push as a gather of post-collision values: every window record of a
+  // plane collides in place before its gathers (the halo records redundantly
+  // in both neighbouring tiles: deterministic, identical). Plane p + 1
+  // collides in iteration p, after the row warps' gathers from plane p (a
+  // different ring slot), so one block barrier per plane orders both and the
+  // warps without gathers collide while the row warps gather (LBM_ZP_PUSH_LAG
+  // = 0: collide plane p at the top of iteration p, between two barriers)
+#ifndef LBM_ZP_PUSH_LAG
+#define LBM_ZP_PUSH_LAG 1
+#endif
+  // the row warps' part of iteration p (gathers from plane p, output of p - 1)
+  auto zp_row = [&](int p) {
     mbar_wait(&full[slot(p)], par(p));
     const int s = slot(p);
     int rp[3];
@@ -1341,6 +1336,32 @@ __global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
       lq = l;
     }
     if (p + 1 >= t.zb && p + 1 < t.ze && valid) zp_take_next(g5, at);  // node p + 1
+  };
+  constexpr bool kLag = MODE == kWinPush && LBM_ZP_PUSH_LAG;
+  if constexpr (kLag) {
+    mbar_wait(&full[slot(pb)], par(pb));
+    collide_plane(L, op, sm + slot(pb) * BUF, ph[slot(pb)], t, pb);
+  }
+  for (int p = pb; p <= pe; ++p) {
+    // slot(p - 2) staged iteration p - 1's output: its bulk stores must have
+    // read it, and every thread is done with plane p - 1 (slot(p - 1) stages
+    // this iteration's output)
+    bulk_wait_read();
+    fence_async_smem();
+    __syncthreads();
+    if (warp == TY && p - 2 >= pb && p - 2 + NS <= pe) load(p - 2 + NS);
+    if constexpr (MODE == kWinPush && !kLag) {
+      mbar_wait(&full[slot(p)], par(p));
+      collide_plane(L, op, sm + slot(p) * BUF, ph[slot(p)], t, p);
+      __syncthreads();
+    }
+    if (warp != TY && ty < t.tyv) zp_row(p);
+    if constexpr (kLag) {
+      if (p + 1 <= pe) {
+        mbar_wait(&full[slot(p + 1)], par(p + 1));
+        collide_plane(L, op, sm + slot(p + 1) * BUF, ph[slot(p + 1)], t, p + 1);
+      }
+    }
   }
   bulk_wait_all();
 }

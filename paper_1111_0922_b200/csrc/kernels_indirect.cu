@@ -21,9 +21,11 @@ inline unsigned grid_for(uint64_t n) { return (unsigned)((n + kBlock - 1) / kBlo
 
 __device__ __forceinline__ uint32_t ldidx(const uint32_t* p) { return __ldg(p); }
 
-// local collision over nodes (TS collide, precollide, AA even, SWAP collide)
+// local collision over nodes (TS collide, precollide, AA even, SWAP collide);
+// no indirection, so the direct k_local's register budget (fp64 SoA at 3
+// blocks per SM)
 template <class T, bool AOS, bool RD_OPP, bool WR_OPP>
-__global__ void __launch_bounds__(kBlock, MinBlocks<T>::value) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
+__global__ void __launch_bounds__(kBlock, SoaMinBlocks<T, AOS>::value) k_local_idx(Fld<T, AOS> src, Fld<T, AOS> dst,
                                                       uint32_t first, uint32_t n, Trt<T> op) {
   const uint32_t node = first + blockIdx.x * kBlock + threadIdx.x;
   if (node >= n) return;
