@@ -20,7 +20,13 @@
 namespace lbmgpu {
 namespace dev {
 
-constexpr int kFbX = 32, kFbY = 8, kFbThreads = kFbX * kFbY;
+#ifndef LBM_FB_X
+#define LBM_FB_X 32
+#endif
+#ifndef LBM_FB_Y
+#define LBM_FB_Y 8
+#endif
+constexpr int kFbX = LBM_FB_X, kFbY = LBM_FB_Y, kFbThreads = kFbX * kFbY;
 
 // direction lists of the faces (ascending): incoming from y - 1 (c_y = +1),
 // from y + 1 (c_y = -1), and likewise for x and z

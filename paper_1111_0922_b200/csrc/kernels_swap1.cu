@@ -382,6 +382,129 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
 }
 
 // ---------------------------------------------------------------------------
+// SWAP pull in one sweep, SoA, with the inputs staged by cp.async two nodes
+// ahead. k_swap1's pull reads 14 of a node's 19 inputs in the node's own
+// iteration and collides right after the barrier, so their latency is exposed
+// once per plane (C1 fp64 0.58); reading all 19 one node ahead in registers
+// spills (0.51). Here node z + 2's 19 inputs are copied asynchronously into a
+// thread-private shared-memory column right after iteration z's barrier (the
+// column node z just emptied) and complete before iteration z + 1's barrier:
+// they fly across node z's collision and stores and hold no registers.
+// In-place order: node z + 2's inputs lie in planes z + 1 .. z + 3, rewritten
+// only by their own nodes after barriers z + 1 .. z + 3, and the copies have
+// landed (wait_group 0) before barrier z + 1; crossing inputs come from the
+// last sweep's face buffer as in k_swap1. The same schedule for push (node
+// z + 2's own column staged; LBMGPU_S1_PUSH_ASYNC=1) measured slower than
+// k_swap1's register-held push (C1 fp64 0.82 -> 0.75, fp32 0.53 -> 0.49).
+// ---------------------------------------------------------------------------
+// the address s1_in reads input I from
+template <bool PUSH, bool CM, int I, class T>
+__device__ __forceinline__ const T* s1_src(const S1Tab<T>& F, const T* hprev, const S1Frame& q,
+                                           uint32_t s, uint32_t bounce) {
+  constexpr int X = cx(I), Y = cy(I), Z = cz(I), J = opp(I);
+  const bool local = s1_local<J, -X, -Y, -Z>(q, bounce);
+  if (!local && s1_cross<CM, J, -X, -Y, -Z>(q)) return hprev + s1_in_slot<I>(q);
+  return (PUSH || local) ? F.pl[J] + s : F.sh[I] + s;
+}
+template <bool PUSH, bool CM, class T, int... Is>
+__device__ __forceinline__ void s1_issue(const S1Tab<T>& F, const T* hprev, const S1Frame& q,
+                                         uint32_t s, uint32_t bounce, T* col,
+                                         std::integer_sequence<int, Is...>) {
+  cp_async<(int)sizeof(T)>(col, F.pl[0] + s);
+  (cp_async<(int)sizeof(T)>(col + (Is + 1) * kFbThreads, s1_src<PUSH, CM, Is + 1>(F, hprev, q, s, bounce)),
+   ...);
+}
+template <class T>
+constexpr size_t kS1PaBytes = 2 * 19 * kFbThreads * sizeof(T);
+// resident blocks per SM: fp64 as k_swap1 (2), fp32 4 (C1 pull 0.51 -> 0.56,
+// C4 0.48 -> 0.50 against 3; the face-buffer geometry keeps k_swap1's waves)
+#ifndef LBM_S1_PA_BLOCKS32
+#define LBM_S1_PA_BLOCKS32 4
+#endif
+template <class T>
+struct S1PaBlocks {
+  static constexpr int value = sizeof(T) == 8 ? LBM_S1_BLOCKS : LBM_S1_PA_BLOCKS32;
+};
+
+template <class T, bool PUSH>
+__global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
+    k_swap1_pa(const __grid_constant__ S1Tab<T> F, Lat L, Trt<T> op, FbGeo G, T* __restrict__ hcur,
+               const T* __restrict__ hprev) {
+  extern __shared__ __align__(16) unsigned char s1pa_smem[];
+  T* stg = reinterpret_cast<T*>(s1pa_smem);
+  const int ntile = G.tiles_x * G.tiles_y;
+  const int tile = (int)blockIdx.x % ntile, ch = (int)blockIdx.x / ntile;
+  const FbBlock b = fb_block(L, G, tile % G.tiles_x, tile / G.tiles_x, ch);
+  const int tx = threadIdx.x % kFbX, ty = threadIdx.x / kFbX;
+  const bool act = tx < b.txv && ty < b.tyv;
+  const int x = b.x0 + tx, y = b.y0 + ty;
+  const uint32_t sxy = (uint32_t)L.sxy;
+  const uint32_t s0 = (uint32_t)x + (uint32_t)L.sx * (uint32_t)y;
+  const auto seq = std::make_integer_sequence<int, 18>{};
+  constexpr bool CM = S1Cfg<T, PUSH>::kCrossMask;
+  S1Frame qf;
+  qf.fxl = tx == 0, qf.fxh = tx == b.txv - 1, qf.fyl = ty == 0, qf.fyh = ty == b.tyv - 1;
+  qf.dxl = x == 0, qf.dxh = x == L.nx - 1, qf.dyl = y == 0, qf.dyh = y == L.ny - 1;
+  qf.tx = tx, qf.ty = ty, qf.zc = G.zc;
+  qf.base = (uint32_t)b.base;
+  qf.rx = (uint32_t)G.region;
+  qf.ry = (uint32_t)((long long)G.tiles_x * G.region);
+  qf.rz = (uint32_t)((long long)G.tiles_x * G.tiles_y * G.region);
+  qf.hy = (uint32_t)G.hy, qf.hx = (uint32_t)G.hx, qf.hz = (uint32_t)G.hz;
+  qf.iz = qf.base + qf.hz + (uint32_t)(ty * kFbX + tx);
+  const uint32_t leave_xy = s1_axis_mask(qf.dxl, qf.dxh, kMxm, kMxp) | s1_axis_mask(qf.dyl, qf.dyh, kMym, kMyp);
+  const uint32_t box_xy = s1_axis_mask(qf.fxl, qf.fxh, kMxm, kMxp) | s1_axis_mask(qf.fyl, qf.fyh, kMym, kMyp);
+  auto at_plane = [&](S1Frame& q, int z) {
+    q.pz = z - b.zb;
+    q.fzl = z == b.zb, q.fzh = z == b.ze - 1;
+    q.dzl = z == 0, q.dzh = z == L.nz - 1;
+    q.iy = q.base + q.hy + (uint32_t)(q.pz * 10 * kFbX + tx);
+    q.ix = q.base + q.hx + (uint32_t)(q.pz * 10 * kFbY + ty);
+    if (CM) q.box = box_xy | s1_axis_mask(q.fzl, q.fzh, kMzm, kMzp);
+  };
+  // node z's fluid flag and local-link mask
+  auto cell = [&](int z, uint32_t& bm) {
+    bm = 0;
+    if (!act || z >= b.ze) return false;
+    const bool l = fb_cell(L, x, y, z, bm);
+    if (LBM_S1_LOCALMASK) bm |= leave_xy | s1_axis_mask(z == 0, z == L.nz - 1, kMzm, kMzp);
+    return l;
+  };
+  auto col = [&](int z) { return stg + ((z - b.zb) & 1) * 19 * kFbThreads + threadIdx.x; };
+  auto issue = [&](int z, bool l, uint32_t bm) {
+    if (l) {
+      at_plane(qf, z);
+      s1_issue<PUSH, CM>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
+    }
+    cp_commit();
+  };
+  uint32_t bf, bg;
+  bool lf = cell(b.zb, bf), lg = cell(b.zb + 1, bg);
+  issue(b.zb, lf, bf);
+  issue(b.zb + 1, lg, bg);
+  for (int z = b.zb; z < b.ze; ++z) {
+    cp_wait0();  // nodes z and z + 1 have their inputs (z + 1's plane-z ones before barrier z)
+    __syncthreads();
+    T f[19];
+    if (lf) {
+      const T* c = col(z);
+#pragma unroll
+      for (int i = 0; i < 19; ++i) f[i] = c[i * kFbThreads];
+    }
+    uint32_t bh;
+    const bool lh = cell(z + 2, bh);
+    issue(z + 2, lh, bh);  // into the column node z just emptied
+    if (lf) {
+      collide(op, f);
+      at_plane(qf, z);
+      s1_write<PUSH, CM>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
+    }
+    bf = bg, lf = lg;
+    bg = bh, lg = lh;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SWAP push in one sweep on AoS records. The same face buffers as the SoA
 // kernel: a block never writes a record outside its box, so its box planes
 // can be staged in shared memory whole and leave whole — each record row of
@@ -745,6 +868,18 @@ __global__ void __launch_bounds__(kFbThreads)
 
 }  // namespace
 
+// SoA through k_swap1_pa (LBMGPU_S1_PULL_ASYNC / LBMGPU_S1_PUSH_ASYNC = 1 / 0)
+static bool s1_async(bool push) {
+  static const int on[2] = {[] {
+                              const char* e = std::getenv("LBMGPU_S1_PULL_ASYNC");
+                              return e ? (e[0] == '1' ? 1 : 0) : 1;
+                            }(),
+                            [] {
+                              const char* e = std::getenv("LBMGPU_S1_PUSH_ASYNC");
+                              return e ? (e[0] == '1' ? 1 : 0) : 0;
+                            }()};
+  return on[push ? 1 : 0] != 0;
+}
 // SoA, full-grid direct lattice without halo or ghost planes
 bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (f.aos) {
@@ -760,12 +895,14 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
     return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
   }
   // default: SWAP push in one sweep (C1 fp64 0.81 / fp32 0.53, C4 0.68 / 0.47
-  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull in one sweep only in
-  // fp64 with whole 32-wide x tiles (C1 0.58 vs 0.51; with a ragged last tile,
-  // C4: 0.48 vs 0.50, and fp32: 0.49 / 0.45 vs 0.49 / 0.47, the two passes).
-  // LBMGPU_SWAP_SINGLE=1 / 0 forces it on / off for both.
+  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47); pull in one sweep through
+  // the cp.async-staged k_swap1_pa (C1 fp64 0.70 / fp32 0.51, C4 0.61 / 0.48
+  // vs the two passes' 0.51 / 0.49, 0.50 / 0.47; k_swap1's register-held pull,
+  // LBMGPU_S1_PULL_ASYNC=0, is one sweep only in fp64 with whole 32-wide x
+  // tiles: C1 0.58). LBMGPU_SWAP_SINGLE=1 / 0 forces it on / off for both.
   const char* e = std::getenv("LBMGPU_SWAP_SINGLE");
-  const bool on = e ? e[0] == '1' : (push || (f.prec == Prec::f64 && L.nx % kFbX == 0));
+  const bool on = e ? e[0] == '1'
+                    : (push || s1_async(false) || (f.prec == Prec::f64 && L.nx % kFbX == 0));
   if (!on) return false;
   if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
@@ -809,6 +946,22 @@ static void launch_swap1_aos_t(cudaStream_t st, const DField& f, const Lat& L, c
                                                             G, hcur, hprev);
 }
 
+template <class T, bool PUSH>
+static void launch_swap1_pa(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op,
+                            const FbGeo& G, T* hcur, const T* hprev) {
+  static int set_dev = -1;  // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev) {
+    cudaFuncSetAttribute(k_swap1_pa<T, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kS1PaBytes<T>);
+    set_dev = dev;
+  }
+  const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
+  k_swap1_pa<T, PUSH><<<grid, kFbThreads, kS1PaBytes<T>, st>>>(s1_tab<T>(f, L, PUSH), L, cast_op<T>(op),
+                                                                G, hcur, hprev);
+}
+
 void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev) {
   const FbGeo G = fb_geo(L, s1_blocks(f));
@@ -820,6 +973,16 @@ void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost&
     } else {
       if (push) launch_swap1_aos_t<float, true>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
       else launch_swap1_aos_t<float, false>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+    }
+    return;
+  }
+  if (s1_async(push)) {
+    if (f.prec == Prec::f64) {
+      if (push) launch_swap1_pa<double, true>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
+      else launch_swap1_pa<double, false>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
+    } else {
+      if (push) launch_swap1_pa<float, true>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
+      else launch_swap1_pa<float, false>(st, f, L, op, G, (float*)hcur, (const float*)hprev);
     }
     return;
   }
