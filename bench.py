@@ -466,7 +466,7 @@ def e2e_slabs(L, st, args, dist, nodes_local, nodes):
     st.slab_sync_ghosts()
     st.extract_natural(buf.array)
     t = reduce_max(dist, time.perf_counter() - t0)
-    total = nodes * 19 * 8
+    total = nodes * 19 * (8 if args.precision == 8 else 4)
     return {"value": round(nodes * args.steps / t / 1e6, 2), "unit": "MFLUP/s",
             "h2d_bytes_per_step": total / args.steps, "d2h_bytes_per_step": total / args.steps,
             "seconds": round(t, 4),

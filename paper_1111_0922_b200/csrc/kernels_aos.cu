@@ -1241,7 +1241,7 @@ __device__ __forceinline__ void zp_take_next(T (&g5)[5], At at) {
 template <class T, int MODE>
 __global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
     k_win_zp(Fld<T, true> src, Fld<T, true> dst, Lat L, Trt<T> op, int tiles_x, int tiles_y,
-             int zc) {
+             int zc, int z0, int z1, const T* wlo, const T* whi) {
   static_assert(MODE == kWinPull || MODE == kWinStream || MODE == kWinPush,
                 "z pipeline: gather modes");
   constexpr int TY = ZpCfg<T>::TY, NS = ZpCfg<T>::NS, ROW = ZpCfg<T>::ROW, BUF = ZpCfg<T>::BUF;
@@ -1257,8 +1257,8 @@ __global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
   t.y0 = (tile / tiles_x) * TY;
   t.txv = min(kTX, L.nx - t.x0);
   t.tyv = min(TY, L.ny - t.y0);
-  t.zb = chunk * zc;
-  t.ze = min(L.nz, t.zb + zc);
+  t.zb = z0 + chunk * zc;  // planes [z0, z1) in chunks of zc (CG: one plane group)
+  t.ze = min(z1, t.zb + zc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int b = 0; b < NS; ++b) mbar_init(&full[b], (uint32_t)(t.tyv + 2) * kRowArrivals);
@@ -1269,8 +1269,8 @@ __global__ void __launch_bounds__(ZpThreads<T, MODE>::value, ZpCfg<T>::kBlocks)
   auto slot = [&](int p) { return (p - pb) % NS; };
   auto par = [&](int p) { return (uint32_t)((p - pb) / NS) & 1u; };
   auto load = [&](int p) {
-    load_plane(L, (const T*)src.p, sm + slot(p) * BUF, ph[slot(p)], t, p, (const T*)nullptr,
-               (const T*)nullptr, &full[slot(p)], TY);
+    load_plane(L, (const T*)src.p, sm + slot(p) * BUF, ph[slot(p)], t, p, wlo, whi,
+               &full[slot(p)], TY);
   };
   if (warp == TY)
     for (int p = pb; p <= min(pe, pb + NS - 1); ++p) load(p);
@@ -1771,7 +1771,9 @@ void launch_win(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
 
 template <class T, int MODE>
 void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat& L,
-                   const TrtHost& op) {
+                   const TrtHost& op, int z0 = 0, int z1 = -1, const void* wlo = nullptr,
+                   const void* whi = nullptr) {
+  if (z1 < 0) z1 = L.nz;
   using C = ZpCfg<T>;
   constexpr int kThr = ZpThreads<T, MODE>::value;
   const int per_sm = ensure_smem<k_win_zp<T, MODE>>(kThr, C::kBytes);
@@ -1780,13 +1782,14 @@ void launch_win_zp(cudaStream_t st, const DField& a, const DField& b, const Lat&
   const int tiles_x = (L.nx + kTX - 1) / kTX, tiles_y = (L.ny + C::TY - 1) / C::TY;
   // z planes per block: about 7 waves of resident blocks, 4 .. 64 planes
   const long long tiles = (long long)tiles_x * tiles_y, resident = (long long)sms * per_sm;
-  long long zc = wave_chunk(L.nz, tiles, resident, 2);
+  long long zc = wave_chunk(z1 - z0, tiles, resident, 2);
   if (const char* e = std::getenv("LBMGPU_AOS_ZCHUNK"))
     if (std::atoi(e) > 0) zc = std::atoi(e);
-  zc = std::max(1LL, std::min<long long>(zc, L.nz));
-  const int nzc = (int)((L.nz + zc - 1) / zc);
+  zc = std::max(1LL, std::min<long long>(zc, z1 - z0));
+  const int nzc = (int)((z1 - z0 + zc - 1) / zc);
   k_win_zp<T, MODE><<<(unsigned)(tiles * nzc), kThr, C::kBytes, st>>>(
-      fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc);
+      fld<T, true>(a), fld<T, true>(b), L, cast_op<T>(op), tiles_x, tiles_y, (int)zc, z0, z1,
+      static_cast<const T*>(wlo), static_cast<const T*>(whi));
 }
 
 // OS push through the z pipeline (every window record of a plane collided in
@@ -1809,6 +1812,15 @@ bool ws_f32() {
 bool zpipe_push(bool f64) {
   static const int env = [] {
     const char* e = std::getenv("LBMGPU_AOS_ZPIPE_PUSH");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return env < 0 ? !f64 : env == 1;
+}
+
+// CG plane groups through the z pipeline's push (LBMGPU_AOS_ZPIPE_CG = 1 / 0)
+bool zpipe_cg(bool f64) {
+  static const int env = [] {
+    const char* e = std::getenv("LBMGPU_AOS_ZPIPE_CG");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   return env < 0 ? !f64 : env == 1;
@@ -1934,6 +1946,14 @@ bool aos_push_planes_ok(const DField& src, const Lat& L) {
 void launch_aos_push_planes(cudaStream_t st, const DField& src, const DField& dst, const Lat& L,
                             const TrtHost& op, int z0, int z1, const void* wlo, const void* whi) {
   if (z1 <= z0) return;
+  // the z pipeline's push (the OS-push kernel) on the group's planes
+  if (zpipe_enabled() && zpipe_cg(src.prec == Prec::f64)) {
+    if (src.prec == Prec::f64)
+      launch_win_zp<double, kWinPush>(st, src, dst, L, op, z0, z1, wlo, whi);
+    else
+      launch_win_zp<float, kWinPush>(st, src, dst, L, op, z0, z1, wlo, whi);
+    return;
+  }
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // about two waves of resident blocks over the group's planes
