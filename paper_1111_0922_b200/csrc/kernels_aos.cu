@@ -1390,6 +1390,9 @@ constexpr int kNBw = 5;
 #ifndef LBM_WS_TY32
 #define LBM_WS_TY32 14
 #endif
+#ifndef LBM_WS_TY64
+#define LBM_WS_TY64 6
+#endif
 // write-back warps (measured on C1 fp64: 2 -> AA 0.51, 4 -> 0.66, 6 -> 0.67,
 // 8 -> 0.74, 10 -> 0.77 of the roofline; the row warps' register cap at 512
 // threads costs a few spills); storing the rim slots straight from the row
@@ -1400,7 +1403,7 @@ constexpr int kNBw = 5;
 constexpr int kWsWb = LBM_WS_WB;
 template <class T>
 struct WinSzW {
-  static constexpr int TY = sizeof(T) == 8 ? 6 : LBM_WS_TY32;  // row warps
+  static constexpr int TY = sizeof(T) == 8 ? LBM_WS_TY64 : LBM_WS_TY32;  // row warps
   static constexpr int WR = TY + 2;
   static constexpr int kThreads = 32 * (TY + kWsWb);
   static constexpr int kList = 4 * kWC * 19 + (WR - 4) * 4 * 19;
