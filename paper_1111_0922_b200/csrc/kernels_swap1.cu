@@ -255,6 +255,17 @@ __device__ __forceinline__ void s1_write(const S1Tab<T>& F, T* hcur, const FbGeo
 #ifndef LBM_S1_BLOCKS32
 #define LBM_S1_BLOCKS32 3
 #endif
+// warp-uniform inner fast path of k_swap1's push (per precision)
+#ifndef LBM_S1_PUSH_FAST32
+#define LBM_S1_PUSH_FAST32 0
+#endif
+#ifndef LBM_S1_PUSH_FAST64
+#define LBM_S1_PUSH_FAST64 0
+#endif
+template <class T>
+struct S1PushFast {
+  static constexpr bool value = sizeof(T) == 8 ? LBM_S1_PUSH_FAST64 != 0 : LBM_S1_PUSH_FAST32 != 0;
+};
 template <class T>
 struct S1Blocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_S1_BLOCKS : LBM_S1_BLOCKS32;
@@ -352,6 +363,21 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
   // recomputed (at_plane) before each node's reads and writes
   S1Frame qg = qf;
   T g[19];
+  // warp-uniform inner case (as in k_swap1_pa below): the y / z flags and the
+  // link mask as constants, only the end lanes' x-crossing links remain
+  constexpr bool kFast = S1PushFast<T>::value;
+  const bool row_inner = ty > 0 && ty < b.tyv - 1;
+  auto inner = [&](int z, bool l, uint32_t bm) {
+    if (!kFast) return false;
+    return __all_sync(0xffffffffu, l && bm == 0u && row_inner && z > b.zb && z < b.ze - 1) != 0;
+  };
+  auto inner_frame = [&](int z) {
+    S1Frame qi = qf;
+    at_plane(qi, z);
+    qi.fyl = qi.fyh = qi.fzl = qi.fzh = false;
+    return qi;
+  };
+  bool ff = false, fg = false;
   if (act) {
     lf = fb_cell(L, x, y, b.zb, bf);
     if (LBM_S1_LOCALMASK) bf |= leave_xy | s1_axis_mask(b.zb == 0, b.zb == L.nz - 1, kMzm, kMzp);
@@ -360,15 +386,26 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
   }
   for (int z = b.zb; z < b.ze; ++z) {
     lg = false;
-    if (act && z + 1 < b.ze) {
+    const bool more = act && z + 1 < b.ze;
+    if (more) {
       lg = fb_cell(L, x, y, z + 1, bg);
       if (LBM_S1_LOCALMASK) bg |= leave_xy | s1_axis_mask(z + 1 == 0, z + 1 == L.nz - 1, kMzm, kMzp);
+    }
+    fg = inner(z + 1, lg, bg);
+    if (fg) {
+      const S1Frame qi = inner_frame(z + 1);
+      s1_read<PUSH, false>(F, hprev, G, qi, s0 + (uint32_t)(z + 1) * sxy, 0u, g, seq);
+    } else if (more) {
       S1Frame& qn = TWO ? qg : qf;
       at_plane(qn, z + 1);
       if (lg) s1_read<PUSH, CM>(F, hprev, G, qn, s0 + (uint32_t)(z + 1) * sxy, bg, g, seq);
     }
     __syncthreads();
-    if (lf) {
+    if (ff) {
+      collide(op, f);
+      const S1Frame qi = inner_frame(z);
+      s1_write<PUSH, false>(F, hcur, G, qi, s0 + (uint32_t)z * sxy, 0u, f, seq);
+    } else if (lf) {
       collide(op, f);
       if (!TWO) at_plane(qf, z);
       s1_write<PUSH, CM>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
@@ -377,6 +414,7 @@ __global__ void __launch_bounds__(kFbThreads, S1Blocks<T>::value)
     for (int i = 0; i < 19; ++i) f[i] = g[i];
     bf = bg;
     lf = lg;
+    ff = fg;
     if (TWO) qf = qg;
   }
 }
@@ -421,6 +459,18 @@ constexpr size_t kS1PaBytes = 2 * 19 * kFbThreads * sizeof(T);
 #ifndef LBM_S1_PA_BLOCKS32
 #define LBM_S1_PA_BLOCKS32 4
 #endif
+// warp-uniform inner fast path of k_swap1_pa (per precision)
+// (C1 fp64 pull 0.69 -> 0.74, C4 0.60 -> 0.62; fp32 0.51 -> 0.50: off)
+#ifndef LBM_S1_PA_FAST32
+#define LBM_S1_PA_FAST32 0
+#endif
+#ifndef LBM_S1_PA_FAST64
+#define LBM_S1_PA_FAST64 1
+#endif
+template <class T>
+struct S1PaFast {
+  static constexpr bool value = sizeof(T) == 8 ? LBM_S1_PA_FAST64 != 0 : LBM_S1_PA_FAST32 != 0;
+};
 template <class T>
 struct S1PaBlocks {
   static constexpr int value = sizeof(T) == 8 ? LBM_S1_BLOCKS : LBM_S1_PA_BLOCKS32;
@@ -471,8 +521,28 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
     return l;
   };
   auto col = [&](int z) { return stg + ((z - b.zb) & 1) * 19 * kFbThreads + threadIdx.x; };
-  auto issue = [&](int z, bool l, uint32_t bm) {
-    if (l) {
+  // Warp-uniform inner case (LBM_S1_PA_FAST): the warp's row is not on a y
+  // face of the box, the plane not on a z face and no lane has a local link,
+  // so only the x-crossing directions of the warp's end lanes use the face
+  // buffers. The same templates with the y / z flags and the link mask as
+  // constants: the per-direction tests and slot arithmetic fold away.
+  constexpr bool kFast = S1PaFast<T>::value;
+  const bool row_inner = ty > 0 && ty < b.tyv - 1;  // uniform over a warp (kFbX % 32 == 0)
+  auto inner = [&](int z, bool l, uint32_t bm) {
+    if (!kFast) return false;
+    return __all_sync(0xffffffffu, l && bm == 0u && row_inner && z > b.zb && z < b.ze - 1) != 0;
+  };
+  auto inner_frame = [&](int z) {
+    S1Frame qi = qf;
+    at_plane(qi, z);
+    qi.fyl = qi.fyh = qi.fzl = qi.fzh = false;
+    return qi;
+  };
+  auto issue = [&](int z, bool l, uint32_t bm, bool fast) {
+    if (fast) {
+      const S1Frame qi = inner_frame(z);
+      s1_issue<PUSH, false>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+    } else if (l) {
       at_plane(qf, z);
       s1_issue<PUSH, CM>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
     }
@@ -480,8 +550,9 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   };
   uint32_t bf, bg;
   bool lf = cell(b.zb, bf), lg = cell(b.zb + 1, bg);
-  issue(b.zb, lf, bf);
-  issue(b.zb + 1, lg, bg);
+  bool ff = inner(b.zb, lf, bf), fg = inner(b.zb + 1, lg, bg);
+  issue(b.zb, lf, bf, ff);
+  issue(b.zb + 1, lg, bg, fg);
   for (int z = b.zb; z < b.ze; ++z) {
     cp_wait0();  // nodes z and z + 1 have their inputs (z + 1's plane-z ones before barrier z)
     __syncthreads();
@@ -493,14 +564,19 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
     }
     uint32_t bh;
     const bool lh = cell(z + 2, bh);
-    issue(z + 2, lh, bh);  // into the column node z just emptied
-    if (lf) {
+    const bool fh = inner(z + 2, lh, bh);
+    issue(z + 2, lh, bh, fh);  // into the column node z just emptied
+    if (ff) {
+      collide(op, f);
+      const S1Frame qi = inner_frame(z);
+      s1_write<PUSH, false>(F, hcur, G, qi, s0 + (uint32_t)z * sxy, 0u, f, seq);
+    } else if (lf) {
       collide(op, f);
       at_plane(qf, z);
       s1_write<PUSH, CM>(F, hcur, G, qf, s0 + (uint32_t)z * sxy, bf, f, seq);
     }
-    bf = bg, lf = lg;
-    bg = bh, lg = lh;
+    bf = bg, lf = lg, ff = fg;
+    bg = bh, lg = lh, fg = fh;
   }
 }
 
