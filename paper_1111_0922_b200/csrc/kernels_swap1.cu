@@ -444,13 +444,32 @@ __device__ __forceinline__ const T* s1_src(const S1Tab<T>& F, const T* hprev, co
   if (!local && s1_cross<CM, J, -X, -Y, -Z>(q)) return hprev + s1_in_slot<I>(q);
   return (PUSH || local) ? F.pl[J] + s : F.sh[I] + s;
 }
-template <bool PUSH, bool CM, class T, int... Is>
+// LBM_S1_PA_SPLIT (pull): a node's copies leave in two groups. EARLY: the
+// five c_z = +1 inputs (plane z - 1 of the node: rewritten by the node below
+// one iteration earlier, so they must land before that iteration's barrier);
+// LATE: the other 14 (the node's own plane and the one above, rewritten in
+// the node's own iteration or later), which may stay in flight one iteration
+// longer (wait_group 1 at the top of the loop). Measured slower (C1 fp64 0.74
+// -> 0.64, C4 0.62 -> 0.56; fp32 unchanged), so off: one group, wait_group 0.
+#ifndef LBM_S1_PA_SPLIT
+#define LBM_S1_PA_SPLIT 0
+#endif
+template <bool PUSH>
+__host__ __device__ constexpr bool s1_pa_early(int i) {
+  return PUSH || !LBM_S1_PA_SPLIT || cz(i) == 1;
+}
+template <bool PUSH, bool CM, bool EARLY, int I, class T>
+__device__ __forceinline__ void s1_issue_one(const S1Tab<T>& F, const T* hprev, const S1Frame& q,
+                                             uint32_t s, uint32_t bounce, T* col) {
+  if constexpr (s1_pa_early<PUSH>(I) == EARLY)
+    cp_async<(int)sizeof(T)>(col + I * kFbThreads, s1_src<PUSH, CM, I>(F, hprev, q, s, bounce));
+}
+template <bool PUSH, bool CM, bool EARLY, class T, int... Is>
 __device__ __forceinline__ void s1_issue(const S1Tab<T>& F, const T* hprev, const S1Frame& q,
                                          uint32_t s, uint32_t bounce, T* col,
                                          std::integer_sequence<int, Is...>) {
-  cp_async<(int)sizeof(T)>(col, F.pl[0] + s);
-  (cp_async<(int)sizeof(T)>(col + (Is + 1) * kFbThreads, s1_src<PUSH, CM, Is + 1>(F, hprev, q, s, bounce)),
-   ...);
+  if constexpr (s1_pa_early<PUSH>(0) == EARLY) cp_async<(int)sizeof(T)>(col, F.pl[0] + s);
+  (s1_issue_one<PUSH, CM, EARLY, Is + 1>(F, hprev, q, s, bounce, col), ...);
 }
 template <class T>
 constexpr size_t kS1PaBytes = 2 * 19 * kFbThreads * sizeof(T);
@@ -527,6 +546,7 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   // buffers. The same templates with the y / z flags and the link mask as
   // constants: the per-direction tests and slot arithmetic fold away.
   constexpr bool kFast = S1PaFast<T>::value;
+  constexpr bool kSplit = !PUSH && LBM_S1_PA_SPLIT != 0;
   const bool row_inner = ty > 0 && ty < b.tyv - 1;  // uniform over a warp (kFbX % 32 == 0)
   auto inner = [&](int z, bool l, uint32_t bm) {
     if (!kFast) return false;
@@ -541,10 +561,16 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   auto issue = [&](int z, bool l, uint32_t bm, bool fast) {
     if (fast) {
       const S1Frame qi = inner_frame(z);
-      s1_issue<PUSH, false>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+      s1_issue<PUSH, false, true>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+      if (kSplit) cp_commit();
+      s1_issue<PUSH, false, false>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
     } else if (l) {
       at_plane(qf, z);
-      s1_issue<PUSH, CM>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
+      s1_issue<PUSH, CM, true>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
+      if (kSplit) cp_commit();
+      s1_issue<PUSH, CM, false>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
+    } else if (kSplit) {
+      cp_commit();
     }
     cp_commit();
   };
@@ -554,7 +580,12 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   issue(b.zb, lf, bf, ff);
   issue(b.zb + 1, lg, bg, fg);
   for (int z = b.zb; z < b.ze; ++z) {
-    cp_wait0();  // nodes z and z + 1 have their inputs (z + 1's plane-z ones before barrier z)
+    // node z has all its inputs and node z + 1 its plane-z ones before barrier
+    // z; split: node z + 1's late group may still be in flight
+    if (kSplit)
+      cp_wait1();
+    else
+      cp_wait0();
     __syncthreads();
     T f[19];
     if (lf) {
