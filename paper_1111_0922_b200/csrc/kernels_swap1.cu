@@ -486,6 +486,12 @@ constexpr size_t kS1PaBytes = 2 * 19 * kFbThreads * sizeof(T);
 #ifndef LBM_S1_PA_FAST64
 #define LBM_S1_PA_FAST64 1
 #endif
+// y-face classes (a tile's two edge rows specialised as well): four code
+// paths per block measured far slower (C1 fp64 0.74 -> 0.36, fp32 0.51 ->
+// 0.38: the warps of a block then run different instruction streams), off
+#ifndef LBM_S1_PA_YFACE
+#define LBM_S1_PA_YFACE 0
+#endif
 template <class T>
 struct S1PaFast {
   static constexpr bool value = sizeof(T) == 8 ? LBM_S1_PA_FAST64 != 0 : LBM_S1_PA_FAST32 != 0;
@@ -548,22 +554,41 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   constexpr bool kFast = S1PaFast<T>::value;
   constexpr bool kSplit = !PUSH && LBM_S1_PA_SPLIT != 0;
   const bool row_inner = ty > 0 && ty < b.tyv - 1;  // uniform over a warp (kFbX % 32 == 0)
+  // class of the warp's node at plane z: 0 generic, 1 inner, 2 / 3 the box's
+  // low / high y face (LBM_S1_PA_YFACE: the two edge rows of a tile otherwise
+  // run the generic path and the block's per-plane barrier waits for them)
+  const int row_class = row_inner ? 1 : (!LBM_S1_PA_YFACE || b.tyv < 2 ? 0 : (ty == 0 ? 2 : 3));
   auto inner = [&](int z, bool l, uint32_t bm) {
-    if (!kFast) return false;
-    return __all_sync(0xffffffffu, l && bm == 0u && row_inner && z > b.zb && z < b.ze - 1) != 0;
+    if (!kFast) return 0;
+    const bool ok = __all_sync(0xffffffffu, l && bm == 0u && z > b.zb && z < b.ze - 1) != 0;
+    return ok ? row_class : 0;
   };
-  auto inner_frame = [&](int z) {
+  auto inner_frame = [&](int z, auto yl, auto yh) {
     S1Frame qi = qf;
     at_plane(qi, z);
-    qi.fyl = qi.fyh = qi.fzl = qi.fzh = false;
+    qi.fyl = decltype(yl)::value, qi.fyh = decltype(yh)::value;
+    qi.fzl = qi.fzh = false;
     return qi;
   };
-  auto issue = [&](int z, bool l, uint32_t bm, bool fast) {
-    if (fast) {
-      const S1Frame qi = inner_frame(z);
-      s1_issue<PUSH, false, true>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
-      if (kSplit) cp_commit();
-      s1_issue<PUSH, false, false>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+  auto issue_class = [&](int z, auto yl, auto yh) {
+    const S1Frame qi = inner_frame(z, yl, yh);
+    s1_issue<PUSH, false, true>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+    if (kSplit) cp_commit();
+    s1_issue<PUSH, false, false>(F, hprev, qi, s0 + (uint32_t)z * sxy, 0u, col(z), seq);
+  };
+  auto write_class = [&](int z, const T(&v)[19], auto yl, auto yh) {
+    const S1Frame qi = inner_frame(z, yl, yh);
+    s1_write<PUSH, false>(F, hcur, G, qi, s0 + (uint32_t)z * sxy, 0u, v, seq);
+  };
+  using No = std::false_type;
+  using Yes = std::true_type;
+  auto issue = [&](int z, bool l, uint32_t bm, int fast) {
+    if (fast == 1) {
+      issue_class(z, No{}, No{});
+    } else if (fast == 2) {
+      issue_class(z, Yes{}, No{});
+    } else if (fast == 3) {
+      issue_class(z, No{}, Yes{});
     } else if (l) {
       at_plane(qf, z);
       s1_issue<PUSH, CM, true>(F, hprev, qf, s0 + (uint32_t)z * sxy, bm, col(z), seq);
@@ -576,7 +601,7 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
   };
   uint32_t bf, bg;
   bool lf = cell(b.zb, bf), lg = cell(b.zb + 1, bg);
-  bool ff = inner(b.zb, lf, bf), fg = inner(b.zb + 1, lg, bg);
+  int ff = inner(b.zb, lf, bf), fg = inner(b.zb + 1, lg, bg);
   issue(b.zb, lf, bf, ff);
   issue(b.zb + 1, lg, bg, fg);
   for (int z = b.zb; z < b.ze; ++z) {
@@ -595,12 +620,16 @@ __global__ void __launch_bounds__(kFbThreads, S1PaBlocks<T>::value)
     }
     uint32_t bh;
     const bool lh = cell(z + 2, bh);
-    const bool fh = inner(z + 2, lh, bh);
+    const int fh = inner(z + 2, lh, bh);
     issue(z + 2, lh, bh, fh);  // into the column node z just emptied
     if (ff) {
       collide(op, f);
-      const S1Frame qi = inner_frame(z);
-      s1_write<PUSH, false>(F, hcur, G, qi, s0 + (uint32_t)z * sxy, 0u, f, seq);
+      if (ff == 1)
+        write_class(z, f, No{}, No{});
+      else if (ff == 2)
+        write_class(z, f, Yes{}, No{});
+      else
+        write_class(z, f, No{}, Yes{});
     } else if (lf) {
       collide(op, f);
       at_plane(qf, z);
