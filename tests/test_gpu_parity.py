@@ -307,6 +307,47 @@ def test_cg_sweeps_back_to_back_per_thread_aos(gpu):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("zpipe", ["1", "0"])
+def test_cg_aos_plane_groups_z_pipeline(gpu, zpipe):
+    """AoS CG plane groups through the z-pipeline push (k_win_zp over [z0, z1)
+    with the saved wrap planes; default for fp32, LBMGPU_AOS_ZPIPE_CG=1 forces
+    it for fp64) and through the k_win gather windows (= 0): fp64 bitwise =
+    the oracle, fp32 bitwise = the SoA fp32 stepper; small plane groups and a
+    ragged z chunk, periodic and walled z, a porous mask. In a subprocess:
+    the switches are read once per process."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_1111_0922_b200 as L, oracle\n"
+        "O = oracle.Oracle()\n"
+        "rng = np.random.default_rng(3)\n"
+        "for dims, pol, porous in (((45, 17, 23), (0, 0, 0), False), ((35, 10, 70), (0, 0, 1), False),"
+        " ((40, 12, 21), (0, 1, 0), True)):\n"
+        "    names = tuple('wall' if w else 'periodic' for w in pol)\n"
+        "    mask = (rng.random(dims[0] * dims[1] * dims[2]) > 0.25).astype(np.uint8) if porous else None\n"
+        "    geo = L.GridGeometry(*dims, names, mask)\n"
+        "    f0 = O.random_field(7, geo.fluid_count())\n"
+        "    flow = L.bgk(1.7, (2e-5, 1e-6, -3e-6))\n"
+        "    want = O.ts_run(*dims, list(pol), mask, 1.7, 1.7, [2e-5, 1e-6, -3e-6], f0, 9)\n"
+        "    out = {}\n"
+        "    for prec in (8, 4):\n"
+        "        for lay in ('aos', 'soa'):\n"
+        "            st = L.create_stepper('cg', 'direct', geo, flow,"
+        " L.StepperOptions(layout=lay, precision=prec))\n"
+        "            st.load_natural(f0); st.step_n(9); st.synchronize()\n"
+        "            out[prec, lay] = st.extract_natural()\n"
+        "    assert (out[8, 'aos'].view(np.uint64) == want.view(np.uint64)).all(), (dims, 'f64')\n"
+        "    assert (out[4, 'aos'].view(np.uint64) == out[4, 'soa'].view(np.uint64)).all(), (dims, 'f32')\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ, LBMGPU_AOS_ZPIPE_CG=zpipe, LBMGPU_CG_PLANES="5", LBMGPU_AOS_ZCHUNK="3")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("dims,policy", [
     ((5, 7, 6), ("periodic", "periodic", "periodic")),
     ((33, 9, 5), ("periodic", "periodic", "wall")),
