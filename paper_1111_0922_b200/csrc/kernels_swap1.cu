@@ -1016,6 +1016,14 @@ static bool s1_async(bool push) {
                             }()};
   return on[push ? 1 : 0] != 0;
 }
+// resident blocks per SM of the kernel that will run (the z chunks of the
+// face-buffer geometry are sized for its waves): the staged pull runs four
+// fp32 blocks per SM where k_swap1 runs three (chunks for three: C1 fp32 pull
+// 0.51, for four: 0.55)
+static int s1_blocks(const DField& f, bool push) {
+  if (!f.aos && s1_async(push)) return f.prec == Prec::f64 ? LBM_S1_BLOCKS : LBM_S1_PA_BLOCKS32;
+  return s1_blocks(f);
+}
 // SoA, full-grid direct lattice without halo or ghost planes
 bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (f.aos) {
@@ -1027,7 +1035,7 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
     if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
     if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
       return false;
-    const FbGeo G = fb_geo(L, s1_blocks(f));
+    const FbGeo G = fb_geo(L, s1_blocks(f, push));
     return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
   }
   // default: SWAP push in one sweep (C1 fp64 0.81 / fp32 0.53, C4 0.68 / 0.47
@@ -1044,12 +1052,12 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
     return false;
   // face-buffer slots are 32-bit element offsets
-  const FbGeo G = fb_geo(L, s1_blocks(f));
+  const FbGeo G = fb_geo(L, s1_blocks(f, push));
   return (long long)G.tiles_x * G.tiles_y * G.nchunks * G.region < (1LL << 32);
 }
 
-size_t swap1_face_elems(const DField& f, const Lat& L) {
-  const FbGeo G = fb_geo(L, s1_blocks(f));
+size_t swap1_face_elems(const DField& f, const Lat& L, bool push) {
+  const FbGeo G = fb_geo(L, s1_blocks(f, push));
   return (size_t)G.tiles_x * G.tiles_y * G.nchunks * (size_t)G.region;
 }
 
@@ -1100,7 +1108,7 @@ static void launch_swap1_pa(cudaStream_t st, const DField& f, const Lat& L, cons
 
 void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev) {
-  const FbGeo G = fb_geo(L, s1_blocks(f));
+  const FbGeo G = fb_geo(L, s1_blocks(f, push));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
   if (f.aos) {
     if (f.prec == Prec::f64) {
@@ -1141,7 +1149,7 @@ void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost&
 
 void launch_swap1_faces(cudaStream_t st, const DField& f, const Lat& L, bool push, bool fill,
                         void* h) {
-  const FbGeo G = fb_geo(L, s1_blocks(f));
+  const FbGeo G = fb_geo(L, s1_blocks(f, push));
   const unsigned grid = (unsigned)(G.tiles_x * G.tiles_y * G.nchunks);
 #define S1_F(T, P, FL)                                                                          \
   do {                                                                                          \

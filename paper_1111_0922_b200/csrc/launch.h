@@ -131,7 +131,7 @@ bool launch_swap_fused(cudaStream_t st, const DField& f, const dev::Lat& L, cons
 // field <-> buffer transfers (fill: field -> hprev after a load; flush (push):
 // latest buffer -> field before an extraction)
 bool swap1_ok(const DField& f, const dev::Lat& L, bool push);
-size_t swap1_face_elems(const DField& f, const dev::Lat& L);
+size_t swap1_face_elems(const DField& f, const dev::Lat& L, bool push);
 void launch_swap1(cudaStream_t st, const DField& f, const dev::Lat& L, const TrtHost& op, bool push,
                   void* hcur, const void* hprev);
 void launch_swap1_faces(cudaStream_t st, const DField& f, const dev::Lat& L, bool push, bool fill,

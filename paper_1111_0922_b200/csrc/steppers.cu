@@ -384,7 +384,7 @@ class SwapDirect final : public DirectStepper {
     // (when the two face buffers, ~18 % of the field each, do not fit in the
     // free device memory, the two passes run instead)
     if (!fused_ && swap1_ok(field(f_, soa_stride(g.cells())), L_, !pull_)) {
-      hn_ = swap1_face_elems(field(f_, soa_stride(g.cells())), L_);
+      hn_ = swap1_face_elems(field(f_, soa_stride(g.cells())), L_, !pull_);
       size_t fr = 0, tot = 0;
       CK(cudaMemGetInfo(&fr, &tot));
       if (2 * hn_ * esize() + (size_t(1) << 28) < fr) {
