@@ -1004,24 +1004,28 @@ __global__ void __launch_bounds__(kFbThreads)
 
 }  // namespace
 
-// SoA through k_swap1_pa (LBMGPU_S1_PULL_ASYNC / LBMGPU_S1_PUSH_ASYNC = 1 / 0)
-static bool s1_async(bool push) {
+// SoA through k_swap1_pa (LBMGPU_S1_PULL_ASYNC / LBMGPU_S1_PUSH_ASYNC = 1 / 0).
+// Default: pull in both precisions; push in fp32 only (four blocks per SM:
+// C1 0.52 -> 0.54, C4 0.47 -> 0.49; fp64 push stays register-held, 0.81
+// against 0.74 staged)
+static bool s1_async(bool push, Prec p) {
   static const int on[2] = {[] {
                               const char* e = std::getenv("LBMGPU_S1_PULL_ASYNC");
                               return e ? (e[0] == '1' ? 1 : 0) : 1;
                             }(),
                             [] {
                               const char* e = std::getenv("LBMGPU_S1_PUSH_ASYNC");
-                              return e ? (e[0] == '1' ? 1 : 0) : 0;
+                              return e ? (e[0] == '1' ? 1 : 0) : -1;
                             }()};
-  return on[push ? 1 : 0] != 0;
+  const int v = on[push ? 1 : 0];
+  return v < 0 ? p != Prec::f64 : v != 0;
 }
 // resident blocks per SM of the kernel that will run (the z chunks of the
 // face-buffer geometry are sized for its waves): the staged pull runs four
 // fp32 blocks per SM where k_swap1 runs three (chunks for three: C1 fp32 pull
 // 0.51, for four: 0.55)
 static int s1_blocks(const DField& f, bool push) {
-  if (!f.aos && s1_async(push)) return f.prec == Prec::f64 ? LBM_S1_BLOCKS : LBM_S1_PA_BLOCKS32;
+  if (!f.aos && s1_async(push, f.prec)) return f.prec == Prec::f64 ? LBM_S1_BLOCKS : LBM_S1_PA_BLOCKS32;
   return s1_blocks(f);
 }
 // SoA, full-grid direct lattice without halo or ghost planes
@@ -1046,7 +1050,7 @@ bool swap1_ok(const DField& f, const Lat& L, bool push) {
   // tiles: C1 0.58). LBMGPU_SWAP_SINGLE=1 / 0 forces it on / off for both.
   const char* e = std::getenv("LBMGPU_SWAP_SINGLE");
   const bool on = e ? e[0] == '1'
-                    : (push || s1_async(false) || (f.prec == Prec::f64 && L.nx % kFbX == 0));
+                    : (push || s1_async(false, f.prec) || (f.prec == Prec::f64 && L.nx % kFbX == 0));
   if (!on) return false;
   if (L.ox || L.oy || L.oz || L.zghost || L.znowrap || L.sx != L.nx || L.sy != L.ny) return false;
   if (L.cell_begin != 0 || (unsigned long long)L.ncells != (unsigned long long)L.nx * L.ny * L.nz)
@@ -1120,7 +1124,7 @@ void launch_swap1(cudaStream_t st, const DField& f, const Lat& L, const TrtHost&
     }
     return;
   }
-  if (s1_async(push)) {
+  if (s1_async(push, f.prec)) {
     if (f.prec == Prec::f64) {
       if (push) launch_swap1_pa<double, true>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
       else launch_swap1_pa<double, false>(st, f, L, op, G, (double*)hcur, (const double*)hprev);
